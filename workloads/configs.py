@@ -1,0 +1,228 @@
+"""Seeded synthetic workloads shaped like BASELINE.json's five configs.
+
+This module is shared by the CPU oracle (tests, bench's cpu_baseline leg) and
+the GPU path: it produces geometry, analytic f, quadrature nodes/weights and
+targets.  It contains none of the method's arithmetic (no kernel splitting,
+no Fourier multipliers, no asymptotics).  Recipes follow SURVEY.md §8(d)
+("Synthetic inputs"); deviations are listed in DESIGN.md §Inputs.
+
+A Workload carries
+  tri      (M, 3, 2)  CCW vertices            curved (M,) edge bitmask, circle (cx, cy, rho) or None
+  nodes    (M, 12, 2) quadrature nodes        weights (M, 12)
+  targets  (T, 2)     targets_are_nodes: True when targets == nodes.reshape(-1, 2)
+  field    analytic f spec (workloads.fields)  f (M, 12) = f at the nodes
+  boundary descriptor for the local part: ("circle", cx, cy, rho) | ("rect", x0, y0, x1, y1) | None
+  tol      requested tolerance
+"""
+from dataclasses import dataclass, field as dfield
+from typing import Optional
+
+import numpy as np
+
+from . import fields, geometry
+
+
+@dataclass
+class Workload:
+    name: str
+    tri: np.ndarray
+    curved: np.ndarray
+    circle: Optional[tuple]
+    nodes: np.ndarray
+    weights: np.ndarray
+    targets: np.ndarray
+    targets_are_nodes: bool
+    field: dict
+    f: np.ndarray
+    boundary: Optional[tuple]
+    tol: float
+    meta: dict = dfield(default_factory=dict)
+
+    @property
+    def M(self):
+        return self.tri.shape[0]
+
+    @property
+    def N(self):
+        return self.nodes.shape[0] * self.nodes.shape[1]
+
+    @property
+    def T(self):
+        return self.targets.shape[0]
+
+
+def _orient_ccw(tri):
+    v0, v1, v2 = tri[:, 0], tri[:, 1], tri[:, 2]
+    det = (v1[:, 0] - v0[:, 0]) * (v2[:, 1] - v0[:, 1]) - (v1[:, 1] - v0[:, 1]) * (v2[:, 0] - v0[:, 0])
+    neg = det < 0
+    tri = tri.copy()
+    tri[neg, 1], tri[neg, 2] = tri[neg, 2].copy(), tri[neg, 1].copy()
+    return tri
+
+
+def _finish(name, tri, curved, circle, field, boundary, tol, targets=None, meta=None, f_device=None):
+    nodes, weights = geometry.nodes_weights(tri, curved, circle)
+    f = fields.evaluate(field, nodes[..., 0], nodes[..., 1], device=f_device)
+    if targets is None:
+        tg = nodes.reshape(-1, 2)
+        are_nodes = True
+    else:
+        tg = targets
+        are_nodes = False
+    return Workload(name, tri, curved, circle, nodes, weights, np.ascontiguousarray(tg), are_nodes,
+                    field, f, boundary, tol, meta or {})
+
+
+# --------------------------------------------------------------------------- config 1
+def disk_mesh(M_target=2000, seed=1, tol_count=0.01):
+    """Unit-disk triangulation: boundary ring + jittered hex interior -> Delaunay; hull edges curved."""
+    from scipy.spatial import Delaunay
+    rng = np.random.default_rng(seed)
+
+    def build(a):
+        nb = max(8, int(round(2 * np.pi / a)))
+        th = 2 * np.pi * np.arange(nb) / nb
+        ring = np.stack([np.cos(th), np.sin(th)], 1)
+        r = np.random.default_rng(seed)
+        ny = int(np.ceil(2.2 / (a * np.sqrt(3) / 2)))
+        pts = []
+        for j in range(-ny, ny + 1):
+            yy = j * a * np.sqrt(3) / 2
+            off = 0.5 * a * (j & 1)
+            xs = np.arange(-1.2, 1.2 + a, a) + off
+            pts.append(np.stack([xs, np.full_like(xs, yy)], 1))
+        pts = np.concatenate(pts)
+        pts = pts + r.uniform(-0.15 * a, 0.15 * a, pts.shape)
+        rr = np.hypot(pts[:, 0], pts[:, 1])
+        pts = pts[rr < 1.0 - 0.6 * a]
+        allp = np.concatenate([ring, pts])
+        d = Delaunay(allp)
+        return allp, d.simplices, nb
+
+    lo, hi = 0.02, 0.2
+    for _ in range(60):
+        a = 0.5 * (lo + hi)
+        P, S, nb = build(a)
+        if S.shape[0] > M_target:
+            lo = a
+        else:
+            hi = a
+        if abs(S.shape[0] - M_target) <= tol_count * M_target:
+            break
+    tri = _orient_ccw(P[S])
+    curved = _curved_flags_from_geometry(tri, max_chord=1.5 * 2 * np.sin(np.pi / nb))
+    return tri, curved
+
+
+def _curved_flags_from_geometry(tri, max_chord, rho=1.0, tol=1e-12):
+    """Edge e is an arc iff both ends lie on the circle and they are consecutive ring points."""
+    r = np.hypot(tri[..., 0], tri[..., 1])
+    onb = np.abs(r - rho) < tol
+    curved = np.zeros(tri.shape[0], np.int8)
+    for e in range(3):
+        i, j = e, (e + 1) % 3
+        both = onb[:, i] & onb[:, j]
+        chord = np.hypot(*(tri[:, j] - tri[:, i]).T)
+        curved |= ((both & (chord < max_chord)).astype(np.int8) << e)
+    return curved
+
+
+def config1(M_target=2000, seed=1, f="gauss", tol=1e-8):
+    tri, curved = disk_mesh(M_target, seed)
+    circle = (0.0, 0.0, 1.0)
+    fld = fields.const(1.0) if f == "const" else fields.gauss([1.0], [0.1], [0.2], [0.05])
+    return _finish(f"c1_disk_{f}", tri, curved, circle, fld, ("circle", 0.0, 0.0, 1.0), tol,
+                   meta={"seed": seed})
+
+
+# --------------------------------------------------------------------------- configs 2 / 4
+def square_grid(n, jitter=0.0, rng=None, alternate=False):
+    """n x n cells on [0,1]^2, two triangles per cell; interior vertices jittered by U(+-jitter*h)."""
+    h = 1.0 / n
+    gx, gy = np.meshgrid(np.arange(n + 1) * h, np.arange(n + 1) * h, indexing="ij")
+    V = np.stack([gx, gy], -1)  # (n+1, n+1, 2)
+    if jitter > 0:
+        J = rng.uniform(-jitter * h, jitter * h, V.shape)
+        J[0, :, 0] = J[-1, :, 0] = 0.0
+        J[:, 0, 1] = J[:, -1, 1] = 0.0
+        J[0, :, 1] = J[-1, :, 1] = 0.0  # keep boundary vertices on the boundary, unjittered
+        J[:, 0, 0] = J[:, -1, 0] = 0.0
+        V = V + J
+    a = V[:-1, :-1].reshape(-1, 2)
+    b = V[1:, :-1].reshape(-1, 2)
+    c = V[1:, 1:].reshape(-1, 2)
+    d = V[:-1, 1:].reshape(-1, 2)
+
+    def orient(p, q, r):
+        return (q[:, 0] - p[:, 0]) * (r[:, 1] - p[:, 1]) - (q[:, 1] - p[:, 1]) * (r[:, 0] - p[:, 0])
+
+    # diagonal a-c -> (a,b,c),(a,c,d);  diagonal b-d -> (a,b,d),(b,c,d)
+    ok_ac = (orient(a, b, c) > 0) & (orient(a, c, d) > 0)
+    ok_bd = (orient(a, b, d) > 0) & (orient(b, c, d) > 0)
+    if rng is not None and jitter > 0:
+        pick = rng.random(a.shape[0]) < 0.5
+    elif alternate:
+        pick = np.zeros(a.shape[0], bool)
+    else:
+        pick = np.ones(a.shape[0], bool)
+    use_ac = np.where(ok_ac & ok_bd, pick, ok_ac)
+    t1 = np.where(use_ac[:, None], np.stack([a, b, c], 1).reshape(-1, 6), np.stack([a, b, d], 1).reshape(-1, 6))
+    t2 = np.where(use_ac[:, None], np.stack([a, c, d], 1).reshape(-1, 6), np.stack([b, c, d], 1).reshape(-1, 6))
+    tri = np.concatenate([t1.reshape(-1, 3, 2), t2.reshape(-1, 3, 2)])
+    return _orient_ccw(tri)
+
+
+def cevian_split(tri, frac, rng, umin=1e-3, umax=1e-1):
+    """Split a random fraction of triangles along a cevian from a random side point at
+    relative position u ~ logU[umin, umax] from one end (paper §6.4)."""
+    M = tri.shape[0]
+    k = int(round(frac * M))
+    sel = rng.choice(M, size=k, replace=False)
+    side = rng.integers(0, 3, size=k)
+    u = np.exp(rng.uniform(np.log(umin), np.log(umax), size=k))
+    flip = rng.random(k) < 0.5
+    u = np.where(flip, 1.0 - u, u)
+    t = tri[sel]
+    i = side
+    j = (side + 1) % 3
+    o = (side + 2) % 3
+    ar = np.arange(k)
+    Vi, Vj, Vo = t[ar, i], t[ar, j], t[ar, o]
+    P = (1 - u)[:, None] * Vi + u[:, None] * Vj
+    A = np.stack([Vi, P, Vo], 1)
+    B = np.stack([P, Vj, Vo], 1)
+    keep = np.ones(M, bool)
+    keep[sel] = False
+    out = np.concatenate([tri[keep], A, B])
+    return _orient_ccw(out)
+
+
+def config2(n=309, seed=2, split_frac=0.05, tol=1e-9):
+    rng = np.random.default_rng(seed)
+    tri = square_grid(n, jitter=0.4, rng=rng)
+    tri = cevian_split(tri, split_frac, rng)
+    perm = rng.permutation(tri.shape[0])      # unstructured input order
+    tri = tri[perm]
+    g = np.random.default_rng(seed + 1000)
+    fld = fields.gauss(g.standard_normal(5), g.uniform(0, 1, 5), g.uniform(0, 1, 5), g.uniform(0.02, 0.1, 5) ** 2)
+    return _finish(f"c2_square_jitter_n{n}", tri, np.zeros(tri.shape[0], np.int8), None, fld,
+                   ("rect", 0.0, 0.0, 1.0, 1.0), tol, meta={"seed": seed, "n": n})
+
+
+def config4(n=1414, seed=4, tol=1e-10, kmax=64, f_device=None):
+    rng = np.random.default_rng(seed)
+    tri = square_grid(n)
+    fld = fields.random_fourier(rng, kmax)
+    return _finish(f"c4_square_uniform_n{n}", tri, np.zeros(tri.shape[0], np.int8), None, fld,
+                   ("rect", 0.0, 0.0, 1.0, 1.0), tol, meta={"seed": seed, "n": n}, f_device=f_device)
+
+
+def sample_targets(T, K, seed=12345):
+    """Seeded uniform subsample of K target indices out of T (sorted)."""
+    rng = np.random.default_rng(seed)
+    if K >= T:
+        return np.arange(T)
+    return np.sort(rng.choice(T, size=K, replace=False))
+
+
+CONFIGS = {"c1": config1, "c2": config2, "c4": config4}
