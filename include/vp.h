@@ -1,0 +1,136 @@
+/*
+ * vp.h -- C ABI of the B200-native volume-potential evaluator (libvp.so).
+ *
+ * Computes the 2D Poisson volume potential (§1, eqs. (volpotposgreen)/(GreenPoisson),
+ * lines 55-68)
+ *
+ *     V[f](x) = \int_Omega -(1/2pi) log|x - x'| f(x') dx'
+ *
+ * from source values f at the nodes of a p-point quadrature rule on each of M triangles
+ * (§2.2: "Omega* = U T_j ... p-point quadrature rule ... N = Mp"),
+ * with the paper's heat-kernel splitting V = V_L + V_NH + V_FH (eqs. (heatdecomp),
+ * (heatdecompdefs), lines 264-286):
+ *   - V_NH + V_FH (the "history") via a NUFFT: type-1 spreading of f*w onto two uniform grids,
+ *     FFT, multiplication by the split kernels' transforms, inverse FFT, type-2 interpolation
+ *     (§3, Steps 1-4, lines 767-898);
+ *   - V_L (the local part) from the asymptotic expansion at each target (§4,
+ *     eq. (vplocO5) lines 1061-1087 with the sign reading of DESIGN.md, and the interior /
+ *     on-boundary forms lines 1116-1127).
+ *
+ * All array arguments are DEVICE pointers (CUDA global memory, e.g. from torch tensors) unless
+ * the function name ends in _host.  Layouts are C-contiguous, fp64.  No exception crosses the
+ * ABI: every entry point returns a vp_status; vp_strerror() gives a static message.
+ * Thread safety: distinct plans may be used concurrently; one plan must not be evaluated
+ * concurrently with itself (it owns scratch grids).
+ */
+#ifndef VP_H_
+#define VP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  VP_OK = 0,
+  VP_ERR_ARG = -1,          /* null pointer, non-positive size, inconsistent option */
+  VP_ERR_TOL = -2,          /* tol outside [1e-14, 1e-2] */
+  VP_ERR_NONFINITE = -3,    /* NaN/Inf in nodes, weights, targets or f */
+  VP_ERR_GEOMETRY = -4,     /* boundary descriptor invalid / targets outside it */
+  VP_ERR_UNSUPPORTED = -5,  /* option combination not implemented */
+  VP_ERR_OOM = -6,          /* device allocation failed or grid too large */
+  VP_ERR_CUDA = -7,         /* CUDA runtime error */
+  VP_ERR_CUFFT = -8         /* cuFFT error */
+} vp_status;
+
+/* Boundary of Omega, needed by the boundary-aware local part V_L (§4, eq. (vplocO5);
+ * §2.2 lines 657-674 closest point).  kind = NONE means "no boundary terms" (valid when f vanishes
+ * within 12 sqrt(delta_1) of the boundary). */
+enum { VP_BDRY_NONE = 0, VP_BDRY_CIRCLE = 1, VP_BDRY_RECT = 2 };
+typedef struct {
+  int32_t kind;
+  double p[4]; /* CIRCLE: cx, cy, radius.   RECT (axis-aligned): x0, y0, x1, y1 */
+} vp_boundary;
+
+/* How the Taylor jet of f at each target is estimated from nodal data (paper silent; DESIGN.md
+ * reading R6). */
+enum { VP_DERIV_AUTO = 0, VP_DERIV_KNN = 1, VP_DERIV_TRIANGLE = 2 };
+/* which parts of V to evaluate (tests) */
+enum { VP_PART_HISTORY = 1, VP_PART_LOCAL = 2, VP_PART_ALL = 3 };
+
+/* Options; a zero-initialised struct (or NULL) means defaults. */
+typedef struct {
+  double C;                  /* delta_1 = C * Dx^2, Dx^2 = sum(w)/N. 0 -> 3 */
+  double delta2_over_delta1; /* 0 -> 32 */
+  double delta1_override;    /* > 0: use this delta_1 directly */
+  double eps_nufft;          /* NUFFT / truncation tolerance; 0 -> tol */
+  int32_t series_order;      /* interior V_L terms n_L in sum_n delta^n Lap^{n-1} f / n!; 0 -> 3 */
+  int32_t deriv_mode;        /* VP_DERIV_* */
+  int32_t deriv_degree;      /* least-squares polynomial degree for KNN jets; 0 -> 6 (4 if N > 4e6) */
+  int32_t deriv_k;           /* neighbours for KNN jets; 0 -> 2 * #monomials */
+  int32_t parts;             /* VP_PART_*; 0 -> ALL */
+  int32_t targets_are_nodes; /* 1: targets[t] == tri_nodes[t] (T == M p); enables the node fast path */
+  vp_boundary boundary;
+  void *cuda_stream;         /* cudaStream_t for vp_eval; NULL -> legacy default stream */
+} vp_opts;
+
+/* Plan parameters chosen by vp_plan (diagnostics; all derived from the rules in DESIGN.md). */
+typedef struct {
+  int64_t M, N, T;
+  int32_t p, w_es;           /* quadrature points per triangle; ES kernel width */
+  double beta_es;            /* ES kernel shape */
+  double dx2, delta1, delta2;
+  double kmax_nh, kmax_fh, L_nh, L_fh, R_trunc;
+  int64_t nf_nh, nf_fh;      /* fine grid size per dimension (sigma = 2) */
+  int64_t nmode_nh, nmode_fh;
+  double x0, y0, S;          /* centre and side of the bounding square of nodes and targets */
+  int32_t deriv_mode, deriv_degree, deriv_k;
+  int64_t n_boundary_targets;
+  double plan_ms;
+  int64_t device_bytes;      /* device memory owned by the plan */
+} vp_info;
+
+typedef struct vp_plan_s *vp_handle;
+
+/* Build a plan.  tri_nodes [M][p][2], weights [M][p] (>= 0, zero allowed for degenerate
+ * triangles), targets [T][2]; all device pointers, read during the call only (the plan copies
+ * and reorders what it keeps).  tol in [1e-14, 1e-2].  Synchronises the stream. */
+vp_status vp_plan(const double *tri_nodes, const double *weights, int64_t M, int32_t p,
+                  const double *targets, int64_t T, double tol, const vp_opts *opts, vp_handle *out);
+
+/* Evaluate V at the plan's targets.  f [M][p] (device, same order as tri_nodes), out [T]
+ * (device, fully overwritten).  Asynchronous on the plan's stream. */
+vp_status vp_eval(vp_handle plan, const double *f, double *out);
+
+/* Same, with HOST buffers: copies f host->device, evaluates, copies out device->host, and
+ * synchronises.  Pinned host memory is recommended. */
+vp_status vp_eval_host(vp_handle plan, const double *f_host, double *out_host);
+
+/* Release all device memory and cuFFT plans owned by the plan.  NULL is accepted. */
+vp_status vp_destroy(vp_handle plan);
+
+const char *vp_strerror(vp_status s);
+
+vp_status vp_get_info(vp_handle plan, vp_info *info);
+
+/* Per-phase device times (ms) of the last vp_eval when profiling is on (vp_set_profiling).
+ * names: "zero", "spread", "fft_fwd", "multiply", "fft_inv", "interp_local"; n_out <= 16. */
+vp_status vp_set_profiling(vp_handle plan, int32_t on);
+vp_status vp_get_phase_times(vp_handle plan, double *ms, int32_t *n_out, const char **names);
+
+/* Number of kernels vp_eval launches (excluding cuFFT-internal kernels) and cuFFT executions. */
+vp_status vp_eval_launch_count(vp_handle plan, int32_t *kernels, int32_t *fft_execs);
+
+/* Check f [M][p] (device) for NaN/Inf: VP_OK or VP_ERR_NONFINITE.  Synchronises. */
+vp_status vp_check_finite(vp_handle plan, const double *f);
+
+/* Human-readable detail of the last CUDA / cuFFT failure on this thread. */
+const char *vp_last_error_detail(void);
+
+const char *vp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VP_H_ */

@@ -1,0 +1,212 @@
+"""B200-native evaluator of the 2D Poisson volume potential (arXiv 2409.11998 hot path).
+
+Thin ctypes binding over the C ABI of libvp.so (include/vp.h): argument marshalling only; every
+step of the method runs in the library's sm_100a kernels (+ cuFFT).  torch is used for device
+memory and streams.  There is no CPU fallback: if libvp.so is missing or CUDA is unavailable,
+constructing a Plan raises.
+
+    plan = Plan(nodes, weights, targets, tol, boundary=("rect", 0, 0, 1, 1), targets_are_nodes=True)
+    V = plan.eval(f)          # torch cuda tensor [T]
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvp.so")
+
+VP_OK, VP_ERR_ARG, VP_ERR_TOL, VP_ERR_NONFINITE, VP_ERR_GEOMETRY, VP_ERR_UNSUPPORTED, VP_ERR_OOM, VP_ERR_CUDA, \
+    VP_ERR_CUFFT = 0, -1, -2, -3, -4, -5, -6, -7, -8
+BDRY = {None: 0, "none": 0, "circle": 1, "rect": 2}
+DERIV = {"auto": 0, "knn": 1, "triangle": 2}
+PART_HISTORY, PART_LOCAL, PART_ALL = 1, 2, 3
+
+EXPORTED = ["vp_plan", "vp_eval", "vp_eval_host", "vp_destroy", "vp_strerror", "vp_get_info", "vp_set_profiling",
+            "vp_get_phase_times", "vp_eval_launch_count", "vp_check_finite", "vp_last_error_detail", "vp_version"]
+
+
+class VpBoundary(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("p", ctypes.c_double * 4)]
+
+
+class VpOpts(ctypes.Structure):
+    _fields_ = [("C", ctypes.c_double), ("delta2_over_delta1", ctypes.c_double),
+                ("delta1_override", ctypes.c_double), ("eps_nufft", ctypes.c_double),
+                ("series_order", ctypes.c_int32), ("deriv_mode", ctypes.c_int32),
+                ("deriv_degree", ctypes.c_int32), ("deriv_k", ctypes.c_int32), ("parts", ctypes.c_int32),
+                ("targets_are_nodes", ctypes.c_int32), ("boundary", VpBoundary), ("cuda_stream", ctypes.c_void_p)]
+
+
+class VpInfo(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int64), ("N", ctypes.c_int64), ("T", ctypes.c_int64),
+                ("p", ctypes.c_int32), ("w_es", ctypes.c_int32), ("beta_es", ctypes.c_double),
+                ("dx2", ctypes.c_double), ("delta1", ctypes.c_double), ("delta2", ctypes.c_double),
+                ("kmax_nh", ctypes.c_double), ("kmax_fh", ctypes.c_double), ("L_nh", ctypes.c_double),
+                ("L_fh", ctypes.c_double), ("R_trunc", ctypes.c_double), ("nf_nh", ctypes.c_int64),
+                ("nf_fh", ctypes.c_int64), ("nmode_nh", ctypes.c_int64), ("nmode_fh", ctypes.c_int64),
+                ("x0", ctypes.c_double), ("y0", ctypes.c_double), ("S", ctypes.c_double),
+                ("deriv_mode", ctypes.c_int32), ("deriv_degree", ctypes.c_int32), ("deriv_k", ctypes.c_int32),
+                ("n_boundary_targets", ctypes.c_int64), ("plan_ms", ctypes.c_double),
+                ("device_bytes", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libvp.so (raises if it is not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2409_11998_b200.build` (or __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32, d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+        L.vp_plan.argtypes = [vp, vp, i64, i32, vp, i64, d, ctypes.POINTER(VpOpts), ctypes.POINTER(vp)]
+        L.vp_eval.argtypes = [vp, vp, vp]
+        L.vp_eval_host.argtypes = [vp, vp, vp]
+        L.vp_destroy.argtypes = [vp]
+        L.vp_strerror.argtypes = [ctypes.c_int]
+        L.vp_strerror.restype = ctypes.c_char_p
+        L.vp_get_info.argtypes = [vp, ctypes.POINTER(VpInfo)]
+        L.vp_set_profiling.argtypes = [vp, i32]
+        L.vp_get_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32),
+                                         ctypes.POINTER(ctypes.c_char_p)]
+        L.vp_eval_launch_count.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+        L.vp_check_finite.argtypes = [vp, vp]
+        L.vp_last_error_detail.restype = ctypes.c_char_p
+        L.vp_version.restype = ctypes.c_char_p
+        for name in EXPORTED:
+            L[name].restype = L[name].restype if name in ("vp_strerror", "vp_last_error_detail", "vp_version") else ctypes.c_int
+        L.vp_debug_local_coef.argtypes = [ctypes.c_int, vp, d, d, d, ctypes.c_int, ctypes.c_int, vp]
+        L.vp_debug_local_coef.restype = ctypes.c_int
+        L.vp_debug_mult.argtypes = [ctypes.c_int, d, d, d]
+        L.vp_debug_mult.restype = d
+        L.vp_debug_e1.argtypes = [d]
+        L.vp_debug_e1.restype = d
+        _lib = L
+    return _lib
+
+
+class VpError(RuntimeError):
+    def __init__(self, status, where):
+        self.status = status
+        detail = lib().vp_last_error_detail().decode()
+        super().__init__(f"{where}: {lib().vp_strerror(status).decode()} ({status}) {detail}")
+
+
+def _check(status, where):
+    if status != VP_OK:
+        raise VpError(status, where)
+
+
+def _dev_f64(t, shape_last=None):
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch tensor")
+    if t.device.type != "cuda" or t.dtype != torch.float64 or not t.is_contiguous():
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    return t
+
+
+class Plan:
+    """vp_plan / vp_eval / vp_destroy as a Python object (argument marshalling only)."""
+
+    def __init__(self, tri_nodes, weights, targets, tol, *, C=0.0, delta2_over_delta1=0.0, delta1_override=0.0,
+                 eps_nufft=0.0, series_order=0, deriv="knn", deriv_degree=0, deriv_k=0, parts=PART_ALL,
+                 targets_are_nodes=False, boundary=None, stream=None):
+        import torch
+        L = lib()
+        tri_nodes = _dev_f64(tri_nodes)
+        weights = _dev_f64(weights)
+        targets = _dev_f64(targets)
+        M, p = int(weights.shape[0]), int(weights.shape[1])
+        if tri_nodes.numel() != 2 * M * p or targets.dim() != 2 or targets.shape[1] != 2:
+            raise ValueError("shapes: tri_nodes [M,p,2], weights [M,p], targets [T,2]")
+        T = int(targets.shape[0])
+        o = VpOpts()
+        o.C, o.delta2_over_delta1, o.delta1_override, o.eps_nufft = C, delta2_over_delta1, delta1_override, eps_nufft
+        o.series_order, o.deriv_mode, o.deriv_degree, o.deriv_k = series_order, DERIV[deriv], deriv_degree, deriv_k
+        o.parts, o.targets_are_nodes = parts, 1 if targets_are_nodes else 0
+        if boundary is not None and boundary[0] not in (None, "none"):
+            o.boundary.kind = BDRY[boundary[0]]
+            for i, v in enumerate(boundary[1:5]):
+                o.boundary.p[i] = float(v)
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        self.stream = stream
+        o.cuda_stream = ctypes.c_void_p(stream.cuda_stream)
+        h = ctypes.c_void_p()
+        _check(L.vp_plan(tri_nodes.data_ptr(), weights.data_ptr(), M, p, targets.data_ptr(), T, float(tol),
+                         ctypes.byref(o), ctypes.byref(h)), "vp_plan")
+        self.h = h
+        self.M, self.p, self.T, self.N = M, p, T, M * p
+
+    def eval(self, f, out=None):
+        import torch
+        f = _dev_f64(f)
+        if f.numel() != self.N:
+            raise ValueError("f must have M*p entries")
+        if out is None:
+            out = torch.empty(self.T, dtype=torch.float64, device=f.device)
+        _check(lib().vp_eval(self.h, f.data_ptr(), out.data_ptr()), "vp_eval")
+        return out
+
+    def eval_host(self, f_host, out_host=None):
+        """f_host: numpy float64 (ideally pinned, e.g. torch pinned tensor .numpy()); returns numpy [T]."""
+        f_host = np.ascontiguousarray(f_host, dtype=np.float64).reshape(-1)
+        if out_host is None:
+            out_host = np.empty(self.T)
+        _check(lib().vp_eval_host(self.h, f_host.ctypes.data, out_host.ctypes.data), "vp_eval_host")
+        return out_host
+
+    def check_finite(self, f):
+        f = _dev_f64(f)
+        return lib().vp_check_finite(self.h, f.data_ptr()) == VP_OK
+
+    def info(self):
+        I = VpInfo()
+        _check(lib().vp_get_info(self.h, ctypes.byref(I)), "vp_get_info")
+        return I.as_dict()
+
+    def set_profiling(self, on=True):
+        _check(lib().vp_set_profiling(self.h, 1 if on else 0), "vp_set_profiling")
+
+    def phase_times(self):
+        ms = (ctypes.c_double * 16)()
+        names = (ctypes.c_char_p * 16)()
+        n = ctypes.c_int32()
+        _check(lib().vp_get_phase_times(self.h, ms, ctypes.byref(n), names), "vp_get_phase_times")
+        return {names[i].decode(): ms[i] for i in range(n.value)}
+
+    def launch_count(self):
+        k, f = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().vp_eval_launch_count(self.h, ctypes.byref(k), ctypes.byref(f)), "vp_eval_launch_count")
+        return k.value, f.value
+
+    def destroy(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib().vp_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def debug_local_coef(kind, bp, x, y, delta, nterms=3, deg=6):
+    """Host evaluation of the local-part Taylor-coefficient weights (vp_math.cuh) for tests."""
+    c = np.zeros(15)
+    bpa = np.ascontiguousarray(bp, np.float64)
+    b = lib().vp_debug_local_coef(BDRY[kind] if isinstance(kind, str) else kind, bpa.ctypes.data, x, y, delta,
+                                  nterms, deg, c.ctypes.data)
+    return bool(b), c
+
+
+def debug_mult(kind, k2, a, b):
+    return lib().vp_debug_mult(kind, k2, a, b)

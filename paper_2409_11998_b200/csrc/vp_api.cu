@@ -1,0 +1,546 @@
+// vp_api.cu -- the C ABI of libvp.so (include/vp.h): plan construction and evaluation.
+//
+// Plan (§3 "Input" and "Step 1", lines 782-821; readings R1-R5 of DESIGN.md):
+//   Dx^2 = sum(w)/N, delta1 = C Dx^2 (C = 3), delta2 = 32 delta1; k_max = sqrt(ln(1/eps)/delta);
+//   periods L_NH = S + sqrt(4 delta2 z_eps) (E1(z_eps) = eps), R = sqrt2 S + sqrt(4 delta2 ln(1/eps)),
+//   L_FH = S + R + sqrt(4 delta2 ln(1/eps)); modes n = 2 ceil(L k_max / 2pi); fine grids nf = 2n
+//   (next 2,3,5,7-smooth); ES kernel width w = ceil(log10(1/eps)) + 1, beta = 2.30 w.
+//   Sources and targets are binned into 32x32 tiles of the NH fine grid and sorted (CUB radix sort);
+//   the local-part stencils are built (vp_local.cu); cuFFT D2Z/Z2D plans share one work area.
+// Eval (one stream, no host synchronisation): zero grids -> spread -> D2Z x2 -> multiply x2 ->
+//   Z2D x2 -> interpolation + local part + scatter.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "vp_common.cuh"
+#include "vp_math.cuh"
+
+static thread_local std::string g_last_error;
+void vp_set_last_error(const std::string &s) { g_last_error = s; }
+
+extern "C" const char *vp_strerror(vp_status s) {
+  switch (s) {
+    case VP_OK: return "ok";
+    case VP_ERR_ARG: return "invalid argument";
+    case VP_ERR_TOL: return "tolerance outside [1e-14, 1e-2]";
+    case VP_ERR_NONFINITE: return "non-finite value in input";
+    case VP_ERR_GEOMETRY: return "invalid geometry / boundary descriptor";
+    case VP_ERR_UNSUPPORTED: return "unsupported option combination";
+    case VP_ERR_OOM: return "out of device memory (or grid too large)";
+    case VP_ERR_CUDA: return "CUDA runtime error";
+    case VP_ERR_CUFFT: return "cuFFT error";
+  }
+  return "unknown status";
+}
+
+extern "C" const char *vp_version(void) { return "vp 0.1 (sm_100a, fp64)"; }
+extern "C" const char *vp_last_error_detail(void) { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------------------------------------
+// host helpers
+static double host_e1(double x) {  // exponential integral E1, x > 0 (series / continued fraction)
+  if (x <= 1.0) {
+    double s = 0.0, t = 1.0;
+    for (int k = 1; k < 80; k++) {
+      t *= -x / k;
+      s -= t / k;
+      if (fabs(t / k) < 1e-17 * fabs(s)) break;
+    }
+    return -0.5772156649015329 - log(x) + s;
+  }
+  double b = x + 1.0, c = 1e300, d = 1.0 / b, h = d;
+  for (int i = 1; i < 400; i++) {
+    double an = -(double)i * i;
+    b += 2.0;
+    d = 1.0 / (an * d + b);
+    c = b + an / c;
+    double del = c * d;
+    h *= del;
+    if (fabs(del - 1.0) < 1e-16) break;
+  }
+  return h * exp(-x);
+}
+
+static double solve_e1(double eps) {  // z with E1(z) = eps
+  double z = log(1.0 / eps);
+  for (int it = 0; it < 100; it++) {
+    double f = host_e1(z) - eps;
+    double df = -exp(-z) / z;
+    double dz = f / df;
+    z -= dz;
+    if (fabs(dz) < 1e-12 * z) break;
+  }
+  return z;
+}
+
+static int64_t next_smooth(int64_t n) {  // smallest even 2^a 3^b 5^c 7^d >= n
+  if (n < 2) n = 2;
+  for (int64_t m = n + (n & 1);; m += 2) {
+    int64_t r = m;
+    for (int p : {2, 3, 5, 7})
+      while (r % p == 0) r /= p;
+    if (r == 1) return m;
+  }
+}
+
+static void gauss_legendre01(int n, std::vector<double> &x, std::vector<double> &w) {
+  x.resize(n);
+  w.resize(n);
+  for (int i = 0; i < n; i++) {
+    double z = cos(VP_PI * (i + 0.75) / (n + 0.5)), pp = 1.0;
+    for (int it = 0; it < 100; it++) {
+      double p1 = 1.0, p2 = 0.0;
+      for (int j = 1; j <= n; j++) {
+        double p3 = p2;
+        p2 = p1;
+        p1 = ((2.0 * j - 1.0) * z * p2 - (j - 1.0) * p3) / j;
+      }
+      pp = n * (z * p1 - p2) / (z * z - 1.0);
+      double dz = p1 / pp;
+      z -= dz;
+      if (fabs(dz) < 1e-16) break;
+    }
+    x[i] = 0.5 * (1.0 - z);
+    w[i] = 1.0 / ((1.0 - z * z) * pp * pp);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// validation / statistics of the inputs (one pass over nodes, weights and targets)
+struct Stats {
+  double sumw, xmin, xmax, ymin, ymax;
+  int bad;
+};
+
+__global__ void k_stats(const double *__restrict__ nodes, const double *__restrict__ w, int64_t N,
+                        const double *__restrict__ tg, int64_t T, double *out_sum, double *out_box, int *out_bad) {
+  double s = 0.0, x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
+  int bad = 0;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N + T; i += stride) {
+    double x, y;
+    if (i < N) {
+      x = nodes[2 * i];
+      y = nodes[2 * i + 1];
+      double ww = w[i];
+      if (!isfinite(ww) || ww < 0.0) bad = 1;
+      s += ww;
+    } else {
+      x = tg[2 * (i - N)];
+      y = tg[2 * (i - N) + 1];
+    }
+    if (!isfinite(x) || !isfinite(y)) bad = 1;
+    x0 = fmin(x0, x); x1 = fmax(x1, x); y0 = fmin(y0, y); y1 = fmax(y1, y);
+  }
+  typedef cub::BlockReduce<double, 256> BR;
+  __shared__ typename BR::TempStorage ts;
+  double bs = BR(ts).Sum(s);
+  __syncthreads();
+  double bx0 = BR(ts).Reduce(x0, cub::Min());
+  __syncthreads();
+  double bx1 = BR(ts).Reduce(x1, cub::Max());
+  __syncthreads();
+  double by0 = BR(ts).Reduce(y0, cub::Min());
+  __syncthreads();
+  double by1 = BR(ts).Reduce(y1, cub::Max());
+  __syncthreads();
+  int any = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    out_sum[blockIdx.x] = bs;
+    out_box[4 * blockIdx.x] = bx0;
+    out_box[4 * blockIdx.x + 1] = bx1;
+    out_box[4 * blockIdx.x + 2] = by0;
+    out_box[4 * blockIdx.x + 3] = by1;
+    if (any) *out_bad = 1;
+  }
+}
+
+__global__ void k_check_finite(const double *__restrict__ f, int64_t n, int *bad) {
+  int b = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(f[i])) b = 1;
+  if (__syncthreads_or(b) && threadIdx.x == 0) *bad = 1;
+}
+
+// ---------------------------------------------------------------------------------------------
+static void setup_grid(vp_plan_s *P, VpGrid &G, int kind, double L, double kmax) {
+  G.kind = kind;
+  G.L = L;
+  int64_t n = 2 * (int64_t)ceil(L * kmax / (2.0 * VP_PI));
+  if (n < 4) n = 4;
+  G.nmode = n;
+  G.nf = next_smooth(2 * n);
+  if (G.nf < 2 * P->w) G.nf = next_smooth(2 * P->w);
+  G.h = L / (double)G.nf;
+  G.ox = P->cx - 0.5 * L;
+  G.oy = P->cy - 0.5 * L;
+  G.row = 2 * (G.nf / 2 + 1);
+  if ((double)G.nf * (double)G.row * 8.0 > 120e9) throw VpError{VP_ERR_OOM};
+  // ES deconvolution: Phi(k) = 2 alpha int_0^1 psi(s) cos(k alpha s) ds, alpha = w h / 2
+  int64_t nh = G.nmode / 2;
+  std::vector<double> dec(nh + 1), gx, gw;
+  gauss_legendre01(2 * P->w + 40, gx, gw);
+  double alpha = P->w * G.h / 2.0;
+  for (int64_t m = 0; m <= nh; m++) {
+    double k = 2.0 * VP_PI * m / L, s = 0.0;
+    for (size_t q = 0; q < gx.size(); q++) s += gw[q] * vp_es(gx[q], P->beta) * cos(k * alpha * gx[q]);
+    double Phi = 2.0 * alpha * s;
+    dec[m] = 1.0 / (Phi * Phi);
+  }
+  G.deconv = vp_alloc<double>(P, nh + 1);
+  VP_CUDA(cudaMemcpy(G.deconv, dec.data(), sizeof(double) * (nh + 1), cudaMemcpyHostToDevice));
+  G.data = vp_alloc<double>(P, (size_t)G.nf * G.row);
+}
+
+static void make_fft_plans(vp_plan_s *P) {
+  size_t ws[4] = {0, 0, 0, 0}, wmax = 0;
+  VpGrid *gs[2] = {&P->nh, &P->fh};
+  for (int g = 0; g < 2; g++) {
+    VpGrid &G = *gs[g];
+    long long n[2] = {G.nf, G.nf};
+    long long rin[2] = {G.nf, G.row};         // real layout (padded rows)
+    long long cin[2] = {G.nf, G.row / 2};     // complex layout
+    VP_CUFFT(cufftCreate(&G.fwd));
+    VP_CUFFT(cufftCreate(&G.inv));
+    VP_CUFFT(cufftSetAutoAllocation(G.fwd, 0));
+    VP_CUFFT(cufftSetAutoAllocation(G.inv, 0));
+    VP_CUFFT(cufftMakePlanMany64(G.fwd, 2, n, rin, 1, G.nf * G.row, cin, 1, G.nf * (G.row / 2), CUFFT_D2Z, 1,
+                                 &ws[2 * g]));
+    VP_CUFFT(cufftMakePlanMany64(G.inv, 2, n, cin, 1, G.nf * (G.row / 2), rin, 1, G.nf * G.row, CUFFT_Z2D, 1,
+                                 &ws[2 * g + 1]));
+    G.has_plans = true;
+  }
+  for (int i = 0; i < 4; i++) wmax = std::max(wmax, ws[i]);
+  void *work = vp_alloc<char>(P, wmax + 256);
+  for (int g = 0; g < 2; g++) {
+    VP_CUFFT(cufftSetWorkArea(gs[g]->fwd, work));
+    VP_CUFFT(cufftSetWorkArea(gs[g]->inv, work));
+    VP_CUFFT(cufftSetStream(gs[g]->fwd, P->stream));
+    VP_CUFFT(cufftSetStream(gs[g]->inv, P->stream));
+  }
+}
+
+static void build_tiles(vp_plan_s *P, const double *nodes_dev, const double *weights_dev) {
+  VpTiles &Tl = P->tiles;
+  Tl.TS = 32;
+  double cell = Tl.TS * P->nh.h;
+  Tl.ntx = (P->nh.nf + Tl.TS - 1) / Tl.TS;
+  Tl.nty = Tl.ntx;
+  P->sx = vp_alloc<double>(P, P->N);
+  P->sy = vp_alloc<double>(P, P->N);
+  P->sperm = vp_alloc<int32_t>(P, P->N);
+  int64_t *bs = nullptr;
+  int64_t nb = vp_sort_points(P, nodes_dev, P->N, P->nh.ox, P->nh.oy, cell, Tl.ntx, Tl.nty, P->sx, P->sy, nullptr,
+                              P->sperm, &bs);
+  // sorted weights
+  P->sw = vp_alloc<double>(P, P->N);
+  {
+    // gather weights by the permutation on the host-free path: simple kernel
+    extern void vp_gather_f64(const double *src, const int32_t *perm, int64_t n, double *dst, cudaStream_t s);
+    vp_gather_f64(weights_dev, P->sperm, P->N, P->sw, P->stream);
+  }
+  std::vector<int64_t> h(nb + 1);
+  VP_CUDA(cudaMemcpyAsync(h.data(), bs, sizeof(int64_t) * (nb + 1), cudaMemcpyDeviceToHost, P->stream));
+  VP_CUDA(cudaStreamSynchronize(P->stream));
+  const int64_t MAXSUB = 1024;
+  std::vector<int4> subs;
+  for (int64_t b = 0; b < nb; b++) {
+    int64_t s0 = h[b], s1 = h[b + 1];
+    for (int64_t s = s0; s < s1; s += MAXSUB)
+      subs.push_back(make_int4((int)(b % Tl.ntx), (int)(b / Tl.ntx), (int)s, (int)std::min(MAXSUB, s1 - s)));
+  }
+  Tl.nsub = (int64_t)subs.size();
+  Tl.sub = vp_alloc<int4>(P, subs.size());
+  if (!subs.empty())
+    VP_CUDA(cudaMemcpy(Tl.sub, subs.data(), sizeof(int4) * subs.size(), cudaMemcpyHostToDevice));
+  P->fh_tile_w = (int)ceil(Tl.TS * P->nh.h / P->fh.h) + P->w + 4;
+}
+
+__global__ void k_gather_f64(const double *__restrict__ src, const int32_t *__restrict__ perm, int64_t n,
+                             double *__restrict__ dst) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[perm[i]];
+}
+void vp_gather_f64(const double *src, const int32_t *perm, int64_t n, double *dst, cudaStream_t s) {
+  if (n == 0) return;
+  k_gather_f64<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, perm, n, dst);
+  VP_CHECK_LAUNCH();
+}
+
+static void free_plan(vp_plan_s *P) {
+  if (!P) return;
+  for (VpGrid *G : {&P->nh, &P->fh}) {
+    if (G->has_plans) {
+      cufftDestroy(G->fwd);
+      cufftDestroy(G->inv);
+    }
+  }
+  for (void *p : P->allocs) cudaFree(p);
+  if (P->ev_init)
+    for (int i = 0; i < 8; i++) cudaEventDestroy(P->ev[i]);
+  delete P;
+}
+
+extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int64_t M, int32_t p,
+                             const double *targets, int64_t T, double tol, const vp_opts *opts, vp_handle *out) {
+  if (!out) return VP_ERR_ARG;
+  *out = nullptr;
+  if (!tri_nodes || !weights || !targets || M <= 0 || p <= 0 || T <= 0) return VP_ERR_ARG;
+  if (!(tol >= 1e-14 && tol <= 1e-2)) return VP_ERR_TOL;
+  int64_t N = M * (int64_t)p;
+  if (N >= ((int64_t)1 << 31) || T >= ((int64_t)1 << 31)) return VP_ERR_UNSUPPORTED;
+  vp_plan_s *P = new vp_plan_s();
+  auto t0 = std::chrono::steady_clock::now();
+  try {
+    P->M = M; P->p = p; P->N = N; P->T = T; P->tol = tol;
+    if (opts) P->opts = *opts;
+    vp_opts &o = P->opts;
+    if (o.targets_are_nodes && T != N) throw VpError{VP_ERR_ARG};
+    if (o.parts < 0 || o.parts > 3) throw VpError{VP_ERR_ARG};
+    if (o.boundary.kind == VP_BDRY_CIRCLE && !(o.boundary.p[2] > 0)) throw VpError{VP_ERR_GEOMETRY};
+    if (o.boundary.kind == VP_BDRY_RECT && !(o.boundary.p[2] > o.boundary.p[0] && o.boundary.p[3] > o.boundary.p[1]))
+      throw VpError{VP_ERR_GEOMETRY};
+    if (o.boundary.kind < 0 || o.boundary.kind > 2) throw VpError{VP_ERR_GEOMETRY};
+    P->stream = (cudaStream_t)o.cuda_stream;
+    P->eps = o.eps_nufft > 0 ? o.eps_nufft : tol;
+    // ---- statistics
+    const int nblk = 148 * 4;
+    double *d_sum, *d_box;
+    int *d_bad;
+    VP_CUDA(cudaMallocAsync(&d_sum, sizeof(double) * nblk, P->stream));
+    VP_CUDA(cudaMallocAsync(&d_box, sizeof(double) * 4 * nblk, P->stream));
+    VP_CUDA(cudaMallocAsync(&d_bad, sizeof(int), P->stream));
+    VP_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), P->stream));
+    k_stats<<<nblk, 256, 0, P->stream>>>(tri_nodes, weights, N, targets, T, d_sum, d_box, d_bad);
+    VP_CHECK_LAUNCH();
+    std::vector<double> hs(nblk), hb(4 * nblk);
+    int hbad = 0;
+    VP_CUDA(cudaMemcpyAsync(hs.data(), d_sum, sizeof(double) * nblk, cudaMemcpyDeviceToHost, P->stream));
+    VP_CUDA(cudaMemcpyAsync(hb.data(), d_box, sizeof(double) * 4 * nblk, cudaMemcpyDeviceToHost, P->stream));
+    VP_CUDA(cudaMemcpyAsync(&hbad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
+    VP_CUDA(cudaStreamSynchronize(P->stream));
+    VP_CUDA(cudaFree(d_sum)); VP_CUDA(cudaFree(d_box)); VP_CUDA(cudaFree(d_bad));
+    if (hbad) throw VpError{VP_ERR_NONFINITE};
+    double sumw = 0, x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
+    for (int i = 0; i < nblk; i++) {
+      sumw += hs[i];
+      x0 = std::min(x0, hb[4 * i]); x1 = std::max(x1, hb[4 * i + 1]);
+      y0 = std::min(y0, hb[4 * i + 2]); y1 = std::max(y1, hb[4 * i + 3]);
+    }
+    if (!(sumw > 0)) throw VpError{VP_ERR_ARG};
+    // ---- parameters
+    P->dx2 = sumw / (double)N;
+    double C = o.C > 0 ? o.C : 3.0;
+    double ratio = o.delta2_over_delta1 > 0 ? o.delta2_over_delta1 : 32.0;
+    if (ratio <= 1.0) throw VpError{VP_ERR_ARG};
+    P->delta1 = o.delta1_override > 0 ? o.delta1_override : C * P->dx2;
+    P->delta2 = ratio * P->delta1;
+    P->S = std::max(std::max(x1 - x0, y1 - y0), 1e-300);
+    P->cx = 0.5 * (x0 + x1);
+    P->cy = 0.5 * (y0 + y1);
+    double lne = log(1.0 / P->eps);
+    P->w = std::min(16, std::max(4, (int)ceil(log10(1.0 / P->eps)) + 1));
+    P->beta = 2.30 * P->w;
+    P->kmax_nh = sqrt(lne / P->delta1);
+    P->kmax_fh = sqrt(lne / P->delta2);
+    double zeps = solve_e1(P->eps);
+    double m2 = sqrt(4.0 * P->delta2 * lne);
+    // margins: the kernel decay and (>= w+4 fine cells) so that spreading never wraps
+    double L_nh = P->S + std::max(sqrt(4.0 * P->delta2 * zeps), (P->w + 4) * (VP_PI / P->kmax_nh) / 2.0);
+    P->R = sqrt(2.0) * P->S + m2;
+    double L_fh = P->S + P->R + m2;
+    setup_grid(P, P->nh, 0, L_nh, P->kmax_nh);
+    P->nh.delta_a = P->delta1; P->nh.delta_b = P->delta2;
+    setup_grid(P, P->fh, 1, L_fh, P->kmax_fh);
+    P->fh.delta_a = P->delta2; P->fh.delta_b = P->R;
+    // ---- sources and targets sorted by NH tile
+    build_tiles(P, tri_nodes, weights);
+    P->tx = vp_alloc<double>(P, T);
+    P->ty = vp_alloc<double>(P, T);
+    P->tperm = vp_alloc<int64_t>(P, T);
+    vp_sort_points(P, targets, T, P->nh.ox, P->nh.oy, P->tiles.TS * P->nh.h, P->tiles.ntx, P->tiles.nty, P->tx,
+                   P->ty, P->tperm, nullptr, nullptr);
+    // ---- local part
+    int parts = o.parts ? o.parts : VP_PART_ALL;
+    P->dmode = o.deriv_mode ? o.deriv_mode : VP_DERIV_KNN;
+    if (P->dmode != VP_DERIV_KNN) throw VpError{VP_ERR_UNSUPPORTED};
+    P->deg = o.deriv_degree > 0 ? o.deriv_degree : (N > 4000000 ? 4 : 6);
+    if (P->deg > VP_MAXDEG) throw VpError{VP_ERR_ARG};
+    int nc = vp_ncoef(P->deg);
+    P->K = o.deriv_k > 0 ? o.deriv_k : 2 * nc;
+    if (P->K > 64) P->K = 64;
+    if (P->K < nc) throw VpError{VP_ERR_ARG};
+    if (P->K > N) throw VpError{VP_ERR_ARG};
+    if (parts & VP_PART_LOCAL) {
+      vp_build_local(P, tri_nodes);
+    } else {
+      P->K = 0;
+      P->lalpha = vp_alloc<double>(P, 1);
+      P->lnode = vp_alloc<int32_t>(P, 1);
+      P->lidx = vp_alloc<int32_t>(P, 1);
+      P->lw = vp_alloc<double>(P, 1);
+    }
+    // ---- FFT plans
+    make_fft_plans(P);
+    VP_CUDA(cudaStreamSynchronize(P->stream));
+    VP_CUDA(cudaGetLastError());
+  } catch (VpError &e) {
+    cudaStreamSynchronize(P->stream);
+    cudaGetLastError();
+    free_plan(P);
+    return e.s;
+  } catch (...) {
+    free_plan(P);
+    return VP_ERR_CUDA;
+  }
+  P->plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  *out = P;
+  return VP_OK;
+}
+
+static void record(vp_plan_s *P, int i) {
+  if (P->profiling) cudaEventRecord(P->ev[i], P->stream);
+}
+
+extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
+  if (!P || !f || !out) return VP_ERR_ARG;
+  try {
+    P->n_kernels = 0;
+    P->n_ffts = 0;
+    int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
+    if (P->profiling && !P->ev_init) {
+      for (int i = 0; i < 8; i++) VP_CUDA(cudaEventCreate(&P->ev[i]));
+      P->ev_init = true;
+    }
+    record(P, 0);
+    if (parts & VP_PART_HISTORY) {
+      VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, P->stream));
+      VP_CUDA(cudaMemsetAsync(P->fh.data, 0, sizeof(double) * P->fh.nf * P->fh.row, P->stream));
+      record(P, 1);
+      vp_launch_spread(P, f);
+      record(P, 2);
+      VP_CUFFT(cufftExecD2Z(P->nh.fwd, P->nh.data, (cufftDoubleComplex *)P->nh.data));
+      VP_CUFFT(cufftExecD2Z(P->fh.fwd, P->fh.data, (cufftDoubleComplex *)P->fh.data));
+      record(P, 3);
+      vp_launch_multiply(P, P->nh);
+      vp_launch_multiply(P, P->fh);
+      record(P, 4);
+      VP_CUFFT(cufftExecZ2D(P->nh.inv, (cufftDoubleComplex *)P->nh.data, P->nh.data));
+      VP_CUFFT(cufftExecZ2D(P->fh.inv, (cufftDoubleComplex *)P->fh.data, P->fh.data));
+      P->n_ffts = 4;
+      record(P, 5);
+    } else {
+      for (int i = 1; i <= 5; i++) record(P, i);
+    }
+    vp_launch_interp_local(P, f, out);
+    record(P, 6);
+    P->n_phase = 6;
+  } catch (VpError &e) {
+    return e.s;
+  }
+  return VP_OK;
+}
+
+extern "C" vp_status vp_eval_host(vp_handle P, const double *f_host, double *out_host) {
+  if (!P || !f_host || !out_host) return VP_ERR_ARG;
+  try {
+    if (!P->f_dev) P->f_dev = vp_alloc<double>(P, P->N);
+    if (!P->out_dev) P->out_dev = vp_alloc<double>(P, P->T);
+    VP_CUDA(cudaMemcpyAsync(P->f_dev, f_host, sizeof(double) * P->N, cudaMemcpyHostToDevice, P->stream));
+    vp_status s = vp_eval(P, P->f_dev, P->out_dev);
+    if (s != VP_OK) return s;
+    VP_CUDA(cudaMemcpyAsync(out_host, P->out_dev, sizeof(double) * P->T, cudaMemcpyDeviceToHost, P->stream));
+    VP_CUDA(cudaStreamSynchronize(P->stream));
+  } catch (VpError &e) {
+    return e.s;
+  }
+  return VP_OK;
+}
+
+extern "C" vp_status vp_check_finite(vp_handle P, const double *f) {
+  if (!P || !f) return VP_ERR_ARG;
+  try {
+    int *d_bad, hbad = 0;
+    VP_CUDA(cudaMallocAsync(&d_bad, sizeof(int), P->stream));
+    VP_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), P->stream));
+    k_check_finite<<<148 * 4, 256, 0, P->stream>>>(f, P->N, d_bad);
+    VP_CHECK_LAUNCH();
+    VP_CUDA(cudaMemcpyAsync(&hbad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
+    VP_CUDA(cudaStreamSynchronize(P->stream));
+    VP_CUDA(cudaFree(d_bad));
+    return hbad ? VP_ERR_NONFINITE : VP_OK;
+  } catch (VpError &e) {
+    return e.s;
+  }
+}
+
+extern "C" vp_status vp_destroy(vp_handle P) {
+  if (!P) return VP_OK;
+  cudaStreamSynchronize(P->stream);
+  free_plan(P);
+  return VP_OK;
+}
+
+extern "C" vp_status vp_get_info(vp_handle P, vp_info *I) {
+  if (!P || !I) return VP_ERR_ARG;
+  memset(I, 0, sizeof(*I));
+  I->M = P->M; I->N = P->N; I->T = P->T; I->p = P->p; I->w_es = P->w; I->beta_es = P->beta;
+  I->dx2 = P->dx2; I->delta1 = P->delta1; I->delta2 = P->delta2;
+  I->kmax_nh = P->kmax_nh; I->kmax_fh = P->kmax_fh; I->L_nh = P->nh.L; I->L_fh = P->fh.L; I->R_trunc = P->R;
+  I->nf_nh = P->nh.nf; I->nf_fh = P->fh.nf; I->nmode_nh = P->nh.nmode; I->nmode_fh = P->fh.nmode;
+  I->x0 = P->cx; I->y0 = P->cy; I->S = P->S;
+  I->deriv_mode = P->dmode; I->deriv_degree = P->deg; I->deriv_k = P->K;
+  I->n_boundary_targets = P->n_bdry;
+  I->plan_ms = P->plan_ms;
+  I->device_bytes = P->device_bytes;
+  return VP_OK;
+}
+
+extern "C" vp_status vp_set_profiling(vp_handle P, int32_t on) {
+  if (!P) return VP_ERR_ARG;
+  P->profiling = on != 0;
+  return VP_OK;
+}
+
+static const char *g_phase_names[6] = {"zero", "spread", "fft_fwd", "multiply", "fft_inv", "interp_local"};
+
+extern "C" vp_status vp_get_phase_times(vp_handle P, double *ms, int32_t *n_out, const char **names) {
+  if (!P || !ms || !n_out) return VP_ERR_ARG;
+  if (!P->profiling || !P->ev_init) return VP_ERR_ARG;
+  if (cudaEventSynchronize(P->ev[6]) != cudaSuccess) return VP_ERR_CUDA;
+  for (int i = 0; i < 6; i++) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, P->ev[i], P->ev[i + 1]);
+    ms[i] = t;
+    if (names) names[i] = g_phase_names[i];
+  }
+  *n_out = 6;
+  return VP_OK;
+}
+
+extern "C" vp_status vp_eval_launch_count(vp_handle P, int32_t *kernels, int32_t *fft_execs) {
+  if (!P || !kernels || !fft_execs) return VP_ERR_ARG;
+  *kernels = P->n_kernels;
+  *fft_execs = P->n_ffts;
+  return VP_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// host-callable diagnostics of the method's scalar math (CPU unit tests of host logic)
+extern "C" int vp_debug_local_coef(int kind, const double *bp, double x, double y, double delta, int nterms, int deg,
+                                   double *coef15) {
+  bool b = false;
+  if (kind == VP_BDRY_CIRCLE) b = vp_coef_circle(x, y, bp[0], bp[1], bp[2], delta, nterms, deg, coef15);
+  else if (kind == VP_BDRY_RECT) b = vp_coef_rect(x, y, bp[0], bp[1], bp[2], bp[3], delta, deg, coef15);
+  if (!b) vp_coef_interior(delta, nterms, deg, coef15);
+  return b ? 1 : 0;
+}
+extern "C" double vp_debug_mult(int kind, double k2, double a, double b) {
+  return kind == 0 ? vp_mult_nh(k2, a, b) : vp_mult_fh(k2, a, b);
+}
+extern "C" double vp_debug_e1(double x) { return host_e1(x); }

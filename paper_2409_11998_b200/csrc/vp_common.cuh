@@ -1,0 +1,123 @@
+// vp_common.cuh -- plan layout and shared device/host helpers of libvp.so (product path).
+// No code here is shared with oracle/ (test infrastructure).
+#pragma once
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/vp.h"
+
+#define VP_PI 3.14159265358979323846
+
+// ---------------------------------------------------------------------------------------------
+// error plumbing: every CUDA / cuFFT call inside the library goes through these
+struct VpError {
+  vp_status s;
+};
+#define VP_CUDA(x)                                                 \
+  do {                                                             \
+    cudaError_t e_ = (x);                                          \
+    if (e_ != cudaSuccess) {                                       \
+      vp_set_last_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+      throw VpError{e_ == cudaErrorMemoryAllocation ? VP_ERR_OOM : VP_ERR_CUDA}; \
+    }                                                              \
+  } while (0)
+#define VP_CUFFT(x)                                                \
+  do {                                                             \
+    cufftResult r_ = (x);                                          \
+    if (r_ != CUFFT_SUCCESS) {                                     \
+      vp_set_last_error(std::string(#x) + ": cufft error " + std::to_string((int)r_)); \
+      throw VpError{r_ == CUFFT_ALLOC_FAILED ? VP_ERR_OOM : VP_ERR_CUFFT}; \
+    }                                                              \
+  } while (0)
+#define VP_CHECK_LAUNCH() VP_CUDA(cudaGetLastError())
+
+void vp_set_last_error(const std::string &s);
+
+// ---------------------------------------------------------------------------------------------
+// One uniform periodic fine grid of the NUFFT (§3).
+// Point x lies at fractional grid coordinate g = (x - o)/h; grid node i sits at o + i h.
+struct VpGrid {
+  int64_t nf = 0;     // fine points per dimension (even, 2,3,5,7-smooth)
+  int64_t nmode = 0;  // kept modes per dimension (even); |m| <= nmode/2
+  int64_t row = 0;    // padded row length in doubles for in-place R2C: 2*(nf/2+1)
+  double L = 0, h = 0, ox = 0, oy = 0;
+  double delta_a = 0, delta_b = 0;  // NH: (delta1, delta2); FH: (delta2, R)
+  int kind = 0;                     // 0 = near history, 1 = far history
+  double *data = nullptr;           // nf * row doubles
+  double *deconv = nullptr;         // [nmode/2+1]: 1 / Phi(k_m)^2 (1D ES transform, squared inverse)
+  cufftHandle fwd = 0, inv = 0;
+  bool has_plans = false;
+};
+
+struct VpTiles {          // sorted points binned into TS x TS tiles of the NH fine grid
+  int TS = 32;
+  int64_t ntx = 0, nty = 0;
+  int64_t nsub = 0;       // spreading sub-problems
+  int4 *sub = nullptr;    // (tile_x, tile_y, start, count)
+};
+
+struct vp_plan_s {
+  // sizes
+  int64_t M = 0, N = 0, T = 0;
+  int32_t p = 0;
+  double tol = 0, eps = 0;
+  vp_opts opts{};
+  cudaStream_t stream = nullptr;
+  // parameters
+  double dx2 = 0, delta1 = 0, delta2 = 0, kmax_nh = 0, kmax_fh = 0, R = 0, S = 0, cx = 0, cy = 0;
+  int w = 0;
+  double beta = 0;
+  VpGrid nh, fh;
+  // sources, sorted by NH tile
+  double *sx = nullptr, *sy = nullptr, *sw = nullptr;  // coords, weights
+  int32_t *sperm = nullptr;                            // sorted -> user node index
+  VpTiles tiles;
+  int fh_tile_w = 0;  // FH smem tile width (cells) for one NH tile
+  // targets, sorted by NH tile
+  double *tx = nullptr, *ty = nullptr;
+  int64_t *tperm = nullptr;  // sorted -> user target index
+  // local part: V_L(t) = alpha_t * f(node_t) + sum_k omega_{t,k} f[idx_{t,k}]
+  int K = 0, deg = 0, dmode = 0;
+  int32_t *lidx = nullptr;     // [T][K] user node indices (sorted target order)
+  double *lw = nullptr;        // [T][K]
+  double *lalpha = nullptr;    // [T]
+  int32_t *lnode = nullptr;    // [T] user node index of the target (targets_are_nodes) or -1
+  int64_t n_bdry = 0;
+  // host-side eval staging (vp_eval_host)
+  double *f_dev = nullptr, *out_dev = nullptr;
+  // profiling
+  bool profiling = false;
+  cudaEvent_t ev[8] = {};
+  bool ev_init = false;
+  double phase_ms[8] = {};
+  int n_phase = 0;
+  double plan_ms = 0;
+  int64_t device_bytes = 0;
+  std::vector<void *> allocs;
+  int32_t n_kernels = 0, n_ffts = 0;
+};
+
+// device allocation tracked by the plan
+template <typename T>
+T *vp_alloc(vp_plan_s *P, size_t n) {
+  void *p = nullptr;
+  if (n == 0) n = 1;
+  VP_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  P->allocs.push_back(p);
+  P->device_bytes += (int64_t)(n * sizeof(T));
+  return (T *)p;
+}
+
+// ---------------------------------------------------------------------------------------------
+// launch helpers (defined in the .cu files)
+void vp_launch_spread(vp_plan_s *P, const double *f);
+void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
+void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out);
+void vp_build_local(vp_plan_s *P, const double *nodes_dev);
+int64_t vp_sort_points(vp_plan_s *P, const double *xy, int64_t n, double ox, double oy, double cell,
+                       int64_t nbx, int64_t nby, double *xs, double *ys, int64_t *perm64, int32_t *perm32,
+                       int64_t **bin_start_out);

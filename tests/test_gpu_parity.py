@@ -1,0 +1,142 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * full V vs the oracle's exact integral: relative l2 <= 10 x tol
+  * smooth (history) part vs the direct real-space sum of G_H[delta_1] (and the direct DFT of the same
+    split): relative l2 <= 1e-12 at eps = 1e-13
+"""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import configs, fields
+
+torch = pytest.importorskip("torch")
+import paper_2409_11998_b200 as vp  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def rel_l2(a, b):
+    return float(np.sqrt(np.sum((a - b) ** 2) / np.sum(b ** 2)))
+
+
+def to_dev(w):
+    return (torch.from_numpy(np.ascontiguousarray(w.nodes)).to(DEV), torch.from_numpy(w.weights).to(DEV),
+            torch.from_numpy(np.ascontiguousarray(w.targets)).to(DEV), torch.from_numpy(w.f).to(DEV))
+
+
+def make_plan(w, **kw):
+    nodes, wts, tg, f = to_dev(w)
+    kw.setdefault("boundary", w.boundary)
+    kw.setdefault("targets_are_nodes", w.targets_are_nodes)
+    tol = kw.pop("tol", w.tol)
+    return vp.Plan(nodes, wts, tg, tol, **kw), f
+
+
+# ------------------------------------------------------------------------------------ smooth part
+@pytest.mark.parametrize("which", ["c1", "c2small"])
+def test_smooth_part_vs_direct_GH_sum(which):
+    w = configs.config1() if which == "c1" else configs.config2(n=40)
+    d1 = 3.0 * w.weights.mean()
+    plan, f = make_plan(w, tol=1e-13, parts=vp.PART_HISTORY, delta1_override=d1)
+    V = plan.eval(f).cpu().numpy()
+    idx = configs.sample_targets(w.T, 1500, seed=21)
+    ref = oracle.smooth_direct(w.nodes.reshape(-1, 2), (w.f * w.weights).ravel(), w.targets[idx], d1)
+    e = rel_l2(V[idx], ref)
+    print(which, "smooth rel l2", e, plan.info()["w_es"])
+    assert e < 1e-12
+
+
+def test_smooth_part_vs_direct_dft():
+    rng = np.random.default_rng(31)
+    src = rng.uniform(0.1, 0.9, (400, 2))
+    c = rng.standard_normal(400)
+    # 400 sources as 100 "triangles" of 4 nodes each; weights = c, f = 1 so c_j = f_j w_j
+    nodes = torch.from_numpy(src.reshape(100, 4, 2).copy()).to(DEV)
+    wts = torch.from_numpy(np.abs(c).reshape(100, 4)).to(DEV)
+    fv = torch.from_numpy(np.sign(c).reshape(100, 4)).to(DEV)
+    tg_np = np.concatenate([rng.uniform(0.1, 0.9, (60, 2)), src[:10]])
+    tg = torch.from_numpy(tg_np).to(DEV)
+    d1 = 2e-3
+    plan = vp.Plan(nodes, wts, tg, 1e-13, parts=vp.PART_HISTORY, delta1_override=d1)
+    V = plan.eval(fv).cpu().numpy()
+    p = oracle.dft_params(src, tg_np, d1, 32 * d1, 1e-14)
+    ref = oracle.smooth_dft(src, c, tg_np, d1, 32 * d1, **p)
+    ref2 = oracle.smooth_direct(src, c, tg_np, d1)
+    assert rel_l2(V, ref) < 1e-12
+    assert rel_l2(V, ref2) < 1e-12
+
+
+# ------------------------------------------------------------------------------------ full V
+@pytest.mark.parametrize("f", ["const", "gauss"])
+def test_config1_full_parity(f):
+    w = configs.config1(f=f)
+    plan, fd = make_plan(w)
+    V = plan.eval(fd).cpu().numpy()
+    ref = oracle.workload_potential(w)            # all 24k targets
+    e = rel_l2(V, ref)
+    print("config1", f, "rel l2 vs oracle", e, plan.info())
+    assert e <= 10 * w.tol
+    if f == "const":
+        ex = (1 - (w.targets ** 2).sum(1)) / 4
+        assert rel_l2(V, ex) <= 10 * w.tol
+
+
+def test_config2_full_size_sampled():
+    w = configs.config2()
+    plan, fd = make_plan(w)
+    V = plan.eval(fd).cpu().numpy()
+    idx = configs.sample_targets(w.T, 192, seed=22)
+    ref = oracle.workload_potential(w, idx)
+    e = rel_l2(V[idx], ref)
+    print("config2 rel l2 vs oracle", e, plan.info())
+    assert e <= 10 * w.tol
+
+
+def test_determinism_and_host_path():
+    w = configs.config2(n=60)
+    plan, fd = make_plan(w)
+    a = plan.eval(fd).cpu().numpy()
+    b = plan.eval(fd).cpu().numpy()
+    assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(a))        # atomics order only
+    h = plan.eval_host(w.f)
+    assert np.max(np.abs(h - a)) <= 1e-13 * np.max(np.abs(a))
+
+
+def test_nonfinite_and_degenerate_inputs():
+    w = configs.config2(n=20)
+    nodes, wts, tg, f = to_dev(w)
+    bad = wts.clone()
+    bad[3, 2] = float("nan")
+    with pytest.raises(vp.VpError) as ei:
+        vp.Plan(nodes, bad, tg, 1e-9)
+    assert ei.value.status == vp.VP_ERR_NONFINITE
+    plan = vp.Plan(nodes, wts, tg, 1e-9, boundary=w.boundary, targets_are_nodes=True)
+    fb = f.clone()
+    fb[0, 0] = float("inf")
+    assert not plan.check_finite(fb)
+    assert plan.check_finite(f)
+    # zero-weight (degenerate) triangles are accepted and contribute nothing
+    w0 = wts.clone()
+    w0[:5] = 0.0
+    plan0 = vp.Plan(nodes, w0, tg, 1e-9, boundary=w.boundary, targets_are_nodes=True)
+    V = plan0.eval(f)
+    assert torch.isfinite(V).all()
+
+
+def test_off_node_targets():
+    """Targets that are not quadrature nodes (config 5 style): jets from the kNN fit including f itself."""
+    w = configs.config2(n=100)
+    rng = np.random.default_rng(5)
+    tg_np = rng.uniform(0, 1, (3000, 2))
+    nodes, wts, _, f = to_dev(w)
+    plan = vp.Plan(nodes, wts, torch.from_numpy(tg_np).to(DEV), w.tol, boundary=w.boundary)
+    V = plan.eval(f).cpu().numpy()
+    idx = np.arange(0, 3000, 15)
+    ref = oracle.volume_potential(w.tri, w.curved, w.circle, w.field, tg_np[idx])
+    # n = 100 resolves the narrowest Gaussian (width >= 0.02) only to ~1e-6 by the 12-point rule
+    e = rel_l2(V[idx], ref)
+    print("off-node rel l2", e)
+    assert e < 1e-5
