@@ -1,0 +1,268 @@
+#!/usr/bin/env python
+"""Benchmark: volume-potential evaluations per second (src + tgt points / s) on B200.
+
+One "step" = one vp_eval over the whole workload: spread (NH+FH) -> cuFFT D2Z x2 -> multiply x2 ->
+cuFFT Z2D x2 -> interpolation + local part (all of SURVEY §8(a) rows a4-a11; plan-time rows a1-a3
+are not timed).  Inputs are resident in HBM when the timed region starts; L2 is flushed (256 MiB
+write) between timed steps, outside the per-step CUDA events.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl ours|reference]
+
+N > 1 (torchrun): every rank evaluates its own replica of the workload (the north star fixes one
+GPU per problem), value = total points of all ranks / max-over-ranks time.
+--impl reference times the CPU oracle (the method's definition, oracle/) on the host cores.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "volume-potential evals/sec (src+tgt pts/s) at tol 1e-9; % of B200 HBM roofline"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def make_workload(name):
+    from workloads import configs
+    if name == "c1":
+        return configs.config1(f="gauss")
+    if name == "c2":
+        return configs.config2()
+    if name == "c4":
+        return configs.config4()
+    if name.startswith("c2n"):
+        return configs.config2(n=int(name[3:]))
+    raise SystemExit(f"unknown config {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING recipe)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, n in enumerate(names):
+                if len(r) > 4 + k and r[4 + k].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def oracle_rate(w, n_targets, seed=99):
+    """Time the CPU oracle (as it stands) on a bounded target sample; extrapolate to all targets."""
+    import oracle
+    from workloads import configs
+    idx = configs.sample_targets(w.T, n_targets, seed=seed)
+    t0 = time.perf_counter()
+    oracle.workload_potential(w, idx)
+    dt = time.perf_counter() - t0
+    t_full = dt * w.T / len(idx)
+    return {"value": (w.N + w.T) / t_full, "unit": "pts/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{len(idx)} of {w.T} targets (seeded uniform) against all {w.M} triangles, "
+                      f"{dt:.2f} s measured, extrapolated linearly in T", "seconds": dt}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    w = make_workload(args.config)
+    per_step = args.ref_targets
+    for _ in range(args.warmup):
+        oracle_rate(w, per_step)
+    times = []
+    last = None
+    for s in range(args.steps):
+        last = oracle_rate(w, per_step, seed=1000 + s)
+        times.append(last["seconds"] * w.T / per_step)
+    t_full = float(np.mean(times))
+    val = (w.N + w.T) / t_full
+    cpu = dict(last)
+    cpu.pop("seconds")
+    cpu["value"] = val
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "pts/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "M": w.M, "N_src": w.N, "N_tgt": w.T, "tol": w.tol,
+                       "parallelism": "cpu-oracle"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": val, "unit": "pts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("VP_BENCH_CONFIG", "c2"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-targets", type=int, default=32)
+    ap.add_argument("--cpu-targets", type=int, default=96)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2409_11998_b200 as vp
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = make_workload(args.config)
+    nodes = torch.from_numpy(np.ascontiguousarray(w.nodes)).to(dev)
+    wts = torch.from_numpy(w.weights).to(dev)
+    tg = torch.from_numpy(np.ascontiguousarray(w.targets)).to(dev)
+    f = torch.from_numpy(w.f).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    plan = vp.Plan(nodes, wts, tg, w.tol, boundary=w.boundary, targets_are_nodes=w.targets_are_nodes, stream=stream)
+    info = plan.info()
+    plan.set_profiling(True)
+    out = torch.empty(w.T, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    for _ in range(args.warmup):
+        plan.eval(f, out)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    phases = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for s in range(args.steps):
+            flush.zero_()                       # L2 flush outside the timed events
+            evs[s][0].record(stream)
+            plan.eval(f, out)
+            evs[s][1].record(stream)
+            phases.append(plan.phase_times())   # syncs on this step's last event
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = float(np.mean(step_ms))
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    pts = (w.N + w.T)
+    value = world * pts / (ms_max * 1e-3)
+    kern, ffts = plan.launch_count()
+
+    # ---- roofline of the dominant kernel (algorithmic bytes)
+    ph = {k: float(np.mean([p[k] for p in phases])) for k in phases[0]}
+    grid_cells = info["nf_nh"] ** 2 + info["nf_fh"] ** 2
+    K = info["deriv_k"]
+    bytes_spread = 32.0 * w.N + 8.0 * grid_cells
+    bytes_interp = 24.0 * w.T + 8.0 * grid_cells + (12.0 * K + 8.0) * w.T
+    dom = "spread" if ph["spread"] >= ph["interp_local"] else "interp_local"
+    dom_bytes = bytes_spread if dom == "spread" else bytes_interp
+    peaks, peak_src = load_peaks()
+    achieved = dom_bytes / (ph[dom] * 1e-3) / 1e9
+    roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes": dom_bytes, "kernel_ms": ph[dom]}
+
+    # ---- end-to-end through the public API with host buffers (pinned)
+    f_pin = torch.from_numpy(w.f).pin_memory()
+    out_pin = torch.empty(w.T, dtype=torch.float64).pin_memory()
+    plan.set_profiling(False)
+    plan.eval_host(f_pin.numpy(), out_pin.numpy())
+    e2e_ms = []
+    for s in range(max(3, args.steps // 2)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan.eval_host(f_pin.numpy(), out_pin.numpy())
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e = {"value": world * pts / (float(e2e_t.item()) * 1e-3), "unit": "pts/s", "h2d_bytes_per_step": 8 * w.N,
+           "d2h_bytes_per_step": 8 * w.T, "ms_per_step": float(e2e_t.item())}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = oracle_rate(w, args.cpu_targets)
+            cpu.pop("seconds")
+        line = {"metric": METRIC, "value": value, "unit": "pts/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": w.name, "M": w.M, "N_src": w.N, "N_tgt": w.T, "tol": w.tol,
+                           "parallelism": f"replicas x{world}" if world > 1 else "single-gpu",
+                           "l2": "flushed between steps (256 MiB write outside the step events)",
+                           "nf_nh": info["nf_nh"], "nf_fh": info["nf_fh"], "w_es": info["w_es"],
+                           "deriv": f"knn deg {info['deriv_degree']} K {K}", "plan_ms": info["plan_ms"]},
+                "phase_ms": ph, "wall_ms_per_step": t_wall * 1e3 / args.steps,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clk.summary(), "gpu_launches": kern * args.steps,
+                "cufft_execs": ffts * args.steps}
+        print(json.dumps(line))
+    plan.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -67,7 +67,7 @@ typedef struct {
   double eps_nufft;          /* NUFFT / truncation tolerance; 0 -> tol */
   int32_t series_order;      /* interior V_L terms n_L in sum_n delta^n Lap^{n-1} f / n!; 0 -> 3 */
   int32_t deriv_mode;        /* VP_DERIV_* */
-  int32_t deriv_degree;      /* least-squares polynomial degree for KNN jets; 0 -> 6 (4 if N > 4e6) */
+  int32_t deriv_degree;      /* least-squares polynomial degree for KNN jets; 0 -> 6 (4 if N > 1e6) */
   int32_t deriv_k;           /* neighbours for KNN jets; 0 -> 2 * #monomials */
   int32_t parts;             /* VP_PART_*; 0 -> ALL */
   int32_t targets_are_nodes; /* 1: targets[t] == tri_nodes[t] (T == M p); enables the node fast path */
@@ -115,7 +115,8 @@ const char *vp_strerror(vp_status s);
 vp_status vp_get_info(vp_handle plan, vp_info *info);
 
 /* Per-phase device times (ms) of the last vp_eval when profiling is on (vp_set_profiling).
- * names: "zero", "spread", "fft_fwd", "multiply", "fft_inv", "interp_local"; n_out <= 16. */
+ * names: "zero", "spread", "restrict", "fft_fwd", "multiply", "fft_inv", "prolong", "interp_local";
+ * n_out <= 16. */
 vp_status vp_set_profiling(vp_handle plan, int32_t on);
 vp_status vp_get_phase_times(vp_handle plan, double *ms, int32_t *n_out, const char **names);
 

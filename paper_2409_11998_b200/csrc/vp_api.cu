@@ -181,20 +181,130 @@ static void setup_grid(vp_plan_s *P, VpGrid &G, int kind, double L, double kmax)
   G.oy = P->cy - 0.5 * L;
   G.row = 2 * (G.nf / 2 + 1);
   if ((double)G.nf * (double)G.row * 8.0 > 120e9) throw VpError{VP_ERR_OOM};
-  // ES deconvolution: Phi(k) = 2 alpha int_0^1 psi(s) cos(k alpha s) ds, alpha = w h / 2
-  int64_t nh = G.nmode / 2;
-  std::vector<double> dec(nh + 1), gx, gw;
-  gauss_legendre01(2 * P->w + 40, gx, gw);
-  double alpha = P->w * G.h / 2.0;
-  for (int64_t m = 0; m <= nh; m++) {
-    double k = 2.0 * VP_PI * m / L, s = 0.0;
-    for (size_t q = 0; q < gx.size(); q++) s += gw[q] * vp_es(gx[q], P->beta) * cos(k * alpha * gx[q]);
-    double Phi = 2.0 * alpha * s;
-    dec[m] = 1.0 / (Phi * Phi);
-  }
-  G.deconv = vp_alloc<double>(P, nh + 1);
-  VP_CUDA(cudaMemcpy(G.deconv, dec.data(), sizeof(double) * (nh + 1), cudaMemcpyHostToDevice));
   G.data = vp_alloc<double>(P, (size_t)G.nf * G.row);
+}
+
+// 1D transform of the ES kernel at spacing h: Phi(k) = 2 alpha int_0^1 psi(s) cos(k alpha s) ds, alpha = w h/2
+static double es_transform(const vp_plan_s *P, double h, double k, const std::vector<double> &gx,
+                           const std::vector<double> &gw) {
+  double alpha = P->w * h / 2.0, s = 0.0;
+  for (size_t q = 0; q < gx.size(); q++) s += gw[q] * vp_es(gx[q], P->beta) * cos(k * alpha * gx[q]);
+  return 2.0 * alpha * s;
+}
+
+// deconvolution tables: NH kernel psi_1 (one stage); FH kernel psi_1 * psi_2 (NH spread, then restriction)
+static void setup_deconv(vp_plan_s *P) {
+  std::vector<double> gx, gw;
+  gauss_legendre01(2 * P->w + 60, gx, gw);
+  for (VpGrid *G : {&P->nh, &P->fh}) {
+    int64_t nh = G->nmode / 2;
+    std::vector<double> dec(nh + 1);
+    for (int64_t m = 0; m <= nh; m++) {
+      double k = 2.0 * VP_PI * m / G->L;
+      double Phi = es_transform(P, P->nh.h, k, gx, gw);
+      if (G->kind == 1) Phi *= es_transform(P, P->fh.h, k, gx, gw);
+      dec[m] = 1.0 / (Phi * Phi);
+    }
+    G->deconv = vp_alloc<double>(P, nh + 1);
+    VP_CUDA(cudaMemcpy(G->deconv, dec.data(), sizeof(double) * (nh + 1), cudaMemcpyHostToDevice));
+  }
+  double h1 = P->nh.h, h2 = P->fh.h;
+  P->nh.mult_scale = h1 * h1 / ((double)P->nh.nf * (double)P->nh.nf);
+  P->fh.mult_scale = h2 * h2 * (h1 * h1) * (h1 * h1) / ((double)P->fh.nf * (double)P->fh.nf);
+}
+
+// Horner coefficients of the W ES taps (Chebyshev interpolation at D+1 nodes, then monomial basis in t)
+static void setup_horner(vp_plan_s *P) {
+  const int W = P->w, D = VP_HORNER_DEG(W);
+  memset(&P->horner, 0, sizeof(P->horner));
+  double maxerr = 0.0;
+  for (int k = 0; k < W; k++) {
+    const int n = D + 1;
+    std::vector<double> ch(n, 0.0), fv(n);
+    for (int i = 0; i < n; i++) {
+      double t = cos(VP_PI * (i + 0.5) / n);
+      fv[i] = vp_es((k + 0.5 * (t + 1.0) - 0.5 * W) * 2.0 / W, P->beta);
+    }
+    for (int j = 0; j < n; j++) {
+      double s = 0.0;
+      for (int i = 0; i < n; i++) s += fv[i] * cos(VP_PI * j * (i + 0.5) / n);
+      ch[j] = s * (j == 0 ? 1.0 : 2.0) / n;
+    }
+    // Chebyshev -> monomial: T_0 = 1, T_1 = t, T_{j+1} = 2 t T_j - T_{j-1}
+    std::vector<double> Tm(n, 0.0), Tp(n, 0.0), Tc(n, 0.0), mono(n, 0.0);
+    Tm[0] = 1.0;
+    Tc[1 % n] = (n > 1) ? 1.0 : 0.0;
+    for (int j = 0; j < n; j++) {
+      const std::vector<double> &T = (j == 0) ? Tm : Tc;
+      for (int q = 0; q < n; q++) mono[q] += ch[j] * T[q];
+      if (j >= 1) {
+        for (int q = 0; q < n; q++) Tp[q] = -Tm[q] + (q >= 1 ? 2.0 * Tc[q - 1] : 0.0);
+        Tm = Tc;
+        Tc = Tp;
+      }
+    }
+    for (int q = 0; q < n; q++) P->horner.c[k][q] = mono[q];
+    for (int i = 0; i <= 200; i++) {
+      double t = -1.0 + i / 100.0, acc = mono[D];
+      for (int q = D - 1; q >= 0; q--) acc = acc * t + mono[q];
+      double ex = vp_es((k + 0.5 * (t + 1.0) - 0.5 * W) * 2.0 / W, P->beta);
+      maxerr = std::max(maxerr, fabs(acc - ex));
+    }
+  }
+  P->horner_err = maxerr;
+  if (!(maxerr < 1e-6)) {
+    vp_set_last_error("Horner fit of the ES kernel failed");
+    throw VpError{VP_ERR_CUDA};
+  }
+}
+
+// FH <- NH restriction tables (DESIGN.md §NUFFT two-stage FH).  The same host function evaluates
+// every weight psi_FH((X1(i) - X2(i')) / (w h2 / 2)) so the prolongation is the exact transpose.
+static double rweight(const vp_plan_s *P, int64_t i, int64_t ip) {
+  double d = (P->nh.ox - P->fh.ox) + i * P->nh.h - ip * P->fh.h;
+  return vp_es(d / (0.5 * P->w * P->fh.h), P->beta);
+}
+static void setup_restriction(vp_plan_s *P) {
+  const double h1 = P->nh.h, h2 = P->fh.h, half = 0.5 * P->w * h2, off = P->nh.ox - P->fh.ox;
+  const int64_t n1 = P->nh.nf, n2 = P->fh.nf;
+  P->r_ntap = (int)floor(2.0 * half / h1) + 2;
+  P->t_ntap = P->w + 1;
+  std::vector<int32_t> rlo(n2), tlo(n1);
+  std::vector<double> rw((size_t)n2 * P->r_ntap, 0.0), tw((size_t)n1 * P->t_ntap, 0.0);
+  int64_t elo = -1, ehi = -1;
+  for (int64_t ip = 0; ip < n2; ip++) {
+    // NH indices i with |off + i h1 - ip h2| < half
+    int64_t lo = (int64_t)ceil((ip * h2 - half - off) / h1);
+    rlo[ip] = (int32_t)lo;
+    bool any = false;
+    for (int t = 0; t < P->r_ntap; t++) {
+      int64_t i = lo + t;
+      double wv = rweight(P, i, ip);
+      rw[(size_t)ip * P->r_ntap + t] = wv;
+      if (wv != 0.0 && i >= 0 && i < n1) any = true;
+    }
+    if (any) {
+      if (elo < 0) elo = ip;
+      ehi = ip;
+    }
+  }
+  for (int64_t i = 0; i < n1; i++) {
+    int64_t lo = (int64_t)ceil((off + i * h1 - half) / h2);
+    tlo[i] = (int32_t)lo;
+    for (int t = 0; t < P->t_ntap; t++) tw[(size_t)i * P->t_ntap + t] = rweight(P, i, lo + t);
+  }
+  if (elo < 0) throw VpError{VP_ERR_GEOMETRY};
+  P->e_lo = elo;
+  P->e_n = ehi - elo + 1;
+  P->r_lo = vp_alloc<int32_t>(P, n2);
+  P->t_lo = vp_alloc<int32_t>(P, n1);
+  P->r_w = vp_alloc<double>(P, rw.size());
+  P->t_w = vp_alloc<double>(P, tw.size());
+  VP_CUDA(cudaMemcpy(P->r_lo, rlo.data(), 4 * n2, cudaMemcpyHostToDevice));
+  VP_CUDA(cudaMemcpy(P->t_lo, tlo.data(), 4 * n1, cudaMemcpyHostToDevice));
+  VP_CUDA(cudaMemcpy(P->r_w, rw.data(), 8 * rw.size(), cudaMemcpyHostToDevice));
+  VP_CUDA(cudaMemcpy(P->t_w, tw.data(), 8 * tw.size(), cudaMemcpyHostToDevice));
+  P->scratch = vp_alloc<double>(P, (size_t)n1 * P->e_n);
 }
 
 static void make_fft_plans(vp_plan_s *P) {
@@ -228,37 +338,9 @@ static void make_fft_plans(vp_plan_s *P) {
 static void build_tiles(vp_plan_s *P, const double *nodes_dev, const double *weights_dev) {
   VpTiles &Tl = P->tiles;
   Tl.TS = 32;
-  double cell = Tl.TS * P->nh.h;
   Tl.ntx = (P->nh.nf + Tl.TS - 1) / Tl.TS;
   Tl.nty = Tl.ntx;
-  P->sx = vp_alloc<double>(P, P->N);
-  P->sy = vp_alloc<double>(P, P->N);
-  P->sperm = vp_alloc<int32_t>(P, P->N);
-  int64_t *bs = nullptr;
-  int64_t nb = vp_sort_points(P, nodes_dev, P->N, P->nh.ox, P->nh.oy, cell, Tl.ntx, Tl.nty, P->sx, P->sy, nullptr,
-                              P->sperm, &bs);
-  // sorted weights
-  P->sw = vp_alloc<double>(P, P->N);
-  {
-    // gather weights by the permutation on the host-free path: simple kernel
-    extern void vp_gather_f64(const double *src, const int32_t *perm, int64_t n, double *dst, cudaStream_t s);
-    vp_gather_f64(weights_dev, P->sperm, P->N, P->sw, P->stream);
-  }
-  std::vector<int64_t> h(nb + 1);
-  VP_CUDA(cudaMemcpyAsync(h.data(), bs, sizeof(int64_t) * (nb + 1), cudaMemcpyDeviceToHost, P->stream));
-  VP_CUDA(cudaStreamSynchronize(P->stream));
-  const int64_t MAXSUB = 1024;
-  std::vector<int4> subs;
-  for (int64_t b = 0; b < nb; b++) {
-    int64_t s0 = h[b], s1 = h[b + 1];
-    for (int64_t s = s0; s < s1; s += MAXSUB)
-      subs.push_back(make_int4((int)(b % Tl.ntx), (int)(b / Tl.ntx), (int)s, (int)std::min(MAXSUB, s1 - s)));
-  }
-  Tl.nsub = (int64_t)subs.size();
-  Tl.sub = vp_alloc<int4>(P, subs.size());
-  if (!subs.empty())
-    VP_CUDA(cudaMemcpy(Tl.sub, subs.data(), sizeof(int4) * subs.size(), cudaMemcpyHostToDevice));
-  P->fh_tile_w = (int)ceil(Tl.TS * P->nh.h / P->fh.h) + P->w + 4;
+  vp_build_spread_order(P, nodes_dev, weights_dev);
 }
 
 __global__ void k_gather_f64(const double *__restrict__ src, const int32_t *__restrict__ perm, int64_t n,
@@ -282,7 +364,7 @@ static void free_plan(vp_plan_s *P) {
   }
   for (void *p : P->allocs) cudaFree(p);
   if (P->ev_init)
-    for (int i = 0; i < 8; i++) cudaEventDestroy(P->ev[i]);
+    for (int i = 0; i < 9; i++) cudaEventDestroy(P->ev[i]);
   delete P;
 }
 
@@ -358,6 +440,9 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     P->nh.delta_a = P->delta1; P->nh.delta_b = P->delta2;
     setup_grid(P, P->fh, 1, L_fh, P->kmax_fh);
     P->fh.delta_a = P->delta2; P->fh.delta_b = P->R;
+    setup_horner(P);
+    setup_deconv(P);
+    setup_restriction(P);
     // ---- sources and targets sorted by NH tile
     build_tiles(P, tri_nodes, weights);
     P->tx = vp_alloc<double>(P, T);
@@ -369,7 +454,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     int parts = o.parts ? o.parts : VP_PART_ALL;
     P->dmode = o.deriv_mode ? o.deriv_mode : VP_DERIV_KNN;
     if (P->dmode != VP_DERIV_KNN) throw VpError{VP_ERR_UNSUPPORTED};
-    P->deg = o.deriv_degree > 0 ? o.deriv_degree : (N > 4000000 ? 4 : 6);
+    P->deg = o.deriv_degree > 0 ? o.deriv_degree : (N > 1000000 ? 4 : 6);
     if (P->deg > VP_MAXDEG) throw VpError{VP_ERR_ARG};
     int nc = vp_ncoef(P->deg);
     P->K = o.deriv_k > 0 ? o.deriv_k : 2 * nc;
@@ -414,7 +499,7 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
     P->n_ffts = 0;
     int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
     if (P->profiling && !P->ev_init) {
-      for (int i = 0; i < 8; i++) VP_CUDA(cudaEventCreate(&P->ev[i]));
+      for (int i = 0; i < 9; i++) VP_CUDA(cudaEventCreate(&P->ev[i]));
       P->ev_init = true;
     }
     record(P, 0);
@@ -424,22 +509,26 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
       record(P, 1);
       vp_launch_spread(P, f);
       record(P, 2);
+      vp_launch_restrict(P);
+      record(P, 3);
       VP_CUFFT(cufftExecD2Z(P->nh.fwd, P->nh.data, (cufftDoubleComplex *)P->nh.data));
       VP_CUFFT(cufftExecD2Z(P->fh.fwd, P->fh.data, (cufftDoubleComplex *)P->fh.data));
-      record(P, 3);
+      record(P, 4);
       vp_launch_multiply(P, P->nh);
       vp_launch_multiply(P, P->fh);
-      record(P, 4);
+      record(P, 5);
       VP_CUFFT(cufftExecZ2D(P->nh.inv, (cufftDoubleComplex *)P->nh.data, P->nh.data));
       VP_CUFFT(cufftExecZ2D(P->fh.inv, (cufftDoubleComplex *)P->fh.data, P->fh.data));
+      record(P, 6);
+      vp_launch_prolong(P);
       P->n_ffts = 4;
-      record(P, 5);
+      record(P, 7);
     } else {
-      for (int i = 1; i <= 5; i++) record(P, i);
+      for (int i = 1; i <= 7; i++) record(P, i);
     }
     vp_launch_interp_local(P, f, out);
-    record(P, 6);
-    P->n_phase = 6;
+    record(P, 8);
+    P->n_phase = 8;
   } catch (VpError &e) {
     return e.s;
   }
@@ -507,19 +596,19 @@ extern "C" vp_status vp_set_profiling(vp_handle P, int32_t on) {
   return VP_OK;
 }
 
-static const char *g_phase_names[6] = {"zero", "spread", "fft_fwd", "multiply", "fft_inv", "interp_local"};
+static const char *g_phase_names[8] = {"zero", "spread", "restrict", "fft_fwd", "multiply", "fft_inv", "prolong", "interp_local"};
 
 extern "C" vp_status vp_get_phase_times(vp_handle P, double *ms, int32_t *n_out, const char **names) {
   if (!P || !ms || !n_out) return VP_ERR_ARG;
   if (!P->profiling || !P->ev_init) return VP_ERR_ARG;
-  if (cudaEventSynchronize(P->ev[6]) != cudaSuccess) return VP_ERR_CUDA;
-  for (int i = 0; i < 6; i++) {
+  if (cudaEventSynchronize(P->ev[8]) != cudaSuccess) return VP_ERR_CUDA;
+  for (int i = 0; i < 8; i++) {
     float t = 0.f;
     cudaEventElapsedTime(&t, P->ev[i], P->ev[i + 1]);
     ms[i] = t;
     if (names) names[i] = g_phase_names[i];
   }
-  *n_out = 6;
+  *n_out = 8;
   return VP_OK;
 }
 

@@ -38,6 +38,14 @@ struct VpError {
 void vp_set_last_error(const std::string &s);
 
 // ---------------------------------------------------------------------------------------------
+// ES kernel taps as Horner polynomials: psi(z_k(t)), z_k = (k + (t+1)/2 - W/2) 2/W, t in [-1, 1]
+#define VP_HORNER_MAXW 16
+#define VP_HORNER_DEG(W) ((W) <= 8 ? (W) : ((W)-1))
+struct VpHorner {
+  double c[VP_HORNER_MAXW][VP_HORNER_MAXW];  // c[k][j]: coefficient of t^j for tap k
+};
+
+// ---------------------------------------------------------------------------------------------
 // One uniform periodic fine grid of the NUFFT (§3).
 // Point x lies at fractional grid coordinate g = (x - o)/h; grid node i sits at o + i h.
 struct VpGrid {
@@ -48,7 +56,8 @@ struct VpGrid {
   double delta_a = 0, delta_b = 0;  // NH: (delta1, delta2); FH: (delta2, R)
   int kind = 0;                     // 0 = near history, 1 = far history
   double *data = nullptr;           // nf * row doubles
-  double *deconv = nullptr;         // [nmode/2+1]: 1 / Phi(k_m)^2 (1D ES transform, squared inverse)
+  double *deconv = nullptr;         // [nmode/2+1]: 1 / Phi(k_m)^2 (1D kernel transform, squared inverse)
+  double mult_scale = 0;            // h^2 / nf^2 (NH);  h2^2 h1^4 / nf2^2 (FH, two-stage kernel)
   cufftHandle fwd = 0, inv = 0;
   bool has_plans = false;
 };
@@ -72,11 +81,20 @@ struct vp_plan_s {
   int w = 0;
   double beta = 0;
   VpGrid nh, fh;
-  // sources, sorted by NH tile
+  VpHorner horner{};
+  double horner_err = 0;
+  // sources, sorted by (NH tile, row rank, row) into batches of <= 32 points with distinct rows
   double *sx = nullptr, *sy = nullptr, *sw = nullptr;  // coords, weights
   int32_t *sperm = nullptr;                            // sorted -> user node index
-  VpTiles tiles;
-  int fh_tile_w = 0;  // FH smem tile width (cells) for one NH tile
+  int32_t *bstart = nullptr;                           // batch starts (n_batches + 1)
+  int64_t n_batches = 0;
+  VpTiles tiles;                                       // tiles.sub: warp work items (tx, ty, b0, b1)
+  // FH <- NH restriction tables
+  int32_t *r_lo = nullptr, *t_lo = nullptr;
+  double *r_w = nullptr, *t_w = nullptr;
+  int r_ntap = 0, t_ntap = 0;
+  int64_t e_lo = 0, e_n = 0;
+  double *scratch = nullptr;                           // n1 x e_n
   // targets, sorted by NH tile
   double *tx = nullptr, *ty = nullptr;
   int64_t *tperm = nullptr;  // sorted -> user target index
@@ -91,9 +109,9 @@ struct vp_plan_s {
   double *f_dev = nullptr, *out_dev = nullptr;
   // profiling
   bool profiling = false;
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[12] = {};
   bool ev_init = false;
-  double phase_ms[8] = {};
+  double phase_ms[12] = {};
   int n_phase = 0;
   double plan_ms = 0;
   int64_t device_bytes = 0;
@@ -115,6 +133,9 @@ T *vp_alloc(vp_plan_s *P, size_t n) {
 // ---------------------------------------------------------------------------------------------
 // launch helpers (defined in the .cu files)
 void vp_launch_spread(vp_plan_s *P, const double *f);
+void vp_launch_restrict(vp_plan_s *P);
+void vp_launch_prolong(vp_plan_s *P);
+void vp_build_spread_order(vp_plan_s *P, const double *nodes, const double *weights);
 void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out);
 void vp_build_local(vp_plan_s *P, const double *nodes_dev);

@@ -1,19 +1,25 @@
-// vp_nufft.cu -- sm_100a kernels of the history part (§3, Steps 2-4, lines 826-898):
-//   spread  : type-1 spreading of c_j = f_j w_j onto the near-history (NH) and far-history (FH)
-//             fine grids with the ES kernel, one CTA per (NH tile, point chunk), shared-memory tile
-//             accumulation, one global fp64 RED per touched tile cell;
-//   multiply: Fourier-space multiplication by the split kernel's transform (NH: (vnearkspace),
-//             FH: e^{-k^2 delta2} W_R(k), (vfarkspace)/(Wdef)), deconvolution by the ES kernel's
-//             transform (twice: spread and interpolation), trapezoid weight (Dk/2pi)^2 and cuFFT's
-//             1/nf^2 normalisation, with |m_i| <= nmode/2 truncation (k_max, (fouriernhtrunc));
-//   interp  : type-2 interpolation of both grids at the targets, fused with the local part
-//             V_L = alpha f_t + sum_k omega_k f[idx_k] and the scatter to the user's target order.
+// vp_nufft.cu -- sm_100a kernels of the history part (§3, Steps 2-4, lines 826-898).
+//
+// Both history parts share ONE set of per-point kernels on the near-history (NH) fine grid:
+//   spread_nh : type-1 spreading of c_j = f_j w_j onto the NH grid.  One warp per CTA owns a private
+//               (TS+W+3)^2 fp64 shared-memory tile; points were sorted at plan time into "row-rank"
+//               batches (<= 32 points of one tile with pairwise distinct footprint rows), so inside a
+//               footprint row step every lane writes its own grid row: plain LDS/DFMA/STS, no atomics,
+//               one __syncwarp per row.  One global fp64 RED per tile cell at the end.
+//   restrict  : the far-history (FH) grid is obtained from the NH grid by a separable convolution with
+//               the FH-scale ES kernel (g2 = R g1); the FH transform then carries the product kernel
+//               Phi_NH Phi_FH in its deconvolution (DESIGN.md §NUFFT "two-stage FH").
+//   multiply  : Fourier multiplication by the split kernels' transforms (NH: (vnearkspace); FH:
+//               e^{-k^2 delta2} W_R(k), (vfarkspace)/(Wdef)), ES deconvolution, trapezoid weight
+//               (Dk/2pi)^2, cuFFT 1/nf^2, truncation |m_i| <= nmode/2.
+//   prolong   : q1 += R^T q2 (FH potential onto the NH grid).
+//   interp    : type-2 interpolation of the NH grid at the targets fused with the local part
+//               V_L = alpha f_t + sum_k omega_k f[idx_k] and the scatter to the user's order.
+// ES kernel values come from per-tap Horner polynomials (vp_common.cuh VpHorner), degree ~ W-1.
 #include <cub/cub.cuh>
 
 #include "vp_common.cuh"
 #include "vp_math.cuh"
-
-#define VP_MAXW 16
 
 struct GridArgs {
   double *data;
@@ -25,13 +31,20 @@ static GridArgs grid_args(const VpGrid &G) { return GridArgs{G.data, G.nf, G.row
 // fractional grid coordinate of x (identical expression in binning, spreading and interpolation)
 __device__ __forceinline__ double gcoord(double x, double o, double h) { return (x - o) / h; }
 
-// ES weights for the W grid points i0 .. i0+W-1 around fractional coordinate g
-template <int W>
-__device__ __forceinline__ int es_weights(double g, double beta, double *wts) {
-  int i0 = (int)ceil(g - 0.5 * W);
-  const double s = 2.0 / W;
+// ES weights for grid points i0 .. i0+W-1 around fractional coordinate g, by Horner polynomials in
+// t = 2u - 1, u = i0 - (g - W/2) in [0, 1)
+template <int W, int D>
+__device__ __forceinline__ int es_horner(double g, const VpHorner &hp, double *wts) {
+  double s = g - 0.5 * W;
+  int i0 = (int)ceil(s);
+  double t = 2.0 * (i0 - s) - 1.0;
 #pragma unroll
-  for (int k = 0; k < W; k++) wts[k] = vp_es((i0 + k - g) * s, beta);
+  for (int k = 0; k < W; k++) {
+    double acc = hp.c[k][D];
+#pragma unroll
+    for (int j = D - 1; j >= 0; j--) acc = fma(acc, t, hp.c[k][j]);
+    wts[k] = acc;
+  }
   return i0;
 }
 
@@ -41,83 +54,115 @@ __device__ __forceinline__ int64_t wrapi(int64_t i, int64_t n) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// spreading: one CTA per sub-problem (tile_x, tile_y, start, count)
-template <int W>
-__global__ void __launch_bounds__(256) k_spread(const int4 *__restrict__ sub, const double *__restrict__ sx,
-                                                const double *__restrict__ sy, const double *__restrict__ sw,
-                                                const int32_t *__restrict__ sperm, const double *__restrict__ f,
-                                                GridArgs g1, GridArgs g2, int TS, int fhw, double beta) {
-  extern __shared__ double smem[];
-  const int nw = TS + W + 1;            // NH smem tile width
-  double *s1 = smem;                    // nw * nw
-  double *s2 = smem + nw * nw;          // fhw * fhw
-  const int4 sp = sub[blockIdx.x];
-  const int64_t t1x = (int64_t)sp.x * TS - (W / 2 + 1), t1y = (int64_t)sp.y * TS - (W / 2 + 1);
-  // FH tile origin covering this NH tile's spatial extent
-  const double xlo = g1.ox + (double)sp.x * TS * g1.h, ylo = g1.oy + (double)sp.y * TS * g1.h;
-  const int64_t t2x = (int64_t)floor(gcoord(xlo, g2.ox, g2.h)) - (W / 2 + 1);
-  const int64_t t2y = (int64_t)floor(gcoord(ylo, g2.oy, g2.h)) - (W / 2 + 1);
-  for (int i = threadIdx.x; i < nw * nw + fhw * fhw; i += blockDim.x) smem[i] = 0.0;
-  __syncthreads();
-  for (int j = sp.z + threadIdx.x; j < sp.z + sp.w; j += blockDim.x) {
-    const double x = sx[j], y = sy[j];
-    const double c = f[sperm[j]] * sw[j];
-    double wx[W], wy[W];
-    {
-      int ix = es_weights<W>(gcoord(x, g1.ox, g1.h), beta, wx);
-      int iy = es_weights<W>(gcoord(y, g1.oy, g1.h), beta, wy);
-      int lx = (int)(ix - t1x), ly = (int)(iy - t1y);
-#pragma unroll
-      for (int b = 0; b < W; b++) {
-        double cy = c * wy[b];
-        double *rowp = s1 + (ly + b) * nw + lx;
-#pragma unroll
-        for (int a = 0; a < W; a++) atomicAdd(rowp + a, cy * wx[a]);
-      }
+// plan-time keys for the row-rank ordering
+__global__ void k_spread_keys(const double *__restrict__ xy, int64_t n, GridArgs g, int TS, int W, int64_t ntx,
+                              int64_t nty, uint64_t *__restrict__ keys, int32_t *__restrict__ idx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double gx = gcoord(xy[2 * i], g.ox, g.h), gy = gcoord(xy[2 * i + 1], g.oy, g.h);
+  int64_t tx = (int64_t)floor(gx / TS), ty = (int64_t)floor(gy / TS);
+  tx = tx < 0 ? 0 : (tx >= ntx ? ntx - 1 : tx);
+  ty = ty < 0 ? 0 : (ty >= nty ? nty - 1 : ty);
+  int64_t j0 = (int64_t)ceil(gy - 0.5 * W);
+  int64_t lrow = j0 - (ty * TS - (W / 2 + 1));
+  lrow = lrow < 0 ? 0 : (lrow > 255 ? 255 : lrow);
+  keys[i] = ((uint64_t)(ty * ntx + tx) << 32) | (uint64_t)lrow;
+  idx[i] = (int32_t)i;
+}
+
+// level (rank within equal (tile,row) runs) -> second key (tile, level, row)
+__global__ void k_rank_keys(const uint64_t *__restrict__ k1, int64_t n, uint64_t *__restrict__ k2) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t key = k1[i];
+  int64_t lo = 0, hi = i;  // run start by binary search (lower_bound)
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (k1[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  uint64_t level = (uint64_t)(i - lo);
+  uint64_t tile = key >> 32, lrow = key & 0xff;
+  k2[i] = (tile << 40) | (level << 8) | lrow;
+}
+
+// batch heads: new (tile, level) or every 32 points of one level
+__global__ void k_batch_heads(const uint64_t *__restrict__ k2, int64_t n, int32_t *__restrict__ head) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t grp = k2[i] >> 8;
+  int h = 0;
+  if (i == 0 || (k2[i - 1] >> 8) != grp) {
+    h = 1;
+  } else {
+    int64_t lo = 0, hi = i;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if ((k2[mid] >> 8) < grp) lo = mid + 1; else hi = mid;
     }
-    {
-      int ix = es_weights<W>(gcoord(x, g2.ox, g2.h), beta, wx);
-      int iy = es_weights<W>(gcoord(y, g2.oy, g2.h), beta, wy);
-      int lx = (int)(ix - t2x), ly = (int)(iy - t2y);
+    h = ((i - lo) % 32) == 0;
+  }
+  head[i] = h;
+}
+
+// ---------------------------------------------------------------------------------------------
+// NH spreading: one warp per work item (tile_x, tile_y, first batch, end batch)
+template <int W, int D>
+__global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items, const int32_t *__restrict__ bstart,
+                                                  const double *__restrict__ sx, const double *__restrict__ sy,
+                                                  const double *__restrict__ sw, const int32_t *__restrict__ sperm,
+                                                  const double *__restrict__ f, GridArgs g, int TS,
+                                                  const __grid_constant__ VpHorner hp) {
+  extern __shared__ double tile[];
+  const int nw = TS + W + 3;
+  const int lane = threadIdx.x;
+  const int4 it = items[blockIdx.x];
+  const int64_t ox = (int64_t)it.x * TS - (W / 2 + 1), oy = (int64_t)it.y * TS - (W / 2 + 1);
+  for (int i = lane; i < nw * nw; i += 32) tile[i] = 0.0;
+  __syncwarp();
+  for (int b = it.z; b < it.w; b++) {
+    const int s = bstart[b], n = bstart[b + 1] - s;
+    const bool act = lane < n;
+    double wx[W], wy[W], c = 0.0;
+    int lx = 0, ly = 0;
+    if (act) {
+      const int j = s + lane;
+      const double x = sx[j], y = sy[j];
+      c = f[sperm[j]] * sw[j];
+      lx = (int)(es_horner<W, D>(gcoord(x, g.ox, g.h), hp, wx) - ox);
+      ly = (int)(es_horner<W, D>(gcoord(y, g.oy, g.h), hp, wy) - oy);
+    }
 #pragma unroll
-      for (int b = 0; b < W; b++) {
-        double cy = c * wy[b];
-        double *rowp = s2 + (ly + b) * fhw + lx;
+    for (int r = 0; r < W; r++) {
+      if (act) {
+        double *rowp = tile + (ly + r) * nw + lx;
+        const double cr = c * wy[r];
+        double v[W];
 #pragma unroll
-        for (int a = 0; a < W; a++) atomicAdd(rowp + a, cy * wx[a]);
+        for (int a = 0; a < W; a++) v[a] = rowp[a];
+#pragma unroll
+        for (int a = 0; a < W; a++) rowp[a] = fma(cr, wx[a], v[a]);
       }
+      __syncwarp();
     }
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nw * nw; i += blockDim.x) {
-    double v = s1[i];
+  for (int i = lane; i < nw * nw; i += 32) {
+    double v = tile[i];
     if (v != 0.0) {
-      int64_t gx = wrapi(t1x + i % nw, g1.nf), gy = wrapi(t1y + i / nw, g1.nf);
-      atomicAdd(g1.data + gy * g1.row + gx, v);
-    }
-  }
-  for (int i = threadIdx.x; i < fhw * fhw; i += blockDim.x) {
-    double v = s2[i];
-    if (v != 0.0) {
-      int64_t gx = wrapi(t2x + i % fhw, g2.nf), gy = wrapi(t2y + i / fhw, g2.nf);
-      atomicAdd(g2.data + gy * g2.row + gx, v);
+      int64_t gx = wrapi(ox + i % nw, g.nf), gy = wrapi(oy + i / nw, g.nf);
+      atomicAdd(g.data + gy * g.row + gx, v);
     }
   }
 }
 
 template <int W>
 static void launch_spread_w(vp_plan_s *P, const double *f) {
-  int nw = P->tiles.TS + W + 1;
-  size_t sm = sizeof(double) * ((size_t)nw * nw + (size_t)P->fh_tile_w * P->fh_tile_w);
-  static bool attr = false;
-  if (!attr) {
-    VP_CUDA(cudaFuncSetAttribute(k_spread<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  constexpr int D = VP_HORNER_DEG(W);
+  int nw = P->tiles.TS + W + 3;
+  size_t sm = sizeof(double) * (size_t)nw * nw;
   if (P->tiles.nsub == 0) return;
-  k_spread<W><<<(unsigned)P->tiles.nsub, 256, sm, P->stream>>>(P->tiles.sub, P->sx, P->sy, P->sw, P->sperm, f,
-                                                              grid_args(P->nh), grid_args(P->fh), P->tiles.TS,
-                                                              P->fh_tile_w, P->beta);
+  k_spread_nh<W, D><<<(unsigned)P->tiles.nsub, 32, sm, P->stream>>>(P->tiles.sub, P->bstart, P->sx, P->sy, P->sw,
+                                                                    P->sperm, f, grid_args(P->nh), P->tiles.TS,
+                                                                    P->horner);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
@@ -130,6 +175,116 @@ void vp_launch_spread(vp_plan_s *P, const double *f) {
 #undef CASE
     default: throw VpError{VP_ERR_UNSUPPORTED};
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// FH restriction / prolongation (separable, gather form).  Tap table for FH index i':
+// NH indices rlo[i'] .. rlo[i'] + ntap-1, weights rw[i'][t] = psi_FH(X1(i) - X2(i')).
+// Transposed table for NH index i: FH indices tlo[i] .. tlo[i] + ntt-1, weights tw[i][t].
+struct RestrictArgs {
+  const int32_t *rlo;
+  const double *rw;
+  int ntap;
+  const int32_t *tlo;
+  const double *tw;
+  int ntt;
+  int64_t e_lo, ne;  // effective FH index range [e_lo, e_lo + ne)
+  int64_t n1, row1, n2, row2;
+};
+
+// pass A: tA[r][e] = sum_t rw[e_lo+e][t] g1[r][rlo + t]
+__global__ void k_restrict_x(const double *__restrict__ g1, double *__restrict__ tA, RestrictArgs a) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t r = blockIdx.y;
+  if (e >= a.ne) return;
+  int64_t ip = a.e_lo + e;
+  const int32_t lo = a.rlo[ip];
+  const double *w = a.rw + ip * a.ntap;
+  const double *src = g1 + r * a.row1;
+  double acc = 0.0;
+  for (int t = 0; t < a.ntap; t++) {
+    int64_t i = lo + t;
+    if (i >= 0 && i < a.n1) acc = fma(w[t], __ldg(src + i), acc);
+  }
+  tA[r * a.ne + e] = acc;
+}
+
+// pass B: g2[e_lo+ey][e_lo+ex] = sum_t rw[e_lo+ey][t] tA[rlo + t][ex]
+__global__ void k_restrict_y(const double *__restrict__ tA, double *__restrict__ g2, RestrictArgs a) {
+  int64_t ex = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t ey = blockIdx.y;
+  if (ex >= a.ne) return;
+  int64_t jp = a.e_lo + ey;
+  const int32_t lo = a.rlo[jp];
+  const double *w = a.rw + jp * a.ntap;
+  double acc = 0.0;
+  for (int t = 0; t < a.ntap; t++) {
+    int64_t r = lo + t;
+    if (r >= 0 && r < a.n1) acc = fma(w[t], __ldg(tA + r * a.ne + ex), acc);
+  }
+  g2[jp * a.row2 + a.e_lo + ex] = acc;
+}
+
+// prolongation pass B^T: t2[r][ex] = sum_t tw[r][t] q2[tlo[r] + t][e_lo + ex]
+__global__ void k_prolong_y(const double *__restrict__ q2, double *__restrict__ t2, RestrictArgs a) {
+  int64_t ex = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t r = blockIdx.y;
+  if (ex >= a.ne) return;
+  const int32_t lo = a.tlo[r];
+  const double *w = a.tw + r * a.ntt;
+  double acc = 0.0;
+  for (int t = 0; t < a.ntt; t++) {
+    int64_t jp = lo + t;
+    if (jp >= 0 && jp < a.n2) acc = fma(w[t], __ldg(q2 + jp * a.row2 + a.e_lo + ex), acc);
+  }
+  t2[r * a.ne + ex] = acc;
+}
+
+// prolongation pass A^T: q1[r][i] += sum_t tw[i][t] t2[r][tlo[i] + t - e_lo]
+__global__ void k_prolong_x(const double *__restrict__ t2, double *__restrict__ q1, RestrictArgs a) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t r = blockIdx.y;
+  if (i >= a.n1) return;
+  const int32_t lo = a.tlo[i];
+  const double *w = a.tw + i * a.ntt;
+  const double *src = t2 + r * a.ne;
+  double acc = 0.0;
+  for (int t = 0; t < a.ntt; t++) {
+    int64_t e = lo + t - a.e_lo;
+    if (e >= 0 && e < a.ne) acc = fma(w[t], __ldg(src + e), acc);
+  }
+  q1[r * a.row1 + i] += acc;
+}
+
+static RestrictArgs restrict_args(vp_plan_s *P) {
+  RestrictArgs a;
+  a.rlo = P->r_lo; a.rw = P->r_w; a.ntap = P->r_ntap;
+  a.tlo = P->t_lo; a.tw = P->t_w; a.ntt = P->t_ntap;
+  a.e_lo = P->e_lo; a.ne = P->e_n;
+  a.n1 = P->nh.nf; a.row1 = P->nh.row; a.n2 = P->fh.nf; a.row2 = P->fh.row;
+  return a;
+}
+
+void vp_launch_restrict(vp_plan_s *P) {
+  RestrictArgs a = restrict_args(P);
+  dim3 bA((unsigned)((a.ne + 127) / 128), (unsigned)a.n1);
+  k_restrict_x<<<bA, 128, 0, P->stream>>>(P->nh.data, P->scratch, a);
+  VP_CHECK_LAUNCH();
+  dim3 bB((unsigned)((a.ne + 127) / 128), (unsigned)a.ne);
+  k_restrict_y<<<bB, 128, 0, P->stream>>>(P->scratch, P->fh.data, a);
+  VP_CHECK_LAUNCH();
+  P->n_kernels += 2;
+}
+
+void vp_launch_prolong(vp_plan_s *P) {
+  RestrictArgs a = restrict_args(P);
+  dim3 bB((unsigned)((a.ne + 127) / 128), (unsigned)a.n1);
+  k_prolong_y<<<bB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a);
+  VP_CHECK_LAUNCH();
+  dim3 bA((unsigned)((a.n1 + 127) / 128), (unsigned)a.n1);
+  k_prolong_x<<<bA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a);
+  VP_CHECK_LAUNCH();
+  P->n_kernels += 2;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -163,44 +318,18 @@ void vp_launch_multiply(vp_plan_s *P, VpGrid &G) {
   int64_t total = G.nf * ncol;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   double dk = 2.0 * VP_PI / G.L;
-  // M(k) h^2 / (nf^2 Phi(k1)^2 Phi(k2)^2): deconv holds 1/Phi^2
-  double scale = G.h * G.h / ((double)G.nf * (double)G.nf);
-  k_multiply<<<blocks, 256, 0, P->stream>>>(G.data, G.nf, G.row, G.nmode / 2, G.deconv, dk, scale, G.kind,
+  k_multiply<<<blocks, 256, 0, P->stream>>>(G.data, G.nf, G.row, G.nmode / 2, G.deconv, dk, G.mult_scale, G.kind,
                                             G.delta_a, G.delta_b);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
 
 // ---------------------------------------------------------------------------------------------
-// interpolation + local part + scatter to user order
-template <int W>
-__device__ __forceinline__ double interp_one(const GridArgs &g, double x, double y, double beta) {
-  double wx[W], wy[W];
-  int ix = es_weights<W>(gcoord(x, g.ox, g.h), beta, wx);
-  int iy = es_weights<W>(gcoord(y, g.oy, g.h), beta, wy);
-  double acc = 0.0;
-  bool inside = ix >= 0 && iy >= 0 && ix + W <= g.nf && iy + W <= g.nf;
-#pragma unroll
-  for (int b = 0; b < W; b++) {
-    double racc = 0.0;
-    if (inside) {
-      const double *rp = g.data + (int64_t)(iy + b) * g.row + ix;
-#pragma unroll
-      for (int a = 0; a < W; a++) racc += wx[a] * __ldg(rp + a);
-    } else {
-      int64_t yy = wrapi(iy + b, g.nf);
-#pragma unroll
-      for (int a = 0; a < W; a++) racc += wx[a] * __ldg(g.data + yy * g.row + wrapi(ix + a, g.nf));
-    }
-    acc += wy[b] * racc;
-  }
-  return acc;
-}
-
-template <int W>
+// interpolation (NH grid, which also carries the prolongated FH field) + local part + scatter
+template <int W, int D>
 __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__ tx, const double *__restrict__ ty,
-                                                      const int64_t *__restrict__ tperm, int64_t T, GridArgs g1,
-                                                      GridArgs g2, double beta, int do_hist,
+                                                      const int64_t *__restrict__ tperm, int64_t T, GridArgs g,
+                                                      const __grid_constant__ VpHorner hp, int do_hist,
                                                       const double *__restrict__ f, const double *__restrict__ lalpha,
                                                       const int32_t *__restrict__ lnode,
                                                       const int32_t *__restrict__ lidx, const double *__restrict__ lw,
@@ -209,8 +338,24 @@ __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__
   if (t >= T) return;
   double v = 0.0;
   if (do_hist) {
-    double x = tx[t], y = ty[t];
-    v = interp_one<W>(g1, x, y, beta) + interp_one<W>(g2, x, y, beta);
+    double wx[W], wy[W];
+    int ix = es_horner<W, D>(gcoord(tx[t], g.ox, g.h), hp, wx);
+    int iy = es_horner<W, D>(gcoord(ty[t], g.oy, g.h), hp, wy);
+    bool inside = ix >= 0 && iy >= 0 && ix + W <= g.nf && iy + W <= g.nf;
+#pragma unroll
+    for (int b = 0; b < W; b++) {
+      double racc = 0.0;
+      if (inside) {
+        const double *rp = g.data + (int64_t)(iy + b) * g.row + ix;
+#pragma unroll
+        for (int a = 0; a < W; a++) racc = fma(wx[a], __ldg(rp + a), racc);
+      } else {
+        int64_t yy = wrapi(iy + b, g.nf);
+#pragma unroll
+        for (int a = 0; a < W; a++) racc = fma(wx[a], __ldg(g.data + yy * g.row + wrapi(ix + a, g.nf)), racc);
+      }
+      v = fma(wy[b], racc, v);
+    }
   }
   if (do_local) {
     double vl = 0.0;
@@ -218,7 +363,7 @@ __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__
     if (nd >= 0) vl = lalpha[t] * f[nd];
     const int32_t *ip = lidx + t * (int64_t)K;
     const double *wp = lw + t * (int64_t)K;
-    for (int k = 0; k < K; k++) vl += wp[k] * f[ip[k]];
+    for (int k = 0; k < K; k++) vl = fma(wp[k], __ldg(f + ip[k]), vl);
     v += vl;
   }
   out[tperm[t]] = v;
@@ -226,13 +371,13 @@ __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__
 
 template <int W>
 static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
+  constexpr int D = VP_HORNER_DEG(W);
   int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
   unsigned blocks = (unsigned)((P->T + 255) / 256);
   if (!blocks) return;
-  k_interp_local<W><<<blocks, 256, 0, P->stream>>>(P->tx, P->ty, P->tperm, P->T, grid_args(P->nh), grid_args(P->fh),
-                                                   P->beta, (parts & VP_PART_HISTORY) ? 1 : 0, f, P->lalpha,
-                                                   P->lnode, P->lidx, P->lw, P->K,
-                                                   (parts & VP_PART_LOCAL) ? 1 : 0, out);
+  k_interp_local<W, D><<<blocks, 256, 0, P->stream>>>(P->tx, P->ty, P->tperm, P->T, grid_args(P->nh), P->horner,
+                                                      (parts & VP_PART_HISTORY) ? 1 : 0, f, P->lalpha, P->lnode,
+                                                      P->lidx, P->lw, P->K, (parts & VP_PART_LOCAL) ? 1 : 0, out);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
@@ -248,7 +393,89 @@ void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// binning + sort of points into a uniform grid of bins (plan time)
+// plan-time: sort sources into row-rank batches and build the per-warp work items
+__global__ void k_gather_src(const double *__restrict__ xy, const double *__restrict__ w, const int32_t *__restrict__ idx,
+                             int64_t n, double *__restrict__ xs, double *__restrict__ ys, double *__restrict__ ws,
+                             int32_t *__restrict__ perm) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t j = idx[i];
+  xs[i] = xy[2 * (int64_t)j];
+  ys[i] = xy[2 * (int64_t)j + 1];
+  ws[i] = w[j];
+  perm[i] = j;
+}
+
+void vp_build_spread_order(vp_plan_s *P, const double *nodes, const double *weights) {
+  cudaStream_t s = P->stream;
+  const int64_t n = P->N;
+  VpTiles &Tl = P->tiles;
+  uint64_t *k1, *k1s, *k2, *k2s;
+  int32_t *i1, *i1s, *i2s, *head;
+  VP_CUDA(cudaMallocAsync(&k1, 8 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&k1s, 8 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&k2, 8 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&k2s, 8 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&i1, 4 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&i1s, 4 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&i2s, 4 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&head, 4 * (n + 1), s));
+  unsigned nb = (unsigned)((n + 255) / 256);
+  k_spread_keys<<<nb, 256, 0, s>>>(nodes, n, grid_args(P->nh), Tl.TS, P->w, Tl.ntx, Tl.nty, k1, i1);
+  VP_CHECK_LAUNCH();
+  size_t tb = 0, tb2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s);
+  void *tmp;
+  VP_CUDA(cudaMallocAsync(&tmp, std::max(tb, tb2) + 16, s));
+  VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
+  k_rank_keys<<<nb, 256, 0, s>>>(k1s, n, k2);
+  VP_CHECK_LAUNCH();
+  VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
+  k_batch_heads<<<nb, 256, 0, s>>>(k2s, n, head);
+  VP_CHECK_LAUNCH();
+  P->sx = vp_alloc<double>(P, n);
+  P->sy = vp_alloc<double>(P, n);
+  P->sw = vp_alloc<double>(P, n);
+  P->sperm = vp_alloc<int32_t>(P, n);
+  k_gather_src<<<nb, 256, 0, s>>>(nodes, weights, i2s, n, P->sx, P->sy, P->sw, P->sperm);
+  VP_CHECK_LAUNCH();
+  // host: batches and work items
+  std::vector<uint64_t> hk(n);
+  std::vector<int32_t> hh(n);
+  VP_CUDA(cudaMemcpyAsync(hk.data(), k2s, 8 * n, cudaMemcpyDeviceToHost, s));
+  VP_CUDA(cudaMemcpyAsync(hh.data(), head, 4 * n, cudaMemcpyDeviceToHost, s));
+  VP_CUDA(cudaStreamSynchronize(s));
+  std::vector<int32_t> bst;
+  std::vector<int64_t> btile;
+  for (int64_t i = 0; i < n; i++)
+    if (hh[i]) {
+      bst.push_back((int32_t)i);
+      btile.push_back((int64_t)(hk[i] >> 40));
+    }
+  int64_t nbat = (int64_t)bst.size();
+  bst.push_back((int32_t)n);
+  const int MAXB = 48;  // batches per warp work item
+  std::vector<int4> items;
+  for (int64_t b = 0; b < nbat;) {
+    int64_t t = btile[b], e = b;
+    while (e < nbat && btile[e] == t && e - b < MAXB) e++;
+    items.push_back(make_int4((int)(t % Tl.ntx), (int)(t / Tl.ntx), (int)b, (int)e));
+    b = e;
+  }
+  P->n_batches = nbat;
+  P->bstart = vp_alloc<int32_t>(P, bst.size());
+  VP_CUDA(cudaMemcpy(P->bstart, bst.data(), 4 * bst.size(), cudaMemcpyHostToDevice));
+  Tl.nsub = (int64_t)items.size();
+  Tl.sub = vp_alloc<int4>(P, items.size());
+  if (!items.empty()) VP_CUDA(cudaMemcpy(Tl.sub, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
+  for (void *p : {(void *)k1, (void *)k1s, (void *)k2, (void *)k2s, (void *)i1, (void *)i1s, (void *)i2s, (void *)head,
+                  tmp})
+    VP_CUDA(cudaFreeAsync(p, s));
+}
+
+// ---------------------------------------------------------------------------------------------
+// binning + sort of points into a uniform grid of bins (plan time; targets and kNN bins)
 __global__ void k_bin_keys(const double *__restrict__ xy, int64_t n, double ox, double oy, double cell, int64_t nbx,
                            int64_t nby, uint32_t *__restrict__ keys, int32_t *__restrict__ idx,
                            unsigned long long *__restrict__ counts) {
@@ -276,9 +503,6 @@ __global__ void k_gather_xy(const double *__restrict__ xy, const int32_t *__rest
   if (p32) p32[i] = j;
 }
 
-// Sort n points (interleaved xy, device) into bins (row-major by, bx); returns sorted coordinates
-// and the permutation (sorted -> input index).  bin_start (device, nbins+1, caller-owned via
-// plan allocs) is returned if bin_start_out != NULL.  Uses CUB radix sort (stable).
 int64_t vp_sort_points(vp_plan_s *P, const double *xy, int64_t n, double ox, double oy, double cell, int64_t nbx,
                        int64_t nby, double *xs, double *ys, int64_t *perm64, int32_t *perm32,
                        int64_t **bin_start_out) {
@@ -311,17 +535,14 @@ int64_t vp_sort_points(vp_plan_s *P, const double *xy, int64_t n, double ox, dou
   }
   if (bin_start_out) {
     int64_t *bs = vp_alloc<int64_t>(P, nb + 1);
-    // exclusive scan of counts (as int64) -> bin_start
-    {
-      size_t tb2 = 0;
-      cub::DeviceScan::ExclusiveSum(nullptr, tb2, (const unsigned long long *)counts, (unsigned long long *)bs,
-                                    (int)(nb + 1), s);
-      void *tmp2 = nullptr;
-      VP_CUDA(cudaMallocAsync(&tmp2, tb2 + 16, s));
-      VP_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, tb2, (const unsigned long long *)counts, (unsigned long long *)bs,
-                                            (int)(nb + 1), s));
-      VP_CUDA(cudaFreeAsync(tmp2, s));
-    }
+    size_t tb2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb2, (const unsigned long long *)counts, (unsigned long long *)bs,
+                                  (int)(nb + 1), s);
+    void *tmp2 = nullptr;
+    VP_CUDA(cudaMallocAsync(&tmp2, tb2 + 16, s));
+    VP_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, tb2, (const unsigned long long *)counts, (unsigned long long *)bs,
+                                          (int)(nb + 1), s));
+    VP_CUDA(cudaFreeAsync(tmp2, s));
     *bin_start_out = bs;
   }
   VP_CUDA(cudaFreeAsync(tmp, s));
