@@ -252,6 +252,7 @@ static void setup_horner(vp_plan_s *P) {
     }
   }
   P->horner_err = maxerr;
+  vp_upload_horner(W, P->horner);
   if (!(maxerr < 1e-6)) {
     vp_set_last_error("Horner fit of the ES kernel failed");
     throw VpError{VP_ERR_CUDA};

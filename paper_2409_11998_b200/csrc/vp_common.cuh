@@ -133,6 +133,7 @@ T *vp_alloc(vp_plan_s *P, size_t n) {
 // ---------------------------------------------------------------------------------------------
 // launch helpers (defined in the .cu files)
 void vp_launch_spread(vp_plan_s *P, const double *f);
+void vp_upload_horner(int W, const VpHorner &h);
 void vp_launch_restrict(vp_plan_s *P);
 void vp_launch_prolong(vp_plan_s *P);
 void vp_build_spread_order(vp_plan_s *P, const double *nodes, const double *weights);

@@ -24,26 +24,33 @@
 struct GridArgs {
   double *data;
   int64_t nf, row;
-  double ox, oy, h;
+  double ox, oy, h, inv_h;
 };
-static GridArgs grid_args(const VpGrid &G) { return GridArgs{G.data, G.nf, G.row, G.ox, G.oy, G.h}; }
+static GridArgs grid_args(const VpGrid &G) { return GridArgs{G.data, G.nf, G.row, G.ox, G.oy, G.h, 1.0 / G.h}; }
 
 // fractional grid coordinate of x (identical expression in binning, spreading and interpolation)
-__device__ __forceinline__ double gcoord(double x, double o, double h) { return (x - o) / h; }
+__device__ __forceinline__ double gcoord(double x, double o, double inv_h) { return (x - o) * inv_h; }
+
+// Horner tables of the ES taps for every width W (beta = 2.30 W fixed, so the table depends on W only)
+__constant__ double c_horner[VP_HORNER_MAXW - 3][VP_HORNER_MAXW][VP_HORNER_MAXW];
+
+void vp_upload_horner(int W, const VpHorner &h) {
+  VP_CUDA(cudaMemcpyToSymbol(c_horner, &h.c[0][0], sizeof(h.c), sizeof(h.c) * (size_t)(W - 4)));
+}
 
 // ES weights for grid points i0 .. i0+W-1 around fractional coordinate g, by Horner polynomials in
 // t = 2u - 1, u = i0 - (g - W/2) in [0, 1)
 template <int W, int D>
-__device__ __forceinline__ int es_horner(double g, const VpHorner &hp, double *wts) {
+__device__ __forceinline__ int es_horner(double g, double *wts) {
   double s = g - 0.5 * W;
   int i0 = (int)ceil(s);
   double t = 2.0 * (i0 - s) - 1.0;
 #pragma unroll
-  for (int k = 0; k < W; k++) {
-    double acc = hp.c[k][D];
+  for (int k = 0; k < W; k++) wts[k] = c_horner[W - 4][k][D];
 #pragma unroll
-    for (int j = D - 1; j >= 0; j--) acc = fma(acc, t, hp.c[k][j]);
-    wts[k] = acc;
+  for (int j = D - 1; j >= 0; j--) {
+#pragma unroll
+    for (int k = 0; k < W; k++) wts[k] = fma(wts[k], t, c_horner[W - 4][k][j]);
   }
   return i0;
 }
@@ -54,50 +61,74 @@ __device__ __forceinline__ int64_t wrapi(int64_t i, int64_t n) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// plan-time keys for the row-rank ordering
+// plan-time keys for the batch ordering: (tile, footprint row, footprint column) of each point
 __global__ void k_spread_keys(const double *__restrict__ xy, int64_t n, GridArgs g, int TS, int W, int64_t ntx,
                               int64_t nty, uint64_t *__restrict__ keys, int32_t *__restrict__ idx) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  double gx = gcoord(xy[2 * i], g.ox, g.h), gy = gcoord(xy[2 * i + 1], g.oy, g.h);
+  double gx = gcoord(xy[2 * i], g.ox, g.inv_h), gy = gcoord(xy[2 * i + 1], g.oy, g.inv_h);
   int64_t tx = (int64_t)floor(gx / TS), ty = (int64_t)floor(gy / TS);
   tx = tx < 0 ? 0 : (tx >= ntx ? ntx - 1 : tx);
   ty = ty < 0 ? 0 : (ty >= nty ? nty - 1 : ty);
-  int64_t j0 = (int64_t)ceil(gy - 0.5 * W);
-  int64_t lrow = j0 - (ty * TS - (W / 2 + 1));
+  int64_t lrow = (int64_t)ceil(gy - 0.5 * W) - (ty * TS - (W / 2 + 1));
+  int64_t lcol = (int64_t)ceil(gx - 0.5 * W) - (tx * TS - (W / 2 + 1));
   lrow = lrow < 0 ? 0 : (lrow > 255 ? 255 : lrow);
-  keys[i] = ((uint64_t)(ty * ntx + tx) << 32) | (uint64_t)lrow;
+  lcol = lcol < 0 ? 0 : (lcol > 255 ? 255 : lcol);
+  keys[i] = ((uint64_t)(ty * ntx + tx) << 32) | ((uint64_t)lrow << 16) | (uint64_t)lcol;
   idx[i] = (int32_t)i;
 }
 
-// level (rank within equal (tile,row) runs) -> second key (tile, level, row)
-__global__ void k_rank_keys(const uint64_t *__restrict__ k1, int64_t n, uint64_t *__restrict__ k2) {
+__global__ void k_tile_heads(const uint64_t *__restrict__ k1, int64_t n, int32_t *__restrict__ head) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint64_t key = k1[i];
-  int64_t lo = 0, hi = i;  // run start by binary search (lower_bound)
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (k1[mid] < key) lo = mid + 1; else hi = mid;
+  head[i] = (i == 0 || (k1[i - 1] >> 32) != (k1[i] >> 32)) ? 1 : 0;
+}
+
+// Greedy level assignment, one thread per non-empty tile: points in (row, column) order; a point
+// takes the lowest level whose last point in the same row ends at least W columns to its left.
+// Points of one level therefore never write the same grid cell within a footprint-row step.
+#define VP_MAXLV 128
+__global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restrict__ tstart, int64_t ntile,
+                         int64_t n, int W, uint64_t *__restrict__ k2) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= ntile) return;
+  int64_t s0 = tstart[t], s1 = (t + 1 < ntile) ? tstart[t + 1] : n;
+  int16_t last[VP_MAXLV];
+  int cur_row = -1, nlv = 0, overflow = 0;
+  for (int64_t i = s0; i < s1; i++) {
+    uint64_t key = k1[i];
+    int row = (int)((key >> 16) & 0xff), col = (int)(key & 0xff);
+    if (row != cur_row) {
+      cur_row = row;
+      nlv = 0;
+      overflow = 0;
+    }
+    int lv = -1;
+    for (int l = 0; l < nlv; l++)
+      if (last[l] <= col - W) { lv = l; break; }
+    if (lv < 0) {
+      if (nlv < VP_MAXLV) lv = nlv++;
+      else lv = VP_MAXLV + overflow++;
+    }
+    if (lv < VP_MAXLV) last[lv] = (int16_t)col;
+    uint64_t tile = key >> 32;
+    k2[i] = (tile << 40) | ((uint64_t)lv << 16) | ((uint64_t)row << 8) | (uint64_t)(col & 0xff);
   }
-  uint64_t level = (uint64_t)(i - lo);
-  uint64_t tile = key >> 32, lrow = key & 0xff;
-  k2[i] = (tile << 40) | (level << 8) | lrow;
 }
 
 // batch heads: new (tile, level) or every 32 points of one level
 __global__ void k_batch_heads(const uint64_t *__restrict__ k2, int64_t n, int32_t *__restrict__ head) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint64_t grp = k2[i] >> 8;
+  uint64_t grp = k2[i] >> 16;
   int h = 0;
-  if (i == 0 || (k2[i - 1] >> 8) != grp) {
+  if (i == 0 || (k2[i - 1] >> 16) != grp) {
     h = 1;
   } else {
     int64_t lo = 0, hi = i;
     while (lo < hi) {
       int64_t mid = (lo + hi) >> 1;
-      if ((k2[mid] >> 8) < grp) lo = mid + 1; else hi = mid;
+      if ((k2[mid] >> 16) < grp) lo = mid + 1; else hi = mid;
     }
     h = ((i - lo) % 32) == 0;
   }
@@ -110,8 +141,7 @@ template <int W, int D>
 __global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items, const int32_t *__restrict__ bstart,
                                                   const double *__restrict__ sx, const double *__restrict__ sy,
                                                   const double *__restrict__ sw, const int32_t *__restrict__ sperm,
-                                                  const double *__restrict__ f, GridArgs g, int TS,
-                                                  const __grid_constant__ VpHorner hp) {
+                                                  const double *__restrict__ f, GridArgs g, int TS) {
   extern __shared__ double tile[];
   const int nw = TS + W + 3;
   const int lane = threadIdx.x;
@@ -128,8 +158,8 @@ __global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items
       const int j = s + lane;
       const double x = sx[j], y = sy[j];
       c = f[sperm[j]] * sw[j];
-      lx = (int)(es_horner<W, D>(gcoord(x, g.ox, g.h), hp, wx) - ox);
-      ly = (int)(es_horner<W, D>(gcoord(y, g.oy, g.h), hp, wy) - oy);
+      lx = (int)(es_horner<W, D>(gcoord(x, g.ox, g.inv_h), wx) - ox);
+      ly = (int)(es_horner<W, D>(gcoord(y, g.oy, g.inv_h), wy) - oy);
     }
 #pragma unroll
     for (int r = 0; r < W; r++) {
@@ -145,11 +175,19 @@ __global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items
       __syncwarp();
     }
   }
-  for (int i = lane; i < nw * nw; i += 32) {
-    double v = tile[i];
-    if (v != 0.0) {
-      int64_t gx = wrapi(ox + i % nw, g.nf), gy = wrapi(oy + i / nw, g.nf);
-      atomicAdd(g.data + gy * g.row + gx, v);
+  __syncwarp();
+  const bool interior = ox >= 0 && oy >= 0 && ox + nw <= g.nf && oy + nw <= g.nf;
+  for (int rr = 0; rr < nw; rr++) {
+    for (int cc = lane; cc < nw; cc += 32) {
+      double v = tile[rr * nw + cc];
+      if (v != 0.0) {
+        int64_t gx = ox + cc, gy = oy + rr;
+        if (!interior) {
+          gx = wrapi(gx, g.nf);
+          gy = wrapi(gy, g.nf);
+        }
+        atomicAdd(g.data + gy * g.row + gx, v);
+      }
     }
   }
 }
@@ -161,8 +199,7 @@ static void launch_spread_w(vp_plan_s *P, const double *f) {
   size_t sm = sizeof(double) * (size_t)nw * nw;
   if (P->tiles.nsub == 0) return;
   k_spread_nh<W, D><<<(unsigned)P->tiles.nsub, 32, sm, P->stream>>>(P->tiles.sub, P->bstart, P->sx, P->sy, P->sw,
-                                                                    P->sperm, f, grid_args(P->nh), P->tiles.TS,
-                                                                    P->horner);
+                                                                    P->sperm, f, grid_args(P->nh), P->tiles.TS);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
@@ -329,7 +366,7 @@ void vp_launch_multiply(vp_plan_s *P, VpGrid &G) {
 template <int W, int D>
 __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__ tx, const double *__restrict__ ty,
                                                       const int64_t *__restrict__ tperm, int64_t T, GridArgs g,
-                                                      const __grid_constant__ VpHorner hp, int do_hist,
+                                                      int do_hist,
                                                       const double *__restrict__ f, const double *__restrict__ lalpha,
                                                       const int32_t *__restrict__ lnode,
                                                       const int32_t *__restrict__ lidx, const double *__restrict__ lw,
@@ -339,8 +376,8 @@ __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__
   double v = 0.0;
   if (do_hist) {
     double wx[W], wy[W];
-    int ix = es_horner<W, D>(gcoord(tx[t], g.ox, g.h), hp, wx);
-    int iy = es_horner<W, D>(gcoord(ty[t], g.oy, g.h), hp, wy);
+    int ix = es_horner<W, D>(gcoord(tx[t], g.ox, g.inv_h), wx);
+    int iy = es_horner<W, D>(gcoord(ty[t], g.oy, g.inv_h), wy);
     bool inside = ix >= 0 && iy >= 0 && ix + W <= g.nf && iy + W <= g.nf;
 #pragma unroll
     for (int b = 0; b < W; b++) {
@@ -375,7 +412,7 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
   int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
   unsigned blocks = (unsigned)((P->T + 255) / 256);
   if (!blocks) return;
-  k_interp_local<W, D><<<blocks, 256, 0, P->stream>>>(P->tx, P->ty, P->tperm, P->T, grid_args(P->nh), P->horner,
+  k_interp_local<W, D><<<blocks, 256, 0, P->stream>>>(P->tx, P->ty, P->tperm, P->T, grid_args(P->nh),
                                                       (parts & VP_PART_HISTORY) ? 1 : 0, f, P->lalpha, P->lnode,
                                                       P->lidx, P->lw, P->K, (parts & VP_PART_LOCAL) ? 1 : 0, out);
   VP_CHECK_LAUNCH();
@@ -429,8 +466,26 @@ void vp_build_spread_order(vp_plan_s *P, const double *nodes, const double *weig
   void *tmp;
   VP_CUDA(cudaMallocAsync(&tmp, std::max(tb, tb2) + 16, s));
   VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
-  k_rank_keys<<<nb, 256, 0, s>>>(k1s, n, k2);
-  VP_CHECK_LAUNCH();
+  {
+    // non-empty tile ranges
+    k_tile_heads<<<nb, 256, 0, s>>>(k1s, n, head);
+    VP_CHECK_LAUNCH();
+    int32_t *tst, *d_nt;
+    VP_CUDA(cudaMallocAsync(&tst, 4 * (n + 1), s));
+    VP_CUDA(cudaMallocAsync(&d_nt, 4, s));
+    size_t tb3 = 0;
+    cub::CountingInputIterator<int32_t> cnt(0);
+    cub::DeviceSelect::Flagged(nullptr, tb3, cnt, head, tst, d_nt, (int)n, s);
+    void *tmp3;
+    VP_CUDA(cudaMallocAsync(&tmp3, tb3 + 16, s));
+    VP_CUDA(cub::DeviceSelect::Flagged(tmp3, tb3, cnt, head, tst, d_nt, (int)n, s));
+    int32_t nt = 0;
+    VP_CUDA(cudaMemcpyAsync(&nt, d_nt, 4, cudaMemcpyDeviceToHost, s));
+    VP_CUDA(cudaStreamSynchronize(s));
+    k_levels<<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(k1s, tst, nt, n, P->w, k2);
+    VP_CHECK_LAUNCH();
+    for (void *p : {(void *)tst, (void *)d_nt, tmp3}) VP_CUDA(cudaFreeAsync(p, s));
+  }
   VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
   k_batch_heads<<<nb, 256, 0, s>>>(k2s, n, head);
   VP_CHECK_LAUNCH();
