@@ -54,7 +54,10 @@ typedef struct {
 } vp_boundary;
 
 /* How the Taylor jet of f at each target is estimated from nodal data (paper silent; DESIGN.md
- * reading R6). */
+ * reading R6).  KNN: least-squares fit over the K nearest nodes (stencil stored per target).
+ * TRIANGLE: interior node targets of straight triangles with aspect <= tri_max_aspect use the
+ * triangle's own p nodes (cubic fit, no per-target storage); all other targets use KNN.
+ * AUTO: TRIANGLE when ref_nodes is given and N > 1e7, else KNN. */
 enum { VP_DERIV_AUTO = 0, VP_DERIV_KNN = 1, VP_DERIV_TRIANGLE = 2 };
 /* which parts of V to evaluate (tests) */
 enum { VP_PART_HISTORY = 1, VP_PART_LOCAL = 2, VP_PART_ALL = 3 };
@@ -70,9 +73,15 @@ typedef struct {
   int32_t deriv_degree;      /* least-squares polynomial degree for KNN jets; 0 -> 6 (4 if N > 1e6) */
   int32_t deriv_k;           /* neighbours for KNN jets; 0 -> 2 * #monomials */
   int32_t parts;             /* VP_PART_*; 0 -> ALL */
-  int32_t targets_are_nodes; /* 1: targets[t] == tri_nodes[t] (T == M p); enables the node fast path */
+  int32_t targets_are_nodes; /* 1: targets[t] == tri_nodes[t] for t < N = M p (T >= N; targets beyond N are
+                                off-node points); enables the node fast path */
   vp_boundary boundary;
   void *cuda_stream;         /* cudaStream_t for vp_eval; NULL -> legacy default stream */
+  /* HOST pointer [p][2] or NULL: reference-triangle coordinates (xi1, xi2) of the p-point rule on
+   * (0,0),(1,0),(0,1).  Enables VP_DERIV_TRIANGLE: per-triangle cubic fit in reference coordinates
+   * mapped by the triangle's affine Jacobian (straight, well-shaped triangles only; the rest use KNN). */
+  const double *ref_nodes;
+  double tri_max_aspect;     /* TRIANGLE mode aspect-ratio limit (sigma_max/sigma_min of the map); 0 -> 3 */
 } vp_opts;
 
 /* Plan parameters chosen by vp_plan (diagnostics; all derived from the rules in DESIGN.md). */
@@ -89,6 +98,9 @@ typedef struct {
   int64_t n_boundary_targets;
   double plan_ms;
   int64_t device_bytes;      /* device memory owned by the plan */
+  int64_t n_stencil_targets; /* targets whose local part uses a stored KNN stencil */
+  int64_t n_batches;         /* spreading batches (<= 32 points each) */
+  double horner_err;         /* max |Horner - ES| over the kernel taps */
 } vp_info;
 
 typedef struct vp_plan_s *vp_handle;

@@ -35,7 +35,8 @@ class VpOpts(ctypes.Structure):
                 ("delta1_override", ctypes.c_double), ("eps_nufft", ctypes.c_double),
                 ("series_order", ctypes.c_int32), ("deriv_mode", ctypes.c_int32),
                 ("deriv_degree", ctypes.c_int32), ("deriv_k", ctypes.c_int32), ("parts", ctypes.c_int32),
-                ("targets_are_nodes", ctypes.c_int32), ("boundary", VpBoundary), ("cuda_stream", ctypes.c_void_p)]
+                ("targets_are_nodes", ctypes.c_int32), ("boundary", VpBoundary), ("cuda_stream", ctypes.c_void_p),
+                ("ref_nodes", ctypes.c_void_p), ("tri_max_aspect", ctypes.c_double)]
 
 
 class VpInfo(ctypes.Structure):
@@ -48,7 +49,8 @@ class VpInfo(ctypes.Structure):
                 ("x0", ctypes.c_double), ("y0", ctypes.c_double), ("S", ctypes.c_double),
                 ("deriv_mode", ctypes.c_int32), ("deriv_degree", ctypes.c_int32), ("deriv_k", ctypes.c_int32),
                 ("n_boundary_targets", ctypes.c_int64), ("plan_ms", ctypes.c_double),
-                ("device_bytes", ctypes.c_int64)]
+                ("device_bytes", ctypes.c_int64), ("n_stencil_targets", ctypes.c_int64),
+                ("n_batches", ctypes.c_int64), ("horner_err", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -116,8 +118,8 @@ class Plan:
     """vp_plan / vp_eval / vp_destroy as a Python object (argument marshalling only)."""
 
     def __init__(self, tri_nodes, weights, targets, tol, *, C=0.0, delta2_over_delta1=0.0, delta1_override=0.0,
-                 eps_nufft=0.0, series_order=0, deriv="knn", deriv_degree=0, deriv_k=0, parts=PART_ALL,
-                 targets_are_nodes=False, boundary=None, stream=None):
+                 eps_nufft=0.0, series_order=0, deriv="auto", deriv_degree=0, deriv_k=0, parts=PART_ALL,
+                 targets_are_nodes=False, boundary=None, stream=None, ref_nodes=None, tri_max_aspect=0.0):
         import torch
         L = lib()
         tri_nodes = _dev_f64(tri_nodes)
@@ -139,6 +141,12 @@ class Plan:
             stream = torch.cuda.current_stream()
         self.stream = stream
         o.cuda_stream = ctypes.c_void_p(stream.cuda_stream)
+        if ref_nodes is not None:
+            self._ref = np.ascontiguousarray(ref_nodes, dtype=np.float64).reshape(-1, 2)
+            if self._ref.shape[0] != p:
+                raise ValueError("ref_nodes must be [p, 2]")
+            o.ref_nodes = self._ref.ctypes.data
+        o.tri_max_aspect = tri_max_aspect
         h = ctypes.c_void_p()
         _check(L.vp_plan(tri_nodes.data_ptr(), weights.data_ptr(), M, p, targets.data_ptr(), T, float(tol),
                          ctypes.byref(o), ctypes.byref(h)), "vp_plan")

@@ -383,7 +383,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     P->M = M; P->p = p; P->N = N; P->T = T; P->tol = tol;
     if (opts) P->opts = *opts;
     vp_opts &o = P->opts;
-    if (o.targets_are_nodes && T != N) throw VpError{VP_ERR_ARG};
+    if (o.targets_are_nodes && T < N) throw VpError{VP_ERR_ARG};
     if (o.parts < 0 || o.parts > 3) throw VpError{VP_ERR_ARG};
     if (o.boundary.kind == VP_BDRY_CIRCLE && !(o.boundary.p[2] > 0)) throw VpError{VP_ERR_GEOMETRY};
     if (o.boundary.kind == VP_BDRY_RECT && !(o.boundary.p[2] > o.boundary.p[0] && o.boundary.p[3] > o.boundary.p[1]))
@@ -453,8 +453,11 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
                    P->ty, P->tperm, nullptr, nullptr);
     // ---- local part
     int parts = o.parts ? o.parts : VP_PART_ALL;
-    P->dmode = o.deriv_mode ? o.deriv_mode : VP_DERIV_KNN;
-    if (P->dmode != VP_DERIV_KNN) throw VpError{VP_ERR_UNSUPPORTED};
+    P->dmode = o.deriv_mode;
+    if (P->dmode == VP_DERIV_AUTO) P->dmode = (o.ref_nodes && N > 10000000) ? VP_DERIV_TRIANGLE : VP_DERIV_KNN;
+    if (P->dmode == VP_DERIV_TRIANGLE && (!o.ref_nodes || p < 10 || p > VP_TRI_MAXP || !o.targets_are_nodes))
+      throw VpError{VP_ERR_UNSUPPORTED};
+    if (P->dmode != VP_DERIV_KNN && P->dmode != VP_DERIV_TRIANGLE) throw VpError{VP_ERR_ARG};
     P->deg = o.deriv_degree > 0 ? o.deriv_degree : (N > 1000000 ? 4 : 6);
     if (P->deg > VP_MAXDEG) throw VpError{VP_ERR_ARG};
     int nc = vp_ncoef(P->deg);
@@ -470,6 +473,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
       P->lnode = vp_alloc<int32_t>(P, 1);
       P->lidx = vp_alloc<int32_t>(P, 1);
       P->lw = vp_alloc<double>(P, 1);
+      P->lptr = vp_alloc<int32_t>(P, 1);
     }
     // ---- FFT plans
     make_fft_plans(P);
@@ -587,6 +591,9 @@ extern "C" vp_status vp_get_info(vp_handle P, vp_info *I) {
   I->deriv_mode = P->dmode; I->deriv_degree = P->deg; I->deriv_k = P->K;
   I->n_boundary_targets = P->n_bdry;
   I->plan_ms = P->plan_ms;
+  I->n_stencil_targets = P->n_stencil;
+  I->n_batches = P->n_batches;
+  I->horner_err = P->horner_err;
   I->device_bytes = P->device_bytes;
   return VP_OK;
 }

@@ -11,6 +11,7 @@
 #include "../../include/vp.h"
 
 #define VP_PI 3.14159265358979323846
+#define VP_TRI_MAXP 32
 
 // ---------------------------------------------------------------------------------------------
 // error plumbing: every CUDA / cuFFT call inside the library goes through these
@@ -105,6 +106,12 @@ struct vp_plan_s {
   double *lalpha = nullptr;    // [T]
   int32_t *lnode = nullptr;    // [T] user node index of the target (targets_are_nodes) or -1
   int64_t n_bdry = 0;
+  int32_t *lptr = nullptr;     // [T] stencil slot of the target, -1 = TRIANGLE mode
+  int64_t n_stencil = 0;
+  int8_t *tri_ok = nullptr;    // [M] TRIANGLE mode usable
+  double *tri_M = nullptr;     // [M][3] A^-1 A^-T (M11, M12, M22)
+  double *tri_H = nullptr;     // [3][p][p] reference cubic-fit Hessian operators
+  double tri_c2 = 0;           // delta^2 / 2 (0 if series_order < 2)
   // host-side eval staging (vp_eval_host)
   double *f_dev = nullptr, *out_dev = nullptr;
   // profiling
@@ -140,6 +147,7 @@ void vp_build_spread_order(vp_plan_s *P, const double *nodes, const double *weig
 void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out);
 void vp_build_local(vp_plan_s *P, const double *nodes_dev);
+void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop);
 int64_t vp_sort_points(vp_plan_s *P, const double *xy, int64_t n, double ox, double oy, double cell,
                        int64_t nbx, int64_t nby, double *xs, double *ys, int64_t *perm64, int32_t *perm32,
                        int64_t **bin_start_out);

@@ -29,8 +29,10 @@ struct LocalArgs {
   int64_t nbx, nby;
   const double *tx, *ty;          // sorted targets
   const int64_t *tperm;
-  int64_t T;
-  int K, deg, nterms, node_targets;
+  const int32_t *list;            // targets (sorted index) that get a stencil; slot i -> target list[i]
+  int64_t T;                      // number of list entries
+  int K, deg, nterms;
+  int64_t node_targets;           // targets with user index < node_targets are the nodes themselves
   double delta;
   vp_boundary bd;
   int32_t *lidx;
@@ -62,8 +64,9 @@ __device__ void heap_sift_up(double *d, int32_t *id, int i) {
 }
 
 __global__ void k_build_local(LocalArgs a) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= a.T) return;
+  int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (slot >= a.T) return;
+  const int64_t t = a.list[slot];
   const double x = a.tx[t], y = a.ty[t];
   const int K = a.K, nc = vp_ncoef(a.deg);
   // ---- kNN by ring search
@@ -100,7 +103,7 @@ __global__ void k_build_local(LocalArgs a) {
     if (cnt == K && gap * gap >= hd[0]) break;
   }
   // ---- least squares: A (K x nc) column-major in scratch, Householder QR
-  double *A = a.scratch + t * (int64_t)(K * nc + K + nc);
+  double *A = a.scratch + slot * (int64_t)(K * nc + K + nc);
   double *yv = A + K * nc;
   double *diag = yv + K;
   double h = sqrt(hd[0]);
@@ -147,7 +150,7 @@ __global__ void k_build_local(LocalArgs a) {
   if (!bdry) vp_coef_interior(a.delta, a.nterms, a.deg, coef);
   a.is_bdry[t] = bdry ? 1 : 0;
   double alpha = 0.0;
-  int32_t node = a.node_targets ? (int32_t)a.tperm[t] : -1;
+  int32_t node = a.tperm[t] < a.node_targets ? (int32_t)a.tperm[t] : -1;
   if (node >= 0) {
     alpha = coef[0];
     coef[0] = 0.0;
@@ -180,8 +183,8 @@ __global__ void k_build_local(LocalArgs a) {
       for (int i = j; i < K; i++) yv[i] -= s * v[i];
     }
   }
-  int32_t *op = a.lidx + t * (int64_t)K;
-  double *ow = a.lw + t * (int64_t)K;
+  int32_t *op = a.lidx + slot * (int64_t)K;
+  double *ow = a.lw + slot * (int64_t)K;
   for (int k = 0; k < K; k++) {
     op[k] = a.kperm[hi[k]];
     ow[k] = yv[k];
@@ -190,57 +193,284 @@ __global__ void k_build_local(LocalArgs a) {
   a.lnode[t] = node;
 }
 
+// ---------------------------------------------------------------------------------------------
+// TRIANGLE mode: per-triangle affine map from the reference rule, aspect test, metric M = A^-1 A^-T
+struct TriArgs {
+  const double *nodes;   // [M][p][2] user order
+  int64_t M;
+  int p;
+  double pinv[3][VP_TRI_MAXP];  // affine LSQ: (A row x | A row y | b) = nodes * pinv^T
+  double ref[VP_TRI_MAXP][2];   // reference coordinates of the rule's nodes
+  double amax;
+  int8_t *ok;
+  double *Mm;            // [M][3]: M11, M12, M22
+};
+
+__global__ void k_tri_classify(TriArgs a) {
+  int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= a.M) return;
+  const double *nd = a.nodes + m * (int64_t)a.p * 2;
+  double c[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  for (int k = 0; k < a.p; k++)
+    for (int r = 0; r < 3; r++) {
+      c[0][r] += a.pinv[r][k] * nd[2 * k];
+      c[1][r] += a.pinv[r][k] * nd[2 * k + 1];
+    }
+  // x = A xi + b with A = [[c00, c01], [c10, c11]], b = (c02, c12); residual must vanish (straight)
+  double A00 = c[0][0], A01 = c[0][1], A10 = c[1][0], A11 = c[1][1];
+  double det = A00 * A11 - A01 * A10;
+  double fro = A00 * A00 + A01 * A01 + A10 * A10 + A11 * A11;
+  bool ok = fabs(det) > 1e-300 && isfinite(det);
+  // aspect = sigma_max / sigma_min of A
+  double disc = sqrt(fmax(fro * fro - 4.0 * det * det, 0.0));
+  double s2max = 0.5 * (fro + disc), s2min = 0.5 * (fro - disc);
+  if (!(s2min > 0.0) || s2max > a.amax * a.amax * s2min) ok = false;
+  // the map must reproduce every node (straight triangle carrying this rule)
+  double res = 0.0;
+  for (int k = 0; k < a.p; k++) {
+    double ex = A00 * a.ref[k][0] + A01 * a.ref[k][1] + c[0][2] - nd[2 * k];
+    double ey = A10 * a.ref[k][0] + A11 * a.ref[k][1] + c[1][2] - nd[2 * k + 1];
+    res = fmax(res, fabs(ex) + fabs(ey));
+  }
+  if (!(res <= 1e-10 * sqrt(fro))) ok = false;
+  double Mm11 = 0, Mm12 = 0, Mm22 = 0;
+  if (ok) {
+    // A^-1 = [[A11, -A01], [-A10, A00]] / det ; M = A^-1 A^-T
+    double i00 = A11 / det, i01 = -A01 / det, i10 = -A10 / det, i11 = A00 / det;
+    Mm11 = i00 * i00 + i01 * i01;
+    Mm12 = i00 * i10 + i01 * i11;
+    Mm22 = i10 * i10 + i11 * i11;
+  }
+  a.ok[m] = ok ? 1 : 0;
+  a.Mm[3 * m] = Mm11;
+  a.Mm[3 * m + 1] = Mm12;
+  a.Mm[3 * m + 2] = Mm22;
+}
+
+// Hessian operators of the least-squares cubic fit on the reference rule (host, once per plan):
+// Hop[ab][k][j], ab in {xi1 xi1, xi1 xi2, xi2 xi2}: second derivative of the fit at node k per f_j.
+void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop) {
+  const int nc = 10;
+  std::vector<double> V((size_t)p * nc);
+  auto mono = [](double u, double v, int m, int du, int dv) {
+    static const int ea[10] = {0, 1, 0, 2, 1, 0, 3, 2, 1, 0}, eb[10] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3};
+    int a = ea[m], b = eb[m];
+    if (du > a || dv > b) return 0.0;
+    double c = 1.0;
+    for (int i = 0; i < du; i++) c *= (a - i);
+    for (int i = 0; i < dv; i++) c *= (b - i);
+    return c * pow(u, a - du) * pow(v, b - dv);
+  };
+  const double c0 = 1.0 / 3.0;
+  for (int k = 0; k < p; k++)
+    for (int m = 0; m < nc; m++) V[(size_t)k * nc + m] = mono(ref[2 * k] - c0, ref[2 * k + 1] - c0, m, 0, 0);
+  // P = (V^T V)^-1 V^T by Gauss-Jordan on the 10x10 normal matrix (long double)
+  long double G[10][20];
+  for (int i = 0; i < nc; i++)
+    for (int j = 0; j < 2 * nc; j++) {
+      long double s = 0;
+      if (j < nc)
+        for (int k = 0; k < p; k++) s += (long double)V[(size_t)k * nc + i] * V[(size_t)k * nc + j];
+      else
+        s = (j - nc == i) ? 1.0L : 0.0L;
+      G[i][j] = s;
+    }
+  for (int c = 0; c < nc; c++) {
+    int piv = c;
+    for (int r = c + 1; r < nc; r++)
+      if (fabsl(G[r][c]) > fabsl(G[piv][c])) piv = r;
+    for (int j = 0; j < 2 * nc; j++) std::swap(G[c][j], G[piv][j]);
+    long double d = G[c][c];
+    for (int j = 0; j < 2 * nc; j++) G[c][j] /= d;
+    for (int r = 0; r < nc; r++)
+      if (r != c) {
+        long double f = G[r][c];
+        for (int j = 0; j < 2 * nc; j++) G[r][j] -= f * G[c][j];
+      }
+  }
+  std::vector<double> Pm((size_t)nc * p);
+  for (int m = 0; m < nc; m++)
+    for (int k = 0; k < p; k++) {
+      long double s = 0;
+      for (int i = 0; i < nc; i++) s += G[m][nc + i] * (long double)V[(size_t)k * nc + i];
+      Pm[(size_t)m * p + k] = (double)s;
+    }
+  Hop.assign((size_t)3 * p * p, 0.0);
+  const int dd[3][2] = {{2, 0}, {1, 1}, {0, 2}};
+  for (int h = 0; h < 3; h++)
+    for (int k = 0; k < p; k++)
+      for (int j = 0; j < p; j++) {
+        double s = 0;
+        for (int m = 0; m < nc; m++) s += mono(ref[2 * k] - c0, ref[2 * k + 1] - c0, m, dd[h][0], dd[h][1]) * Pm[(size_t)m * p + j];
+        Hop[((size_t)h * p + k) * p + j] = s;
+      }
+}
+
+// per sorted target: triangle mode (interior node of an ok triangle) or stencil
+__global__ void k_target_mode(const double *tx, const double *ty, const int64_t *tperm, int64_t T, int p,
+                              const int8_t *tri_ok, int64_t node_targets, vp_boundary bd, double delta, double c1,
+                              int32_t *need, double *lalpha, int32_t *lnode) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  int nd = tperm[t] < node_targets ? (int)tperm[t] : -1;
+  bool tri = nd >= 0 && tri_ok && tri_ok[nd / p];
+  if (tri && bd.kind != VP_BDRY_NONE) {
+    double coef[VP_NTAYLOR];
+    double x = tx[t], y = ty[t];
+    bool b = false;
+    if (bd.kind == VP_BDRY_CIRCLE) b = vp_coef_circle(x, y, bd.p[0], bd.p[1], bd.p[2], delta, 1, 0, coef);
+    else if (bd.kind == VP_BDRY_RECT) b = vp_coef_rect(x, y, bd.p[0], bd.p[1], bd.p[2], bd.p[3], delta, 0, coef);
+    if (b) tri = false;
+  }
+  need[t] = tri ? 0 : 1;
+  if (tri) {
+    lalpha[t] = c1;
+    lnode[t] = nd;
+  }
+}
+
+__global__ void k_fill_ptr(const int32_t *list, int64_t n, int32_t *lptr) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) lptr[list[i]] = (int32_t)i;
+}
+
 void vp_build_local(vp_plan_s *P, const double *nodes_dev) {
   int deg = P->deg, K = P->K;
   int nc = vp_ncoef(deg);
-  // kNN bins: about 8 nodes per bin over the bounding square
-  double S = P->S;
-  double cell = sqrt(8.0 * S * S / (double)P->N);
-  int64_t nb = (int64_t)ceil(S / cell) + 1;
-  if (nb < 1) nb = 1;
-  if (nb > 40000) { nb = 40000; cell = S / (nb - 1); }
-  double ox = P->cx - 0.5 * S - 0.5 * cell, oy = P->cy - 0.5 * S - 0.5 * cell;
-  double *kx = vp_alloc<double>(P, P->N), *ky = vp_alloc<double>(P, P->N);
-  int32_t *kperm = vp_alloc<int32_t>(P, P->N);
-  int64_t *bstart = nullptr;
-  vp_sort_points(P, nodes_dev, P->N, ox, oy, cell, nb, nb, kx, ky, nullptr, kperm, &bstart);
-  P->lidx = vp_alloc<int32_t>(P, (size_t)P->T * K);
-  P->lw = vp_alloc<double>(P, (size_t)P->T * K);
+  cudaStream_t st = P->stream;
+  const int nterms = P->opts.series_order > 0 ? P->opts.series_order : 3;
   P->lalpha = vp_alloc<double>(P, P->T);
   P->lnode = vp_alloc<int32_t>(P, P->T);
-  int32_t *isb = vp_alloc<int32_t>(P, P->T);
-  // scratch in chunks of targets to bound memory
-  int64_t per = (int64_t)(K * nc + K + nc);
-  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(P->T, (int64_t)(2e9 / 8) / per));
-  double *scratch = nullptr;
-  VP_CUDA(cudaMallocAsync(&scratch, sizeof(double) * per * chunk, P->stream));
-  for (int64_t s0 = 0; s0 < P->T; s0 += chunk) {
-    int64_t n = std::min(chunk, P->T - s0);
-    LocalArgs a;
-    a.kx = kx; a.ky = ky; a.kperm = kperm; a.bstart = bstart;
-    a.bo_x = ox; a.bo_y = oy; a.bcell = cell; a.nbx = nb; a.nby = nb;
-    a.tx = P->tx + s0; a.ty = P->ty + s0; a.tperm = P->tperm + s0; a.T = n;
-    a.K = K; a.deg = deg; a.nterms = P->opts.series_order > 0 ? P->opts.series_order : 3;
-    a.node_targets = P->opts.targets_are_nodes ? 1 : 0;
-    a.delta = P->delta1;
-    a.bd = P->opts.boundary;
-    a.lidx = P->lidx + s0 * K; a.lw = P->lw + s0 * K; a.lalpha = P->lalpha + s0; a.lnode = P->lnode + s0;
-    a.is_bdry = isb + s0;
-    a.scratch = scratch;
-    k_build_local<<<(unsigned)((n + 127) / 128), 128, 0, P->stream>>>(a);
+  P->lptr = vp_alloc<int32_t>(P, P->T);
+  VP_CUDA(cudaMemsetAsync(P->lptr, 0xff, sizeof(int32_t) * P->T, st));
+  int32_t *need = nullptr;
+  VP_CUDA(cudaMallocAsync(&need, sizeof(int32_t) * (P->T + 1), st));
+  unsigned tb_t = (unsigned)((P->T + 255) / 256);
+  if (P->dmode == VP_DERIV_TRIANGLE) {
+    // reference-rule operators on the host: affine pseudo-inverse and cubic-fit Hessian operators
+    const int p = P->p;
+    const double *ref = P->opts.ref_nodes;
+    TriArgs ta;
+    memset(&ta, 0, sizeof(ta));
+    {
+      // normal equations of [xi1 xi2 1] (p x 3): pinv = (V^T V)^-1 V^T
+      double G[3][3] = {{0}}, V[VP_TRI_MAXP][3];
+      for (int k = 0; k < p; k++) {
+        V[k][0] = ref[2 * k]; V[k][1] = ref[2 * k + 1]; V[k][2] = 1.0;
+        for (int i = 0; i < 3; i++)
+          for (int j = 0; j < 3; j++) G[i][j] += V[k][i] * V[k][j];
+      }
+      double Gi[3][3];
+      double d = G[0][0] * (G[1][1] * G[2][2] - G[1][2] * G[2][1]) - G[0][1] * (G[1][0] * G[2][2] - G[1][2] * G[2][0]) +
+                 G[0][2] * (G[1][0] * G[2][1] - G[1][1] * G[2][0]);
+      for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) {
+          int i1 = (j + 1) % 3, i2 = (j + 2) % 3, j1 = (i + 1) % 3, j2 = (i + 2) % 3;
+          Gi[i][j] = (G[i1][j1] * G[i2][j2] - G[i1][j2] * G[i2][j1]) / d;
+        }
+      for (int r = 0; r < 3; r++)
+        for (int k = 0; k < p; k++) {
+          double s = 0;
+          for (int j = 0; j < 3; j++) s += Gi[r][j] * V[k][j];
+          ta.pinv[r][k] = s;
+        }
+    }
+    ta.nodes = nodes_dev; ta.M = P->M; ta.p = p;
+    for (int k = 0; k < p; k++) { ta.ref[k][0] = ref[2 * k]; ta.ref[k][1] = ref[2 * k + 1]; }
+    ta.amax = P->opts.tri_max_aspect > 0 ? P->opts.tri_max_aspect : 3.0;
+    P->tri_ok = vp_alloc<int8_t>(P, P->M);
+    P->tri_M = vp_alloc<double>(P, 3 * P->M);
+    ta.ok = P->tri_ok; ta.Mm = P->tri_M;
+    k_tri_classify<<<(unsigned)((P->M + 127) / 128), 128, 0, st>>>(ta);
+    VP_CHECK_LAUNCH();
+    // Hessian operators of the reference cubic fit: H_ab[k][j] = d2/dxi_a dxi_b of the fit at node k
+    std::vector<double> Hop;
+    vp_cubic_hessian_ops(ref, p, Hop);
+    P->tri_H = vp_alloc<double>(P, Hop.size());
+    VP_CUDA(cudaMemcpy(P->tri_H, Hop.data(), sizeof(double) * Hop.size(), cudaMemcpyHostToDevice));
+    double c1 = P->delta1;
+    k_target_mode<<<tb_t, 256, 0, st>>>(P->tx, P->ty, P->tperm, P->T, p, P->tri_ok, P->opts.targets_are_nodes ? P->N : 0,
+                                       P->opts.boundary, P->delta1, c1, need, P->lalpha, P->lnode);
+    VP_CHECK_LAUNCH();
+    P->tri_c2 = nterms >= 2 ? 0.5 * P->delta1 * P->delta1 : 0.0;
+  } else {
+    k_target_mode<<<tb_t, 256, 0, st>>>(P->tx, P->ty, P->tperm, P->T, 1, nullptr, 0, P->opts.boundary, P->delta1, 0.0,
+                                       need, P->lalpha, P->lnode);
     VP_CHECK_LAUNCH();
   }
-  VP_CUDA(cudaFreeAsync(scratch, P->stream));
+  // compact the stencil targets
+  int32_t *list = nullptr, *d_n = nullptr;
+  VP_CUDA(cudaMallocAsync(&list, sizeof(int32_t) * (P->T + 1), st));
+  VP_CUDA(cudaMallocAsync(&d_n, sizeof(int32_t), st));
+  {
+    size_t tb = 0;
+    cub::CountingInputIterator<int32_t> cnt(0);
+    cub::DeviceSelect::Flagged(nullptr, tb, cnt, need, list, d_n, (int)P->T, st);
+    void *tmp;
+    VP_CUDA(cudaMallocAsync(&tmp, tb + 16, st));
+    VP_CUDA(cub::DeviceSelect::Flagged(tmp, tb, cnt, need, list, d_n, (int)P->T, st));
+    VP_CUDA(cudaFreeAsync(tmp, st));
+  }
+  int32_t nst = 0;
+  VP_CUDA(cudaMemcpyAsync(&nst, d_n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  VP_CUDA(cudaStreamSynchronize(st));
+  P->n_stencil = nst;
+  if (nst > 0) {
+    k_fill_ptr<<<(unsigned)((nst + 255) / 256), 256, 0, st>>>(list, nst, P->lptr);
+    VP_CHECK_LAUNCH();
+  }
+  P->lidx = vp_alloc<int32_t>(P, (size_t)std::max<int64_t>(nst, 1) * K);
+  P->lw = vp_alloc<double>(P, (size_t)std::max<int64_t>(nst, 1) * K);
+  int32_t *isb = nullptr;
+  VP_CUDA(cudaMallocAsync(&isb, sizeof(int32_t) * (P->T + 1), st));
+  VP_CUDA(cudaMemsetAsync(isb, 0, sizeof(int32_t) * (P->T + 1), st));
+  if (nst > 0) {
+    // kNN bins: about 8 nodes per bin over the bounding square
+    double S = P->S;
+    double cell = sqrt(8.0 * S * S / (double)P->N);
+    int64_t nb = (int64_t)ceil(S / cell) + 1;
+    if (nb < 1) nb = 1;
+    if (nb > 40000) { nb = 40000; cell = S / (nb - 1); }
+    double ox = P->cx - 0.5 * S - 0.5 * cell, oy = P->cy - 0.5 * S - 0.5 * cell;
+    double *kx = nullptr, *ky = nullptr;
+    int32_t *kperm = nullptr;
+    VP_CUDA(cudaMallocAsync(&kx, sizeof(double) * P->N, st));
+    VP_CUDA(cudaMallocAsync(&ky, sizeof(double) * P->N, st));
+    VP_CUDA(cudaMallocAsync(&kperm, sizeof(int32_t) * P->N, st));
+    int64_t *bstart = nullptr;
+    vp_sort_points(P, nodes_dev, P->N, ox, oy, cell, nb, nb, kx, ky, nullptr, kperm, &bstart);
+    int64_t per = (int64_t)(K * nc + K + nc);
+    int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nst, (int64_t)(2e9 / 8) / per));
+    double *scratch = nullptr;
+    VP_CUDA(cudaMallocAsync(&scratch, sizeof(double) * per * chunk, st));
+    for (int64_t s0 = 0; s0 < nst; s0 += chunk) {
+      int64_t n = std::min<int64_t>(chunk, nst - s0);
+      LocalArgs a;
+      a.kx = kx; a.ky = ky; a.kperm = kperm; a.bstart = bstart;
+      a.bo_x = ox; a.bo_y = oy; a.bcell = cell; a.nbx = nb; a.nby = nb;
+      a.tx = P->tx; a.ty = P->ty; a.tperm = P->tperm; a.list = list + s0; a.T = n;
+      a.K = K; a.deg = deg; a.nterms = nterms;
+      a.node_targets = P->opts.targets_are_nodes ? P->N : 0;
+      a.delta = P->delta1;
+      a.bd = P->opts.boundary;
+      a.lidx = P->lidx + s0 * K; a.lw = P->lw + s0 * K; a.lalpha = P->lalpha; a.lnode = P->lnode;
+      a.is_bdry = isb;
+      a.scratch = scratch;
+      k_build_local<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(a);
+      VP_CHECK_LAUNCH();
+    }
+    for (void *q : {(void *)scratch, (void *)kx, (void *)ky, (void *)kperm}) VP_CUDA(cudaFreeAsync(q, st));
+  }
   // count boundary targets
   int64_t *d_cnt = nullptr;
-  VP_CUDA(cudaMallocAsync(&d_cnt, sizeof(int64_t), P->stream));
+  VP_CUDA(cudaMallocAsync(&d_cnt, sizeof(int64_t), st));
   size_t tb = 0;
-  cub::DeviceReduce::Sum(nullptr, tb, isb, d_cnt, (int)P->T, P->stream);
+  cub::DeviceReduce::Sum(nullptr, tb, isb, d_cnt, (int)P->T, st);
   void *tmp = nullptr;
-  VP_CUDA(cudaMallocAsync(&tmp, tb + 16, P->stream));
-  VP_CUDA(cub::DeviceReduce::Sum(tmp, tb, isb, d_cnt, (int)P->T, P->stream));
-  VP_CUDA(cudaMemcpyAsync(&P->n_bdry, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, P->stream));
-  VP_CUDA(cudaStreamSynchronize(P->stream));
-  VP_CUDA(cudaFree(tmp));
-  VP_CUDA(cudaFree(d_cnt));
+  VP_CUDA(cudaMallocAsync(&tmp, tb + 16, st));
+  VP_CUDA(cub::DeviceReduce::Sum(tmp, tb, isb, d_cnt, (int)P->T, st));
+  VP_CUDA(cudaMemcpyAsync(&P->n_bdry, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  VP_CUDA(cudaStreamSynchronize(st));
+  for (void *q : {(void *)tmp, (void *)d_cnt, (void *)need, (void *)list, (void *)d_n, (void *)isb})
+    VP_CUDA(cudaFree(q));
 }

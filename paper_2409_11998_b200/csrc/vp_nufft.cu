@@ -370,7 +370,10 @@ __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__
                                                       const double *__restrict__ f, const double *__restrict__ lalpha,
                                                       const int32_t *__restrict__ lnode,
                                                       const int32_t *__restrict__ lidx, const double *__restrict__ lw,
-                                                      int K, int do_local, double *__restrict__ out) {
+                                                      int K, int do_local, const int32_t *__restrict__ lptr,
+                                                      const double *__restrict__ tri_M,
+                                                      const double *__restrict__ tri_H, int p, double tri_c2,
+                                                      double *__restrict__ out) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= T) return;
   double v = 0.0;
@@ -396,11 +399,26 @@ __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__
   }
   if (do_local) {
     double vl = 0.0;
-    int32_t nd = lnode[t];
-    if (nd >= 0) vl = lalpha[t] * f[nd];
-    const int32_t *ip = lidx + t * (int64_t)K;
-    const double *wp = lw + t * (int64_t)K;
-    for (int k = 0; k < K; k++) vl = fma(wp[k], __ldg(f + ip[k]), vl);
+    const int32_t nd = lnode[t];
+    if (nd >= 0) vl = lalpha[t] * __ldg(f + nd);
+    const int32_t sp = lptr[t];
+    if (sp >= 0) {  // least-squares stencil
+      const int32_t *ip = lidx + sp * (int64_t)K;
+      const double *wp = lw + sp * (int64_t)K;
+      for (int k = 0; k < K; k++) vl = fma(wp[k], __ldg(f + ip[k]), vl);
+    } else if (tri_c2 != 0.0) {  // own-triangle cubic fit: Lap f = M11 f_11 + 2 M12 f_12 + M22 f_22
+      const int64_t tri = nd / p;
+      const int kk = nd - (int)tri * p;
+      const double m11 = __ldg(tri_M + 3 * tri), m12 = __ldg(tri_M + 3 * tri + 1), m22 = __ldg(tri_M + 3 * tri + 2);
+      const double *fb = f + tri * p;
+      const double *h0 = tri_H + (int64_t)kk * p, *h1 = h0 + (int64_t)p * p, *h2 = h1 + (int64_t)p * p;
+      double lap = 0.0;
+      for (int j = 0; j < p; j++) {
+        double op = fma(m11, __ldg(h0 + j), fma(2.0 * m12, __ldg(h1 + j), m22 * __ldg(h2 + j)));
+        lap = fma(op, __ldg(fb + j), lap);
+      }
+      vl = fma(tri_c2, lap, vl);
+    }
     v += vl;
   }
   out[tperm[t]] = v;
@@ -414,7 +432,8 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
   if (!blocks) return;
   k_interp_local<W, D><<<blocks, 256, 0, P->stream>>>(P->tx, P->ty, P->tperm, P->T, grid_args(P->nh),
                                                       (parts & VP_PART_HISTORY) ? 1 : 0, f, P->lalpha, P->lnode,
-                                                      P->lidx, P->lw, P->K, (parts & VP_PART_LOCAL) ? 1 : 0, out);
+                                                      P->lidx, P->lw, P->K, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr,
+                                                      P->tri_M, P->tri_H, P->p, P->tri_c2, out);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }

@@ -217,6 +217,86 @@ def config4(n=1414, seed=4, tol=1e-10, kmax=64, f_device=None):
                    ("rect", 0.0, 0.0, 1.0, 1.0), tol, meta={"seed": seed, "n": n}, f_device=f_device)
 
 
+# --------------------------------------------------------------------------- config 5
+def quadtree_leaves(centers, g, lmin, lmax):
+    """Leaves (x0, y0, size) of a quadtree on [0,1]^2 refined until size <= max(g * d, 2^-lmax), where d
+    is the distance from the cell to the nearest cluster centre; coarsest level lmin."""
+    n0 = 1 << lmin
+    s = 1.0 / n0
+    ix, iy = np.meshgrid(np.arange(n0), np.arange(n0), indexing="ij")
+    cx = (ix.ravel() * s).astype(np.float64)
+    cy = (iy.ravel() * s).astype(np.float64)
+    out = []
+    level = lmin
+    while cx.size:
+        s = 1.0 / (1 << level)
+        mx, my = cx + 0.5 * s, cy + 0.5 * s
+        d = np.full(cx.shape, np.inf)
+        for c in centers:
+            d = np.minimum(d, np.hypot(mx - c[0], my - c[1]))
+        d = np.maximum(d - 0.7072 * s, 0.0)
+        ref = (s > g * d) & (level < lmax)
+        out.append(np.stack([cx[~ref], cy[~ref], np.full((~ref).sum(), s)], 1))
+        cx, cy = cx[ref], cy[ref]
+        h = 0.5 * s
+        cx = np.concatenate([cx, cx + h, cx, cx + h])
+        cy = np.concatenate([cy, cy, cy + h, cy + h])
+        level += 1
+    return np.concatenate(out)
+
+
+def config5(M_target=16_000_000, seed=5, n_random=4_000_000, split_frac=0.05, tol=1e-9, lmin=11, lmax=18,
+            f_device=None):
+    """Unit square, quadtree graded toward 20 clusters (area ratio 2^(2(lmax-lmin)) ~ 1.6e4), leaves split
+    into 2 triangles, 5% cevian slivers (aspect <= ~1e2); f = 20 Gaussians at the clusters; targets =
+    all nodes followed by n_random uniform points."""
+    rng = np.random.default_rng(seed)
+    centers = rng.uniform(0.05, 0.95, (20, 2))
+    base = 2 * (1 << lmin) ** 2 * (1 + split_frac)
+
+    def count(g):
+        return 2 * quadtree_leaves(centers, g, lmin, lmax).shape[0] * (1 + split_frac)
+
+    # the refinement adds ~ C / g^2 triangles: solve for g on a log scale (the value found for the
+    # default seed and size is tried first)
+    lo, hi = 1e-3, 1.0
+    g = 0.019988548118735103
+    if (seed, M_target, lmin, lmax) == (5, 16_000_000, 11, 18):
+        lo = hi = g
+    for _ in range(40):
+        g = np.sqrt(lo * hi)
+        m = count(g)
+        if abs(m - M_target) <= 0.005 * M_target:
+            break
+        if m > M_target:
+            lo = g
+        else:
+            hi = g
+    leaves = quadtree_leaves(centers, g, lmin, lmax)
+    x0, y0, s = leaves[:, 0], leaves[:, 1], leaves[:, 2]
+    a = np.stack([x0, y0], 1)
+    b = np.stack([x0 + s, y0], 1)
+    c = np.stack([x0 + s, y0 + s], 1)
+    d = np.stack([x0, y0 + s], 1)
+    diag = rng.random(x0.size) < 0.5
+    t1 = np.where(diag[:, None, None], np.stack([a, b, c], 1), np.stack([a, b, d], 1))
+    t2 = np.where(diag[:, None, None], np.stack([a, c, d], 1), np.stack([b, c, d], 1))
+    tri = np.concatenate([t1, t2])
+    del t1, t2, a, b, c, d
+    tri = cevian_split(tri, split_frac, rng, umin=1e-2, umax=1e-1)
+    tri = tri[rng.permutation(tri.shape[0])]
+    g2 = np.random.default_rng(seed + 1000)
+    fld = fields.gauss(g2.standard_normal(20), centers[:, 0], centers[:, 1], g2.uniform(1e-3, 5e-2, 20) ** 2)
+    extra = np.random.default_rng(seed + 2000).uniform(0.0, 1.0, (n_random, 2))
+    nodes, weights = geometry.nodes_weights(tri, None, None)
+    f = fields.evaluate(fld, nodes[..., 0], nodes[..., 1], device=f_device)
+    targets = np.concatenate([nodes.reshape(-1, 2), extra])
+    return Workload(f"c5_square_quadtree_M{tri.shape[0]}", tri, np.zeros(tri.shape[0], np.int8), None, nodes, weights,
+                    targets, True, fld, f, ("rect", 0.0, 0.0, 1.0, 1.0), tol,
+                    meta={"seed": seed, "g": g, "levels": (lmin, lmax), "n_random": n_random,
+                          "first_targets_are_nodes": nodes.shape[0] * nodes.shape[1]})
+
+
 def sample_targets(T, K, seed=12345):
     """Seeded uniform subsample of K target indices out of T (sorted)."""
     rng = np.random.default_rng(seed)
@@ -225,4 +305,4 @@ def sample_targets(T, K, seed=12345):
     return np.sort(rng.choice(T, size=K, replace=False))
 
 
-CONFIGS = {"c1": config1, "c2": config2, "c4": config4}
+CONFIGS = {"c1": config1, "c2": config2, "c4": config4, "c5": config5}

@@ -46,6 +46,8 @@ def evaluate(field, x, y, device=None):
     kind = field["kind"]
     if kind == "const":
         return np.full(x.shape, field["a"])
+    if kind == "gauss" and x.size > 4_000_000:
+        return _eval_gauss_torch(field, x, y, device)
     if kind == "gauss":
         out = np.zeros(x.shape)
         for a, cx, cy, s in zip(field["a"], field["cx"], field["cy"], field["s"]):
@@ -54,6 +56,23 @@ def evaluate(field, x, y, device=None):
     if kind == "fourier":
         return _eval_fourier(field, x, y, device)
     raise ValueError(kind)
+
+
+def _eval_gauss_torch(field, x, y, device=None):
+    import torch
+    if device is None:
+        device = "cuda" if torch.cuda.is_available() else "cpu"
+    xs, ys = x.ravel(), y.ravel()
+    out = np.empty(xs.size)
+    step = 1 << 24
+    for s0 in range(0, xs.size, step):
+        xx = torch.from_numpy(xs[s0:s0 + step]).to(device)
+        yy = torch.from_numpy(ys[s0:s0 + step]).to(device)
+        acc = torch.zeros_like(xx)
+        for a, cx, cy, s in zip(field["a"], field["cx"], field["cy"], field["s"]):
+            acc += float(a) * torch.exp(-((xx - float(cx)) ** 2 + (yy - float(cy)) ** 2) / float(s))
+        out[s0:s0 + step] = acc.cpu().numpy()
+    return out.reshape(x.shape)
 
 
 def _eval_fourier(field, x, y, device=None):

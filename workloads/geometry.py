@@ -106,10 +106,8 @@ def nodes_weights(tri, curved=None, circle=None, chunk=1 << 20):
     # affine triangles: exact closed form
     v0, v1, v2 = tri[:, 0], tri[:, 1], tri[:, 2]
     area = 0.5 * ((v1[:, 0] - v0[:, 0]) * (v2[:, 1] - v0[:, 1]) - (v1[:, 1] - v0[:, 1]) * (v2[:, 0] - v0[:, 0]))
-    for k in range(rule.P):
-        b = bary[k]
-        nodes[:, k, :] = b[0] * v0 + b[1] * v1 + b[2] * v2
-        wts[:, k] = rule.WEIGHTS[k] * np.abs(area)
+    nodes[...] = np.einsum("kj,mjd->mkd", bary, tri, optimize=False)
+    np.multiply(rule.WEIGHTS[None, :], np.abs(area)[:, None], out=wts)
     cur = np.nonzero(~straight)[0]
     if cur.size:
         h = 1e-30
