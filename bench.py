@@ -113,6 +113,22 @@ def oracle_rate(w, n_targets, seed=99):
                       f"{dt:.2f} s measured, extrapolated linearly in T", "seconds": dt}
 
 
+def max_over_ranks(x, dev=None):
+    """Max of a per-rank float over all ranks (identity at world size 1); NCCL on the GPU, gloo in tests."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_rate(world, pts_per_rank, ms_max):
+    """Whole-job throughput: replicas (DESIGN.md §7 "replicas only") -> all ranks' points / slowest rank's time."""
+    return world * pts_per_rank / (ms_max * 1e-3)
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -201,12 +217,9 @@ def main():
     torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms = float(np.mean(step_ms))
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = max_over_ranks(ms, dev)
     pts = (w.N + w.T)
-    value = world * pts / (ms_max * 1e-3)
+    value = aggregate_rate(world, pts, ms_max)
     kern, ffts = plan.launch_count()
 
     # ---- roofline of the dominant kernel (algorithmic bytes)
@@ -235,11 +248,9 @@ def main():
         t0 = time.perf_counter()
         plan.eval_host(f_pin.numpy(), out_pin.numpy())
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e = {"value": world * pts / (float(e2e_t.item()) * 1e-3), "unit": "pts/s", "h2d_bytes_per_step": 8 * w.N,
-           "d2h_bytes_per_step": 8 * w.T, "ms_per_step": float(e2e_t.item())}
+    e2e_max = max_over_ranks(float(np.mean(e2e_ms)), dev)
+    e2e = {"value": aggregate_rate(world, pts, e2e_max), "unit": "pts/s", "h2d_bytes_per_step": 8 * w.N,
+           "d2h_bytes_per_step": 8 * w.T, "ms_per_step": e2e_max}
 
     if rank == 0:
         cpu = None

@@ -1,0 +1,55 @@
+"""N > 1 host logic of bench.py on CPU (gloo, world size 2): max-over-ranks timing and the whole-job
+rate of independent replicas (DESIGN.md §7 "replicas only"), and the reference arm's rank gating."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    import bench
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ms_local = [2.0, 5.0][rank]
+    m = bench.max_over_ranks(ms_local)
+    v = bench.aggregate_rate(world, 1000, m)
+    q.put((rank, m, v))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_max_over_ranks_and_rate_gloo():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(60)
+        assert p.exitcode == 0
+    for rank, m, v in res:
+        assert m == 5.0                       # the slowest rank's time
+        assert abs(v - 2 * 1000 / 5e-3) < 1e-6  # all ranks' points over that time
+
+
+def test_world1_identity():
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.max_over_ranks(3.5) == 3.5
+    assert bench.aggregate_rate(1, 100, 1.0) == 1e5
+
+
+def test_reference_arm_nonzero_rank_exits_silently():
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, env=env, timeout=300, cwd=ROOT)
+    assert r.returncode == 0
+    assert r.stdout.strip() == ""
