@@ -82,6 +82,13 @@ typedef struct {
    * mapped by the triangle's affine Jacobian (straight, well-shaped triangles only; the rest use KNN). */
   const double *ref_nodes;
   double tri_max_aspect;     /* TRIANGLE mode aspect-ratio limit (sigma_max/sigma_min of the map); 0 -> 3 */
+  /* Level-band corrections for graded meshes (reading R15; §4.1
+   * telescoping "extends naturally to ... volume").  levels: -1 off, 0 auto (as many levels as the mesh
+   * grading supports, <= 12), > 0 cap.  A target x gets level l(x) = the finest l such that every node y
+   * within level_rho sqrt(delta_l) has delta_l >= level_cmin Dx_loc^2(y), delta_l = delta_1 / 4^l. */
+  int32_t levels;
+  double level_cmin;         /* 0 -> 2 */
+  double level_rho;          /* 0 -> 4 */
 } vp_opts;
 
 /* Plan parameters chosen by vp_plan (diagnostics; all derived from the rules in DESIGN.md). */
@@ -101,6 +108,12 @@ typedef struct {
   int64_t n_stencil_targets; /* targets whose local part uses a stored KNN stencil */
   int64_t n_batches;         /* spreading batches (<= 32 points each) */
   double horner_err;         /* max |Horner - ES| over the kernel taps */
+  int32_t n_levels;          /* finest band level present (0: no level bands) */
+  int64_t n_boxes;           /* band boxes (all levels) */
+  int64_t n_level_targets;   /* targets with level >= 1 */
+  int64_t n_band_pairs;      /* (box, source) pairs spread per eval */
+  int64_t nf_band;           /* band box fine grid per dimension */
+  int64_t level_targets[16]; /* targets per level */
 } vp_info;
 
 typedef struct vp_plan_s *vp_handle;
@@ -127,7 +140,7 @@ const char *vp_strerror(vp_status s);
 vp_status vp_get_info(vp_handle plan, vp_info *info);
 
 /* Per-phase device times (ms) of the last vp_eval when profiling is on (vp_set_profiling).
- * names: "zero", "spread", "restrict", "fft_fwd", "multiply", "fft_inv", "prolong", "interp_local";
+ * names: "zero", "spread", "restrict", "fft_fwd", "multiply", "fft_inv", "prolong", "interp_local", "bands";
  * n_out <= 16. */
 vp_status vp_set_profiling(vp_handle plan, int32_t on);
 vp_status vp_get_phase_times(vp_handle plan, double *ms, int32_t *n_out, const char **names);

@@ -36,7 +36,8 @@ class _Field(ctypes.Structure):
 
 
 class _Opts(ctypes.Structure):
-    _fields_ = [("eta_far", ctypes.c_double), ("eta_polar", ctypes.c_double), ("nthreads", ctypes.c_int32)]
+    _fields_ = [("eta_far", ctypes.c_double), ("eta_polar", ctypes.c_double), ("nthreads", ctypes.c_int32),
+                ("assume_resolved", ctypes.c_int32)]
 
 
 _lib = None
@@ -61,6 +62,8 @@ def lib():
         _lib.orc_smooth_direct.argtypes = [i64, p, p, i64, p, d, p]
         _lib.orc_smooth_dft.argtypes = [i64, p, p, i64, p, d, d, d, i64, d, i64, d, d, d, p]
         _lib.orc_num_threads.restype = ctypes.c_int
+        _lib.orc_resolve_rules.argtypes = [i64, p, p, p, ctypes.POINTER(_Field), p]
+        _lib.orc_resolve_rules.restype = ctypes.c_int
     return _lib
 
 
@@ -94,12 +97,15 @@ def _field_struct(field):
     return F, keep
 
 
-def _opts(eta_far=0.0, eta_polar=0.0, nthreads=0):
-    return _Opts(eta_far, eta_polar, nthreads)
+def _opts(eta_far=0.0, eta_polar=0.0, nthreads=0, assume_resolved=False):
+    return _Opts(eta_far, eta_polar, nthreads, 1 if assume_resolved else 0)
 
 
-def volume_potential(tri, curved, circle, field, targets, eta_far=0.0, eta_polar=0.0, nthreads=0):
-    """V*(targets) = sum over triangles of int_T G(x - y) f(y) dy (exact up to quadrature ~1e-13)."""
+def volume_potential(tri, curved, circle, field, targets, eta_far=0.0, eta_polar=0.0, nthreads=0,
+                     assume_resolved=False):
+    """V*(targets) = sum over triangles of int_T G(x - y) f(y) dy (exact up to quadrature ~1e-13).
+    assume_resolved: far field by the own 12-point rule on every triangle (skip the resolution ladder); valid
+    only when resolve_rules() returns 0 for every triangle (checked on samples by the callers' tests)."""
     tri = np.ascontiguousarray(tri, np.float64)
     M = tri.shape[0]
     cur = np.ascontiguousarray(curved, np.int8) if curved is not None else None
@@ -108,16 +114,31 @@ def volume_potential(tri, curved, circle, field, targets, eta_far=0.0, eta_polar
     out = np.empty(tg.shape[0])
     F, keep = _field_struct(field)
     rc = lib().orc_volume_potential(M, _ptr(tri), _ptr(cur), _ptr(circ), ctypes.byref(F), tg.shape[0], _ptr(tg),
-                                    _ptr(out), ctypes.byref(_opts(eta_far, eta_polar, nthreads)))
+                                    _ptr(out), ctypes.byref(_opts(eta_far, eta_polar, nthreads, assume_resolved)))
     if rc != 0:
         raise RuntimeError(f"oracle failed rc={rc}")
     return out
 
 
 def workload_potential(w, target_idx=None, **kw):
-    """Oracle V* for a workloads.configs.Workload at targets[target_idx] (all if None)."""
+    """Oracle V* for a workloads.configs.Workload at targets[target_idx] (all if None).
+    Fourier fields (config 4) use assume_resolved (pinned by tests/test_oracle.py::test_fourier_field_resolved)."""
     tg = w.targets if target_idx is None else w.targets[target_idx]
+    if w.field["kind"] == "fourier":
+        kw.setdefault("assume_resolved", True)
     return volume_potential(w.tri, w.curved, w.circle, w.field, tg, **kw)
+
+
+def resolve_rules(tri, field, curved=None, circle=None):
+    """Per-triangle far-field rule the oracle's resolution ladder picks (0 = own 12-point rule)."""
+    tri = np.ascontiguousarray(tri, np.float64)
+    M = tri.shape[0]
+    cur = np.ascontiguousarray(curved, np.int8) if curved is not None else None
+    circ = np.ascontiguousarray(circle, np.float64) if circle is not None else None
+    out = np.empty(M, np.int32)
+    F, keep = _field_struct(field)
+    lib().orc_resolve_rules(M, _ptr(tri), _ptr(cur), _ptr(circ), ctypes.byref(F), _ptr(out))
+    return out
 
 
 def triangle_integral(tri3, field, target, curved=0, circle=None, eta_far=0.0, eta_polar=0.0):

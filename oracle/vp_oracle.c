@@ -428,6 +428,9 @@ typedef struct {
   double eta_far;    /* >= : own 12-point rule (default 6) */
   double eta_polar;  /* <  : polar rule (default 0.25) */
   int32_t nthreads;  /* 0 = OpenMP default */
+  int32_t assume_resolved; /* 1: skip the per-triangle resolution ladder (far field = own 12-point rule on every
+                              triangle).  Only for fields the 12-point rule resolves everywhere; the caller
+                              checks that claim with orc_resolve_rules on a sample (tests/test_oracle.py). */
 } orc_opts;
 
 static int duffy_n(double eta) {
@@ -524,11 +527,12 @@ static void init_all(const orc_field *F) {
 }
 
 static void opts_default(orc_opts *o, const orc_opts *in) {
-  o->eta_far = 6.0; o->eta_polar = 0.5; o->nthreads = 0;
+  o->eta_far = 6.0; o->eta_polar = 0.5; o->nthreads = 0; o->assume_resolved = 0;
   if (in) {
     if (in->eta_far > 0) o->eta_far = in->eta_far;
     if (in->eta_polar > 0) o->eta_polar = in->eta_polar;
     o->nthreads = in->nthreads;
+    o->assume_resolved = in->assume_resolved;
   }
 }
 
@@ -555,7 +559,7 @@ int orc_volume_potential(int64_t M, const double *tri, const int8_t *curved, con
     double rb = 0.0;
     for (int k = 0; k < 3; k++) { double r = hypot(t.v[k][0] - gx, t.v[k][1] - gy); if (r > rb) rb = r; }
     cen[4 * m] = gx; cen[4 * m + 1] = gy; cen[4 * m + 2] = rb + t.sag; cen[4 * m + 3] = t.diam;
-    nres[m] = resolve_rule(&t, F, gx, gy);
+    nres[m] = o.assume_resolved ? 0 : resolve_rule(&t, F, gx, gy);
   }
   off[0] = 0;
   for (int64_t m = 0; m < M; m++) off[m + 1] = off[m] + (nres[m] ? (int64_t)nres[m] * nres[m] : 12);

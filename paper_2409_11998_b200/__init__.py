@@ -36,7 +36,8 @@ class VpOpts(ctypes.Structure):
                 ("series_order", ctypes.c_int32), ("deriv_mode", ctypes.c_int32),
                 ("deriv_degree", ctypes.c_int32), ("deriv_k", ctypes.c_int32), ("parts", ctypes.c_int32),
                 ("targets_are_nodes", ctypes.c_int32), ("boundary", VpBoundary), ("cuda_stream", ctypes.c_void_p),
-                ("ref_nodes", ctypes.c_void_p), ("tri_max_aspect", ctypes.c_double)]
+                ("ref_nodes", ctypes.c_void_p), ("tri_max_aspect", ctypes.c_double), ("levels", ctypes.c_int32),
+                ("level_cmin", ctypes.c_double), ("level_rho", ctypes.c_double)]
 
 
 class VpInfo(ctypes.Structure):
@@ -50,10 +51,14 @@ class VpInfo(ctypes.Structure):
                 ("deriv_mode", ctypes.c_int32), ("deriv_degree", ctypes.c_int32), ("deriv_k", ctypes.c_int32),
                 ("n_boundary_targets", ctypes.c_int64), ("plan_ms", ctypes.c_double),
                 ("device_bytes", ctypes.c_int64), ("n_stencil_targets", ctypes.c_int64),
-                ("n_batches", ctypes.c_int64), ("horner_err", ctypes.c_double)]
+                ("n_batches", ctypes.c_int64), ("horner_err", ctypes.c_double), ("n_levels", ctypes.c_int32),
+                ("n_boxes", ctypes.c_int64), ("n_level_targets", ctypes.c_int64), ("n_band_pairs", ctypes.c_int64),
+                ("nf_band", ctypes.c_int64), ("level_targets", ctypes.c_int64 * 16)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["level_targets"] = list(self.level_targets)
+        return d
 
 
 _lib = None
@@ -119,7 +124,8 @@ class Plan:
 
     def __init__(self, tri_nodes, weights, targets, tol, *, C=0.0, delta2_over_delta1=0.0, delta1_override=0.0,
                  eps_nufft=0.0, series_order=0, deriv="auto", deriv_degree=0, deriv_k=0, parts=PART_ALL,
-                 targets_are_nodes=False, boundary=None, stream=None, ref_nodes=None, tri_max_aspect=0.0):
+                 targets_are_nodes=False, boundary=None, stream=None, ref_nodes=None, tri_max_aspect=0.0, levels=0,
+                 level_cmin=0.0, level_rho=0.0):
         import torch
         L = lib()
         tri_nodes = _dev_f64(tri_nodes)
@@ -147,6 +153,7 @@ class Plan:
                 raise ValueError("ref_nodes must be [p, 2]")
             o.ref_nodes = self._ref.ctypes.data
         o.tri_max_aspect = tri_max_aspect
+        o.levels, o.level_cmin, o.level_rho = levels, level_cmin, level_rho
         h = ctypes.c_void_p()
         _check(L.vp_plan(tri_nodes.data_ptr(), weights.data_ptr(), M, p, targets.data_ptr(), T, float(tol),
                          ctypes.byref(o), ctypes.byref(h)), "vp_plan")

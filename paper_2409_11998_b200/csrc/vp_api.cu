@@ -66,7 +66,7 @@ static double host_e1(double x) {  // exponential integral E1, x > 0 (series / c
   return h * exp(-x);
 }
 
-static double solve_e1(double eps) {  // z with E1(z) = eps
+double vp_solve_e1(double eps) {  // z with E1(z) = eps
   double z = log(1.0 / eps);
   for (int it = 0; it < 100; it++) {
     double f = host_e1(z) - eps;
@@ -78,7 +78,7 @@ static double solve_e1(double eps) {  // z with E1(z) = eps
   return z;
 }
 
-static int64_t next_smooth(int64_t n) {  // smallest even 2^a 3^b 5^c 7^d >= n
+int64_t vp_next_smooth(int64_t n) {  // smallest even 2^a 3^b 5^c 7^d >= n
   if (n < 2) n = 2;
   for (int64_t m = n + (n & 1);; m += 2) {
     int64_t r = m;
@@ -174,8 +174,8 @@ static void setup_grid(vp_plan_s *P, VpGrid &G, int kind, double L, double kmax)
   int64_t n = 2 * (int64_t)ceil(L * kmax / (2.0 * VP_PI));
   if (n < 4) n = 4;
   G.nmode = n;
-  G.nf = next_smooth(2 * n);
-  if (G.nf < 2 * P->w) G.nf = next_smooth(2 * P->w);
+  G.nf = vp_next_smooth(2 * n);
+  if (G.nf < 2 * P->w) G.nf = vp_next_smooth(2 * P->w);
   G.h = L / (double)G.nf;
   G.ox = P->cx - 0.5 * L;
   G.oy = P->cy - 0.5 * L;
@@ -190,6 +190,17 @@ static double es_transform(const vp_plan_s *P, double h, double k, const std::ve
   double alpha = P->w * h / 2.0, s = 0.0;
   for (size_t q = 0; q < gx.size(); q++) s += gw[q] * vp_es(gx[q], P->beta) * cos(k * alpha * gx[q]);
   return 2.0 * alpha * s;
+}
+
+// 1 / Phi(2 pi m / L)^2, m = 0..nhalf, for the ES kernel at spacing h (deconvolution table)
+void vp_es_deconv_table(const vp_plan_s *P, double h, double L, int64_t nhalf, std::vector<double> &out) {
+  std::vector<double> gx, gw;
+  gauss_legendre01(2 * P->w + 60, gx, gw);
+  out.resize(nhalf + 1);
+  for (int64_t m = 0; m <= nhalf; m++) {
+    double Phi = es_transform(P, h, 2.0 * VP_PI * m / L, gx, gw);
+    out[m] = 1.0 / (Phi * Phi);
+  }
 }
 
 // deconvolution tables: NH kernel psi_1 (one stage); FH kernel psi_1 * psi_2 (NH spread, then restriction)
@@ -336,13 +347,6 @@ static void make_fft_plans(vp_plan_s *P) {
   }
 }
 
-static void build_tiles(vp_plan_s *P, const double *nodes_dev, const double *weights_dev) {
-  VpTiles &Tl = P->tiles;
-  Tl.TS = 32;
-  Tl.ntx = (P->nh.nf + Tl.TS - 1) / Tl.TS;
-  Tl.nty = Tl.ntx;
-  vp_build_spread_order(P, nodes_dev, weights_dev);
-}
 
 __global__ void k_gather_f64(const double *__restrict__ src, const int32_t *__restrict__ perm, int64_t n,
                              double *__restrict__ dst) {
@@ -363,9 +367,13 @@ static void free_plan(vp_plan_s *P) {
       cufftDestroy(G->inv);
     }
   }
+  if (P->bands.has_plans) {
+    cufftDestroy(P->bands.fwd);
+    cufftDestroy(P->bands.inv);
+  }
   for (void *p : P->allocs) cudaFree(p);
   if (P->ev_init)
-    for (int i = 0; i < 9; i++) cudaEventDestroy(P->ev[i]);
+    for (int i = 0; i < 10; i++) cudaEventDestroy(P->ev[i]);
   delete P;
 }
 
@@ -431,7 +439,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     P->beta = 2.30 * P->w;
     P->kmax_nh = sqrt(lne / P->delta1);
     P->kmax_fh = sqrt(lne / P->delta2);
-    double zeps = solve_e1(P->eps);
+    double zeps = vp_solve_e1(P->eps);
     double m2 = sqrt(4.0 * P->delta2 * lne);
     // margins: the kernel decay and (>= w+4 fine cells) so that spreading never wraps
     double L_nh = P->S + std::max(sqrt(4.0 * P->delta2 * zeps), (P->w + 4) * (VP_PI / P->kmax_nh) / 2.0);
@@ -445,14 +453,21 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     setup_deconv(P);
     setup_restriction(P);
     // ---- sources and targets sorted by NH tile
-    build_tiles(P, tri_nodes, weights);
+    vp_build_spread_order(P, P->sp, tri_nodes, weights, nullptr, N, grid_args(P->nh));
     P->tx = vp_alloc<double>(P, T);
     P->ty = vp_alloc<double>(P, T);
     P->tperm = vp_alloc<int64_t>(P, T);
-    vp_sort_points(P, targets, T, P->nh.ox, P->nh.oy, P->tiles.TS * P->nh.h, P->tiles.ntx, P->tiles.nty, P->tx,
+    vp_sort_points(P, targets, T, P->nh.ox, P->nh.oy, P->sp.tiles.TS * P->nh.h, P->sp.tiles.ntx, P->sp.tiles.nty, P->tx,
                    P->ty, P->tperm, nullptr, nullptr);
-    // ---- local part
+    // ---- graded meshes: per-target levels and band boxes (a12)
     int parts = o.parts ? o.parts : VP_PART_ALL;
+    if (parts & VP_PART_LOCAL) {
+      vp_build_levels(P, tri_nodes, weights);
+    } else {
+      P->bands.tlev = vp_alloc<int8_t>(P, T);
+      VP_CUDA(cudaMemsetAsync(P->bands.tlev, 0, T, P->stream));
+    }
+    // ---- local part
     P->dmode = o.deriv_mode;
     if (P->dmode == VP_DERIV_AUTO) P->dmode = (o.ref_nodes && N > 10000000) ? VP_DERIV_TRIANGLE : VP_DERIV_KNN;
     if (P->dmode == VP_DERIV_TRIANGLE && (!o.ref_nodes || p < 10 || p > VP_TRI_MAXP || !o.targets_are_nodes))
@@ -504,7 +519,7 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
     P->n_ffts = 0;
     int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
     if (P->profiling && !P->ev_init) {
-      for (int i = 0; i < 9; i++) VP_CUDA(cudaEventCreate(&P->ev[i]));
+      for (int i = 0; i < 10; i++) VP_CUDA(cudaEventCreate(&P->ev[i]));
       P->ev_init = true;
     }
     record(P, 0);
@@ -512,7 +527,7 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
       VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, P->stream));
       VP_CUDA(cudaMemsetAsync(P->fh.data, 0, sizeof(double) * P->fh.nf * P->fh.row, P->stream));
       record(P, 1);
-      vp_launch_spread(P, f);
+      vp_launch_spread(P, P->sp, grid_args(P->nh), f);
       record(P, 2);
       vp_launch_restrict(P);
       record(P, 3);
@@ -533,7 +548,9 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
     }
     vp_launch_interp_local(P, f, out);
     record(P, 8);
-    P->n_phase = 8;
+    if (parts & VP_PART_LOCAL) vp_launch_bands(P, f, out);
+    record(P, 9);
+    P->n_phase = 9;
   } catch (VpError &e) {
     return e.s;
   }
@@ -592,9 +609,15 @@ extern "C" vp_status vp_get_info(vp_handle P, vp_info *I) {
   I->n_boundary_targets = P->n_bdry;
   I->plan_ms = P->plan_ms;
   I->n_stencil_targets = P->n_stencil;
-  I->n_batches = P->n_batches;
+  I->n_batches = P->sp.n_batches;
   I->horner_err = P->horner_err;
   I->device_bytes = P->device_bytes;
+  I->n_levels = P->bands.nlev;
+  I->n_boxes = P->bands.nbox;
+  I->n_level_targets = P->bands.n_lt;
+  I->n_band_pairs = P->bands.n_pairs;
+  I->nf_band = P->bands.nfb;
+  for (int i = 0; i < 16; i++) I->level_targets[i] = P->bands.lev_count[i];
   return VP_OK;
 }
 
@@ -604,19 +627,20 @@ extern "C" vp_status vp_set_profiling(vp_handle P, int32_t on) {
   return VP_OK;
 }
 
-static const char *g_phase_names[8] = {"zero", "spread", "restrict", "fft_fwd", "multiply", "fft_inv", "prolong", "interp_local"};
+static const char *g_phase_names[9] = {"zero",    "spread",  "restrict",     "fft_fwd", "multiply",
+                                       "fft_inv", "prolong", "interp_local", "bands"};
 
 extern "C" vp_status vp_get_phase_times(vp_handle P, double *ms, int32_t *n_out, const char **names) {
   if (!P || !ms || !n_out) return VP_ERR_ARG;
   if (!P->profiling || !P->ev_init) return VP_ERR_ARG;
-  if (cudaEventSynchronize(P->ev[8]) != cudaSuccess) return VP_ERR_CUDA;
-  for (int i = 0; i < 8; i++) {
+  if (cudaEventSynchronize(P->ev[9]) != cudaSuccess) return VP_ERR_CUDA;
+  for (int i = 0; i < 9; i++) {
     float t = 0.f;
     cudaEventElapsedTime(&t, P->ev[i], P->ev[i + 1]);
     ms[i] = t;
     if (names) names[i] = g_phase_names[i];
   }
-  *n_out = 8;
+  *n_out = 9;
   return VP_OK;
 }
 

@@ -63,11 +63,53 @@ struct VpGrid {
   bool has_plans = false;
 };
 
-struct VpTiles {          // sorted points binned into TS x TS tiles of the NH fine grid
+struct VpTiles {          // sorted points binned into TS x TS tiles of a fine grid
   int TS = 32;
   int64_t ntx = 0, nty = 0;
   int64_t nsub = 0;       // spreading sub-problems
-  int4 *sub = nullptr;    // (tile_x, tile_y, start, count)
+  int4 *sub = nullptr;    // (tile_x, tile_y, first batch, end batch)
+};
+
+// Grid description passed to kernels: point x sits at fractional cell (x - o) * inv_h of a periodic
+// nfx x nfy grid whose rows are `row` doubles apart.
+struct GridArgs {
+  double *data;
+  int64_t nfx, nfy, row;
+  double ox, oy, h, inv_h;
+};
+inline GridArgs grid_args(const VpGrid &G) { return GridArgs{G.data, G.nf, G.nf, G.row, G.ox, G.oy, G.h, 1.0 / G.h}; }
+
+// Points prepared for the atomic-free tile spreading kernel (vp_nufft.cu k_spread_nh): sorted by
+// (tile, row-rank level, row) into batches of <= 32 points with pairwise distinct footprint rows.
+struct VpSpreadSet {
+  double *sx = nullptr, *sy = nullptr, *sw = nullptr;  // coords (in the grid's frame), weights
+  int32_t *sperm = nullptr;                            // sorted -> user node index (f gather)
+  int32_t *bstart = nullptr;                           // batch starts (n_batches + 1)
+  int64_t n_batches = 0;
+  VpTiles tiles;
+};
+
+// Level-band corrections for graded meshes: per-target level
+// l(x) in 0..nlev, bands B_l (l = 1..l(x)) by box-local NUFFTs on one "virtual" grid of nbox boxes
+// (box b = rows [b nfb, (b+1) nfb)), V_L evaluated with delta_{l(x)} = delta_1 / 4^{l(x)}.
+struct VpBands {
+  int nlev = 0;                   // finest level present (0 = no bands)
+  int64_t nbox = 0, nfb = 0, rowb = 0, nmode = 0;
+  int margin = 0, core = 0;       // fine cells
+  double *grid = nullptr;         // nbox * nfb * rowb
+  int32_t *box_level = nullptr;   // [nbox]
+  double *lev_par = nullptr;      // [nlev + 1][4]: delta_l, delta_{l-1}, dk_l, scale_l
+  double *deconv = nullptr;       // [nmode/2 + 1] grid-unit 1/Phi^2
+  cufftHandle fwd = 0, inv = 0;
+  bool has_plans = false;
+  VpSpreadSet sp;
+  int64_t n_lt = 0, n_ent = 0;    // targets with level >= 1; (target, level) entries
+  int32_t *lt_t = nullptr;        // [n_lt] sorted target index
+  int32_t *lt_off = nullptr;      // [n_lt + 1]
+  double *ent_x = nullptr, *ent_y = nullptr;  // [n_ent] virtual-grid coordinates
+  int64_t n_pairs = 0;            // (box, source) pairs spread
+  int8_t *tlev = nullptr;         // [T] level per sorted target
+  int64_t lev_count[16] = {};     // targets per level
 };
 
 struct vp_plan_s {
@@ -85,11 +127,9 @@ struct vp_plan_s {
   VpHorner horner{};
   double horner_err = 0;
   // sources, sorted by (NH tile, row rank, row) into batches of <= 32 points with distinct rows
-  double *sx = nullptr, *sy = nullptr, *sw = nullptr;  // coords, weights
-  int32_t *sperm = nullptr;                            // sorted -> user node index
-  int32_t *bstart = nullptr;                           // batch starts (n_batches + 1)
-  int64_t n_batches = 0;
-  VpTiles tiles;                                       // tiles.sub: warp work items (tx, ty, b0, b1)
+  VpSpreadSet sp;
+  // graded-mesh level bands (a12)
+  VpBands bands;
   // FH <- NH restriction tables
   int32_t *r_lo = nullptr, *t_lo = nullptr;
   double *r_w = nullptr, *t_w = nullptr;
@@ -139,11 +179,17 @@ T *vp_alloc(vp_plan_s *P, size_t n) {
 
 // ---------------------------------------------------------------------------------------------
 // launch helpers (defined in the .cu files)
-void vp_launch_spread(vp_plan_s *P, const double *f);
+void vp_launch_spread(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *f);
+void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const double *w, const int32_t *node_of,
+                           int64_t n, const GridArgs &g);
+void vp_build_levels(vp_plan_s *P, const double *nodes, const double *weights);
+void vp_launch_bands(vp_plan_s *P, const double *f, double *out);
+double vp_solve_e1(double eps);
+int64_t vp_next_smooth(int64_t n);
+void vp_es_deconv_table(const vp_plan_s *P, double h, double L, int64_t nhalf, std::vector<double> &out);
 void vp_upload_horner(int W, const VpHorner &h);
 void vp_launch_restrict(vp_plan_s *P);
 void vp_launch_prolong(vp_plan_s *P);
-void vp_build_spread_order(vp_plan_s *P, const double *nodes, const double *weights);
 void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out);
 void vp_build_local(vp_plan_s *P, const double *nodes_dev);

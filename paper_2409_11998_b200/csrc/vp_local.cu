@@ -35,11 +35,13 @@ struct LocalArgs {
   int64_t node_targets;           // targets with user index < node_targets are the nodes themselves
   double delta;
   vp_boundary bd;
-  int32_t *lidx;
+  int32_t *lidx;                  // stencils, k-major: entry k of slot s at [k * stride + s]
   double *lw, *lalpha;
+  int64_t slot0, stride;          // global slot of list entry 0; number of stencil slots
   int32_t *lnode;
   int32_t *is_bdry;
   double *scratch;                // per-thread LSQ scratch: K*nc + K doubles
+  const int8_t *tlev;             // [T] band level of the sorted target: V_L uses delta / 4^level
 };
 
 __device__ void heap_sift_down(double *d, int32_t *id, int n, int i) {
@@ -143,11 +145,12 @@ __global__ void k_build_local(LocalArgs a) {
   // ---- geometry coefficients of V_L in the Taylor basis
   double coef[VP_NTAYLOR];
   bool bdry = false;
+  const double delta = a.tlev ? a.delta * pow(0.25, (double)a.tlev[t]) : a.delta;
   if (a.bd.kind == VP_BDRY_CIRCLE)
-    bdry = vp_coef_circle(x, y, a.bd.p[0], a.bd.p[1], a.bd.p[2], a.delta, a.nterms, a.deg, coef);
+    bdry = vp_coef_circle(x, y, a.bd.p[0], a.bd.p[1], a.bd.p[2], delta, a.nterms, a.deg, coef);
   else if (a.bd.kind == VP_BDRY_RECT)
-    bdry = vp_coef_rect(x, y, a.bd.p[0], a.bd.p[1], a.bd.p[2], a.bd.p[3], a.delta, a.deg, coef);
-  if (!bdry) vp_coef_interior(a.delta, a.nterms, a.deg, coef);
+    bdry = vp_coef_rect(x, y, a.bd.p[0], a.bd.p[1], a.bd.p[2], a.bd.p[3], delta, a.deg, coef);
+  if (!bdry) vp_coef_interior(delta, a.nterms, a.deg, coef);
   a.is_bdry[t] = bdry ? 1 : 0;
   double alpha = 0.0;
   int32_t node = a.tperm[t] < a.node_targets ? (int32_t)a.tperm[t] : -1;
@@ -183,11 +186,10 @@ __global__ void k_build_local(LocalArgs a) {
       for (int i = j; i < K; i++) yv[i] -= s * v[i];
     }
   }
-  int32_t *op = a.lidx + slot * (int64_t)K;
-  double *ow = a.lw + slot * (int64_t)K;
+  const int64_t gs = a.slot0 + slot;
   for (int k = 0; k < K; k++) {
-    op[k] = a.kperm[hi[k]];
-    ow[k] = yv[k];
+    a.lidx[k * a.stride + gs] = a.kperm[hi[k]];
+    a.lw[k * a.stride + gs] = yv[k];
   }
   a.lalpha[t] = alpha;
   a.lnode[t] = node;
@@ -309,11 +311,11 @@ void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop) {
 // per sorted target: triangle mode (interior node of an ok triangle) or stencil
 __global__ void k_target_mode(const double *tx, const double *ty, const int64_t *tperm, int64_t T, int p,
                               const int8_t *tri_ok, int64_t node_targets, vp_boundary bd, double delta, double c1,
-                              int32_t *need, double *lalpha, int32_t *lnode) {
+                              const int8_t *tlev, int32_t *need, double *lalpha, int32_t *lnode) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= T) return;
   int nd = tperm[t] < node_targets ? (int)tperm[t] : -1;
-  bool tri = nd >= 0 && tri_ok && tri_ok[nd / p];
+  bool tri = nd >= 0 && tri_ok && tri_ok[nd / p] && !(tlev && tlev[t] > 0);
   if (tri && bd.kind != VP_BDRY_NONE) {
     double coef[VP_NTAYLOR];
     double x = tx[t], y = ty[t];
@@ -390,12 +392,12 @@ void vp_build_local(vp_plan_s *P, const double *nodes_dev) {
     VP_CUDA(cudaMemcpy(P->tri_H, Hop.data(), sizeof(double) * Hop.size(), cudaMemcpyHostToDevice));
     double c1 = P->delta1;
     k_target_mode<<<tb_t, 256, 0, st>>>(P->tx, P->ty, P->tperm, P->T, p, P->tri_ok, P->opts.targets_are_nodes ? P->N : 0,
-                                       P->opts.boundary, P->delta1, c1, need, P->lalpha, P->lnode);
+                                       P->opts.boundary, P->delta1, c1, P->bands.tlev, need, P->lalpha, P->lnode);
     VP_CHECK_LAUNCH();
     P->tri_c2 = nterms >= 2 ? 0.5 * P->delta1 * P->delta1 : 0.0;
   } else {
     k_target_mode<<<tb_t, 256, 0, st>>>(P->tx, P->ty, P->tperm, P->T, 1, nullptr, 0, P->opts.boundary, P->delta1, 0.0,
-                                       need, P->lalpha, P->lnode);
+                                       P->bands.tlev, need, P->lalpha, P->lnode);
     VP_CHECK_LAUNCH();
   }
   // compact the stencil targets
@@ -453,9 +455,10 @@ void vp_build_local(vp_plan_s *P, const double *nodes_dev) {
       a.node_targets = P->opts.targets_are_nodes ? P->N : 0;
       a.delta = P->delta1;
       a.bd = P->opts.boundary;
-      a.lidx = P->lidx + s0 * K; a.lw = P->lw + s0 * K; a.lalpha = P->lalpha; a.lnode = P->lnode;
+      a.lidx = P->lidx; a.lw = P->lw; a.slot0 = s0; a.stride = nst; a.lalpha = P->lalpha; a.lnode = P->lnode;
       a.is_bdry = isb;
       a.scratch = scratch;
+      a.tlev = P->bands.tlev;
       k_build_local<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(a);
       VP_CHECK_LAUNCH();
     }

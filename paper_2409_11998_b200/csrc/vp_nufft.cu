@@ -21,12 +21,6 @@
 #include "vp_common.cuh"
 #include "vp_math.cuh"
 
-struct GridArgs {
-  double *data;
-  int64_t nf, row;
-  double ox, oy, h, inv_h;
-};
-static GridArgs grid_args(const VpGrid &G) { return GridArgs{G.data, G.nf, G.row, G.ox, G.oy, G.h, 1.0 / G.h}; }
 
 // fractional grid coordinate of x (identical expression in binning, spreading and interpolation)
 __device__ __forceinline__ double gcoord(double x, double o, double inv_h) { return (x - o) * inv_h; }
@@ -87,13 +81,21 @@ __global__ void k_tile_heads(const uint64_t *__restrict__ k1, int64_t n, int32_t
 // Greedy level assignment, one thread per non-empty tile: points in (row, column) order; a point
 // takes the lowest level whose last point in the same row ends at least W columns to its left.
 // Points of one level therefore never write the same grid cell within a footprint-row step.
+// Inside a level, points are then ordered rank-major over the shared-memory bank slot of their
+// footprint origin (res = (row * nw + col) mod 16, 16 slots of 8 B per 128 B wavefront): a chunk of
+// 32 consecutive points holds at most 2 points per slot when the slots are evenly populated, so the
+// row-step LDS/STS of a batch need ~2 wavefronts instead of the ~4-5 of random columns.
 #define VP_MAXLV 128
+#define VP_RANKLV 24
 __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restrict__ tstart, int64_t ntile,
-                         int64_t n, int W, uint64_t *__restrict__ k2) {
+                         int64_t n, int W, int nw, uint64_t *__restrict__ k2) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= ntile) return;
   int64_t s0 = tstart[t], s1 = (t + 1 < ntile) ? tstart[t + 1] : n;
   int16_t last[VP_MAXLV];
+  uint16_t rank[VP_RANKLV][16];
+  for (int l = 0; l < VP_RANKLV; l++)
+    for (int r = 0; r < 16; r++) rank[l][r] = 0;
   int cur_row = -1, nlv = 0, overflow = 0;
   for (int64_t i = s0; i < s1; i++) {
     uint64_t key = k1[i];
@@ -111,8 +113,15 @@ __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restr
       else lv = VP_MAXLV + overflow++;
     }
     if (lv < VP_MAXLV) last[lv] = (int16_t)col;
+    if (lv > 4095) lv = 4095;
+    const int res = (row * nw + col) & 15;
+    int rk = 0;
+    if (lv < VP_RANKLV) {
+      rk = rank[lv][res]++;
+      if (rk > 4095) rk = 4095;
+    }
     uint64_t tile = key >> 32;
-    k2[i] = (tile << 40) | ((uint64_t)lv << 16) | ((uint64_t)row << 8) | (uint64_t)(col & 0xff);
+    k2[i] = (tile << 40) | ((uint64_t)lv << 28) | ((uint64_t)rk << 16) | ((uint64_t)res << 12);
   }
 }
 
@@ -120,15 +129,15 @@ __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restr
 __global__ void k_batch_heads(const uint64_t *__restrict__ k2, int64_t n, int32_t *__restrict__ head) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint64_t grp = k2[i] >> 16;
+  uint64_t grp = k2[i] >> 28;
   int h = 0;
-  if (i == 0 || (k2[i - 1] >> 16) != grp) {
+  if (i == 0 || (k2[i - 1] >> 28) != grp) {
     h = 1;
   } else {
     int64_t lo = 0, hi = i;
     while (lo < hi) {
       int64_t mid = (lo + hi) >> 1;
-      if ((k2[mid] >> 16) < grp) lo = mid + 1; else hi = mid;
+      if ((k2[mid] >> 28) < grp) lo = mid + 1; else hi = mid;
     }
     h = ((i - lo) % 32) == 0;
   }
@@ -176,15 +185,15 @@ __global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items
     }
   }
   __syncwarp();
-  const bool interior = ox >= 0 && oy >= 0 && ox + nw <= g.nf && oy + nw <= g.nf;
+  const bool interior = ox >= 0 && oy >= 0 && ox + nw <= g.nfx && oy + nw <= g.nfy;
   for (int rr = 0; rr < nw; rr++) {
     for (int cc = lane; cc < nw; cc += 32) {
       double v = tile[rr * nw + cc];
       if (v != 0.0) {
         int64_t gx = ox + cc, gy = oy + rr;
         if (!interior) {
-          gx = wrapi(gx, g.nf);
-          gy = wrapi(gy, g.nf);
+          gx = wrapi(gx, g.nfx);
+          gy = wrapi(gy, g.nfy);
         }
         atomicAdd(g.data + gy * g.row + gx, v);
       }
@@ -193,21 +202,21 @@ __global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items
 }
 
 template <int W>
-static void launch_spread_w(vp_plan_s *P, const double *f) {
+static void launch_spread_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *f) {
   constexpr int D = VP_HORNER_DEG(W);
-  int nw = P->tiles.TS + W + 3;
+  int nw = S.tiles.TS + W + 3;
   size_t sm = sizeof(double) * (size_t)nw * nw;
-  if (P->tiles.nsub == 0) return;
-  k_spread_nh<W, D><<<(unsigned)P->tiles.nsub, 32, sm, P->stream>>>(P->tiles.sub, P->bstart, P->sx, P->sy, P->sw,
-                                                                    P->sperm, f, grid_args(P->nh), P->tiles.TS);
+  if (S.tiles.nsub == 0) return;
+  k_spread_nh<W, D><<<(unsigned)S.tiles.nsub, 32, sm, P->stream>>>(S.tiles.sub, S.bstart, S.sx, S.sy, S.sw, S.sperm,
+                                                                   f, g, S.tiles.TS);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
 
-void vp_launch_spread(vp_plan_s *P, const double *f) {
+void vp_launch_spread(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *f) {
   switch (P->w) {
 #define CASE(W) \
-  case W: launch_spread_w<W>(P, f); break;
+  case W: launch_spread_w<W>(P, S, g, f); break;
     CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
     default: throw VpError{VP_ERR_UNSUPPORTED};
@@ -370,7 +379,7 @@ __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__
                                                       const double *__restrict__ f, const double *__restrict__ lalpha,
                                                       const int32_t *__restrict__ lnode,
                                                       const int32_t *__restrict__ lidx, const double *__restrict__ lw,
-                                                      int K, int do_local, const int32_t *__restrict__ lptr,
+                                                      int K, int64_t n_sten, int do_local, const int32_t *__restrict__ lptr,
                                                       const double *__restrict__ tri_M,
                                                       const double *__restrict__ tri_H, int p, double tri_c2,
                                                       double *__restrict__ out) {
@@ -381,7 +390,7 @@ __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__
     double wx[W], wy[W];
     int ix = es_horner<W, D>(gcoord(tx[t], g.ox, g.inv_h), wx);
     int iy = es_horner<W, D>(gcoord(ty[t], g.oy, g.inv_h), wy);
-    bool inside = ix >= 0 && iy >= 0 && ix + W <= g.nf && iy + W <= g.nf;
+    bool inside = ix >= 0 && iy >= 0 && ix + W <= g.nfx && iy + W <= g.nfy;
 #pragma unroll
     for (int b = 0; b < W; b++) {
       double racc = 0.0;
@@ -390,9 +399,9 @@ __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__
 #pragma unroll
         for (int a = 0; a < W; a++) racc = fma(wx[a], __ldg(rp + a), racc);
       } else {
-        int64_t yy = wrapi(iy + b, g.nf);
+        int64_t yy = wrapi(iy + b, g.nfy);
 #pragma unroll
-        for (int a = 0; a < W; a++) racc = fma(wx[a], __ldg(g.data + yy * g.row + wrapi(ix + a, g.nf)), racc);
+        for (int a = 0; a < W; a++) racc = fma(wx[a], __ldg(g.data + yy * g.row + wrapi(ix + a, g.nfx)), racc);
       }
       v = fma(wy[b], racc, v);
     }
@@ -403,9 +412,10 @@ __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__
     if (nd >= 0) vl = lalpha[t] * __ldg(f + nd);
     const int32_t sp = lptr[t];
     if (sp >= 0) {  // least-squares stencil
-      const int32_t *ip = lidx + sp * (int64_t)K;
-      const double *wp = lw + sp * (int64_t)K;
-      for (int k = 0; k < K; k++) vl = fma(wp[k], __ldg(f + ip[k]), vl);
+      // k-major stencil layout: consecutive targets (lanes) read consecutive slots -> coalesced
+      const int32_t *ip = lidx + sp;
+      const double *wp = lw + sp;
+      for (int k = 0; k < K; k++) vl = fma(__ldcs(wp + k * n_sten), __ldg(f + __ldcs(ip + k * n_sten)), vl);
     } else if (tri_c2 != 0.0) {  // own-triangle cubic fit: Lap f = M11 f_11 + 2 M12 f_12 + M22 f_22
       const int64_t tri = nd / p;
       const int kk = nd - (int)tri * p;
@@ -432,7 +442,7 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
   if (!blocks) return;
   k_interp_local<W, D><<<blocks, 256, 0, P->stream>>>(P->tx, P->ty, P->tperm, P->T, grid_args(P->nh),
                                                       (parts & VP_PART_HISTORY) ? 1 : 0, f, P->lalpha, P->lnode,
-                                                      P->lidx, P->lw, P->K, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr,
+                                                      P->lidx, P->lw, P->K, P->n_stencil, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr,
                                                       P->tri_M, P->tri_H, P->p, P->tri_c2, out);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
@@ -451,21 +461,32 @@ void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out) {
 // ---------------------------------------------------------------------------------------------
 // plan-time: sort sources into row-rank batches and build the per-warp work items
 __global__ void k_gather_src(const double *__restrict__ xy, const double *__restrict__ w, const int32_t *__restrict__ idx,
-                             int64_t n, double *__restrict__ xs, double *__restrict__ ys, double *__restrict__ ws,
-                             int32_t *__restrict__ perm) {
+                             const int32_t *__restrict__ node_of, int64_t n, double *__restrict__ xs,
+                             double *__restrict__ ys, double *__restrict__ ws, int32_t *__restrict__ perm) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   int32_t j = idx[i];
   xs[i] = xy[2 * (int64_t)j];
   ys[i] = xy[2 * (int64_t)j + 1];
   ws[i] = w[j];
-  perm[i] = j;
+  perm[i] = node_of ? node_of[j] : j;
 }
 
-void vp_build_spread_order(vp_plan_s *P, const double *nodes, const double *weights) {
+// Sort n points (xy interleaved, in the frame of grid g) into the batch order of k_spread_nh.
+// node_of (optional) maps a point to the user node whose f it carries.
+void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const double *weights,
+                           const int32_t *node_of, int64_t n, const GridArgs &g) {
   cudaStream_t s = P->stream;
-  const int64_t n = P->N;
-  VpTiles &Tl = P->tiles;
+  VpTiles &Tl = S.tiles;
+  Tl.TS = 32;
+  Tl.ntx = (g.nfx + Tl.TS - 1) / Tl.TS;
+  Tl.nty = (g.nfy + Tl.TS - 1) / Tl.TS;
+  if (n == 0) {
+    S.sx = vp_alloc<double>(P, 1); S.sy = vp_alloc<double>(P, 1); S.sw = vp_alloc<double>(P, 1);
+    S.sperm = vp_alloc<int32_t>(P, 1); S.bstart = vp_alloc<int32_t>(P, 1);
+    S.n_batches = 0; Tl.nsub = 0; Tl.sub = vp_alloc<int4>(P, 1);
+    return;
+  }
   uint64_t *k1, *k1s, *k2, *k2s;
   int32_t *i1, *i1s, *i2s, *head;
   VP_CUDA(cudaMallocAsync(&k1, 8 * (n + 1), s));
@@ -477,7 +498,7 @@ void vp_build_spread_order(vp_plan_s *P, const double *nodes, const double *weig
   VP_CUDA(cudaMallocAsync(&i2s, 4 * (n + 1), s));
   VP_CUDA(cudaMallocAsync(&head, 4 * (n + 1), s));
   unsigned nb = (unsigned)((n + 255) / 256);
-  k_spread_keys<<<nb, 256, 0, s>>>(nodes, n, grid_args(P->nh), Tl.TS, P->w, Tl.ntx, Tl.nty, k1, i1);
+  k_spread_keys<<<nb, 256, 0, s>>>(xy, n, g, Tl.TS, P->w, Tl.ntx, Tl.nty, k1, i1);
   VP_CHECK_LAUNCH();
   size_t tb = 0, tb2 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s);
@@ -501,18 +522,18 @@ void vp_build_spread_order(vp_plan_s *P, const double *nodes, const double *weig
     int32_t nt = 0;
     VP_CUDA(cudaMemcpyAsync(&nt, d_nt, 4, cudaMemcpyDeviceToHost, s));
     VP_CUDA(cudaStreamSynchronize(s));
-    k_levels<<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(k1s, tst, nt, n, P->w, k2);
+    k_levels<<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(k1s, tst, nt, n, P->w, Tl.TS + P->w + 3, k2);
     VP_CHECK_LAUNCH();
     for (void *p : {(void *)tst, (void *)d_nt, tmp3}) VP_CUDA(cudaFreeAsync(p, s));
   }
   VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
   k_batch_heads<<<nb, 256, 0, s>>>(k2s, n, head);
   VP_CHECK_LAUNCH();
-  P->sx = vp_alloc<double>(P, n);
-  P->sy = vp_alloc<double>(P, n);
-  P->sw = vp_alloc<double>(P, n);
-  P->sperm = vp_alloc<int32_t>(P, n);
-  k_gather_src<<<nb, 256, 0, s>>>(nodes, weights, i2s, n, P->sx, P->sy, P->sw, P->sperm);
+  S.sx = vp_alloc<double>(P, n);
+  S.sy = vp_alloc<double>(P, n);
+  S.sw = vp_alloc<double>(P, n);
+  S.sperm = vp_alloc<int32_t>(P, n);
+  k_gather_src<<<nb, 256, 0, s>>>(xy, weights, i2s, node_of, n, S.sx, S.sy, S.sw, S.sperm);
   VP_CHECK_LAUNCH();
   // host: batches and work items
   std::vector<uint64_t> hk(n);
@@ -537,9 +558,9 @@ void vp_build_spread_order(vp_plan_s *P, const double *nodes, const double *weig
     items.push_back(make_int4((int)(t % Tl.ntx), (int)(t / Tl.ntx), (int)b, (int)e));
     b = e;
   }
-  P->n_batches = nbat;
-  P->bstart = vp_alloc<int32_t>(P, bst.size());
-  VP_CUDA(cudaMemcpy(P->bstart, bst.data(), 4 * bst.size(), cudaMemcpyHostToDevice));
+  S.n_batches = nbat;
+  S.bstart = vp_alloc<int32_t>(P, bst.size());
+  VP_CUDA(cudaMemcpy(S.bstart, bst.data(), 4 * bst.size(), cudaMemcpyHostToDevice));
   Tl.nsub = (int64_t)items.size();
   Tl.sub = vp_alloc<int4>(P, items.size());
   if (!items.empty()) VP_CUDA(cudaMemcpy(Tl.sub, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
@@ -626,4 +647,90 @@ int64_t vp_sort_points(vp_plan_s *P, const double *xy, int64_t n, double ox, dou
   VP_CUDA(cudaFreeAsync(idx2, s));
   VP_CUDA(cudaFreeAsync(counts, s));
   return nb;
+}
+
+// ---------------------------------------------------------------------------------------------
+// level bands (a12; plan in vp_levels.cu): multiply every box's half spectrum by its level's band
+// multiplier (e^{-k^2 delta_l} - e^{-k^2 delta_{l-1}})/k^2, grid-unit deconvolution, scale 1/(h_l^2 nfb^2)
+__global__ void k_multiply_bands(double *__restrict__ data, int64_t nbox, int64_t nf, int64_t row, int64_t half_modes,
+                                 const int32_t *__restrict__ box_level, const double *__restrict__ lev_par,
+                                 const double *__restrict__ deconv) {
+  const int64_t ncol = nf / 2 + 1;
+  const int64_t per = nf * ncol, total = nbox * per;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = id / per, rem = id - b * per;
+    int64_t r = rem / ncol, c = rem - r * ncol;
+    int64_t m2 = r <= nf / 2 ? r : r - nf, a2 = m2 < 0 ? -m2 : m2;
+    double *z = data + (b * nf + r) * row + 2 * c;
+    if (c > half_modes || a2 > half_modes) {
+      z[0] = 0.0;
+      z[1] = 0.0;
+      continue;
+    }
+    const double *lp = lev_par + 4 * box_level[b];
+    double k2 = lp[2] * lp[2] * ((double)c * c + (double)m2 * m2);
+    double fac = vp_mult_nh(k2, lp[0], lp[1]) * lp[3] * deconv[c] * deconv[a2];
+    z[0] *= fac;
+    z[1] *= fac;
+  }
+}
+
+// bands at their targets: out[user(t)] += sum over the target's levels of the box interpolant
+template <int W, int D>
+__global__ void __launch_bounds__(256) k_interp_bands(const int32_t *__restrict__ lt_t,
+                                                      const int32_t *__restrict__ lt_off, int64_t n_lt,
+                                                      const double *__restrict__ ex, const double *__restrict__ ey,
+                                                      GridArgs g, const int64_t *__restrict__ tperm,
+                                                      double *__restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_lt) return;
+  double v = 0.0;
+  for (int32_t e = lt_off[i]; e < lt_off[i + 1]; e++) {
+    double wx[W], wy[W];
+    int ix = es_horner<W, D>(ex[e], wx);
+    int iy = es_horner<W, D>(ey[e], wy);
+#pragma unroll
+    for (int b = 0; b < W; b++) {
+      const double *rp = g.data + (int64_t)(iy + b) * g.row + ix;
+      double racc = 0.0;
+#pragma unroll
+      for (int a = 0; a < W; a++) racc = fma(wx[a], __ldg(rp + a), racc);
+      v = fma(wy[b], racc, v);
+    }
+  }
+  out[tperm[lt_t[i]]] += v;
+}
+
+template <int W>
+static void launch_interp_bands_w(vp_plan_s *P, const GridArgs &g, double *out) {
+  constexpr int D = VP_HORNER_DEG(W);
+  VpBands &B = P->bands;
+  k_interp_bands<W, D><<<(unsigned)((B.n_lt + 255) / 256), 256, 0, P->stream>>>(B.lt_t, B.lt_off, B.n_lt, B.ent_x,
+                                                                               B.ent_y, g, P->tperm, out);
+  VP_CHECK_LAUNCH();
+  P->n_kernels++;
+}
+
+void vp_launch_bands(vp_plan_s *P, const double *f, double *out) {
+  VpBands &B = P->bands;
+  if (B.nlev == 0 || B.nbox == 0) return;
+  GridArgs g{B.grid, B.nfb, B.nbox * B.nfb, B.rowb, 0.0, 0.0, 1.0, 1.0};
+  VP_CUDA(cudaMemsetAsync(B.grid, 0, sizeof(double) * B.nbox * B.nfb * B.rowb, P->stream));
+  vp_launch_spread(P, B.sp, g, f);
+  VP_CUFFT(cufftExecD2Z(B.fwd, B.grid, (cufftDoubleComplex *)B.grid));
+  int64_t total = B.nbox * B.nfb * (B.nfb / 2 + 1);
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_multiply_bands<<<blocks, 256, 0, P->stream>>>(B.grid, B.nbox, B.nfb, B.rowb, B.nmode / 2, B.box_level, B.lev_par,
+                                                  B.deconv);
+  VP_CHECK_LAUNCH();
+  P->n_kernels++;
+  VP_CUFFT(cufftExecZ2D(B.inv, (cufftDoubleComplex *)B.grid, B.grid));
+  P->n_ffts += 2;
+  switch (P->w) {
+#define CASE(W) \
+  case W: launch_interp_bands_w<W>(P, g, out); break;
+    CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+    default: throw VpError{VP_ERR_UNSUPPORTED};
+  }
 }

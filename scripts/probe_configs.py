@@ -7,7 +7,7 @@ import oracle
 import paper_2409_11998_b200 as vp
 from workloads import configs, rule
 
-def run(w, modes=("knn", "triangle"), ntg=48, seed=3):
+def run(w, modes=("knn", "triangle"), ntg=48, seed=3, levels=(0,)):
     dev = "cuda"
     nodes = torch.from_numpy(np.ascontiguousarray(w.nodes)).to(dev)
     wts = torch.from_numpy(w.weights).to(dev)
@@ -20,10 +20,10 @@ def run(w, modes=("knn", "triangle"), ntg=48, seed=3):
     ref = oracle.workload_potential(w, idx)
     t_or = time.time() - t0
     out = {"name": w.name, "M": w.M, "N": w.N, "T": w.T, "oracle_s": t_or, "n_idx": len(idx)}
-    for m in modes:
+    for m, lev in [(m, l) for m in modes for l in levels]:
         t0 = time.time()
         plan = vp.Plan(nodes, wts, tg, w.tol, boundary=w.boundary, targets_are_nodes=True, deriv=m,
-                       ref_nodes=rule.BARY[:, 1:3])
+                       ref_nodes=rule.BARY[:, 1:3], levels=lev)
         torch.cuda.synchronize()
         tp = time.time() - t0
         plan.set_profiling(True)
@@ -36,8 +36,11 @@ def run(w, modes=("knn", "triangle"), ntg=48, seed=3):
             sel = idx >= w.N
             eo = float(np.sqrt(np.sum((V[idx][sel] - ref[sel]) ** 2) / np.sum(ref[sel] ** 2)))
         inf = plan.info()
-        out[m] = {"rel_l2": e, "rel_l2_offnode": eo, "plan_s": tp, "eval_ms": sum(ph.values()), "phases": ph,
-                  "n_stencil": inf["n_stencil_targets"], "nf_nh": inf["nf_nh"], "mem_GB": inf["device_bytes"] / 1e9}
+        out[f"{m}_lev{lev}"] = {"rel_l2": e, "rel_l2_offnode": eo, "plan_s": tp, "eval_ms": sum(ph.values()),
+                                "phases": ph, "n_stencil": inf["n_stencil_targets"], "nf_nh": inf["nf_nh"],
+                                "mem_GB": inf["device_bytes"] / 1e9, "levels": inf["n_levels"],
+                                "level_targets": inf["level_targets"][:8], "boxes": inf["n_boxes"]}
+        print(json.dumps(out[f"{m}_lev{lev}"]), flush=True)
         plan.destroy()
         del plan
         torch.cuda.empty_cache()
@@ -50,6 +53,12 @@ if __name__ == "__main__":
     elif which == "c5s":
         run(configs.config5(M_target=int(float(sys.argv[2])), lmin=int(sys.argv[3]), lmax=int(sys.argv[4]), n_random=100000))
     elif which == "c5":
-        run(configs.config5(), modes=("triangle",), ntg=16)
+        t0 = time.time()
+        w = configs.config5()
+        print("c5 generated", w.M, w.N, w.T, time.time() - t0, flush=True)
+        run(w, modes=("triangle",), ntg=48, levels=(-1, 0))
     elif which == "c4":
-        run(configs.config4(), modes=("triangle",), ntg=16)
+        t0 = time.time()
+        w = configs.config4()
+        print("c4 generated", w.M, w.N, time.time() - t0, flush=True)
+        run(w, modes=("triangle",), ntg=48)

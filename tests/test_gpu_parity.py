@@ -140,3 +140,40 @@ def test_off_node_targets():
     e = rel_l2(V[idx], ref)
     print("off-node rel l2", e)
     assert e < 1e-5
+
+
+# ------------------------------------------------------------------------------------ graded meshes (a12)
+def _near_source_idx(w, n, seed):
+    d = np.hypot(w.targets[:, 0] - 0.3, w.targets[:, 1] + 0.2)
+    near = np.nonzero(d < 6e-3)[0]
+    return near[configs.sample_targets(near.size, n, seed=seed)]
+
+
+def test_config3_small_levels():
+    """Scaled-down config 3 (graded star, nonconforming patches): the level bands make the parity bar reachable;
+    one global delta_1 does not (R15)."""
+    w = configs.config3(M_target=60000, lmin=7, lmax=13, g=0.1)
+    idx = np.unique(np.concatenate([configs.sample_targets(w.T, 512, seed=33), _near_source_idx(w, 256, 34)]))
+    ref = oracle.workload_potential(w, idx)
+    plan, fd = make_plan(w)
+    info = plan.info()
+    V = plan.eval(fd).cpu().numpy()
+    e = rel_l2(V[idx], ref)
+    print("config3 small levels", info["n_levels"], info["level_targets"][:8], "rel l2", e)
+    assert info["n_levels"] >= 3
+    assert e <= 10 * w.tol
+    plan0, _ = make_plan(w, levels=-1)
+    e0 = rel_l2(plan0.eval(fd).cpu().numpy()[idx], ref)
+    print("config3 small, global delta only:", e0)
+    assert e0 > 100 * e
+
+
+def test_config3_full_size_sampled():
+    w = configs.config3()
+    idx = np.unique(np.concatenate([configs.sample_targets(w.T, 256, seed=35), _near_source_idx(w, 64, 36)]))
+    ref = oracle.workload_potential(w, idx)
+    plan, fd = make_plan(w)
+    V = plan.eval(fd).cpu().numpy()
+    e = rel_l2(V[idx], ref)
+    print("config3 full rel l2", e, plan.info()["n_levels"], plan.info()["level_targets"][:8])
+    assert e <= 10 * w.tol

@@ -227,3 +227,20 @@ def test_oracle_own_nodes_match_generator():
     n, wt = oracle.rule12_nodes(w.tri, w.curved, w.circle)
     assert np.max(np.abs(n - w.nodes)) < 1e-14
     assert np.max(np.abs(wt - w.weights)) < 1e-15
+
+
+def test_fourier_field_resolved():
+    """Config 4's Fourier field (|k| <= 64) is resolved by the 12-point rule on its 1414^2-cell mesh: on a patch of
+    that mesh the far field by the own 12-point rule (assume_resolved, the fast path oracle.workload_potential
+    uses for Fourier fields) agrees with the oracle's full resolution ladder (Duffy up to 30 x 30 per triangle)."""
+    from workloads import configs, fields
+    rng = np.random.default_rng(4)
+    tri = configs.square_grid(1414)
+    fld = fields.random_fourier(rng, 64)
+    c = tri.mean(1)
+    patch = tri[(c[:, 0] > 0.5) & (c[:, 0] < 0.52) & (c[:, 1] > 0.5) & (c[:, 1] < 0.52)]
+    assert patch.shape[0] > 500
+    tg = np.array([[0.5101, 0.5137], [0.6, 0.45], [0.53, 0.515]])
+    a = oracle.volume_potential(patch, None, None, fld, tg)
+    b = oracle.volume_potential(patch, None, None, fld, tg, assume_resolved=True)
+    assert np.max(np.abs(a - b)) < 1e-12 * np.max(np.abs(a))

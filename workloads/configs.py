@@ -297,6 +297,172 @@ def config5(M_target=16_000_000, seed=5, n_random=4_000_000, split_frac=0.05, to
                           "first_targets_are_nodes": nodes.shape[0] * nodes.shape[1]})
 
 
+# --------------------------------------------------------------------------- config 3
+def star_radius(th, a=0.3, k=5):
+    return 1.0 + a * np.cos(k * th)
+
+
+def _graded_points(x0, y0, ext, s0, src, g, h_min, nlev):
+    """Vertices of a forest of quadtrees with root cells of side s0 covering [x0, x0+ext]^2, refined while
+    the cell side exceeds h(d) = h_min + g d (d = distance from the cell to the source), nlev extra levels."""
+    n0 = int(np.ceil(ext / s0))
+    ix, iy = np.meshgrid(np.arange(n0), np.arange(n0), indexing="ij")
+    cx = x0 + ix.ravel() * s0
+    cy = y0 + iy.ravel() * s0
+    leaves = []
+    level = 0
+    while cx.size:
+        s = s0 / (1 << level)
+        d = np.maximum(np.hypot(cx + 0.5 * s - src[0], cy + 0.5 * s - src[1]) - 0.7072 * s, 0.0)
+        ref = (s > h_min + g * d) & (level < nlev)
+        leaves.append(np.stack([cx[~ref], cy[~ref], np.full((~ref).sum(), s)], 1))
+        cx, cy = cx[ref], cy[ref]
+        h = 0.5 * s
+        cx = np.concatenate([cx, cx + h, cx, cx + h])
+        cy = np.concatenate([cy, cy, cy + h, cy + h])
+        level += 1
+    L = np.concatenate(leaves)
+    # leaf corners + centres (centres keep Delaunay away from co-circular lattice squares)
+    pts = np.concatenate([L[:, :2], L[:, :2] + L[:, 2:3] * [1, 0], L[:, :2] + L[:, 2:3] * [0, 1],
+                          L[:, :2] + L[:, 2:3], L[:, :2] + 0.5 * L[:, 2:3]])
+    q = np.round((pts - [x0, y0]) / (s0 / (1 << (nlev + 2)))).astype(np.int64)
+    _, keep = np.unique(q[:, 0] * (1 << 31) + q[:, 1], return_index=True)
+    keep = np.sort(keep)
+    return pts[keep], np.concatenate([L[:, 2]] * 5)[keep]
+
+
+def config3(M_target=1_000_000, seed=3, tol=1e-9, n_sectors=16, r_core=0.25, g=0.025, lmin=10, lmax=16,
+            gap=1e-4, B_fixed=None):
+    """Star domain r(theta) = 1 + 0.3 cos 5 theta, covered by independently triangulated patches (a core disk
+    and n_sectors annular sectors), each shrunk inward by U[0, gap] per side so that neighbouring patches leave
+    gaps and hanging nodes; the point density is graded toward the source (0.3, -0.2) with h(d) = h_min + g d
+    (quadtree levels lmin..lmax, area ratio ~ 4^(lmax-lmin)); f = exp(-|x - (0.3,-0.2)|^2 / 1e-3^2).
+    Boundary edges are straight chords; f vanishes (< 1e-300) near the boundary, so no boundary
+    descriptor is needed (R9).  SURVEY §8(d) c3."""
+    from scipy.spatial import Delaunay
+    rng = np.random.default_rng(seed)
+    src = np.array([0.3, -0.2])
+    th0 = np.arctan2(src[1], src[0]) - np.pi / n_sectors   # the source sits mid-sector, far from every seam
+    wdt = 2 * np.pi / n_sectors
+    shrink = rng.uniform(0.0, gap, (n_sectors + 1, 4))
+
+    def sector_dist(c, k):
+        """signed distance (approx.) of points c to the boundary of shrunken patch k (> 0 inside)"""
+        s_in, s_out, s_a, s_b = shrink[k]
+        rr = np.hypot(c[:, 0], c[:, 1])
+        if k == n_sectors:
+            return (r_core - s_out) - rr
+        a = th0 + wdt * k
+        b = a + wdt
+        tt = np.arctan2(c[:, 1], c[:, 0])
+        da = -c[:, 0] * np.sin(a) + c[:, 1] * np.cos(a) - s_a
+        db = c[:, 0] * np.sin(b) - c[:, 1] * np.cos(b) - s_b
+        dr_in = rr - (r_core + s_in)
+        dr_out = (star_radius(tt) - s_out - rr) * 0.55       # |dr/ds| <= 1/0.55 on the star (slope bound)
+        d = np.minimum(np.minimum(da, db), np.minimum(dr_in, dr_out))
+        return np.where(np.mod(tt - a, 2 * np.pi) < wdt + 1e-12, d, -1.0)
+
+    def local_h(c, B):
+        return np.minimum(B / (1 << lmin), B / (1 << lmax) + g * np.hypot(c[:, 0] - src[0], c[:, 1] - src[1]))
+
+    def sample_curve(fn, t0, t1, B):
+        """points along a parametric curve fn(t) at the local spacing"""
+        ts = np.linspace(t0, t1, 64)
+        P = fn(ts)
+        seg = np.hypot(*np.diff(P, axis=0).T)
+        h = local_h(0.5 * (P[1:] + P[:-1]), B)
+        n = np.concatenate([[0], np.cumsum(seg / h)])
+        m = max(2, int(np.ceil(n[-1])))
+        tt = np.interp(np.linspace(0, n[-1], m + 1), n, ts)
+        return fn(tt)
+
+    def patch_tris(B):
+        h_min = B / (1 << lmax) * 1.01
+        pts, size = _graded_points(-1.32, -1.32, 2.64, B / (1 << lmin), src, g, h_min, lmax - lmin)
+        pts = pts + rng.uniform(-0.05, 0.05, pts.shape) * size[:, None]
+        out = []
+        for k in range(n_sectors + 1):
+            s_in, s_out, s_a, s_b = shrink[k]
+            d = sector_dist(pts, k)
+            P = [pts[d > 0.3 * size]]
+            if k == n_sectors:
+                rc = r_core - s_out
+                P.append(sample_curve(lambda t: rc * np.stack([np.cos(t), np.sin(t)], 1), 0, 2 * np.pi, B)[:-1])
+            else:
+                a = th0 + wdt * k
+                b = a + wdt
+                na = np.array([-np.sin(a), np.cos(a)])
+                nb = np.array([np.sin(b), -np.cos(b)])
+                ua = np.array([np.cos(a), np.sin(a)])
+                ub = np.array([np.cos(b), np.sin(b)])
+                # corners of the shrunken sector (on the offset rays)
+                def ray_pt(u, n, s, rad):
+                    t = np.sqrt(np.maximum(rad ** 2 - s ** 2, 0.0))
+                    return t * u + s * n
+                def r_outer_on_ray(u, n, s):
+                    t = 1.0
+                    for _ in range(60):   # fixed point: point on the offset ray at the star radius - s_out
+                        p = t * u + s * n
+                        t = np.sqrt(max((star_radius(np.arctan2(p[1], p[0])) - s_out) ** 2 - s * s, 0.0))
+                    return t
+                ta0 = np.sqrt((r_core + s_in) ** 2 - s_a ** 2)
+                ta1 = r_outer_on_ray(ua, na, s_a)
+                tb0 = np.sqrt((r_core + s_in) ** 2 - s_b ** 2)
+                tb1 = r_outer_on_ray(ub, nb, s_b)
+                P.append(sample_curve(lambda t: t[:, None] * ua + s_a * na, ta0, ta1, B))
+                P.append(sample_curve(lambda t: t[:, None] * ub + s_b * nb, tb0, tb1, B))
+                pa0, pb0 = ta0 * ua + s_a * na, tb0 * ub + s_b * nb
+                pa1, pb1 = ta1 * ua + s_a * na, tb1 * ub + s_b * nb
+                a_in0, a_in1 = np.arctan2(pa0[1], pa0[0]), np.arctan2(pb0[1], pb0[0])
+                a_out0, a_out1 = np.arctan2(pa1[1], pa1[0]), np.arctan2(pb1[1], pb1[0])
+                a_in1 = a_in0 + np.mod(a_in1 - a_in0, 2 * np.pi)
+                a_out1 = a_out0 + np.mod(a_out1 - a_out0, 2 * np.pi)
+                ri = r_core + s_in
+                P.append(sample_curve(lambda t: ri * np.stack([np.cos(t), np.sin(t)], 1), a_in0, a_in1, B)[1:-1])
+                P.append(sample_curve(lambda t: (star_radius(t) - s_out)[:, None] * np.stack([np.cos(t), np.sin(t)], 1),
+                                      a_out0, a_out1, B)[1:-1])
+            P = np.concatenate(P)
+            if P.shape[0] < 3:
+                continue
+            D = Delaunay(P)
+            T = P[D.simplices]
+            ok = sector_dist(T.mean(1), k) > 0
+            T = T[ok]
+            # drop the flat hull slivers Delaunay builds on (nearly) collinear boundary samples
+            e2 = np.max([np.sum((T[:, (q + 1) % 3] - T[:, q]) ** 2, 1) for q in range(3)], axis=0)
+            ar = 0.5 * np.abs((T[:, 1, 0] - T[:, 0, 0]) * (T[:, 2, 1] - T[:, 0, 1])
+                              - (T[:, 1, 1] - T[:, 0, 1]) * (T[:, 2, 0] - T[:, 0, 0]))
+            out.append(T[ar > e2 / 400.0])
+        return np.concatenate(out)
+
+    # the background spacing is set by the box side B (level lmin cells); solve B for M_target
+    lo, hi = 2.0, 6.0
+    if B_fixed is not None:
+        lo = hi = B_fixed
+    elif (M_target, seed, lmin, lmax, g, n_sectors) == (1_000_000, 3, 10, 16, 0.025, 16) and _C3_DEFAULT_B:
+        lo = hi = _C3_DEFAULT_B
+    for _ in range(30):
+        B = 0.5 * (lo + hi)
+        tri = patch_tris(B)
+        if abs(tri.shape[0] - M_target) <= 0.005 * M_target or lo == hi:
+            break
+        if tri.shape[0] > M_target:
+            lo = B
+        else:
+            hi = B
+    tri = _orient_ccw(tri)
+    area = 0.5 * np.abs((tri[:, 1, 0] - tri[:, 0, 0]) * (tri[:, 2, 1] - tri[:, 0, 1])
+                        - (tri[:, 1, 1] - tri[:, 0, 1]) * (tri[:, 2, 0] - tri[:, 0, 0]))
+    tri = tri[area > 0]
+    tri = tri[rng.permutation(tri.shape[0])]
+    fld = fields.gauss([1.0], [src[0]], [src[1]], [1e-3 ** 2])
+    return _finish(f"c3_star_graded_M{tri.shape[0]}", tri, np.zeros(tri.shape[0], np.int8), None, fld, None, tol,
+                   meta={"seed": seed, "B": B, "g": g, "levels": (lmin, lmax), "gap": gap, "src": tuple(src)})
+
+
+_C3_DEFAULT_B = 4.34375
+
+
 def sample_targets(T, K, seed=12345):
     """Seeded uniform subsample of K target indices out of T (sorted)."""
     rng = np.random.default_rng(seed)
