@@ -451,7 +451,9 @@ static void moments_12(const orc_tri *t, const orc_field *F, double gx, double g
     double X, Y, Jm[4];
     tri_map(t, g_r12[k][1], g_r12[k][2], &X, &Y, Jm);
     double w = g_w12[k] * 0.5 * fabs(Jm[0] * Jm[3] - Jm[1] * Jm[2]) * field_eval(F, X, Y);
-    double a = (X - gx) / D, b = (Y - gy) / D;
+    /* moment coordinates in the reference triangle (exact; physical X - gx loses digits on tiny triangles) */
+    double a = g_r12[k][1] - 1.0 / 3.0, b = g_r12[k][2] - 1.0 / 3.0;
+    (void)gx; (void)gy; (void)D;
     mom[0] += w; mom[1] += w * a; mom[2] += w * b; mom[3] += w * a * a; mom[4] += w * a * b; mom[5] += w * b * b;
     *absw += fabs(w);
   }
@@ -464,7 +466,8 @@ static void moments_duffy(const orc_tri *t, const orc_field *F, double gx, doubl
       double u = g_glx[n][i], v = g_glx[n][j], X, Y, Jm[4];
       tri_map(t, u, (1.0 - u) * v, &X, &Y, Jm);
       double w = g_glw[n][i] * g_glw[n][j] * (1.0 - u) * fabs(Jm[0] * Jm[3] - Jm[1] * Jm[2]) * field_eval(F, X, Y);
-      double a = (X - gx) / D, b = (Y - gy) / D;
+      double a = u - 1.0 / 3.0, b = (1.0 - u) * v - 1.0 / 3.0;
+      (void)gx; (void)gy; (void)D;
       mom[0] += w; mom[1] += w * a; mom[2] += w * b; mom[3] += w * a * a; mom[4] += w * a * b; mom[5] += w * b * b;
       *absw += fabs(w);
     }
@@ -474,14 +477,20 @@ static double mom_diff(const double *a, const double *b) {
   for (int k = 0; k < 6; k++) d = fmax(d, fabs(a[k] - b[k]));
   return d;
 }
+/* fscale = max |f| over the domain's nodes: a triangle whose integrand is below 1e-6 fscale everywhere is
+ * resolved to an absolute 1e-19 fscale |T| (its contribution to V is negligible at any tolerance) instead of
+ * to its own (possibly 1e-200) size -- otherwise Gaussian tails demand 30 x 30 rules for nothing. */
+static double g_fscale = 0.0;
 static int resolve_rule(const orc_tri *t, const orc_field *F, double gx, double gy) {
   if (F->kind == 0 && !t->curved) return 0;
   static const int ladder[4] = {8, 14, 20, 30};
   double m12[6], mA[6], mB[6], s12, sA, sB;
-  const double tolr = 1e-15;
+  const double tolr = 1e-13;  /* per-triangle relative accuracy; the rounding floor of the sums is ~1e-15 */
   moments_12(t, F, gx, gy, t->diam, m12, &s12);
   moments_duffy(t, F, gx, gy, t->diam, ladder[0], mA, &sA);
-  double scale = fmax(sA, 1e-300);
+  double area = 0.5 * fabs((t->v[1][0] - t->v[0][0]) * (t->v[2][1] - t->v[0][1]) -
+                           (t->v[1][1] - t->v[0][1]) * (t->v[2][0] - t->v[0][0]));
+  double scale = fmax(fmax(sA, 1e-6 * g_fscale * area), 1e-300);
   if (mom_diff(m12, mA) <= tolr * scale) return 0;
   for (int r = 0; r + 1 < 4; r++) {
     moments_duffy(t, F, gx, gy, t->diam, ladder[r + 1], mB, &sB);
@@ -536,6 +545,22 @@ static void opts_default(orc_opts *o, const orc_opts *in) {
   }
 }
 
+static void set_fscale(int64_t M, const double *tri, const int8_t *curved, const double *circle, const orc_field *F) {
+  double mx = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : mx)
+  for (int64_t m = 0; m < M; m++) {
+    orc_tri t;
+    load_tri(&t, tri, curved, circle, m);
+    for (int k = 0; k < 12; k++) {
+      double X, Y;
+      tri_map(&t, g_r12[k][1], g_r12[k][2], &X, &Y, NULL);
+      double v = fabs(field_eval(F, X, Y));
+      if (v > mx) mx = v;
+    }
+  }
+  g_fscale = mx;
+}
+
 /* V*(targets) for a triangulation (tri: M x 3 x 2 CCW; curved: M edge bitmasks or NULL;
  * circle: (cx, cy, rho) or NULL).  Returns 0 on success, -6 on allocation failure. */
 int orc_volume_potential(int64_t M, const double *tri, const int8_t *curved, const double *circle,
@@ -551,6 +576,7 @@ int orc_volume_potential(int64_t M, const double *tri, const int8_t *curved, con
   int32_t *nres = malloc(sizeof(int32_t) * (size_t)M);
   int64_t *off = malloc(sizeof(int64_t) * ((size_t)M + 1));
   if (!cen || !nres || !off) { free(cen); free(nres); free(off); return -6; }
+  set_fscale(M, tri, curved, circle, F);
 #pragma omp parallel for schedule(dynamic, 256)
   for (int64_t m = 0; m < M; m++) {
     orc_tri t;
@@ -623,6 +649,7 @@ int orc_volume_potential(int64_t M, const double *tri, const int8_t *curved, con
 int orc_resolve_rules(int64_t M, const double *tri, const int8_t *curved, const double *circle,
                       const orc_field *F, int32_t *nres) {
   init_all(F);
+  set_fscale(M, tri, curved, circle, F);
 #pragma omp parallel for schedule(dynamic, 256)
   for (int64_t m = 0; m < M; m++) {
     orc_tri t;
@@ -641,6 +668,7 @@ double orc_triangle_integral(const double *tri3, int8_t curved, const double *ci
   init_all(F);
   orc_tri t;
   load_tri(&t, tri3, &curved, circle, 0);
+  set_fscale(1, tri3, &curved, circle, F);
   double gx = (t.v[0][0] + t.v[1][0] + t.v[2][0]) / 3.0, gy = (t.v[0][1] + t.v[1][1] + t.v[2][1]) / 3.0;
   int n = resolve_rule(&t, F, gx, gy);
   double d = tri_dist(&t, px, py) - t.sag;

@@ -454,11 +454,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     setup_restriction(P);
     // ---- sources and targets sorted by NH tile
     vp_build_spread_order(P, P->sp, tri_nodes, weights, nullptr, N, grid_args(P->nh));
-    P->tx = vp_alloc<double>(P, T);
-    P->ty = vp_alloc<double>(P, T);
-    P->tperm = vp_alloc<int64_t>(P, T);
-    vp_sort_points(P, targets, T, P->nh.ox, P->nh.oy, P->sp.tiles.TS * P->nh.h, P->sp.tiles.ntx, P->sp.tiles.nty, P->tx,
-                   P->ty, P->tperm, nullptr, nullptr);
+    vp_build_interp_order(P, targets, T);
     // ---- graded meshes: per-target levels and band boxes (a12)
     int parts = o.parts ? o.parts : VP_PART_ALL;
     if (parts & VP_PART_LOCAL) {

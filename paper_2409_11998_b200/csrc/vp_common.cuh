@@ -136,9 +136,12 @@ struct vp_plan_s {
   int r_ntap = 0, t_ntap = 0;
   int64_t e_lo = 0, e_n = 0;
   double *scratch = nullptr;                           // n1 x e_n
-  // targets, sorted by NH tile
+  // targets, sorted by (TSI x TSI NH-grid tile, bank-slot rank) and cut into interpolation work items
   double *tx = nullptr, *ty = nullptr;
   int64_t *tperm = nullptr;  // sorted -> user target index
+  int TSI = 64;
+  int4 *items = nullptr;     // (tile_x, tile_y, first target, end target)
+  int64_t n_items = 0;
   // local part: V_L(t) = alpha_t * f(node_t) + sum_k omega_{t,k} f[idx_{t,k}]
   int K = 0, deg = 0, dmode = 0;
   int32_t *lidx = nullptr;     // [T][K] user node indices (sorted target order)
@@ -192,6 +195,7 @@ void vp_launch_restrict(vp_plan_s *P);
 void vp_launch_prolong(vp_plan_s *P);
 void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out);
+void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n);
 void vp_build_local(vp_plan_s *P, const double *nodes_dev);
 void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop);
 int64_t vp_sort_points(vp_plan_s *P, const double *xy, int64_t n, double ox, double oy, double cell,

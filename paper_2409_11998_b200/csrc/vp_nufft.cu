@@ -49,6 +49,10 @@ __device__ __forceinline__ int es_horner(double g, double *wts) {
   return i0;
 }
 
+__global__ void k_gather_xy(const double *__restrict__ xy, const int32_t *__restrict__ idx, int64_t n,
+                            double *__restrict__ xs, double *__restrict__ ys, int64_t *__restrict__ p64,
+                            int32_t *__restrict__ p32);
+
 __device__ __forceinline__ int64_t wrapi(int64_t i, int64_t n) {
   i %= n;
   return i < 0 ? i + n : i;
@@ -88,7 +92,7 @@ __global__ void k_tile_heads(const uint64_t *__restrict__ k1, int64_t n, int32_t
 #define VP_MAXLV 128
 #define VP_RANKLV 24
 __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restrict__ tstart, int64_t ntile,
-                         int64_t n, int W, int nw, uint64_t *__restrict__ k2) {
+                         int64_t n, int W, int nw, uint64_t *__restrict__ k2, int *__restrict__ overflow_flag) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= ntile) return;
   int64_t s0 = tstart[t], s1 = (t + 1 < ntile) ? tstart[t + 1] : n;
@@ -113,15 +117,17 @@ __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restr
       else lv = VP_MAXLV + overflow++;
     }
     if (lv < VP_MAXLV) last[lv] = (int16_t)col;
-    if (lv > 4095) lv = 4095;
+    // lv must stay exact (two points of one row never share a level): 20 bits; very dense rows (> 2^20
+    // points) are rejected at plan time by the caller's overflow check
     const int res = (row * nw + col) & 15;
     int rk = 0;
     if (lv < VP_RANKLV) {
       rk = rank[lv][res]++;
-      if (rk > 4095) rk = 4095;
+      if (rk > 0xFFFF) rk = 0xFFFF;
     }
+    if (lv > 0xFFFFF) lv = 0xFFFFF, *overflow_flag = 1;
     uint64_t tile = key >> 32;
-    k2[i] = (tile << 40) | ((uint64_t)lv << 28) | ((uint64_t)rk << 16) | ((uint64_t)res << 12);
+    k2[i] = (tile << 40) | ((uint64_t)lv << 20) | ((uint64_t)rk << 4) | (uint64_t)res;
   }
 }
 
@@ -129,15 +135,15 @@ __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restr
 __global__ void k_batch_heads(const uint64_t *__restrict__ k2, int64_t n, int32_t *__restrict__ head) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint64_t grp = k2[i] >> 28;
+  uint64_t grp = k2[i] >> 20;
   int h = 0;
-  if (i == 0 || (k2[i - 1] >> 28) != grp) {
+  if (i == 0 || (k2[i - 1] >> 20) != grp) {
     h = 1;
   } else {
     int64_t lo = 0, hi = i;
     while (lo < hi) {
       int64_t mid = (lo + hi) >> 1;
-      if ((k2[mid] >> 28) < grp) lo = mid + 1; else hi = mid;
+      if ((k2[mid] >> 20) < grp) lo = mid + 1; else hi = mid;
     }
     h = ((i - lo) % 32) == 0;
   }
@@ -371,11 +377,16 @@ void vp_launch_multiply(vp_plan_s *P, VpGrid &G) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// interpolation (NH grid, which also carries the prolongated FH field) + local part + scatter
+// interpolation (NH grid, which also carries the prolongated FH field) + local part + scatter.
+// One CTA of 256 threads per work item (tile_x, tile_y, t0, t1): the (TSI+W+3)^2 grid window of a
+// TSI x TSI tile is staged once in shared memory (coalesced rows), then every thread interpolates
+// targets t0 + tid, t0 + tid + 256, ... from shared memory.  Targets were ordered at plan time
+// rank-major over the bank slot of their footprint origin (vp_build_interp_order), so the 32
+// row-reads of a warp spread over the 16 8-byte bank slots.
 template <int W, int D>
-__global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__ tx, const double *__restrict__ ty,
-                                                      const int64_t *__restrict__ tperm, int64_t T, GridArgs g,
-                                                      int do_hist,
+__global__ void __launch_bounds__(256) k_interp_local(const int4 *__restrict__ items, int TSI,
+                                                      const double *__restrict__ tx, const double *__restrict__ ty,
+                                                      const int64_t *__restrict__ tperm, GridArgs g, int do_hist,
                                                       const double *__restrict__ f, const double *__restrict__ lalpha,
                                                       const int32_t *__restrict__ lnode,
                                                       const int32_t *__restrict__ lidx, const double *__restrict__ lw,
@@ -383,69 +394,167 @@ __global__ void __launch_bounds__(256) k_interp_local(const double *__restrict__
                                                       const double *__restrict__ tri_M,
                                                       const double *__restrict__ tri_H, int p, double tri_c2,
                                                       double *__restrict__ out) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  double v = 0.0;
+  extern __shared__ double tile[];
+  const int nw = TSI + W + 3;
+  const int4 it = items[blockIdx.x];
+  const int64_t ox = (int64_t)it.x * TSI - (W / 2 + 1), oy = (int64_t)it.y * TSI - (W / 2 + 1);
   if (do_hist) {
-    double wx[W], wy[W];
-    int ix = es_horner<W, D>(gcoord(tx[t], g.ox, g.inv_h), wx);
-    int iy = es_horner<W, D>(gcoord(ty[t], g.oy, g.inv_h), wy);
-    bool inside = ix >= 0 && iy >= 0 && ix + W <= g.nfx && iy + W <= g.nfy;
-#pragma unroll
-    for (int b = 0; b < W; b++) {
-      double racc = 0.0;
-      if (inside) {
-        const double *rp = g.data + (int64_t)(iy + b) * g.row + ix;
-#pragma unroll
-        for (int a = 0; a < W; a++) racc = fma(wx[a], __ldg(rp + a), racc);
-      } else {
-        int64_t yy = wrapi(iy + b, g.nfy);
-#pragma unroll
-        for (int a = 0; a < W; a++) racc = fma(wx[a], __ldg(g.data + yy * g.row + wrapi(ix + a, g.nfx)), racc);
-      }
-      v = fma(wy[b], racc, v);
+    const bool interior = ox >= 0 && oy >= 0 && ox + nw <= g.nfx && oy + nw <= g.nfy;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int r = warp; r < nw; r += 8) {
+      const int64_t gy = interior ? oy + r : wrapi(oy + r, g.nfy);
+      const double *src = g.data + gy * g.row;
+      for (int c = lane; c < nw; c += 32) tile[r * nw + c] = __ldg(src + (interior ? ox + c : wrapi(ox + c, g.nfx)));
     }
+    __syncthreads();
   }
-  if (do_local) {
-    double vl = 0.0;
-    const int32_t nd = lnode[t];
-    if (nd >= 0) vl = lalpha[t] * __ldg(f + nd);
-    const int32_t sp = lptr[t];
-    if (sp >= 0) {  // least-squares stencil
-      // k-major stencil layout: consecutive targets (lanes) read consecutive slots -> coalesced
-      const int32_t *ip = lidx + sp;
-      const double *wp = lw + sp;
-      for (int k = 0; k < K; k++) vl = fma(__ldcs(wp + k * n_sten), __ldg(f + __ldcs(ip + k * n_sten)), vl);
-    } else if (tri_c2 != 0.0) {  // own-triangle cubic fit: Lap f = M11 f_11 + 2 M12 f_12 + M22 f_22
-      const int64_t tri = nd / p;
-      const int kk = nd - (int)tri * p;
-      const double m11 = __ldg(tri_M + 3 * tri), m12 = __ldg(tri_M + 3 * tri + 1), m22 = __ldg(tri_M + 3 * tri + 2);
-      const double *fb = f + tri * p;
-      const double *h0 = tri_H + (int64_t)kk * p, *h1 = h0 + (int64_t)p * p, *h2 = h1 + (int64_t)p * p;
-      double lap = 0.0;
-      for (int j = 0; j < p; j++) {
-        double op = fma(m11, __ldg(h0 + j), fma(2.0 * m12, __ldg(h1 + j), m22 * __ldg(h2 + j)));
-        lap = fma(op, __ldg(fb + j), lap);
+  for (int t = it.z + threadIdx.x; t < it.w; t += blockDim.x) {
+    double v = 0.0;
+    if (do_hist) {
+      double wx[W], wy[W];
+      const int lx = (int)(es_horner<W, D>(gcoord(tx[t], g.ox, g.inv_h), wx) - ox);
+      const int ly = (int)(es_horner<W, D>(gcoord(ty[t], g.oy, g.inv_h), wy) - oy);
+      const double *rp = tile + ly * nw + lx;
+#pragma unroll
+      for (int b = 0; b < W; b++) {
+        double racc = 0.0;
+#pragma unroll
+        for (int a = 0; a < W; a++) racc = fma(wx[a], rp[b * nw + a], racc);
+        v = fma(wy[b], racc, v);
       }
-      vl = fma(tri_c2, lap, vl);
     }
-    v += vl;
+    if (do_local) {
+      double vl = 0.0;
+      const int32_t nd = lnode[t];
+      if (nd >= 0) vl = lalpha[t] * __ldg(f + nd);
+      const int32_t sp = lptr[t];
+      if (sp >= 0) {  // least-squares stencil, k-major: consecutive targets read consecutive slots
+        const int32_t *ip = lidx + sp;
+        const double *wp = lw + sp;
+        for (int k = 0; k < K; k++) vl = fma(__ldcs(wp + k * n_sten), __ldg(f + __ldcs(ip + k * n_sten)), vl);
+      } else if (tri_c2 != 0.0) {  // own-triangle cubic fit: Lap f = M11 f_11 + 2 M12 f_12 + M22 f_22
+        const int64_t tri = nd / p;
+        const int kk = nd - (int)tri * p;
+        const double m11 = __ldg(tri_M + 3 * tri), m12 = __ldg(tri_M + 3 * tri + 1), m22 = __ldg(tri_M + 3 * tri + 2);
+        const double *fb = f + tri * p;
+        const double *h0 = tri_H + (int64_t)kk * p, *h1 = h0 + (int64_t)p * p, *h2 = h1 + (int64_t)p * p;
+        double lap = 0.0;
+        for (int j = 0; j < p; j++) {
+          double op = fma(m11, __ldg(h0 + j), fma(2.0 * m12, __ldg(h1 + j), m22 * __ldg(h2 + j)));
+          lap = fma(op, __ldg(fb + j), lap);
+        }
+        vl = fma(tri_c2, lap, vl);
+      }
+      v += vl;
+    }
+    out[tperm[t]] = v;
   }
-  out[tperm[t]] = v;
 }
 
 template <int W>
 static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
   constexpr int D = VP_HORNER_DEG(W);
   int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
-  unsigned blocks = (unsigned)((P->T + 255) / 256);
-  if (!blocks) return;
-  k_interp_local<W, D><<<blocks, 256, 0, P->stream>>>(P->tx, P->ty, P->tperm, P->T, grid_args(P->nh),
-                                                      (parts & VP_PART_HISTORY) ? 1 : 0, f, P->lalpha, P->lnode,
-                                                      P->lidx, P->lw, P->K, P->n_stencil, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr,
-                                                      P->tri_M, P->tri_H, P->p, P->tri_c2, out);
+  if (P->n_items == 0) return;
+  const int TSI = P->TSI, nw = TSI + W + 3;
+  const int do_hist = (parts & VP_PART_HISTORY) ? 1 : 0;
+  size_t sm = do_hist ? sizeof(double) * (size_t)nw * nw : 0;
+  static bool attr_set[17] = {};
+  if (!attr_set[W]) {
+    VP_CUDA(cudaFuncSetAttribute(k_interp_local<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(double) * (TSI + W + 3) * (TSI + W + 3))));
+    attr_set[W] = true;
+  }
+  k_interp_local<W, D><<<(unsigned)P->n_items, 256, sm, P->stream>>>(
+      P->items, TSI, P->tx, P->ty, P->tperm, grid_args(P->nh), do_hist, f, P->lalpha, P->lnode, P->lidx, P->lw, P->K,
+      P->n_stencil, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr, P->tri_M, P->tri_H, P->p, P->tri_c2, out);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
+}
+
+// ---------------------------------------------------------------------------------------------
+// plan-time: order the targets by (TSI-tile, rank within bank slot, bank slot) and cut the tiles into
+// work items of <= VP_INTERP_CHUNK targets
+#define VP_INTERP_CHUNK 4096
+__global__ void k_interp_keys1(const double *__restrict__ xy, int64_t n, GridArgs g, int TSI, int W, int64_t ntx,
+                               int64_t nty, uint64_t *__restrict__ keys, int32_t *__restrict__ idx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double gx = gcoord(xy[2 * i], g.ox, g.inv_h), gy = gcoord(xy[2 * i + 1], g.oy, g.inv_h);
+  int64_t tx = (int64_t)floor(gx / TSI), ty = (int64_t)floor(gy / TSI);
+  tx = tx < 0 ? 0 : (tx >= ntx ? ntx - 1 : tx);
+  ty = ty < 0 ? 0 : (ty >= nty ? nty - 1 : ty);
+  const int nw = TSI + W + 3;
+  int64_t lrow = (int64_t)ceil(gy - 0.5 * W) - (ty * TSI - (W / 2 + 1));
+  int64_t lcol = (int64_t)ceil(gx - 0.5 * W) - (tx * TSI - (W / 2 + 1));
+  const int res = (int)((((lrow * nw + lcol) % 16) + 16) % 16);
+  keys[i] = ((uint64_t)(ty * ntx + tx) << 4) | (uint64_t)res;
+  idx[i] = (int32_t)i;
+}
+
+__global__ void k_interp_keys2(const uint64_t *__restrict__ k1, int64_t n, uint64_t *__restrict__ k2) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t key = k1[i];
+  int64_t lo = 0, hi = i;
+  while (lo < hi) {  // first index of this (tile, slot) group
+    int64_t mid = (lo + hi) >> 1;
+    if (k1[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  uint64_t rank = (uint64_t)(i - lo);
+  if (rank > 0xFFFFF) rank = 0xFFFFF;
+  k2[i] = ((key >> 4) << 24) | (rank << 4) | (key & 15);
+}
+
+void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
+  cudaStream_t s = P->stream;
+  const GridArgs g = grid_args(P->nh);
+  const int TSI = P->TSI;
+  const int64_t ntx = (g.nfx + TSI - 1) / TSI, nty = (g.nfy + TSI - 1) / TSI;
+  uint64_t *k1, *k1s, *k2, *k2s;
+  int32_t *i1, *i1s, *i2s;
+  VP_CUDA(cudaMallocAsync(&k1, 8 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&k1s, 8 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&k2, 8 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&k2s, 8 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&i1, 4 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&i1s, 4 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&i2s, 4 * (n + 1), s));
+  unsigned nb = (unsigned)((n + 255) / 256);
+  k_interp_keys1<<<nb, 256, 0, s>>>(xy, n, g, TSI, P->w, ntx, nty, k1, i1);
+  VP_CHECK_LAUNCH();
+  size_t tb = 0, tb2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s);
+  void *tmp;
+  VP_CUDA(cudaMallocAsync(&tmp, std::max(tb, tb2) + 16, s));
+  VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
+  k_interp_keys2<<<nb, 256, 0, s>>>(k1s, n, k2);
+  VP_CHECK_LAUNCH();
+  VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
+  P->tx = vp_alloc<double>(P, n);
+  P->ty = vp_alloc<double>(P, n);
+  P->tperm = vp_alloc<int64_t>(P, n);
+  k_gather_xy<<<nb, 256, 0, s>>>(xy, i2s, n, P->tx, P->ty, P->tperm, nullptr);
+  VP_CHECK_LAUNCH();
+  std::vector<uint64_t> hk(n);
+  VP_CUDA(cudaMemcpyAsync(hk.data(), k2s, 8 * n, cudaMemcpyDeviceToHost, s));
+  VP_CUDA(cudaStreamSynchronize(s));
+  std::vector<int4> items;
+  for (int64_t i = 0; i < n;) {
+    const uint64_t tile = hk[i] >> 24;
+    int64_t e = i;
+    while (e < n && (hk[e] >> 24) == tile) e++;
+    for (int64_t c = i; c < e; c += VP_INTERP_CHUNK)
+      items.push_back(make_int4((int)(tile % ntx), (int)(tile / ntx), (int)c, (int)std::min<int64_t>(e, c + VP_INTERP_CHUNK)));
+    i = e;
+  }
+  P->n_items = (int64_t)items.size();
+  P->items = vp_alloc<int4>(P, std::max<size_t>(items.size(), 1));
+  if (!items.empty())
+    VP_CUDA(cudaMemcpy(P->items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
+  for (void *q : {(void *)k1, (void *)k1s, (void *)k2, (void *)k2s, (void *)i1, (void *)i1s, (void *)i2s, tmp})
+    VP_CUDA(cudaFreeAsync(q, s));
 }
 
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out) {
@@ -522,8 +631,19 @@ void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const
     int32_t nt = 0;
     VP_CUDA(cudaMemcpyAsync(&nt, d_nt, 4, cudaMemcpyDeviceToHost, s));
     VP_CUDA(cudaStreamSynchronize(s));
-    k_levels<<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(k1s, tst, nt, n, P->w, Tl.TS + P->w + 3, k2);
+    int *d_ovf;
+    VP_CUDA(cudaMallocAsync(&d_ovf, sizeof(int), s));
+    VP_CUDA(cudaMemsetAsync(d_ovf, 0, sizeof(int), s));
+    k_levels<<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(k1s, tst, nt, n, P->w, Tl.TS + P->w + 3, k2, d_ovf);
     VP_CHECK_LAUNCH();
+    int h_ovf = 0;
+    VP_CUDA(cudaMemcpyAsync(&h_ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
+    VP_CUDA(cudaStreamSynchronize(s));
+    VP_CUDA(cudaFreeAsync(d_ovf, s));
+    if (h_ovf) {
+      vp_set_last_error("more than 2^20 points share one footprint row of a spreading tile");
+      throw VpError{VP_ERR_UNSUPPORTED};
+    }
     for (void *p : {(void *)tst, (void *)d_nt, tmp3}) VP_CUDA(cudaFreeAsync(p, s));
   }
   VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
