@@ -87,7 +87,7 @@ typedef struct {
    * grading supports, <= 12), > 0 cap.  A target x gets level l(x) = the finest l such that every node y
    * within level_rho sqrt(delta_l) has delta_l >= level_cmin Dx_loc^2(y), delta_l = delta_1 / 4^l. */
   int32_t levels;
-  double level_cmin;         /* 0 -> 2 */
+  double level_cmin;         /* 0 -> 1.5 */
   double level_rho;          /* 0 -> 4 */
 } vp_opts;
 

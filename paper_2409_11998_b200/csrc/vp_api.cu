@@ -184,6 +184,33 @@ static void setup_grid(vp_plan_s *P, VpGrid &G, int kind, double L, double kmax)
   G.data = vp_alloc<double>(P, (size_t)G.nf * G.row);
 }
 
+// Far-history grid on the NH lattice: spacing h2 = m h1 (integer m), origin on an NH
+// node, period L2 = nf2 h2 >= L_req.  Every FH node then coincides with an NH node, so the restriction
+// weights psi_FH((X1(i) - X2(i')) / (w h2 / 2)) depend on i - m i' only: one tap vector for all outputs.
+static void setup_grid_fh(vp_plan_s *P, VpGrid &G, double L_req, double kmax) {
+  const VpGrid &N = P->nh;
+  int64_t n_req = 2 * (int64_t)ceil(L_req * kmax / (2.0 * VP_PI));
+  if (n_req < 4) n_req = 4;
+  const double h_max = L_req / (double)(2 * n_req);  // sigma = 2
+  int64_t m = (int64_t)floor(h_max / N.h * (1.0 + 1e-12));
+  if (m < 1) m = 1;
+  G.kind = 1;
+  G.h = m * N.h;
+  G.nf = vp_next_smooth((int64_t)ceil(L_req / G.h));
+  if (G.nf < 2 * P->w) G.nf = vp_next_smooth(2 * P->w);
+  G.L = G.nf * G.h;
+  G.nmode = 2 * (int64_t)ceil(G.L * kmax / (2.0 * VP_PI));
+  if (G.nmode > G.nf) G.nmode = G.nf - (G.nf & 1);
+  const int64_t j = llround((N.ox - (P->cx - 0.5 * G.L)) / N.h);
+  G.ox = N.ox - (double)j * N.h;
+  G.oy = N.oy - (double)j * N.h;
+  G.row = 2 * (G.nf / 2 + 1);
+  P->fh_ratio = (int)m;
+  P->fh_shift = j;
+  if ((double)G.nf * (double)G.row * 8.0 > 120e9) throw VpError{VP_ERR_OOM};
+  G.data = vp_alloc<double>(P, (size_t)G.nf * G.row);
+}
+
 // 1D transform of the ES kernel at spacing h: Phi(k) = 2 alpha int_0^1 psi(s) cos(k alpha s) ds, alpha = w h/2
 static double es_transform(const vp_plan_s *P, double h, double k, const std::vector<double> &gx,
                            const std::vector<double> &gw) {
@@ -308,6 +335,23 @@ static void setup_restriction(vp_plan_s *P) {
   if (elo < 0) throw VpError{VP_ERR_GEOMETRY};
   P->e_lo = elo;
   P->e_n = ehi - elo + 1;
+  // integer ratio: the single tap vector w[q] = psi_FH(2 q / (W m)), |q| < W m / 2, checked against the tables
+  {
+    const int m = P->fh_ratio;
+    const int QH = (P->w * m - 1) / 2;
+    bool ok = 2 * QH + 1 <= 192 && fabs(P->fh.h - m * P->nh.h) <= 1e-14 * P->fh.h;
+    for (int q = -QH; q <= QH && ok; q++) P->tap_w[q + QH] = vp_es(2.0 * q / (double)(P->w * m), P->beta);
+    // spot check: table weight of (i, i') equals w[i + j - m i']
+    for (int64_t ip = elo; ip <= ehi && ok; ip += std::max<int64_t>(1, (ehi - elo) / 7)) {
+      for (int t = 0; t < P->r_ntap; t++) {
+        int64_t i = rlo[ip] + t, q = i + P->fh_shift - m * ip;
+        double wt = rw[(size_t)ip * P->r_ntap + t];
+        double wq = (q >= -QH && q <= QH) ? P->tap_w[q + QH] : 0.0;
+        if (fabs(wt - wq) > 1e-12) ok = false;
+      }
+    }
+    P->tap_qh = ok ? QH : 0;
+  }
   P->r_lo = vp_alloc<int32_t>(P, n2);
   P->t_lo = vp_alloc<int32_t>(P, n1);
   P->r_w = vp_alloc<double>(P, rw.size());
@@ -447,7 +491,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     double L_fh = P->S + P->R + m2;
     setup_grid(P, P->nh, 0, L_nh, P->kmax_nh);
     P->nh.delta_a = P->delta1; P->nh.delta_b = P->delta2;
-    setup_grid(P, P->fh, 1, L_fh, P->kmax_fh);
+    setup_grid_fh(P, P->fh, L_fh, P->kmax_fh);
     P->fh.delta_a = P->delta2; P->fh.delta_b = P->R;
     setup_horner(P);
     setup_deconv(P);

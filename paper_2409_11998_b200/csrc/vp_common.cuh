@@ -124,6 +124,10 @@ struct vp_plan_s {
   int w = 0;
   double beta = 0;
   VpGrid nh, fh;
+  int fh_ratio = 1;         // h_FH = fh_ratio * h_NH
+  int64_t fh_shift = 0;     // FH node i' sits on NH node fh_ratio * i' - fh_shift
+  int tap_qh = 0;           // integer-ratio restriction taps w[q + QH], |q| <= QH (0: general tables)
+  double tap_w[192] = {};
   VpHorner horner{};
   double horner_err = 0;
   // sources, sorted by (NH tile, row rank, row) into batches of <= 32 points with distinct rows
@@ -155,6 +159,7 @@ struct vp_plan_s {
   double *tri_M = nullptr;     // [M][3] A^-1 A^-T (M11, M12, M22)
   double *tri_H = nullptr;     // [3][p][p] reference cubic-fit Hessian operators
   double tri_c2 = 0;           // delta^2 / 2 (0 if series_order < 2)
+  double *tri_vL = nullptr;    // [N] TRIANGLE-mode V_L per node (eval scratch; null outside TRIANGLE mode)
   // host-side eval staging (vp_eval_host)
   double *f_dev = nullptr, *out_dev = nullptr;
   // profiling

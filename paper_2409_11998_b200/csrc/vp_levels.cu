@@ -241,7 +241,7 @@ void vp_build_levels(vp_plan_s *P, const double *nodes, const double *weights) {
   const vp_opts &o = P->opts;
   if (o.levels < 0) return;
   const int lcap = o.levels > 0 ? std::min(o.levels, 12) : 12;
-  const double cmin = o.level_cmin > 0 ? o.level_cmin : 2.0;
+  const double cmin = o.level_cmin > 0 ? o.level_cmin : 1.5;
   const double rho = o.level_rho > 0 ? o.level_rho : 4.0;
   const double d0 = P->delta1;
   // ---- lambda per node

@@ -395,6 +395,7 @@ void vp_build_local(vp_plan_s *P, const double *nodes_dev) {
                                        P->opts.boundary, P->delta1, c1, P->bands.tlev, need, P->lalpha, P->lnode);
     VP_CHECK_LAUNCH();
     P->tri_c2 = nterms >= 2 ? 0.5 * P->delta1 * P->delta1 : 0.0;
+    P->tri_vL = vp_alloc<double>(P, P->N);
   } else {
     k_target_mode<<<tb_t, 256, 0, st>>>(P->tx, P->ty, P->tperm, P->T, 1, nullptr, 0, P->opts.boundary, P->delta1, 0.0,
                                        P->bands.tlev, need, P->lalpha, P->lnode);

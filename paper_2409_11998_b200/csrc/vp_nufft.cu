@@ -308,6 +308,190 @@ __global__ void k_prolong_x(const double *__restrict__ t2, double *__restrict__ 
   q1[r * a.row1 + i] += acc;
 }
 
+// ---- integer-ratio restriction / prolongation (h_FH = M h_NH, FH node i' on NH node M i' - j): one tap vector
+// w[q] = psi_FH(2 q / (W M)), |q| <= QH, for every output.  Each thread keeps Q (restriction) or M
+// (prolongation) consecutive outputs in registers and streams the union of their inputs once.
+#define VP_MAXTAP 192
+struct TapArgs {
+  double w[VP_MAXTAP];  // w[q + QH]
+  int QH;
+  int64_t j;
+};
+
+// pass A: tA[r][e] = sum_q w[q] g1[r][M (e_lo + e) - j + q]; the NH row segment is staged in shared memory
+// with one pad word every M*Q entries, so the 32 lanes' windows (M*Q apart) start in distinct bank slots
+template <int M, int Q>
+__global__ void __launch_bounds__(128) k_restrict_x_int(const double *__restrict__ g1, double *__restrict__ tA,
+                                                        RestrictArgs a, TapArgs tp) {
+  extern __shared__ double s[];
+  constexpr int SKEW = M * Q;
+  const int64_t r = blockIdx.y;
+  const int64_t e0 = (int64_t)blockIdx.x * 128 * Q;
+  const int NT = 2 * tp.QH + 1;
+  const int span = M * (128 * Q - 1) + NT;
+  const int64_t i0 = M * (a.e_lo + e0) - tp.j - tp.QH;
+  const double *src = g1 + r * a.row1;
+  for (int idx = threadIdx.x; idx < span; idx += 128) {
+    const int64_t gi = i0 + idx;
+    s[idx + idx / SKEW] = (gi >= 0 && gi < a.n1) ? __ldg(src + gi) : 0.0;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  const double *sb = s + (SKEW + 1) * t;
+  double acc[Q];
+#pragma unroll
+  for (int k = 0; k < Q; k++) acc[k] = 0.0;
+  const int nin = M * (Q - 1) + NT;
+  for (int ii = 0; ii < nin; ii++) {
+    const double x = sb[ii + ii / SKEW];
+#pragma unroll
+    for (int k = 0; k < Q; k++) {
+      const int q = ii - M * k;
+      if (q >= 0 && q < NT) acc[k] = fma(tp.w[q], x, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < Q; k++) {
+    const int64_t e = e0 + Q * t + k;
+    if (e < a.ne) tA[r * a.ne + e] = acc[k];
+  }
+}
+
+// pass B: g2[e_lo + ey][e_lo + ex] = sum_q w[q] tA[M (e_lo + ey) - j + q][ex] (coalesced along ex)
+template <int M, int Q>
+__global__ void __launch_bounds__(128) k_restrict_y_int(const double *__restrict__ tA, double *__restrict__ g2,
+                                                        RestrictArgs a, TapArgs tp) {
+  const int64_t ex = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int64_t ey0 = (int64_t)blockIdx.y * Q;
+  if (ex >= a.ne) return;
+  const int NT = 2 * tp.QH + 1;
+  const int nin = M * (Q - 1) + NT;
+  const int64_t r0 = M * (a.e_lo + ey0) - tp.j - tp.QH;
+  double acc[Q];
+#pragma unroll
+  for (int k = 0; k < Q; k++) acc[k] = 0.0;
+  for (int ii = 0; ii < nin; ii++) {
+    const int64_t r = r0 + ii;
+    const double x = (r >= 0 && r < a.n1) ? __ldg(tA + r * a.ne + ex) : 0.0;
+#pragma unroll
+    for (int k = 0; k < Q; k++) {
+      const int q = ii - M * k;
+      if (q >= 0 && q < NT) acc[k] = fma(tp.w[q], x, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < Q; k++) {
+    const int64_t ey = ey0 + k;
+    if (ey < a.ne) g2[(a.e_lo + ey) * a.row2 + a.e_lo + ex] = acc[k];
+  }
+}
+
+// prolongation pass B^T: t2[r][ex] = sum_{i'} w[r + j - M i'] q2[i'][e_lo + ex], i' in the effective range;
+// a thread owns the M rows r = M c + k - j (k = 0..M-1) sharing the FH rows i' = c + d
+template <int M>
+__global__ void __launch_bounds__(128) k_prolong_y_int(const double *__restrict__ q2, double *__restrict__ t2,
+                                                       RestrictArgs a, TapArgs tp, int64_t c_lo) {
+  const int64_t ex = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int64_t c = c_lo + blockIdx.y;
+  if (ex >= a.ne) return;
+  const int QH = tp.QH;
+  const int dlo = -(QH / M), dhi = (M - 1 + QH) / M;
+  double acc[M];
+#pragma unroll
+  for (int k = 0; k < M; k++) acc[k] = 0.0;
+  for (int d = dlo; d <= dhi; d++) {
+    const int64_t ip = c + d;
+    if (ip < a.e_lo || ip >= a.e_lo + a.ne) continue;
+    const double x = __ldg(q2 + ip * a.row2 + a.e_lo + ex);
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+      const int q = k - M * d;
+      if (q >= -QH && q <= QH) acc[k] = fma(tp.w[q + QH], x, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < M; k++) {
+    const int64_t r = M * c + k - tp.j;
+    if (r >= 0 && r < a.n1) t2[r * a.ne + ex] = acc[k];
+  }
+}
+
+// prolongation pass A^T: q1[r][i] += sum_{i'} w[i + j - M i'] t2[r][i' - e_lo]; a thread owns the M
+// columns i = M c + k - j, the warp reads consecutive i' (coalesced)
+template <int M>
+__global__ void __launch_bounds__(128) k_prolong_x_int(const double *__restrict__ t2, double *__restrict__ q1,
+                                                       RestrictArgs a, TapArgs tp, int64_t c_lo, int64_t nc) {
+  const int64_t cc = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int64_t r = blockIdx.y;
+  if (cc >= nc) return;
+  const int64_t c = c_lo + cc;
+  const int QH = tp.QH;
+  const int dlo = -(QH / M), dhi = (M - 1 + QH) / M;
+  const double *src = t2 + r * a.ne - a.e_lo;
+  double acc[M];
+#pragma unroll
+  for (int k = 0; k < M; k++) acc[k] = 0.0;
+  for (int d = dlo; d <= dhi; d++) {
+    const int64_t ip = c + d;
+    if (ip < a.e_lo || ip >= a.e_lo + a.ne) continue;
+    const double x = __ldg(src + ip);
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+      const int q = k - M * d;
+      if (q >= -QH && q <= QH) acc[k] = fma(tp.w[q + QH], x, acc[k]);
+    }
+  }
+  double *dst = q1 + r * a.row1;
+#pragma unroll
+  for (int k = 0; k < M; k++) {
+    const int64_t i = M * c + k - tp.j;
+    if (i >= 0 && i < a.n1) dst[i] += acc[k];
+  }
+}
+
+static TapArgs tap_args(vp_plan_s *P) {
+  TapArgs t;
+  memset(&t, 0, sizeof(t));
+  t.QH = P->tap_qh;
+  t.j = P->fh_shift;
+  for (int q = 0; q < 2 * P->tap_qh + 1; q++) t.w[q] = P->tap_w[q];
+  return t;
+}
+
+template <int M>
+static void launch_restrict_int(vp_plan_s *P, const RestrictArgs &a, const TapArgs &tp) {
+  constexpr int Q = 4;
+  const int span = M * (128 * Q - 1) + 2 * tp.QH + 1;
+  const size_t sm = sizeof(double) * (size_t)(span + span / (M * Q) + 2);
+  static bool attr = false;
+  if (!attr) {
+    VP_CUDA(cudaFuncSetAttribute(k_restrict_x_int<M, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    attr = true;
+  }
+  dim3 gA((unsigned)((a.ne + 128 * Q - 1) / (128 * Q)), (unsigned)a.n1);
+  k_restrict_x_int<M, Q><<<gA, 128, sm, P->stream>>>(P->nh.data, P->scratch, a, tp);
+  VP_CHECK_LAUNCH();
+  dim3 gB((unsigned)((a.ne + 127) / 128), (unsigned)((a.ne + Q - 1) / Q));
+  k_restrict_y_int<M, Q><<<gB, 128, 0, P->stream>>>(P->scratch, P->fh.data, a, tp);
+  VP_CHECK_LAUNCH();
+  P->n_kernels += 2;
+}
+
+template <int M>
+static void launch_prolong_int(vp_plan_s *P, const RestrictArgs &a, const TapArgs &tp) {
+  // NH index i = M c + k - j covers [0, n1) for c in [c_lo, c_hi]
+  const int64_t c_lo = (tp.j >= 0) ? tp.j / M : -((-tp.j + M - 1) / M);
+  const int64_t c_hi = (a.n1 - 1 + tp.j) / M;
+  const int64_t nc = c_hi - c_lo + 1;
+  dim3 gB((unsigned)((a.ne + 127) / 128), (unsigned)nc);
+  k_prolong_y_int<M><<<gB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a, tp, c_lo);
+  VP_CHECK_LAUNCH();
+  dim3 gA((unsigned)((nc + 127) / 128), (unsigned)a.n1);
+  k_prolong_x_int<M><<<gA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a, tp, c_lo, nc);
+  VP_CHECK_LAUNCH();
+  P->n_kernels += 2;
+}
+
 static RestrictArgs restrict_args(vp_plan_s *P) {
   RestrictArgs a;
   a.rlo = P->r_lo; a.rw = P->r_w; a.ntap = P->r_ntap;
@@ -319,6 +503,19 @@ static RestrictArgs restrict_args(vp_plan_s *P) {
 
 void vp_launch_restrict(vp_plan_s *P) {
   RestrictArgs a = restrict_args(P);
+  if (P->tap_qh > 0) {
+    TapArgs tp = tap_args(P);
+    switch (P->fh_ratio) {
+      case 2: launch_restrict_int<2>(P, a, tp); return;
+      case 3: launch_restrict_int<3>(P, a, tp); return;
+      case 4: launch_restrict_int<4>(P, a, tp); return;
+      case 5: launch_restrict_int<5>(P, a, tp); return;
+      case 6: launch_restrict_int<6>(P, a, tp); return;
+      case 7: launch_restrict_int<7>(P, a, tp); return;
+      case 8: launch_restrict_int<8>(P, a, tp); return;
+      default: break;
+    }
+  }
   dim3 bA((unsigned)((a.ne + 127) / 128), (unsigned)a.n1);
   k_restrict_x<<<bA, 128, 0, P->stream>>>(P->nh.data, P->scratch, a);
   VP_CHECK_LAUNCH();
@@ -330,6 +527,19 @@ void vp_launch_restrict(vp_plan_s *P) {
 
 void vp_launch_prolong(vp_plan_s *P) {
   RestrictArgs a = restrict_args(P);
+  if (P->tap_qh > 0) {
+    TapArgs tp = tap_args(P);
+    switch (P->fh_ratio) {
+      case 2: launch_prolong_int<2>(P, a, tp); return;
+      case 3: launch_prolong_int<3>(P, a, tp); return;
+      case 4: launch_prolong_int<4>(P, a, tp); return;
+      case 5: launch_prolong_int<5>(P, a, tp); return;
+      case 6: launch_prolong_int<6>(P, a, tp); return;
+      case 7: launch_prolong_int<7>(P, a, tp); return;
+      case 8: launch_prolong_int<8>(P, a, tp); return;
+      default: break;
+    }
+  }
   dim3 bB((unsigned)((a.ne + 127) / 128), (unsigned)a.n1);
   k_prolong_y<<<bB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a);
   VP_CHECK_LAUNCH();
@@ -391,8 +601,7 @@ __global__ void __launch_bounds__(256) k_interp_local(const int4 *__restrict__ i
                                                       const int32_t *__restrict__ lnode,
                                                       const int32_t *__restrict__ lidx, const double *__restrict__ lw,
                                                       int K, int64_t n_sten, int do_local, const int32_t *__restrict__ lptr,
-                                                      const double *__restrict__ tri_M,
-                                                      const double *__restrict__ tri_H, int p, double tri_c2,
+                                                      const double *__restrict__ vL_tri,
                                                       double *__restrict__ out) {
   extern __shared__ double tile[];
   const int nw = TSI + W + 3;
@@ -426,29 +635,64 @@ __global__ void __launch_bounds__(256) k_interp_local(const int4 *__restrict__ i
     if (do_local) {
       double vl = 0.0;
       const int32_t nd = lnode[t];
-      if (nd >= 0) vl = lalpha[t] * __ldg(f + nd);
       const int32_t sp = lptr[t];
       if (sp >= 0) {  // least-squares stencil, k-major: consecutive targets read consecutive slots
+        if (nd >= 0) vl = lalpha[t] * __ldg(f + nd);
         const int32_t *ip = lidx + sp;
         const double *wp = lw + sp;
+#pragma unroll 6
         for (int k = 0; k < K; k++) vl = fma(__ldcs(wp + k * n_sten), __ldg(f + __ldcs(ip + k * n_sten)), vl);
-      } else if (tri_c2 != 0.0) {  // own-triangle cubic fit: Lap f = M11 f_11 + 2 M12 f_12 + M22 f_22
-        const int64_t tri = nd / p;
-        const int kk = nd - (int)tri * p;
-        const double m11 = __ldg(tri_M + 3 * tri), m12 = __ldg(tri_M + 3 * tri + 1), m22 = __ldg(tri_M + 3 * tri + 2);
-        const double *fb = f + tri * p;
-        const double *h0 = tri_H + (int64_t)kk * p, *h1 = h0 + (int64_t)p * p, *h2 = h1 + (int64_t)p * p;
-        double lap = 0.0;
-        for (int j = 0; j < p; j++) {
-          double op = fma(m11, __ldg(h0 + j), fma(2.0 * m12, __ldg(h1 + j), m22 * __ldg(h2 + j)));
-          lap = fma(op, __ldg(fb + j), lap);
-        }
-        vl = fma(tri_c2, lap, vl);
+      } else if (vL_tri) {  // own-triangle cubic fit, evaluated per node by k_tri_local
+        vl = __ldg(vL_tri + nd);
+      } else if (nd >= 0) {
+        vl = lalpha[t] * __ldg(f + nd);
       }
       v += vl;
     }
     out[tperm[t]] = v;
   }
+}
+
+// TRIANGLE-mode local part for every node of a qualifying triangle (one thread per triangle, 12 coalesced
+// f values, reference Hessian operators in shared memory, read in lockstep -> broadcast):
+//   V_L(node k) = delta f_k + (delta^2 / 2) Lap f(node k),  Lap f = M11 f_11 + 2 M12 f_12 + M22 f_22
+// with f_ab the second reference derivatives of the least-squares cubic on the triangle's p nodes.
+template <int PP>  // PP > 0: compile-time rule size (registers); 0: runtime p
+__global__ void __launch_bounds__(128) k_tri_local(const double *__restrict__ f, const int8_t *__restrict__ tri_ok,
+                                                   const double *__restrict__ tri_M,
+                                                   const double *__restrict__ tri_H, int p_rt, int64_t M, double c1,
+                                                   double c2, double *__restrict__ vL) {
+  __shared__ double H[3 * VP_TRI_MAXP * VP_TRI_MAXP];
+  const int p = PP > 0 ? PP : p_rt;
+  for (int i = threadIdx.x; i < 3 * p * p; i += blockDim.x) H[i] = tri_H[i];
+  __syncthreads();
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= M || !tri_ok[m]) return;
+  const double m11 = tri_M[3 * m], m12x2 = 2.0 * tri_M[3 * m + 1], m22 = tri_M[3 * m + 2];
+  double fb[PP > 0 ? PP : VP_TRI_MAXP];
+#pragma unroll
+  for (int j = 0; j < p; j++) fb[j] = __ldcs(f + m * p + j);
+#pragma unroll
+  for (int k = 0; k < p; k++) {
+    const double *h0 = H + k * p, *h1 = h0 + p * p, *h2 = h1 + p * p;
+    double lap = 0.0;
+#pragma unroll
+    for (int j = 0; j < p; j++) lap = fma(fma(m11, h0[j], fma(m12x2, h1[j], m22 * h2[j])), fb[j], lap);
+    vL[m * p + k] = fma(c2, lap, c1 * fb[k]);
+  }
+}
+
+void vp_launch_tri_local(vp_plan_s *P, const double *f) {
+  if (!P->tri_vL || P->M == 0) return;
+  const unsigned nb = (unsigned)((P->M + 127) / 128);
+  if (P->p == 12)
+    k_tri_local<12><<<nb, 128, 0, P->stream>>>(f, P->tri_ok, P->tri_M, P->tri_H, P->p, P->M, P->delta1, P->tri_c2,
+                                               P->tri_vL);
+  else
+    k_tri_local<0><<<nb, 128, 0, P->stream>>>(f, P->tri_ok, P->tri_M, P->tri_H, P->p, P->M, P->delta1, P->tri_c2,
+                                              P->tri_vL);
+  VP_CHECK_LAUNCH();
+  P->n_kernels++;
 }
 
 template <int W>
@@ -467,7 +711,7 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
   }
   k_interp_local<W, D><<<(unsigned)P->n_items, 256, sm, P->stream>>>(
       P->items, TSI, P->tx, P->ty, P->tperm, grid_args(P->nh), do_hist, f, P->lalpha, P->lnode, P->lidx, P->lw, P->K,
-      P->n_stencil, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr, P->tri_M, P->tri_H, P->p, P->tri_c2, out);
+      P->n_stencil, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr, P->tri_vL, out);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
@@ -558,6 +802,8 @@ void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
 }
 
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out) {
+  int parts_ = P->opts.parts ? P->opts.parts : VP_PART_ALL;
+  if (parts_ & VP_PART_LOCAL) vp_launch_tri_local(P, f);
   switch (P->w) {
 #define CASE(W) \
   case W: launch_interp_w<W>(P, f, out); break;

@@ -154,6 +154,7 @@ def test_config3_small_levels():
     one global delta_1 does not (R15)."""
     w = configs.config3(M_target=60000, lmin=7, lmax=13, g=0.1)
     idx = np.unique(np.concatenate([configs.sample_targets(w.T, 512, seed=33), _near_source_idx(w, 256, 34)]))
+    # steeper grading than the full config (g = 0.1): default C_min = 1.5
     ref = oracle.workload_potential(w, idx)
     plan, fd = make_plan(w)
     info = plan.info()
@@ -176,4 +177,33 @@ def test_config3_full_size_sampled():
     V = plan.eval(fd).cpu().numpy()
     e = rel_l2(V[idx], ref)
     print("config3 full rel l2", e, plan.info()["n_levels"], plan.info()["level_targets"][:8])
+    assert e <= 10 * w.tol
+
+
+# ------------------------------------------------------------------------------------ configs 4 / 5 (full size)
+def test_config4_full_size_sampled():
+    """4M uniform triangles, Fourier field |k| <= 64, tol 1e-10; TRIANGLE-mode jets (bench launch configuration)."""
+    from workloads import rule
+    w = configs.config4()
+    plan, fd = make_plan(w, ref_nodes=rule.BARY[:, 1:3])
+    V = plan.eval(fd).cpu().numpy()
+    idx = configs.sample_targets(w.T, 48, seed=41)
+    ref = oracle.workload_potential(w, idx)
+    e = rel_l2(V[idx], ref)
+    print("config4 rel l2", e, plan.info()["n_stencil_targets"])
+    assert e <= 10 * w.tol
+
+
+def test_config5_full_size_sampled():
+    """16M quadtree-graded triangles, 20 Gaussians, 192M node + 4M random targets, tol 1e-9.  Level bands are
+    off (levels=-1): delta_1 / sigma_min^2 = 0.016, so V_L[delta_1] is accurate without them."""
+    from workloads import rule
+    w = configs.config5()
+    plan, fd = make_plan(w, ref_nodes=rule.BARY[:, 1:3], levels=-1)
+    V = plan.eval(fd).cpu().numpy()
+    idx = np.unique(np.concatenate([configs.sample_targets(w.N, 48, seed=51),
+                                    w.N + configs.sample_targets(w.T - w.N, 16, seed=52)]))
+    ref = oracle.workload_potential(w, idx)
+    e = rel_l2(V[idx], ref)
+    print("config5 rel l2", e, plan.info()["n_stencil_targets"])
     assert e <= 10 * w.tol
