@@ -160,6 +160,7 @@ struct vp_plan_s {
   double *tri_H = nullptr;     // [3][p][p] reference cubic-fit Hessian operators
   double tri_c2 = 0;           // delta^2 / 2 (0 if series_order < 2)
   double *tri_vL = nullptr;    // [N] TRIANGLE-mode V_L per node (eval scratch; null outside TRIANGLE mode)
+  double *st_vL = nullptr;     // [n_stencil] stencil part of V_L per stencil slot (eval scratch)
   // host-side eval staging (vp_eval_host)
   double *f_dev = nullptr, *out_dev = nullptr;
   // profiling

@@ -319,7 +319,7 @@ void vp_build_levels(vp_plan_s *P, const double *nodes, const double *weights) {
   bg.y_lo = y_lo;
   double r_over_h = 8.0 * sqrt(zeps * lne) / VP_PI;  // sqrt(4 delta_{l-1} z) / h_l, level independent
   B.margin = (int)ceil(r_over_h) + P->w / 2 + 2;
-  B.nfb = vp_next_smooth(4 * (int64_t)B.margin);
+  B.nfb = vp_next_smooth(8 * (int64_t)B.margin);  // core = nfb - 2 margin ~ 3/4 nfb: ~1.8x box overlap
   B.core = (int)(B.nfb - 2 * B.margin);
   B.rowb = 2 * (B.nfb / 2 + 1);
   B.nmode = B.nfb / 2;

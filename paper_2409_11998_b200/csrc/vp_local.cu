@@ -422,6 +422,7 @@ void vp_build_local(vp_plan_s *P, const double *nodes_dev) {
     k_fill_ptr<<<(unsigned)((nst + 255) / 256), 256, 0, st>>>(list, nst, P->lptr);
     VP_CHECK_LAUNCH();
   }
+  P->st_vL = vp_alloc<double>(P, (size_t)std::max<int64_t>(nst, 1));
   P->lidx = vp_alloc<int32_t>(P, (size_t)std::max<int64_t>(nst, 1) * K);
   P->lw = vp_alloc<double>(P, (size_t)std::max<int64_t>(nst, 1) * K);
   int32_t *isb = nullptr;

@@ -82,72 +82,69 @@ __global__ void k_tile_heads(const uint64_t *__restrict__ k1, int64_t n, int32_t
   head[i] = (i == 0 || (k1[i - 1] >> 32) != (k1[i] >> 32)) ? 1 : 0;
 }
 
-// Greedy level assignment, one thread per non-empty tile: points in (row, column) order; a point
-// takes the lowest level whose last point in the same row ends at least W columns to its left.
-// Points of one level therefore never write the same grid cell within a footprint-row step.
-// Inside a level, points are then ordered rank-major over the shared-memory bank slot of their
-// footprint origin (res = (row * nw + col) mod 16, 16 slots of 8 B per 128 B wavefront): a chunk of
-// 32 consecutive points holds at most 2 points per slot when the slots are evenly populated, so the
-// row-step LDS/STS of a batch need ~2 wavefronts instead of the ~4-5 of random columns.
-#define VP_MAXLV 128
-#define VP_RANKLV 24
-__global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restrict__ tstart, int64_t ntile,
-                         int64_t n, int W, int nw, uint64_t *__restrict__ k2, int *__restrict__ overflow_flag) {
+// Batch packing, one thread per non-empty tile (plan time).  Points arrive in (footprint row, column)
+// order; each goes to the first open batch (of up to PK_B) where
+//   (hard) no point with the same footprint start row overlaps its W columns -- so inside a row step of
+//          k_spread_nh no two lanes touch the same shared-memory cell (no atomics needed), and
+//   (soft) its shared-memory bank slot (row * nw + col) mod 16 (16 slots of 8 B per 128 B wavefront) holds
+//          fewer than 2 points -- so a warp-wide LDS/STS of the batch needs ~2 wavefronts, the minimum for
+//          8-byte accesses.
+// A batch that reaches 32 points is closed.  Output key: tile << 40 | batch id (local to the tile).
+#define PK_B 32
+#define PK_ROWS 48
+__global__ void k_pack_batches(const uint64_t *__restrict__ k1, const int32_t *__restrict__ tstart, int64_t ntile,
+                               int64_t n, int W, int nw, uint64_t *__restrict__ k2, int *__restrict__ overflow_flag) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= ntile) return;
   int64_t s0 = tstart[t], s1 = (t + 1 < ntile) ? tstart[t + 1] : n;
-  int16_t last[VP_MAXLV];
-  uint16_t rank[VP_RANKLV][16];
-  for (int l = 0; l < VP_RANKLV; l++)
-    for (int r = 0; r < 16; r++) rank[l][r] = 0;
-  int cur_row = -1, nlv = 0, overflow = 0;
+  uint8_t rowend[PK_B][PK_ROWS];
+  uint8_t slot[PK_B][16];
+  uint8_t cnt[PK_B];
+  uint32_t bid[PK_B];
+  int nopen = 0;
+  uint32_t next_id = 0;
+  auto reset = [&](int b) {
+    for (int r = 0; r < PK_ROWS; r++) rowend[b][r] = 0;
+    for (int r = 0; r < 16; r++) slot[b][r] = 0;
+    cnt[b] = 0;
+    bid[b] = next_id++;
+  };
   for (int64_t i = s0; i < s1; i++) {
-    uint64_t key = k1[i];
-    int row = (int)((key >> 16) & 0xff), col = (int)(key & 0xff);
-    if (row != cur_row) {
-      cur_row = row;
-      nlv = 0;
-      overflow = 0;
-    }
-    int lv = -1;
-    for (int l = 0; l < nlv; l++)
-      if (last[l] <= col - W) { lv = l; break; }
-    if (lv < 0) {
-      if (nlv < VP_MAXLV) lv = nlv++;
-      else lv = VP_MAXLV + overflow++;
-    }
-    if (lv < VP_MAXLV) last[lv] = (int16_t)col;
-    // lv must stay exact (two points of one row never share a level): 20 bits; very dense rows (> 2^20
-    // points) are rejected at plan time by the caller's overflow check
+    const uint64_t key = k1[i];
+    const int row = (int)((key >> 16) & 0xff), col = (int)(key & 0xff);
+    if (row >= PK_ROWS || col + W > 255) { *overflow_flag = 1; continue; }
     const int res = (row * nw + col) & 15;
-    int rk = 0;
-    if (lv < VP_RANKLV) {
-      rk = rank[lv][res]++;
-      if (rk > 0xFFFF) rk = 0xFFFF;
+    int best = -1, soft = -1;
+    for (int b = 0; b < nopen; b++) {
+      if (rowend[b][row] <= col) {
+        if (slot[b][res] < 2) { best = b; break; }
+        if (soft < 0) soft = b;
+      }
     }
-    if (lv > 0xFFFFF) lv = 0xFFFFF, *overflow_flag = 1;
-    uint64_t tile = key >> 32;
-    k2[i] = (tile << 40) | ((uint64_t)lv << 20) | ((uint64_t)rk << 4) | (uint64_t)res;
+    if (best < 0) {
+      if (nopen < PK_B) {
+        best = nopen++;
+        reset(best);
+      } else if (soft >= 0) {
+        best = soft;
+      } else {  // every open batch conflicts on this row: close the fullest and start afresh in its place
+        best = 0;
+        for (int b = 1; b < PK_B; b++)
+          if (cnt[b] > cnt[best]) best = b;
+        reset(best);
+      }
+    }
+    k2[i] = ((key >> 32) << 40) | (uint64_t)bid[best];
+    rowend[best][row] = (uint8_t)(col + W);
+    slot[best][res]++;
+    if (++cnt[best] == 32) reset(best);
   }
 }
 
-// batch heads: new (tile, level) or every 32 points of one level
 __global__ void k_batch_heads(const uint64_t *__restrict__ k2, int64_t n, int32_t *__restrict__ head) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint64_t grp = k2[i] >> 20;
-  int h = 0;
-  if (i == 0 || (k2[i - 1] >> 20) != grp) {
-    h = 1;
-  } else {
-    int64_t lo = 0, hi = i;
-    while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if ((k2[mid] >> 20) < grp) lo = mid + 1; else hi = mid;
-    }
-    h = ((i - lo) % 32) == 0;
-  }
-  head[i] = h;
+  head[i] = (i == 0 || k2[i - 1] != k2[i]) ? 1 : 0;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -602,6 +599,7 @@ __global__ void __launch_bounds__(256) k_interp_local(const int4 *__restrict__ i
                                                       const int32_t *__restrict__ lidx, const double *__restrict__ lw,
                                                       int K, int64_t n_sten, int do_local, const int32_t *__restrict__ lptr,
                                                       const double *__restrict__ vL_tri,
+                                                      const double *__restrict__ vL_st,
                                                       double *__restrict__ out) {
   extern __shared__ double tile[];
   const int nw = TSI + W + 3;
@@ -636,12 +634,9 @@ __global__ void __launch_bounds__(256) k_interp_local(const int4 *__restrict__ i
       double vl = 0.0;
       const int32_t nd = lnode[t];
       const int32_t sp = lptr[t];
-      if (sp >= 0) {  // least-squares stencil, k-major: consecutive targets read consecutive slots
+      if (sp >= 0) {  // least-squares stencil, applied by k_local_stencil
         if (nd >= 0) vl = lalpha[t] * __ldg(f + nd);
-        const int32_t *ip = lidx + sp;
-        const double *wp = lw + sp;
-#pragma unroll 6
-        for (int k = 0; k < K; k++) vl = fma(__ldcs(wp + k * n_sten), __ldg(f + __ldcs(ip + k * n_sten)), vl);
+        vl += __ldcs(vL_st + sp);
       } else if (vL_tri) {  // own-triangle cubic fit, evaluated per node by k_tri_local
         vl = __ldg(vL_tri + nd);
       } else if (nd >= 0) {
@@ -682,7 +677,26 @@ __global__ void __launch_bounds__(128) k_tri_local(const double *__restrict__ f,
   }
 }
 
+// KNN-stencil local part, one thread per stencil slot: vL_st[s] = sum_k w[k][s] f[idx[k][s]] (k-major layout:
+// the warp streams consecutive slots, 12 B per entry, HBM-bound; f gathers hit L2)
+__global__ void __launch_bounds__(256) k_local_stencil(const int32_t *__restrict__ lidx, const double *__restrict__ lw,
+                                                       int K, int64_t S, const double *__restrict__ f,
+                                                       double *__restrict__ vL_st) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  double acc = 0.0;
+#pragma unroll 8
+  for (int k = 0; k < K; k++) acc = fma(__ldcs(lw + k * S + s), __ldg(f + __ldcs(lidx + k * S + s)), acc);
+  vL_st[s] = acc;
+}
+
 void vp_launch_tri_local(vp_plan_s *P, const double *f) {
+  if (P->n_stencil > 0 && P->st_vL) {
+    k_local_stencil<<<(unsigned)((P->n_stencil + 255) / 256), 256, 0, P->stream>>>(P->lidx, P->lw, P->K, P->n_stencil,
+                                                                                   f, P->st_vL);
+    VP_CHECK_LAUNCH();
+    P->n_kernels++;
+  }
   if (!P->tri_vL || P->M == 0) return;
   const unsigned nb = (unsigned)((P->M + 127) / 128);
   if (P->p == 12)
@@ -711,7 +725,7 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
   }
   k_interp_local<W, D><<<(unsigned)P->n_items, 256, sm, P->stream>>>(
       P->items, TSI, P->tx, P->ty, P->tperm, grid_args(P->nh), do_hist, f, P->lalpha, P->lnode, P->lidx, P->lw, P->K,
-      P->n_stencil, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr, P->tri_vL, out);
+      P->n_stencil, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr, P->tri_vL, P->st_vL, out);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
@@ -880,14 +894,14 @@ void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const
     int *d_ovf;
     VP_CUDA(cudaMallocAsync(&d_ovf, sizeof(int), s));
     VP_CUDA(cudaMemsetAsync(d_ovf, 0, sizeof(int), s));
-    k_levels<<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(k1s, tst, nt, n, P->w, Tl.TS + P->w + 3, k2, d_ovf);
+    k_pack_batches<<<(unsigned)((nt + 63) / 64), 64, 0, s>>>(k1s, tst, nt, n, P->w, Tl.TS + P->w + 3, k2, d_ovf);
     VP_CHECK_LAUNCH();
     int h_ovf = 0;
     VP_CUDA(cudaMemcpyAsync(&h_ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
     VP_CUDA(cudaStreamSynchronize(s));
     VP_CUDA(cudaFreeAsync(d_ovf, s));
     if (h_ovf) {
-      vp_set_last_error("more than 2^20 points share one footprint row of a spreading tile");
+      vp_set_last_error("spreading tile key out of range");
       throw VpError{VP_ERR_UNSUPPORTED};
     }
     for (void *p : {(void *)tst, (void *)d_nt, tmp3}) VP_CUDA(cudaFreeAsync(p, s));

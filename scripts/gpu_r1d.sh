@@ -1,0 +1,11 @@
+set -x
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 2000 python -m pytest tests -m gpu -q -s > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo bench=$?
+timeout 900 python bench.py --steps 5 --warmup 3 --config c5 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo bench5=$?
+timeout 900 python bench.py --steps 5 --warmup 3 --config c3 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo bench3=$?
+timeout 900 python bench.py --steps 5 --warmup 3 --config c4 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo bench4=$?
+timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_spread_nh|k_interp_local|k_restrict_x_int|k_prolong_x_int|k_tri" -s 5 -c 5 -o gpurun_out/prof_c2d python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
+timeout 900 python bench.py --steps 2 --warmup 3 --config c5 --no-cpu-baseline > gpurun_out/plain5.log 2>&1 && \
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5.csv python bench.py --steps 2 --warmup 3 --config c5 --no-cpu-baseline > gpurun_out/ncu_launch5.log 2>&1; echo ncu5=$?
