@@ -82,69 +82,69 @@ __global__ void k_tile_heads(const uint64_t *__restrict__ k1, int64_t n, int32_t
   head[i] = (i == 0 || (k1[i - 1] >> 32) != (k1[i] >> 32)) ? 1 : 0;
 }
 
-// Batch packing, one thread per non-empty tile (plan time).  Points arrive in (footprint row, column)
-// order; each goes to the first open batch (of up to PK_B) where
-//   (hard) no point with the same footprint start row overlaps its W columns -- so inside a row step of
-//          k_spread_nh no two lanes touch the same shared-memory cell (no atomics needed), and
-//   (soft) its shared-memory bank slot (row * nw + col) mod 16 (16 slots of 8 B per 128 B wavefront) holds
-//          fewer than 2 points -- so a warp-wide LDS/STS of the batch needs ~2 wavefronts, the minimum for
-//          8-byte accesses.
-// A batch that reaches 32 points is closed.  Output key: tile << 40 | batch id (local to the tile).
-#define PK_B 32
-#define PK_ROWS 48
-__global__ void k_pack_batches(const uint64_t *__restrict__ k1, const int32_t *__restrict__ tstart, int64_t ntile,
-                               int64_t n, int W, int nw, uint64_t *__restrict__ k2, int *__restrict__ overflow_flag) {
+// Level assignment, one thread per non-empty tile: points of one footprint row that share a level are
+// >= W columns apart, so points of one level never write the same grid cell within a row step.
+// Inside a level, points are then ordered rank-major over the shared-memory bank slot of their
+// footprint origin (res = (row * nw + col) mod 16, 16 slots of 8 B per 128 B wavefront): a chunk of
+// 32 consecutive points holds at most 2 points per slot when the slots are evenly populated, so the
+// row-step LDS/STS of a batch need ~2 wavefronts instead of the ~4-5 of random columns.
+#define VP_RANKLV 24
+__global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restrict__ tstart, int64_t ntile,
+                         int64_t n, int W, int nw, uint64_t *__restrict__ k2, int *__restrict__ overflow_flag) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= ntile) return;
-  int64_t s0 = tstart[t], s1 = (t + 1 < ntile) ? tstart[t + 1] : n;
-  uint8_t rowend[PK_B][PK_ROWS];
-  uint8_t slot[PK_B][16];
-  uint8_t cnt[PK_B];
-  uint32_t bid[PK_B];
-  int nopen = 0;
-  uint32_t next_id = 0;
-  auto reset = [&](int b) {
-    for (int r = 0; r < PK_ROWS; r++) rowend[b][r] = 0;
-    for (int r = 0; r < 16; r++) slot[b][r] = 0;
-    cnt[b] = 0;
-    bid[b] = next_id++;
-  };
-  for (int64_t i = s0; i < s1; i++) {
-    const uint64_t key = k1[i];
-    const int row = (int)((key >> 16) & 0xff), col = (int)(key & 0xff);
-    if (row >= PK_ROWS || col + W > 255) { *overflow_flag = 1; continue; }
-    const int res = (row * nw + col) & 15;
-    int best = -1, soft = -1;
-    for (int b = 0; b < nopen; b++) {
-      if (rowend[b][row] <= col) {
-        if (slot[b][res] < 2) { best = b; break; }
-        if (soft < 0) soft = b;
-      }
+  const int64_t s0 = tstart[t], s1 = (t + 1 < ntile) ? tstart[t + 1] : n;
+  uint16_t rank[VP_RANKLV][16];
+  for (int l = 0; l < VP_RANKLV; l++)
+    for (int r = 0; r < 16; r++) rank[l][r] = 0;
+  const uint64_t tile = k1[s0] >> 32;
+  // rows are contiguous (keys sorted by tile, row, column).  With K = the largest number of points of the row
+  // inside any W-column window, level = (index in the row) mod K is a valid assignment (points i and i + K
+  // are >= W columns apart) and uses the minimum number of levels (the maximum overlap).
+  for (int64_t r0 = s0; r0 < s1;) {
+    const uint64_t row_key = (k1[r0] >> 16) & 0xff;
+    int64_t r1 = r0;
+    while (r1 < s1 && ((k1[r1] >> 16) & 0xff) == row_key) r1++;
+    int64_t K = 1;
+    for (int64_t i = r0, j = r0; i < r1; i++) {  // window [col_i, col_i + W): points j..i with col_j > col_i - W
+      const int ci = (int)(k1[i] & 0xff);
+      while ((int)(k1[j] & 0xff) <= ci - W) j++;
+      if (i - j + 1 > K) K = i - j + 1;
     }
-    if (best < 0) {
-      if (nopen < PK_B) {
-        best = nopen++;
-        reset(best);
-      } else if (soft >= 0) {
-        best = soft;
-      } else {  // every open batch conflicts on this row: close the fullest and start afresh in its place
-        best = 0;
-        for (int b = 1; b < PK_B; b++)
-          if (cnt[b] > cnt[best]) best = b;
-        reset(best);
+    if (K > 0xFFFFF) *overflow_flag = 1;
+    const int row = (int)row_key;
+    for (int64_t i = r0; i < r1; i++) {
+      const int col = (int)(k1[i] & 0xff);
+      const int lv = (int)((i - r0) % K);
+      const int res = (row * nw + col) & 15;
+      int rk = 0;
+      if (lv < VP_RANKLV) {
+        rk = rank[lv][res]++;
+        if (rk > 0xFFFF) rk = 0xFFFF;
       }
+      k2[i] = (tile << 40) | ((uint64_t)(lv & 0xFFFFF) << 20) | ((uint64_t)rk << 4) | (uint64_t)res;
     }
-    k2[i] = ((key >> 32) << 40) | (uint64_t)bid[best];
-    rowend[best][row] = (uint8_t)(col + W);
-    slot[best][res]++;
-    if (++cnt[best] == 32) reset(best);
+    r0 = r1;
   }
 }
 
+// batch heads: new (tile, level) or every 32 points of one level
 __global__ void k_batch_heads(const uint64_t *__restrict__ k2, int64_t n, int32_t *__restrict__ head) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  head[i] = (i == 0 || k2[i - 1] != k2[i]) ? 1 : 0;
+  uint64_t grp = k2[i] >> 20;
+  int h = 0;
+  if (i == 0 || (k2[i - 1] >> 20) != grp) {
+    h = 1;
+  } else {
+    int64_t lo = 0, hi = i;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if ((k2[mid] >> 20) < grp) lo = mid + 1; else hi = mid;
+    }
+    h = ((i - lo) % 32) == 0;
+  }
+  head[i] = h;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -894,14 +894,14 @@ void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const
     int *d_ovf;
     VP_CUDA(cudaMallocAsync(&d_ovf, sizeof(int), s));
     VP_CUDA(cudaMemsetAsync(d_ovf, 0, sizeof(int), s));
-    k_pack_batches<<<(unsigned)((nt + 63) / 64), 64, 0, s>>>(k1s, tst, nt, n, P->w, Tl.TS + P->w + 3, k2, d_ovf);
+    k_levels<<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(k1s, tst, nt, n, P->w, Tl.TS + P->w + 3, k2, d_ovf);
     VP_CHECK_LAUNCH();
     int h_ovf = 0;
     VP_CUDA(cudaMemcpyAsync(&h_ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
     VP_CUDA(cudaStreamSynchronize(s));
     VP_CUDA(cudaFreeAsync(d_ovf, s));
     if (h_ovf) {
-      vp_set_last_error("spreading tile key out of range");
+      vp_set_last_error("more than 2^20 points share one footprint row of a spreading tile");
       throw VpError{VP_ERR_UNSUPPORTED};
     }
     for (void *p : {(void *)tst, (void *)d_nt, tmp3}) VP_CUDA(cudaFreeAsync(p, s));
