@@ -89,6 +89,10 @@ typedef struct {
   int32_t levels;
   double level_cmin;         /* 0 -> 1.5 */
   double level_rho;          /* 0 -> 4 */
+  /* 1: bit-reproducible vp_eval.  The only order-dependent step of the default path is the fp64 atomic add of
+   * spreading-tile halos into the grid; this mode launches the spreading once per tile colour (tx & 1, ty & 1)
+   * with one work item per tile and plain read-add-write (slower on dense tiles). */
+  int32_t deterministic;
 } vp_opts;
 
 /* Plan parameters chosen by vp_plan (diagnostics; all derived from the rules in DESIGN.md). */

@@ -179,9 +179,11 @@ static void setup_grid(vp_plan_s *P, VpGrid &G, int kind, double L, double kmax)
   G.h = L / (double)G.nf;
   G.ox = P->cx - 0.5 * L;
   G.oy = P->cy - 0.5 * L;
-  G.row = 2 * (G.nf / 2 + 1);
-  if ((double)G.nf * (double)G.row * 8.0 > 120e9) throw VpError{VP_ERR_OOM};
+  G.row = G.nf;                 // real grid rows (unpadded); the half spectrum lives in G.cdata
+  G.crow = 2 * (G.nf / 2 + 1);  // doubles per half-spectrum row
+  if ((double)G.nf * (double)(G.row + G.crow) * 8.0 > 120e9) throw VpError{VP_ERR_OOM};
   G.data = vp_alloc<double>(P, (size_t)G.nf * G.row);
+  G.cdata = vp_alloc<double>(P, (size_t)G.nf * G.crow);
 }
 
 // Far-history grid on the NH lattice: spacing h2 = m h1 (integer m), origin on an NH
@@ -204,11 +206,13 @@ static void setup_grid_fh(vp_plan_s *P, VpGrid &G, double L_req, double kmax) {
   const int64_t j = llround((N.ox - (P->cx - 0.5 * G.L)) / N.h);
   G.ox = N.ox - (double)j * N.h;
   G.oy = N.oy - (double)j * N.h;
-  G.row = 2 * (G.nf / 2 + 1);
+  G.row = G.nf;
+  G.crow = 2 * (G.nf / 2 + 1);
   P->fh_ratio = (int)m;
   P->fh_shift = j;
-  if ((double)G.nf * (double)G.row * 8.0 > 120e9) throw VpError{VP_ERR_OOM};
+  if ((double)G.nf * (double)(G.row + G.crow) * 8.0 > 120e9) throw VpError{VP_ERR_OOM};
   G.data = vp_alloc<double>(P, (size_t)G.nf * G.row);
+  G.cdata = vp_alloc<double>(P, (size_t)G.nf * G.crow);
 }
 
 // 1D transform of the ES kernel at spacing h: Phi(k) = 2 alpha int_0^1 psi(s) cos(k alpha s) ds, alpha = w h/2
@@ -369,15 +373,15 @@ static void make_fft_plans(vp_plan_s *P) {
   for (int g = 0; g < 2; g++) {
     VpGrid &G = *gs[g];
     long long n[2] = {G.nf, G.nf};
-    long long rin[2] = {G.nf, G.row};         // real layout (padded rows)
-    long long cin[2] = {G.nf, G.row / 2};     // complex layout
+    long long rin[2] = {G.nf, G.row};         // real layout
+    long long cin[2] = {G.nf, G.crow / 2};    // complex layout
     VP_CUFFT(cufftCreate(&G.fwd));
     VP_CUFFT(cufftCreate(&G.inv));
     VP_CUFFT(cufftSetAutoAllocation(G.fwd, 0));
     VP_CUFFT(cufftSetAutoAllocation(G.inv, 0));
-    VP_CUFFT(cufftMakePlanMany64(G.fwd, 2, n, rin, 1, G.nf * G.row, cin, 1, G.nf * (G.row / 2), CUFFT_D2Z, 1,
+    VP_CUFFT(cufftMakePlanMany64(G.fwd, 2, n, rin, 1, G.nf * G.row, cin, 1, G.nf * (G.crow / 2), CUFFT_D2Z, 1,
                                  &ws[2 * g]));
-    VP_CUFFT(cufftMakePlanMany64(G.inv, 2, n, cin, 1, G.nf * (G.row / 2), rin, 1, G.nf * G.row, CUFFT_Z2D, 1,
+    VP_CUFFT(cufftMakePlanMany64(G.inv, 2, n, cin, 1, G.nf * (G.crow / 2), rin, 1, G.nf * G.row, CUFFT_Z2D, 1,
                                  &ws[2 * g + 1]));
     G.has_plans = true;
   }
@@ -497,6 +501,8 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     setup_deconv(P);
     setup_restriction(P);
     // ---- sources and targets sorted by NH tile
+    P->sp.det = o.deterministic ? 1 : 0;
+    P->bands.sp.det = P->sp.det;
     vp_build_spread_order(P, P->sp, tri_nodes, weights, nullptr, N, grid_args(P->nh));
     vp_build_interp_order(P, targets, T);
     // ---- graded meshes: per-target levels and band boxes (a12)
@@ -571,14 +577,14 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
       record(P, 2);
       vp_launch_restrict(P);
       record(P, 3);
-      VP_CUFFT(cufftExecD2Z(P->nh.fwd, P->nh.data, (cufftDoubleComplex *)P->nh.data));
-      VP_CUFFT(cufftExecD2Z(P->fh.fwd, P->fh.data, (cufftDoubleComplex *)P->fh.data));
+      VP_CUFFT(cufftExecD2Z(P->nh.fwd, P->nh.data, (cufftDoubleComplex *)P->nh.cdata));
+      VP_CUFFT(cufftExecD2Z(P->fh.fwd, P->fh.data, (cufftDoubleComplex *)P->fh.cdata));
       record(P, 4);
       vp_launch_multiply(P, P->nh);
       vp_launch_multiply(P, P->fh);
       record(P, 5);
-      VP_CUFFT(cufftExecZ2D(P->nh.inv, (cufftDoubleComplex *)P->nh.data, P->nh.data));
-      VP_CUFFT(cufftExecZ2D(P->fh.inv, (cufftDoubleComplex *)P->fh.data, P->fh.data));
+      VP_CUFFT(cufftExecZ2D(P->nh.inv, (cufftDoubleComplex *)P->nh.cdata, P->nh.data));
+      VP_CUFFT(cufftExecZ2D(P->fh.inv, (cufftDoubleComplex *)P->fh.cdata, P->fh.data));
       record(P, 6);
       vp_launch_prolong(P);
       P->n_ffts = 4;

@@ -52,11 +52,13 @@ struct VpHorner {
 struct VpGrid {
   int64_t nf = 0;     // fine points per dimension (even, 2,3,5,7-smooth)
   int64_t nmode = 0;  // kept modes per dimension (even); |m| <= nmode/2
-  int64_t row = 0;    // padded row length in doubles for in-place R2C: 2*(nf/2+1)
+  int64_t row = 0;    // real grid row length in doubles (nf)
+  int64_t crow = 0;   // half-spectrum row length in doubles: 2 (nf/2 + 1)
   double L = 0, h = 0, ox = 0, oy = 0;
   double delta_a = 0, delta_b = 0;  // NH: (delta1, delta2); FH: (delta2, R)
   int kind = 0;                     // 0 = near history, 1 = far history
-  double *data = nullptr;           // nf * row doubles
+  double *data = nullptr;           // nf * row doubles (real grid)
+  double *cdata = nullptr;          // nf * crow doubles (half spectrum; out-of-place D2Z / Z2D)
   double *deconv = nullptr;         // [nmode/2+1]: 1 / Phi(k_m)^2 (1D kernel transform, squared inverse)
   double mult_scale = 0;            // h^2 / nf^2 (NH);  h2^2 h1^4 / nf2^2 (FH, two-stage kernel)
   cufftHandle fwd = 0, inv = 0;
@@ -87,6 +89,8 @@ struct VpSpreadSet {
   int32_t *bstart = nullptr;                           // batch starts (n_batches + 1)
   int64_t n_batches = 0;
   VpTiles tiles;
+  int det = 0;                 // deterministic mode: items sorted by tile colour, colour_off[c]..colour_off[c+1]
+  int64_t color_off[5] = {};
 };
 
 // Level-band corrections for graded meshes: per-target level

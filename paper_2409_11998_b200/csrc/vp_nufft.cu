@@ -18,6 +18,8 @@
 // ES kernel values come from per-tap Horner polynomials (vp_common.cuh VpHorner), degree ~ W-1.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "vp_common.cuh"
 #include "vp_math.cuh"
 
@@ -153,7 +155,7 @@ template <int W, int D>
 __global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items, const int32_t *__restrict__ bstart,
                                                   const double *__restrict__ sx, const double *__restrict__ sy,
                                                   const double *__restrict__ sw, const int32_t *__restrict__ sperm,
-                                                  const double *__restrict__ f, GridArgs g, int TS) {
+                                                  const double *__restrict__ f, GridArgs g, int TS, int det) {
   extern __shared__ double tile[];
   const int nw = TS + W + 3;
   const int lane = threadIdx.x;
@@ -198,7 +200,8 @@ __global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items
           gx = wrapi(gx, g.nfx);
           gy = wrapi(gy, g.nfy);
         }
-        atomicAdd(g.data + gy * g.row + gx, v);
+        if (det) g.data[gy * g.row + gx] += v;  // colour-separated launch: no concurrent writer
+        else atomicAdd(g.data + gy * g.row + gx, v);
       }
     }
   }
@@ -210,10 +213,23 @@ static void launch_spread_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &
   int nw = S.tiles.TS + W + 3;
   size_t sm = sizeof(double) * (size_t)nw * nw;
   if (S.tiles.nsub == 0) return;
-  k_spread_nh<W, D><<<(unsigned)S.tiles.nsub, 32, sm, P->stream>>>(S.tiles.sub, S.bstart, S.sx, S.sy, S.sw, S.sperm,
-                                                                   f, g, S.tiles.TS);
-  VP_CHECK_LAUNCH();
-  P->n_kernels++;
+  if (!S.det) {
+    k_spread_nh<W, D><<<(unsigned)S.tiles.nsub, 32, sm, P->stream>>>(S.tiles.sub, S.bstart, S.sx, S.sy, S.sw,
+                                                                     S.sperm, f, g, S.tiles.TS, 0);
+    VP_CHECK_LAUNCH();
+    P->n_kernels++;
+    return;
+  }
+  // deterministic mode: one item per tile, four launches by tile colour (tx & 1, ty & 1); tiles of one colour
+  // have disjoint windows, so the plain read-add-write of each cell has a fixed order
+  for (int c = 0; c < 4; c++) {
+    const int64_t i0 = S.color_off[c], i1 = S.color_off[c + 1];
+    if (i1 <= i0) continue;
+    k_spread_nh<W, D><<<(unsigned)(i1 - i0), 32, sm, P->stream>>>(S.tiles.sub + i0, S.bstart, S.sx, S.sy, S.sw,
+                                                                  S.sperm, f, g, S.tiles.TS, 1);
+    VP_CHECK_LAUNCH();
+    P->n_kernels++;
+  }
 }
 
 void vp_launch_spread(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *f) {
@@ -577,7 +593,7 @@ void vp_launch_multiply(vp_plan_s *P, VpGrid &G) {
   int64_t total = G.nf * ncol;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   double dk = 2.0 * VP_PI / G.L;
-  k_multiply<<<blocks, 256, 0, P->stream>>>(G.data, G.nf, G.row, G.nmode / 2, G.deconv, dk, G.mult_scale, G.kind,
+  k_multiply<<<blocks, 256, 0, P->stream>>>(G.cdata, G.nf, G.crow, G.nmode / 2, G.deconv, dk, G.mult_scale, G.kind,
                                             G.delta_a, G.delta_b);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
@@ -930,13 +946,20 @@ void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const
     }
   int64_t nbat = (int64_t)bst.size();
   bst.push_back((int32_t)n);
-  const int MAXB = 48;  // batches per warp work item
+  const int64_t MAXB = S.det ? INT64_MAX : 48;  // batches per warp work item (deterministic: whole tile)
   std::vector<int4> items;
   for (int64_t b = 0; b < nbat;) {
     int64_t t = btile[b], e = b;
     while (e < nbat && btile[e] == t && e - b < MAXB) e++;
     items.push_back(make_int4((int)(t % Tl.ntx), (int)(t / Tl.ntx), (int)b, (int)e));
     b = e;
+  }
+  if (S.det) {
+    std::stable_sort(items.begin(), items.end(),
+                     [](const int4 &a, const int4 &b) { return ((a.x & 1) | ((a.y & 1) << 1)) < ((b.x & 1) | ((b.y & 1) << 1)); });
+    for (int c = 0; c <= 4; c++) S.color_off[c] = 0;
+    for (const int4 &it : items) S.color_off[((it.x & 1) | ((it.y & 1) << 1)) + 1]++;
+    for (int c = 0; c < 4; c++) S.color_off[c + 1] += S.color_off[c];
   }
   S.n_batches = nbat;
   S.bstart = vp_alloc<int32_t>(P, bst.size());
