@@ -504,6 +504,8 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     P->sp.det = o.deterministic ? 1 : 0;
     P->bands.sp.det = P->sp.det;
     vp_build_spread_order(P, P->sp, tri_nodes, weights, nullptr, N, grid_args(P->nh));
+    P->dmode = o.deriv_mode;
+    if (P->dmode == VP_DERIV_AUTO) P->dmode = (o.ref_nodes && N > 10000000) ? VP_DERIV_TRIANGLE : VP_DERIV_KNN;
     vp_build_interp_order(P, targets, T);
     // ---- graded meshes: per-target levels and band boxes (a12)
     int parts = o.parts ? o.parts : VP_PART_ALL;
@@ -514,8 +516,6 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
       VP_CUDA(cudaMemsetAsync(P->bands.tlev, 0, T, P->stream));
     }
     // ---- local part
-    P->dmode = o.deriv_mode;
-    if (P->dmode == VP_DERIV_AUTO) P->dmode = (o.ref_nodes && N > 10000000) ? VP_DERIV_TRIANGLE : VP_DERIV_KNN;
     if (P->dmode == VP_DERIV_TRIANGLE && (!o.ref_nodes || p < 10 || p > VP_TRI_MAXP || !o.targets_are_nodes))
       throw VpError{VP_ERR_UNSUPPORTED};
     if (P->dmode != VP_DERIV_KNN && P->dmode != VP_DERIV_TRIANGLE) throw VpError{VP_ERR_ARG};

@@ -90,15 +90,11 @@ __global__ void k_tile_heads(const uint64_t *__restrict__ k1, int64_t n, int32_t
 // footprint origin (res = (row * nw + col) mod 16, 16 slots of 8 B per 128 B wavefront): a chunk of
 // 32 consecutive points holds at most 2 points per slot when the slots are evenly populated, so the
 // row-step LDS/STS of a batch need ~2 wavefronts instead of the ~4-5 of random columns.
-#define VP_RANKLV 24
 __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restrict__ tstart, int64_t ntile,
                          int64_t n, int W, int nw, uint64_t *__restrict__ k2, int *__restrict__ overflow_flag) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= ntile) return;
   const int64_t s0 = tstart[t], s1 = (t + 1 < ntile) ? tstart[t + 1] : n;
-  uint16_t rank[VP_RANKLV][16];
-  for (int l = 0; l < VP_RANKLV; l++)
-    for (int r = 0; r < 16; r++) rank[l][r] = 0;
   const uint64_t tile = k1[s0] >> 32;
   // rows are contiguous (keys sorted by tile, row, column).  With K = the largest number of points of the row
   // inside any W-column window, level = (index in the row) mod K is a valid assignment (points i and i + K
@@ -119,15 +115,27 @@ __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restr
       const int col = (int)(k1[i] & 0xff);
       const int lv = (int)((i - r0) % K);
       const int res = (row * nw + col) & 15;
-      int rk = 0;
-      if (lv < VP_RANKLV) {
-        rk = rank[lv][res]++;
-        if (rk > 0xFFFF) rk = 0xFFFF;
-      }
-      k2[i] = (tile << 40) | ((uint64_t)(lv & 0xFFFFF) << 20) | ((uint64_t)rk << 4) | (uint64_t)res;
+      k2[i] = (tile << 40) | ((uint64_t)(lv & 0xFFFFF) << 20) | (uint64_t)res;  // rank bits filled by k_bank_rank
     }
     r0 = r1;
   }
+}
+
+// rank of a point inside its (tile, level, bank slot) group (keys sorted, rank bits zero): sorting by
+// (tile, level, rank, slot) then interleaves the slots, so 32 consecutive points hold <= 2 per slot when the
+// group's slots are evenly populated
+__global__ void k_bank_rank(const uint64_t *__restrict__ ks, int64_t n, uint64_t *__restrict__ kr) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t key = ks[i];
+  int64_t lo = 0, hi = i;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (ks[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  uint64_t rank = (uint64_t)(i - lo);
+  if (rank > 0xFFFF) rank = 0xFFFF;
+  kr[i] = key | (rank << 4);
 }
 
 // batch heads: new (tile, level) or every 32 points of one level
@@ -780,6 +788,23 @@ __global__ void k_interp_keys2(const uint64_t *__restrict__ k1, int64_t n, uint6
   k2[i] = ((key >> 4) << 24) | (rank << 4) | (key & 15);
 }
 
+// TRIANGLE mode: node targets ordered by (tile, triangle, node) so that the per-node V_L reads of a warp are
+// runs of p consecutive nodes (coalesced); other targets follow inside their tile
+__global__ void k_interp_keys_tri(const double *__restrict__ xy, int64_t n, GridArgs g, int TSI, int64_t ntx,
+                                  int64_t nty, int64_t node_targets, int p, uint64_t *__restrict__ keys,
+                                  int32_t *__restrict__ idx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double gx = gcoord(xy[2 * i], g.ox, g.inv_h), gy = gcoord(xy[2 * i + 1], g.oy, g.inv_h);
+  int64_t tx = (int64_t)floor(gx / TSI), ty = (int64_t)floor(gy / TSI);
+  tx = tx < 0 ? 0 : (tx >= ntx ? ntx - 1 : tx);
+  ty = ty < 0 ? 0 : (ty >= nty ? nty - 1 : ty);
+  const uint64_t tri = i < node_targets ? (uint64_t)(i / p) : 0xFFFFFFFFull;
+  const uint64_t k = i < node_targets ? (uint64_t)(i % p) : 0;
+  keys[i] = ((uint64_t)(ty * ntx + tx) << 36) | (tri << 4) | k;
+  idx[i] = (int32_t)i;
+}
+
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
   cudaStream_t s = P->stream;
   const GridArgs g = grid_args(P->nh);
@@ -795,17 +820,27 @@ void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
   VP_CUDA(cudaMallocAsync(&i1s, 4 * (n + 1), s));
   VP_CUDA(cudaMallocAsync(&i2s, 4 * (n + 1), s));
   unsigned nb = (unsigned)((n + 255) / 256);
-  k_interp_keys1<<<nb, 256, 0, s>>>(xy, n, g, TSI, P->w, ntx, nty, k1, i1);
-  VP_CHECK_LAUNCH();
+  const bool tri_order = P->dmode == VP_DERIV_TRIANGLE && P->opts.targets_are_nodes && P->p <= 16 &&
+                         P->M < ((int64_t)1 << 32) && ntx * nty < ((int64_t)1 << 28);
   size_t tb = 0, tb2 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s);
   cub::DeviceRadixSort::SortPairs(nullptr, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s);
   void *tmp;
   VP_CUDA(cudaMallocAsync(&tmp, std::max(tb, tb2) + 16, s));
-  VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
-  k_interp_keys2<<<nb, 256, 0, s>>>(k1s, n, k2);
-  VP_CHECK_LAUNCH();
-  VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
+  int tile_shift = 24;
+  if (tri_order) {
+    k_interp_keys_tri<<<nb, 256, 0, s>>>(xy, n, g, TSI, ntx, nty, P->N, P->p, k1, i1);
+    VP_CHECK_LAUNCH();
+    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k2s, i1, i2s, (int)n, 0, 64, s));
+    tile_shift = 36;
+  } else {
+    k_interp_keys1<<<nb, 256, 0, s>>>(xy, n, g, TSI, P->w, ntx, nty, k1, i1);
+    VP_CHECK_LAUNCH();
+    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
+    k_interp_keys2<<<nb, 256, 0, s>>>(k1s, n, k2);
+    VP_CHECK_LAUNCH();
+    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
+  }
   P->tx = vp_alloc<double>(P, n);
   P->ty = vp_alloc<double>(P, n);
   P->tperm = vp_alloc<int64_t>(P, n);
@@ -816,9 +851,9 @@ void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
   VP_CUDA(cudaStreamSynchronize(s));
   std::vector<int4> items;
   for (int64_t i = 0; i < n;) {
-    const uint64_t tile = hk[i] >> 24;
+    const uint64_t tile = hk[i] >> tile_shift;
     int64_t e = i;
-    while (e < n && (hk[e] >> 24) == tile) e++;
+    while (e < n && (hk[e] >> tile_shift) == tile) e++;
     for (int64_t c = i; c < e; c += VP_INTERP_CHUNK)
       items.push_back(make_int4((int)(tile % ntx), (int)(tile / ntx), (int)c, (int)std::min<int64_t>(e, c + VP_INTERP_CHUNK)));
     i = e;
@@ -922,7 +957,12 @@ void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const
     }
     for (void *p : {(void *)tst, (void *)d_nt, tmp3}) VP_CUDA(cudaFreeAsync(p, s));
   }
+  // (tile, level, slot) order -> bank ranks -> (tile, level, rank, slot) order
   VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
+  k_bank_rank<<<nb, 256, 0, s>>>(k2s, n, k2);
+  VP_CHECK_LAUNCH();
+  VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i2s, i1s, (int)n, 0, 64, s));
+  std::swap(i1s, i2s);
   k_batch_heads<<<nb, 256, 0, s>>>(k2s, n, head);
   VP_CHECK_LAUNCH();
   S.sx = vp_alloc<double>(P, n);
