@@ -90,21 +90,78 @@ __global__ void k_tile_heads(const uint64_t *__restrict__ k1, int64_t n, int32_t
 // footprint origin (res = (row * nw + col) mod 16, 16 slots of 8 B per 128 B wavefront): a chunk of
 // 32 consecutive points holds at most 2 points per slot when the slots are evenly populated, so the
 // row-step LDS/STS of a batch need ~2 wavefronts instead of the ~4-5 of random columns.
+#define PK_B 32
+#define PK_ROWS 48
 __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restrict__ tstart, int64_t ntile,
                          int64_t n, int W, int nw, uint64_t *__restrict__ k2, int *__restrict__ overflow_flag) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= ntile) return;
   const int64_t s0 = tstart[t], s1 = (t + 1 < ntile) ? tstart[t + 1] : n;
   const uint64_t tile = k1[s0] >> 32;
-  // rows are contiguous (keys sorted by tile, row, column).  With K = the largest number of points of the row
-  // inside any W-column window, level = (index in the row) mod K is a valid assignment (points i and i + K
-  // are >= W columns apart) and uses the minimum number of levels (the maximum overlap).
+  // sparse tile (every row has few points): greedy packing into <= PK_B open batches of <= 32 points, first
+  // batch whose row is free at these columns and whose bank slot holds < 2 points -> full batches
+  int64_t maxrow = 0;
+  for (int64_t r0 = s0; r0 < s1;) {
+    int64_t r1 = r0;
+    const uint64_t rk = (k1[r0] >> 16) & 0xff;
+    while (r1 < s1 && ((k1[r1] >> 16) & 0xff) == rk) r1++;
+    if (r1 - r0 > maxrow) maxrow = r1 - r0;
+    r0 = r1;
+  }
+  if (maxrow <= 2 * PK_B && s1 - s0 <= 8192) {
+    uint8_t rowend[PK_B][PK_ROWS];
+    uint8_t slot[PK_B][16];
+    uint8_t cnt[PK_B];
+    uint32_t bid[PK_B];
+    int nopen = 0;
+    uint32_t next_id = 0;
+    bool ok = true;
+    for (int64_t i = s0; i < s1 && ok; i++) {
+      const int row = (int)((k1[i] >> 16) & 0xff), col = (int)(k1[i] & 0xff);
+      if (row >= PK_ROWS || col + W > 255) { ok = false; break; }
+      const int res = (row * nw + col) & 15;
+      int best = -1, soft = -1;
+      for (int b = 0; b < nopen; b++) {
+        if (rowend[b][row] <= col) {
+          if (slot[b][res] < 2) { best = b; break; }
+          if (soft < 0) soft = b;
+        }
+      }
+      if (best < 0) {
+        if (soft >= 0) {
+          best = soft;  // a bank-slot repeat costs one extra wavefront; a new batch costs a whole row sweep
+        } else if (nopen < PK_B) {
+          best = nopen++;
+          for (int r = 0; r < PK_ROWS; r++) rowend[best][r] = 0;
+          for (int r = 0; r < 16; r++) slot[best][r] = 0;
+          cnt[best] = 0;
+          bid[best] = next_id++;
+        } else {  // every open batch is taken on this row: use the level scheme for this tile
+          ok = false;
+          break;
+        }
+      }
+      k2[i] = (tile << 40) | ((uint64_t)(bid[best] & 0xFFFFF) << 20) | (uint64_t)res;
+      rowend[best][row] = (uint8_t)(col + W);
+      slot[best][res]++;
+      if (++cnt[best] == 32) {  // closed: reopen the slot as a fresh batch
+        for (int r = 0; r < PK_ROWS; r++) rowend[best][r] = 0;
+        for (int r = 0; r < 16; r++) slot[best][r] = 0;
+        cnt[best] = 0;
+        bid[best] = next_id++;
+      }
+    }
+    if (ok && next_id <= 0xFFFFF) return;
+  }
+  // dense tile: rows are contiguous (keys sorted by tile, row, column).  With K = the largest number of points
+  // of the row inside any W-column window, level = (index in the row) mod K is a valid assignment (points i and
+  // i + K are >= W columns apart) and uses the minimum number of levels (the maximum overlap).
   for (int64_t r0 = s0; r0 < s1;) {
     const uint64_t row_key = (k1[r0] >> 16) & 0xff;
     int64_t r1 = r0;
     while (r1 < s1 && ((k1[r1] >> 16) & 0xff) == row_key) r1++;
     int64_t K = 1;
-    for (int64_t i = r0, j = r0; i < r1; i++) {  // window [col_i, col_i + W): points j..i with col_j > col_i - W
+    for (int64_t i = r0, j = r0; i < r1; i++) {  // window [col_i - W, col_i]: points j..i with col_j > col_i - W
       const int ci = (int)(k1[i] & 0xff);
       while ((int)(k1[j] & 0xff) <= ci - W) j++;
       if (i - j + 1 > K) K = i - j + 1;
@@ -757,7 +814,7 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
 // ---------------------------------------------------------------------------------------------
 // plan-time: order the targets by (TSI-tile, rank within bank slot, bank slot) and cut the tiles into
 // work items of <= VP_INTERP_CHUNK targets
-#define VP_INTERP_CHUNK 4096
+#define VP_INTERP_CHUNK 16384  // targets per work item: dense tiles reload the grid window once per item
 __global__ void k_interp_keys1(const double *__restrict__ xy, int64_t n, GridArgs g, int TSI, int W, int64_t ntx,
                                int64_t nty, uint64_t *__restrict__ keys, int32_t *__restrict__ idx) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -820,8 +877,9 @@ void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
   VP_CUDA(cudaMallocAsync(&i1s, 4 * (n + 1), s));
   VP_CUDA(cudaMallocAsync(&i2s, 4 * (n + 1), s));
   unsigned nb = (unsigned)((n + 255) / 256);
-  const bool tri_order = P->dmode == VP_DERIV_TRIANGLE && P->opts.targets_are_nodes && P->p <= 16 &&
-                         P->M < ((int64_t)1 << 32) && ntx * nty < ((int64_t)1 << 28);
+  // (tile, triangle, node) order coalesces the per-node V_L reads but costs more shared-memory bank conflicts
+  // than it saves (config 5: interp 9.7 -> 11.8 ms); off
+  const bool tri_order = false;
   size_t tb = 0, tb2 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s);
   cub::DeviceRadixSort::SortPairs(nullptr, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s);
