@@ -122,6 +122,20 @@ def oracle_rate(w, n_targets, seed=99):
                       f"{dt:.2f} s measured, extrapolated linearly in T", "seconds": dt}
 
 
+def ncu_traffic(workload, phase):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the phase's kernels, from the committed ncu
+    --set full captures (profiles/r1/ncu_traffic.json); None if that workload/phase was not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")) as fh:
+            tab = json.load(fh)
+    except Exception:
+        return None, None
+    for prefix, phases in tab.get("workloads", {}).items():
+        if workload.startswith(prefix) and phase in phases:
+            return phases[phase]["bytes"], phases[phase]["source"]
+    return None, None
+
+
 def max_over_ranks(x, dev=None):
     """Max of a per-rank float over all ranks (identity at world size 1); NCCL on the GPU, gloo in tests."""
     import torch
@@ -256,9 +270,11 @@ def main():
     dom_bytes = bytes_spread if dom == "spread" else bytes_interp
     peaks, peak_src = load_peaks()
     achieved = dom_bytes / (ph[dom] * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic(w.name, dom)
     roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src,
-            "algorithmic_bytes": dom_bytes, "kernel_ms": ph[dom]}
+            "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_src,
+            "peak_source": peak_src, "algorithmic_bytes": dom_bytes, "kernel_ms": ph[dom],
+            "co_bound": "shared memory (LSU wavefronts; DESIGN.md §5.1/§5.4)"}
 
     # ---- end-to-end through the public API with host buffers (pinned)
     f_pin = torch.from_numpy(w.f).pin_memory()

@@ -528,6 +528,11 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     if (P->K > N) throw VpError{VP_ERR_ARG};
     if (parts & VP_PART_LOCAL) {
       vp_build_local(P, tri_nodes);
+      if (P->n_stencil > 0) {
+        P->fs = vp_alloc<double>(P, N);
+        P->sp.fs_out = P->fs;
+        vp_remap_stencils(P);
+      }
     } else {
       P->K = 0;
       P->lalpha = vp_alloc<double>(P, 1);

@@ -91,6 +91,7 @@ struct VpSpreadSet {
   VpTiles tiles;
   int det = 0;                 // deterministic mode: items sorted by tile colour, colour_off[c]..colour_off[c+1]
   int64_t color_off[5] = {};
+  double *fs_out = nullptr;    // if set, the spread also writes f in this sorted order
 };
 
 // Level-band corrections for graded meshes: per-target level
@@ -165,6 +166,7 @@ struct vp_plan_s {
   double tri_c2 = 0;           // delta^2 / 2 (0 if series_order < 2)
   double *tri_vL = nullptr;    // [N] TRIANGLE-mode V_L per node (eval scratch; null outside TRIANGLE mode)
   double *st_vL = nullptr;     // [n_stencil] stencil part of V_L per stencil slot (eval scratch)
+  double *fs = nullptr;        // [N] f in spreading order (eval scratch; stencil indices point into it)
   // host-side eval staging (vp_eval_host)
   double *f_dev = nullptr, *out_dev = nullptr;
   // profiling
@@ -206,6 +208,7 @@ void vp_launch_prolong(vp_plan_s *P);
 void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n);
+void vp_remap_stencils(vp_plan_s *P);
 void vp_build_local(vp_plan_s *P, const double *nodes_dev);
 void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop);
 int64_t vp_sort_points(vp_plan_s *P, const double *xy, int64_t n, double ox, double oy, double cell,

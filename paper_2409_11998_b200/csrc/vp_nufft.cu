@@ -220,7 +220,8 @@ template <int W, int D>
 __global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items, const int32_t *__restrict__ bstart,
                                                   const double *__restrict__ sx, const double *__restrict__ sy,
                                                   const double *__restrict__ sw, const int32_t *__restrict__ sperm,
-                                                  const double *__restrict__ f, GridArgs g, int TS, int det) {
+                                                  const double *__restrict__ f, GridArgs g, int TS, int det,
+                                                  double *__restrict__ fs_out) {
   extern __shared__ double tile[];
   const int nw = TS + W + 3;
   const int lane = threadIdx.x;
@@ -236,7 +237,9 @@ __global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items
     if (act) {
       const int j = s + lane;
       const double x = sx[j], y = sy[j];
-      c = f[sperm[j]] * sw[j];
+      const double fj = f[sperm[j]];
+      if (fs_out) fs_out[j] = fj;  // f in spreading order: spatially coherent copy for the stencil gathers
+      c = fj * sw[j];
       lx = (int)(es_horner<W, D>(gcoord(x, g.ox, g.inv_h), wx) - ox);
       ly = (int)(es_horner<W, D>(gcoord(y, g.oy, g.inv_h), wy) - oy);
     }
@@ -280,7 +283,7 @@ static void launch_spread_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &
   if (S.tiles.nsub == 0) return;
   if (!S.det) {
     k_spread_nh<W, D><<<(unsigned)S.tiles.nsub, 32, sm, P->stream>>>(S.tiles.sub, S.bstart, S.sx, S.sy, S.sw,
-                                                                     S.sperm, f, g, S.tiles.TS, 0);
+                                                                     S.sperm, f, g, S.tiles.TS, 0, S.fs_out);
     VP_CHECK_LAUNCH();
     P->n_kernels++;
     return;
@@ -291,7 +294,7 @@ static void launch_spread_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &
     const int64_t i0 = S.color_off[c], i1 = S.color_off[c + 1];
     if (i1 <= i0) continue;
     k_spread_nh<W, D><<<(unsigned)(i1 - i0), 32, sm, P->stream>>>(S.tiles.sub + i0, S.bstart, S.sx, S.sy, S.sw,
-                                                                  S.sperm, f, g, S.tiles.TS, 1);
+                                                                  S.sperm, f, g, S.tiles.TS, 1, S.fs_out);
     VP_CHECK_LAUNCH();
     P->n_kernels++;
   }
@@ -771,10 +774,47 @@ __global__ void __launch_bounds__(256) k_local_stencil(const int32_t *__restrict
   vL_st[s] = acc;
 }
 
+__global__ void k_invert_perm(const int32_t *__restrict__ perm, int64_t n, int32_t *__restrict__ inv) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) inv[perm[i]] = (int32_t)i;
+}
+
+__global__ void k_remap_idx(int32_t *__restrict__ idx, int64_t n, const int32_t *__restrict__ inv) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) idx[i] = inv[idx[i]];
+}
+
+// stencil node indices: user order -> spreading order (plan time)
+void vp_remap_stencils(vp_plan_s *P) {
+  if (P->n_stencil == 0 || P->K == 0) return;
+  int32_t *inv = nullptr;
+  VP_CUDA(cudaMallocAsync(&inv, sizeof(int32_t) * P->N, P->stream));
+  k_invert_perm<<<(unsigned)((P->N + 255) / 256), 256, 0, P->stream>>>(P->sp.sperm, P->N, inv);
+  VP_CHECK_LAUNCH();
+  const int64_t ne = P->n_stencil * (int64_t)P->K;
+  k_remap_idx<<<(unsigned)((ne + 255) / 256), 256, 0, P->stream>>>(P->lidx, ne, inv);
+  VP_CHECK_LAUNCH();
+  VP_CUDA(cudaFreeAsync(inv, P->stream));
+}
+
+__global__ void k_gather_f(const double *__restrict__ f, const int32_t *__restrict__ perm, int64_t n,
+                           double *__restrict__ fs) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) fs[i] = __ldg(f + perm[i]);
+}
+
 void vp_launch_tri_local(vp_plan_s *P, const double *f) {
   if (P->n_stencil > 0 && P->st_vL) {
+    // stencil entries index f in spreading order (P->fs, written by the spread of this eval; gathered here
+    // when the history part is off)
+    int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
+    if (!(parts & VP_PART_HISTORY)) {
+      k_gather_f<<<(unsigned)((P->N + 255) / 256), 256, 0, P->stream>>>(f, P->sp.sperm, P->N, P->fs);
+      VP_CHECK_LAUNCH();
+      P->n_kernels++;
+    }
     k_local_stencil<<<(unsigned)((P->n_stencil + 255) / 256), 256, 0, P->stream>>>(P->lidx, P->lw, P->K, P->n_stencil,
-                                                                                   f, P->st_vL);
+                                                                                   P->fs, P->st_vL);
     VP_CHECK_LAUNCH();
     P->n_kernels++;
   }
