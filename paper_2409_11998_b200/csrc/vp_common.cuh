@@ -132,6 +132,8 @@ struct vp_plan_s {
   int fh_ratio = 1;         // h_FH = fh_ratio * h_NH
   int64_t fh_shift = 0;     // FH node i' sits on NH node fh_ratio * i' - fh_shift
   int tap_qh = 0;           // integer-ratio restriction taps w[q + QH], |q| <= QH (0: general tables)
+  bool prolong_fused = false;   // this eval: prolongation pass A^T applied inside k_interp_local
+  bool no_fuse_prolong = false; // (diagnostics) keep the separate k_prolong_x_int
   double tap_w[192] = {};
   VpHorner horner{};
   double horner_err = 0;

@@ -559,7 +559,7 @@ static void launch_restrict_int(vp_plan_s *P, const RestrictArgs &a, const TapAr
 }
 
 template <int M>
-static void launch_prolong_int(vp_plan_s *P, const RestrictArgs &a, const TapArgs &tp) {
+static void launch_prolong_int(vp_plan_s *P, const RestrictArgs &a, const TapArgs &tp, bool fuse_x) {
   // NH index i = M c + k - j covers [0, n1) for c in [c_lo, c_hi]
   const int64_t c_lo = (tp.j >= 0) ? tp.j / M : -((-tp.j + M - 1) / M);
   const int64_t c_hi = (a.n1 - 1 + tp.j) / M;
@@ -567,6 +567,10 @@ static void launch_prolong_int(vp_plan_s *P, const RestrictArgs &a, const TapArg
   dim3 gB((unsigned)((a.ne + 127) / 128), (unsigned)nc);
   k_prolong_y_int<M><<<gB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a, tp, c_lo);
   VP_CHECK_LAUNCH();
+  if (fuse_x) {  // pass A^T is applied by k_interp_local while it stages its grid windows
+    P->n_kernels++;
+    return;
+  }
   dim3 gA((unsigned)((nc + 127) / 128), (unsigned)a.n1);
   k_prolong_x_int<M><<<gA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a, tp, c_lo, nc);
   VP_CHECK_LAUNCH();
@@ -608,16 +612,18 @@ void vp_launch_restrict(vp_plan_s *P) {
 
 void vp_launch_prolong(vp_plan_s *P) {
   RestrictArgs a = restrict_args(P);
+  P->prolong_fused = false;
   if (P->tap_qh > 0) {
     TapArgs tp = tap_args(P);
+    const bool fuse = !P->no_fuse_prolong;
     switch (P->fh_ratio) {
-      case 2: launch_prolong_int<2>(P, a, tp); return;
-      case 3: launch_prolong_int<3>(P, a, tp); return;
-      case 4: launch_prolong_int<4>(P, a, tp); return;
-      case 5: launch_prolong_int<5>(P, a, tp); return;
-      case 6: launch_prolong_int<6>(P, a, tp); return;
-      case 7: launch_prolong_int<7>(P, a, tp); return;
-      case 8: launch_prolong_int<8>(P, a, tp); return;
+      case 2: launch_prolong_int<2>(P, a, tp, fuse); P->prolong_fused = fuse; return;
+      case 3: launch_prolong_int<3>(P, a, tp, fuse); P->prolong_fused = fuse; return;
+      case 4: launch_prolong_int<4>(P, a, tp, fuse); P->prolong_fused = fuse; return;
+      case 5: launch_prolong_int<5>(P, a, tp, fuse); P->prolong_fused = fuse; return;
+      case 6: launch_prolong_int<6>(P, a, tp, fuse); P->prolong_fused = fuse; return;
+      case 7: launch_prolong_int<7>(P, a, tp, fuse); P->prolong_fused = fuse; return;
+      case 8: launch_prolong_int<8>(P, a, tp, fuse); P->prolong_fused = fuse; return;
       default: break;
     }
   }
@@ -675,7 +681,7 @@ void vp_launch_multiply(vp_plan_s *P, VpGrid &G) {
 // rank-major over the bank slot of their footprint origin (vp_build_interp_order), so the 32
 // row-reads of a warp spread over the 16 8-byte bank slots.
 template <int W, int D>
-__global__ void __launch_bounds__(256) k_interp_local(const int4 *__restrict__ items, int TSI,
+__global__ void __launch_bounds__(256, 4) k_interp_local(const int4 *__restrict__ items, int TSI,
                                                       const double *__restrict__ tx, const double *__restrict__ ty,
                                                       const int64_t *__restrict__ tperm, GridArgs g, int do_hist,
                                                       const double *__restrict__ f, const double *__restrict__ lalpha,
@@ -684,7 +690,8 @@ __global__ void __launch_bounds__(256) k_interp_local(const int4 *__restrict__ i
                                                       int K, int64_t n_sten, int do_local, const int32_t *__restrict__ lptr,
                                                       const double *__restrict__ vL_tri,
                                                       const double *__restrict__ vL_st,
-                                                      double *__restrict__ out) {
+                                                      double *__restrict__ out, const double *__restrict__ t2,
+                                                      RestrictArgs ra, TapArgs tp, int M) {
   extern __shared__ double tile[];
   const int nw = TSI + W + 3;
   const int4 it = items[blockIdx.x];
@@ -692,30 +699,47 @@ __global__ void __launch_bounds__(256) k_interp_local(const int4 *__restrict__ i
   if (do_hist) {
     const bool interior = ox >= 0 && oy >= 0 && ox + nw <= g.nfx && oy + nw <= g.nfy;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int QH = tp.QH, dlo = -(QH / M), dhi = (M - 1 + QH) / M;
     for (int r = warp; r < nw; r += 8) {
       const int64_t gy = interior ? oy + r : wrapi(oy + r, g.nfy);
       const double *src = g.data + gy * g.row;
-      for (int c = lane; c < nw; c += 32) tile[r * nw + c] = __ldg(src + (interior ? ox + c : wrapi(ox + c, g.nfx)));
+      for (int c = lane; c < nw; c += 32) {
+        const int64_t gx = interior ? ox + c : wrapi(ox + c, g.nfx);
+        double v = __ldg(src + gx);
+        if (t2) {  // fused prolongation pass A^T: + sum_{i'} w[gx + j - M i'] t2[gy][i' - e_lo]
+          const int64_t q = gx + tp.j;
+          const int64_t cc = q >= 0 ? q / M : -((-q + M - 1) / M);
+          const int k = (int)(q - cc * M);
+          const double *trow = t2 + gy * ra.ne - ra.e_lo;
+          for (int d = dlo; d <= dhi; d++) {
+            const int64_t ip = cc + d;
+            const int qq = k - M * d;
+            if (ip >= ra.e_lo && ip < ra.e_lo + ra.ne && qq >= -QH && qq <= QH) v = fma(tp.w[qq + QH], __ldg(trow + ip), v);
+          }
+        }
+        tile[r * nw + c] = v;
+      }
     }
     __syncthreads();
   }
-  for (int t = it.z + threadIdx.x; t < it.w; t += blockDim.x) {
-    double v = 0.0;
-    if (do_hist) {
-      double wx[W], wy[W];
-      const int lx = (int)(es_horner<W, D>(gcoord(tx[t], g.ox, g.inv_h), wx) - ox);
-      const int ly = (int)(es_horner<W, D>(gcoord(ty[t], g.oy, g.inv_h), wy) - oy);
-      const double *rp = tile + ly * nw + lx;
-#pragma unroll
-      for (int b = 0; b < W; b++) {
-        double racc = 0.0;
-#pragma unroll
-        for (int a = 0; a < W; a++) racc = fma(wx[a], rp[b * nw + a], racc);
-        v = fma(wy[b], racc, v);
-      }
+  // software pipeline: the next target's coordinates are loaded while the current one is interpolated, and the
+  // current target's local-part value is fetched before its w x w shared-memory sweep (long-latency loads hidden)
+  int t = it.z + threadIdx.x;
+  double xn = 0.0, yn = 0.0;
+  if (t < it.w) {
+    xn = tx[t];
+    yn = ty[t];
+  }
+  for (; t < it.w; t += blockDim.x) {
+    const double xc = xn, yc = yn;
+    const int tn = t + blockDim.x;
+    if (tn < it.w) {
+      xn = tx[tn];
+      yn = ty[tn];
     }
+    const int64_t dst = tperm[t];
+    double vl = 0.0;
     if (do_local) {
-      double vl = 0.0;
       const int32_t nd = lnode[t];
       const int32_t sp = lptr[t];
       if (sp >= 0) {  // least-squares stencil, applied by k_local_stencil
@@ -726,9 +750,22 @@ __global__ void __launch_bounds__(256) k_interp_local(const int4 *__restrict__ i
       } else if (nd >= 0) {
         vl = lalpha[t] * __ldg(f + nd);
       }
-      v += vl;
     }
-    out[tperm[t]] = v;
+    double v = 0.0;
+    if (do_hist) {
+      double wx[W], wy[W];
+      const int lx = (int)(es_horner<W, D>(gcoord(xc, g.ox, g.inv_h), wx) - ox);
+      const int ly = (int)(es_horner<W, D>(gcoord(yc, g.oy, g.inv_h), wy) - oy);
+      const double *rp = tile + ly * nw + lx;
+#pragma unroll
+      for (int b = 0; b < W; b++) {
+        double racc = 0.0;
+#pragma unroll
+        for (int a = 0; a < W; a++) racc = fma(wx[a], rp[b * nw + a], racc);
+        v = fma(wy[b], racc, v);
+      }
+    }
+    out[dst] = v + vl;
   }
 }
 
@@ -844,9 +881,13 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
                                  (int)(sizeof(double) * (TSI + W + 3) * (TSI + W + 3))));
     attr_set[W] = true;
   }
+  const bool fused = do_hist && P->prolong_fused;
+  RestrictArgs ra = restrict_args(P);
+  TapArgs tp = fused ? tap_args(P) : TapArgs{};
   k_interp_local<W, D><<<(unsigned)P->n_items, 256, sm, P->stream>>>(
       P->items, TSI, P->tx, P->ty, P->tperm, grid_args(P->nh), do_hist, f, P->lalpha, P->lnode, P->lidx, P->lw, P->K,
-      P->n_stencil, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr, P->tri_vL, P->st_vL, out);
+      P->n_stencil, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr, P->tri_vL, P->st_vL, out, fused ? P->scratch : nullptr,
+      ra, tp, P->fh_ratio);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
