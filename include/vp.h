@@ -71,7 +71,7 @@ typedef struct {
   int32_t series_order;      /* interior V_L terms n_L in sum_n delta^n Lap^{n-1} f / n!; 0 -> 3 */
   int32_t deriv_mode;        /* VP_DERIV_* */
   int32_t deriv_degree;      /* least-squares polynomial degree for KNN jets; 0 -> 6 (4 if N > 1e6) */
-  int32_t deriv_k;           /* neighbours for KNN jets; 0 -> 2 * #monomials */
+  int32_t deriv_k;           /* neighbours for KNN jets; 0 -> 2 * #monomials (degree >= 5), #monomials + 6 (degree 4) */
   int32_t parts;             /* VP_PART_*; 0 -> ALL */
   int32_t targets_are_nodes; /* 1: targets[t] == tri_nodes[t] for t < N = M p (T >= N; targets beyond N are
                                 off-node points); enables the node fast path */

@@ -522,7 +522,8 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     P->deg = o.deriv_degree > 0 ? o.deriv_degree : (N > 1000000 ? 4 : 6);
     if (P->deg > VP_MAXDEG) throw VpError{VP_ERR_ARG};
     int nc = vp_ncoef(P->deg);
-    P->K = o.deriv_k > 0 ? o.deriv_k : 2 * nc;
+    // K: 2 x #monomials at degree >= 5; degree 4 needs fewer (config 2: 1.30e-9 at K = 17, 20, 24 and 30)
+    P->K = o.deriv_k > 0 ? o.deriv_k : (P->deg >= 5 ? 2 * nc : nc + 6);
     if (P->K > 64) P->K = 64;
     if (P->K < nc) throw VpError{VP_ERR_ARG};
     if (P->K > N) throw VpError{VP_ERR_ARG};
