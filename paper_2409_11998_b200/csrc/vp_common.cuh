@@ -165,6 +165,7 @@ struct vp_plan_s {
   int8_t *tri_ok = nullptr;    // [M] TRIANGLE mode usable
   double *tri_M = nullptr;     // [M][3] A^-1 A^-T (M11, M12, M22)
   double *tri_H = nullptr;     // [3][p][p] reference cubic-fit Hessian operators
+  std::vector<double> tri_H_host;
   double tri_c2 = 0;           // delta^2 / 2 (0 if series_order < 2)
   double *tri_vL = nullptr;    // [N] TRIANGLE-mode V_L per node (eval scratch; null outside TRIANGLE mode)
   double *st_vL = nullptr;     // [n_stencil] stencil part of V_L per stencil slot (eval scratch)

@@ -438,6 +438,44 @@ __global__ void __launch_bounds__(128) k_restrict_x_int(const double *__restrict
   }
 }
 
+// pass A with compile-time tap count (QHC = QH): fully unrolled, every weight a static kernel-parameter
+// (constant-bank) operand of its DFMA, every shared-memory read a static offset
+template <int M, int Q, int QHC>
+__global__ void __launch_bounds__(128) k_restrict_x_fix(const double *__restrict__ g1, double *__restrict__ tA,
+                                                        RestrictArgs a, TapArgs tp) {
+  extern __shared__ double s[];
+  constexpr int SKEW = M * Q, NT = 2 * QHC + 1, NIN = M * (Q - 1) + NT;
+  const int64_t r = blockIdx.y;
+  const int64_t e0 = (int64_t)blockIdx.x * 128 * Q;
+  const int span = M * (128 * Q - 1) + NT;
+  const int64_t i0 = M * (a.e_lo + e0) - tp.j - QHC;
+  const double *src = g1 + r * a.row1;
+  for (int idx = threadIdx.x; idx < span; idx += 128) {
+    const int64_t gi = i0 + idx;
+    s[idx + idx / SKEW] = (gi >= 0 && gi < a.n1) ? __ldg(src + gi) : 0.0;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  const double *sb = s + (SKEW + 1) * t;
+  double acc[Q];
+#pragma unroll
+  for (int k = 0; k < Q; k++) acc[k] = 0.0;
+#pragma unroll
+  for (int ii = 0; ii < NIN; ii++) {
+    const double x = sb[ii + ii / SKEW];
+#pragma unroll
+    for (int k = 0; k < Q; k++) {
+      const int q = ii - M * k;
+      if (q >= 0 && q < NT) acc[k] = fma(tp.w[q], x, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < Q; k++) {
+    const int64_t e = e0 + Q * t + k;
+    if (e < a.ne) tA[r * a.ne + e] = acc[k];
+  }
+}
+
 // pass B: g2[e_lo + ey][e_lo + ex] = sum_q w[q] tA[M (e_lo + ey) - j + q][ex] (coalesced along ex)
 template <int M, int Q>
 __global__ void __launch_bounds__(128) k_restrict_y_int(const double *__restrict__ tA, double *__restrict__ g2,
@@ -550,7 +588,23 @@ static void launch_restrict_int(vp_plan_s *P, const RestrictArgs &a, const TapAr
     attr = true;
   }
   dim3 gA((unsigned)((a.ne + 128 * Q - 1) / (128 * Q)), (unsigned)a.n1);
-  k_restrict_x_int<M, Q><<<gA, 128, sm, P->stream>>>(P->nh.data, P->scratch, a, tp);
+  bool fixed = false;
+#define VP_RFIX(QHV)                                                                                   \
+  if (tp.QH == QHV) {                                                                                  \
+    static bool attr_fix = false;                                                                      \
+    if (!attr_fix) {                                                                                   \
+      VP_CUDA(cudaFuncSetAttribute(k_restrict_x_fix<M, Q, QHV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   96 * 1024));                                                        \
+      attr_fix = true;                                                                                 \
+    }                                                                                                  \
+    k_restrict_x_fix<M, Q, QHV><<<gA, 128, sm, P->stream>>>(P->nh.data, P->scratch, a, tp);           \
+    fixed = true;                                                                                      \
+  }
+  if (M == 5) {  // the ratio delta2/delta1 = 32 gives m = 5 on every config; w = 9, 10, 11 (tol 1e-8 .. 1e-10)
+    VP_RFIX(22) else VP_RFIX(24) else VP_RFIX(27)
+  }
+#undef VP_RFIX
+  if (!fixed) k_restrict_x_int<M, Q><<<gA, 128, sm, P->stream>>>(P->nh.data, P->scratch, a, tp);
   VP_CHECK_LAUNCH();
   dim3 gB((unsigned)((a.ne + 127) / 128), (unsigned)((a.ne + Q - 1) / Q));
   k_restrict_y_int<M, Q><<<gB, 128, 0, P->stream>>>(P->scratch, P->fh.data, a, tp);
@@ -798,6 +852,46 @@ __global__ void __launch_bounds__(128) k_tri_local(const double *__restrict__ f,
   }
 }
 
+// p = 12 (the 12-point rule): reference Hessian operators in the constant bank (uniform, static offsets ->
+// DFMA constant operands, no shared-memory traffic), f and V_L staged through shared memory so that the
+// CTA's 128 x 12 values move as coalesced rows
+__constant__ double c_triH[3 * 12 * 12];
+static double g_triH_uploaded[432];
+static bool g_triH_valid = false;
+
+__global__ void __launch_bounds__(128) k_tri_local12(const double *__restrict__ f, const int8_t *__restrict__ tri_ok,
+                                                     const double *__restrict__ tri_M, int64_t M, double c1, double c2,
+                                                     double *__restrict__ vL) {
+  __shared__ double sf[128 * 12 + 1];
+  const int64_t m0 = (int64_t)blockIdx.x * 128;
+  const int nt = (int)((M - m0) < 128 ? (M - m0) : 128);
+  for (int i = threadIdx.x; i < nt * 12; i += 128) sf[i] = __ldcs(f + m0 * 12 + i);
+  __syncthreads();
+  const int t = threadIdx.x;
+  const int64_t m = m0 + t;
+  if (t < nt && tri_ok[m]) {
+    const double m11 = tri_M[3 * m], m12x2 = 2.0 * tri_M[3 * m + 1], m22 = tri_M[3 * m + 2];
+    double fb[12], out[12];
+#pragma unroll
+    for (int j = 0; j < 12; j++) fb[j] = sf[t * 12 + j];  // stride 12 doubles: 4-way bank spread, once per value
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+      double lap = 0.0;
+#pragma unroll
+      for (int j = 0; j < 12; j++)
+        lap = fma(fma(m11, c_triH[k * 12 + j], fma(m12x2, c_triH[144 + k * 12 + j], m22 * c_triH[288 + k * 12 + j])),
+                  fb[j], lap);
+      out[k] = fma(c2, lap, c1 * fb[k]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 12; k++) sf[t * 12 + k] = out[k];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nt * 12; i += 128)
+    if (tri_ok[m0 + i / 12]) vL[m0 * 12 + i] = sf[i];
+}
+
 // KNN-stencil local part, one thread per stencil slot: vL_st[s] = sum_k w[k][s] f[idx[k][s]] (k-major layout:
 // the warp streams consecutive slots, 12 B per entry, HBM-bound; f gathers hit L2)
 __global__ void __launch_bounds__(256) k_local_stencil(const int32_t *__restrict__ lidx, const double *__restrict__ lw,
@@ -857,10 +951,15 @@ void vp_launch_tri_local(vp_plan_s *P, const double *f) {
   }
   if (!P->tri_vL || P->M == 0) return;
   const unsigned nb = (unsigned)((P->M + 127) / 128);
-  if (P->p == 12)
-    k_tri_local<12><<<nb, 128, 0, P->stream>>>(f, P->tri_ok, P->tri_M, P->tri_H, P->p, P->M, P->delta1, P->tri_c2,
-                                               P->tri_vL);
-  else
+  if (P->p == 12) {
+    // operators depend on the rule only; (re-)upload when this plan's differ from the last uploaded ones
+    if (!g_triH_valid || memcmp(g_triH_uploaded, P->tri_H_host.data(), sizeof(g_triH_uploaded)) != 0) {
+      memcpy(g_triH_uploaded, P->tri_H_host.data(), sizeof(g_triH_uploaded));
+      VP_CUDA(cudaMemcpyToSymbolAsync(c_triH, P->tri_H, sizeof(double) * 432, 0, cudaMemcpyDeviceToDevice, P->stream));
+      g_triH_valid = true;
+    }
+    k_tri_local12<<<nb, 128, 0, P->stream>>>(f, P->tri_ok, P->tri_M, P->M, P->delta1, P->tri_c2, P->tri_vL);
+  } else
     k_tri_local<0><<<nb, 128, 0, P->stream>>>(f, P->tri_ok, P->tri_M, P->tri_H, P->p, P->M, P->delta1, P->tri_c2,
                                               P->tri_vL);
   VP_CHECK_LAUNCH();
