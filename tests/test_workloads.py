@@ -66,3 +66,25 @@ def test_curved_map_endpoints():
         xi1[0], xi2[0] = l[1], l[2]
         x, y = geometry.map_points(w.tri[m:m + 1], w.curved[m:m + 1], w.circle, xi1, xi2)
         assert np.allclose(np.hypot(x, y), 1.0, atol=1e-14)
+
+
+def test_config3_generator_properties():
+    """Scaled config 3: star-shaped, graded (area ratio > 1e3), nonconforming patches with gaps (total area
+    slightly below the star's), positively oriented, no degenerate triangles, f vanishing at the boundary."""
+    w = configs.config3(M_target=60000, lmin=7, lmax=13, g=0.1)
+    t = w.tri
+    area = 0.5 * ((t[:, 1, 0] - t[:, 0, 0]) * (t[:, 2, 1] - t[:, 0, 1]) - (t[:, 1, 1] - t[:, 0, 1]) * (t[:, 2, 0] - t[:, 0, 0]))
+    assert np.all(area > 0)
+    star_area = np.pi * (1.0 + 0.3 ** 2 / 2)       # (1/2) int (1 + 0.3 cos 5t)^2 dt
+    assert star_area * 0.995 < area.sum() < star_area  # chords + gaps remove a little
+    assert area.max() / area.min() > 1e3
+    # every node lies inside the star
+    r = np.hypot(w.nodes[..., 0], w.nodes[..., 1])
+    th = np.arctan2(w.nodes[..., 1], w.nodes[..., 0])
+    assert np.all(r < configs.star_radius(th))
+    assert np.abs(w.f).max() > 0.99 and np.abs(w.f[r > 0.9]).max() < 1e-300
+    # nonconforming: some vertices are not shared with any other triangle of a different patch (hanging
+    # nodes / gaps), i.e. the vertex multiset has many singletons along patch seams
+    v = np.round(t.reshape(-1, 2), 12)
+    _, counts = np.unique(v, axis=0, return_counts=True)
+    assert (counts == 1).sum() > 0
