@@ -772,6 +772,24 @@ __global__ void __launch_bounds__(256, 4) k_interp_local(const int4 *__restrict_
     const bool interior = ox >= 0 && oy >= 0 && ox + nw <= g.nfx && oy + nw <= g.nfy;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int QH = tp.QH, dlo = -(QH / M), dhi = (M - 1 + QH) / M;
+    if (!t2 && interior) {  // common case: flat copy with 4 independent loads in flight per thread
+      const int ncell = nw * nw;
+      const double *base = g.data + oy * g.row + ox;
+      for (int i0 = threadIdx.x; i0 < ncell; i0 += 4 * 256) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int i = i0 + u * 256;
+          if (i < ncell) {
+            const int r = i / nw;
+            v[u] = __ldg(base + (int64_t)r * g.row + (i - r * nw));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (i0 + u * 256 < ncell) tile[i0 + u * 256] = v[u];
+      }
+    } else
     for (int r = warp; r < nw; r += 8) {
       const int64_t gy = interior ? oy + r : wrapi(oy + r, g.nfy);
       const double *src = g.data + gy * g.row;
