@@ -919,7 +919,7 @@ __global__ void __launch_bounds__(128) k_tri_local12(const double *__restrict__ 
                   fb[j], lap);
       out[k] = fma(c2, lap, c1 * fb[k]);
     }
-    __syncwarp();
+    // each thread overwrites only the 12 entries it read itself: no cross-thread hazard
 #pragma unroll
     for (int k = 0; k < 12; k++) sf[t * 12 + k] = out[k];
   }
