@@ -122,14 +122,31 @@ typedef struct {
 
 typedef struct vp_plan_s *vp_handle;
 
-/* Build a plan.  tri_nodes [M][p][2], weights [M][p] (>= 0, zero allowed for degenerate
- * triangles), targets [T][2]; all device pointers, read during the call only (the plan copies
- * and reorders what it keeps).  tol in [1e-14, 1e-2].  Synchronises the stream. */
+/* Build a plan (§3 "Input" and Step 1, lines 782-821: nodes x[j] and smooth weights w[j] of a
+ * p-point rule on M triangles, N = M p (§2.2), targets, tolerance).
+ *   tri_nodes [M][p][2] fp64, x then y, grouped per triangle (device)
+ *   weights   [M][p]    fp64, >= 0; zero allowed (degenerate triangles contribute nothing) (device)
+ *   targets   [T][2]    fp64 (device); with opts->targets_are_nodes the first N targets must equal the nodes
+ *   tol       in [1e-14, 1e-2]: relative accuracy goal for V (NUFFT eps = tol unless opts->eps_nufft)
+ *   opts      NULL or zero-initialised for defaults (see vp_opts)
+ *   out       receives the plan handle (NULL on failure)
+ * The arrays are read during the call only: the plan copies and reorders what it keeps and owns all
+ * device memory it allocates (released by vp_destroy).  Synchronises opts->cuda_stream.
+ * Errors: VP_ERR_ARG (null pointer, M, p or T <= 0, sum of weights == 0, T < N with targets_are_nodes,
+ * bad option), VP_ERR_TOL, VP_ERR_NONFINITE (NaN/Inf or negative weight in the inputs), VP_ERR_GEOMETRY
+ * (invalid boundary descriptor), VP_ERR_UNSUPPORTED (N or T >= 2^31, TRIANGLE mode without ref_nodes,
+ * or a spreading tile row with more than 2^20 points), VP_ERR_OOM (a grid beyond the device),
+ * VP_ERR_CUDA / VP_ERR_CUFFT (runtime failures; vp_last_error_detail says which call). */
 vp_status vp_plan(const double *tri_nodes, const double *weights, int64_t M, int32_t p,
                   const double *targets, int64_t T, double tol, const vp_opts *opts, vp_handle *out);
 
-/* Evaluate V at the plan's targets.  f [M][p] (device, same order as tri_nodes), out [T]
- * (device, fully overwritten).  Asynchronous on the plan's stream. */
+/* Evaluate V = V_NH + V_FH + V_L (PAPER.md eq. (heatdecomp)) at the plan's targets.
+ *   f   [M][p] fp64 source values at the nodes, same order as tri_nodes (device, read only)
+ *   out [T]    fp64, fully overwritten, target order of vp_plan (device)
+ * Asynchronous on the plan's stream (the caller synchronises); one plan must not be evaluated
+ * concurrently with itself.  f is not checked for NaN/Inf here (that would need a host sync): a
+ * non-finite f propagates to out; vp_check_finite tests f explicitly.
+ * Errors: VP_ERR_ARG (null pointer), VP_ERR_CUDA / VP_ERR_CUFFT (launch failures). */
 vp_status vp_eval(vp_handle plan, const double *f, double *out);
 
 /* Same, with HOST buffers: copies f host->device, evaluates, copies out device->host, and
