@@ -749,9 +749,9 @@ void vp_launch_multiply(vp_plan_s *P, VpGrid &G) {
 // interpolation (NH grid, which also carries the prolongated FH field) + local part + scatter.
 // One CTA of 256 threads per work item (tile_x, tile_y, t0, t1): the (TSI+W+3)^2 grid window of a
 // TSI x TSI tile is staged once in shared memory (coalesced rows), then every thread interpolates
-// targets t0 + tid, t0 + tid + 256, ... from shared memory.  Targets were ordered at plan time
-// rank-major over the bank slot of their footprint origin (vp_build_interp_order), so the 32
-// row-reads of a warp spread over the 16 8-byte bank slots.
+// targets t0 + tid, t0 + tid + 256, ... from shared memory.  Targets were ordered at plan time by
+// footprint origin inside the tile (vp_build_interp_order): sparse tiles read consecutive columns,
+// dense cells read the same addresses (broadcasts).
 template <int W, int D>
 __global__ void __launch_bounds__(256, 4) k_interp_local(const int4 *__restrict__ items, int TSI,
                                                       const double *__restrict__ tx, const double *__restrict__ ty,
@@ -1028,7 +1028,7 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// plan-time: order the targets by (TSI-tile, rank within bank slot, bank slot) and cut the tiles into
+// plan-time: order the targets by (TSI-tile, footprint row, footprint column) and cut the tiles into
 // work items of <= VP_INTERP_CHUNK targets
 #define VP_INTERP_CHUNK 16384  // targets per work item: dense tiles reload the grid window once per item
 __global__ void k_interp_keys1(const double *__restrict__ xy, int64_t n, GridArgs g, int TSI, int W, int64_t ntx,
@@ -1039,26 +1039,15 @@ __global__ void k_interp_keys1(const double *__restrict__ xy, int64_t n, GridArg
   int64_t tx = (int64_t)floor(gx / TSI), ty = (int64_t)floor(gy / TSI);
   tx = tx < 0 ? 0 : (tx >= ntx ? ntx - 1 : tx);
   ty = ty < 0 ? 0 : (ty >= nty ? nty - 1 : ty);
-  const int nw = TSI + W + 3;
+  // order inside a tile: by footprint origin (row, column).  Consecutive targets of a sparse tile then read
+  // consecutive columns (distinct bank slots), and the many targets of one dense cell (config-5 clusters) read
+  // the same addresses -- shared-memory broadcasts, one wavefront per instruction
   int64_t lrow = (int64_t)ceil(gy - 0.5 * W) - (ty * TSI - (W / 2 + 1));
   int64_t lcol = (int64_t)ceil(gx - 0.5 * W) - (tx * TSI - (W / 2 + 1));
-  const int res = (int)((((lrow * nw + lcol) % 16) + 16) % 16);
-  keys[i] = ((uint64_t)(ty * ntx + tx) << 4) | (uint64_t)res;
+  lrow = lrow < 0 ? 0 : (lrow > 255 ? 255 : lrow);
+  lcol = lcol < 0 ? 0 : (lcol > 255 ? 255 : lcol);
+  keys[i] = ((uint64_t)(ty * ntx + tx) << 16) | ((uint64_t)lrow << 8) | (uint64_t)lcol;
   idx[i] = (int32_t)i;
-}
-
-__global__ void k_interp_keys2(const uint64_t *__restrict__ k1, int64_t n, uint64_t *__restrict__ k2) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint64_t key = k1[i];
-  int64_t lo = 0, hi = i;
-  while (lo < hi) {  // first index of this (tile, slot) group
-    int64_t mid = (lo + hi) >> 1;
-    if (k1[mid] < key) lo = mid + 1; else hi = mid;
-  }
-  uint64_t rank = (uint64_t)(i - lo);
-  if (rank > 0xFFFFF) rank = 0xFFFFF;
-  k2[i] = ((key >> 4) << 24) | (rank << 4) | (key & 15);
 }
 
 // TRIANGLE mode: node targets ordered by (tile, triangle, node) so that the per-node V_L reads of a warp are
@@ -1110,10 +1099,8 @@ void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
   } else {
     k_interp_keys1<<<nb, 256, 0, s>>>(xy, n, g, TSI, P->w, ntx, nty, k1, i1);
     VP_CHECK_LAUNCH();
-    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
-    k_interp_keys2<<<nb, 256, 0, s>>>(k1s, n, k2);
-    VP_CHECK_LAUNCH();
-    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
+    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k2s, i1, i2s, (int)n, 0, 64, s));
+    tile_shift = 16;
   }
   P->tx = vp_alloc<double>(P, n);
   P->ty = vp_alloc<double>(P, n);
