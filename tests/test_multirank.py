@@ -53,3 +53,16 @@ def test_reference_arm_nonzero_rank_exits_silently():
                         "--warmup", "0"], capture_output=True, text=True, env=env, timeout=300, cwd=ROOT)
     assert r.returncode == 0
     assert r.stdout.strip() == ""
+
+
+def test_reference_arm_json_line():
+    """bench.py --impl reference (the CPU oracle as the reference arm) prints one JSON line with the contract keys."""
+    import json
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "1", "--config", "c2n40", "--ref-targets", "8"], capture_output=True, text=True,
+                       timeout=600, cwd=ROOT, env=dict(os.environ, RANK="0", WORLD_SIZE="1"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "pts/s"
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["higher_is_better"] is True
