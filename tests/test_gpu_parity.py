@@ -237,10 +237,9 @@ def test_tiny_and_ragged_inputs_run():
                        1e-8)
         V = plan.eval(torch.ones(1, 12, dtype=torch.float64, device=DEV)).cpu().numpy()
         assert np.all(np.isfinite(V)) and V.shape == (tg.shape[0],)
-        # far target: V ~ -(area / 2pi) log r
-        if tg.shape[0] == 3:
-            far = -area / (2 * np.pi) * np.log(np.hypot(3.0 - 0.4, -2.0 - 0.43))
-            assert abs(V[1] - far) < 1e-3 * abs(far)
+        if tg.shape[0] == 3:  # the far target sees only the smooth part: exact to the NUFFT tolerance
+            far = oracle.volume_potential(tri, None, None, fields.const(1.0), tg[1:2])[0]
+            assert abs(V[1] - far) < 1e-7 * abs(far)
 
 
 def test_loose_tolerance_parity():
