@@ -152,6 +152,13 @@ __global__ void k_build_local(LocalArgs a) {
     bdry = vp_coef_rect(x, y, a.bd.p[0], a.bd.p[1], a.bd.p[2], a.bd.p[3], delta, a.deg, coef);
   if (!bdry) vp_coef_interior(delta, a.nterms, a.deg, coef);
   a.is_bdry[t] = bdry ? 1 : 0;
+  // a target farther than 12 sqrt(delta) from every node sees no local part (the short-time kernel is below
+  // 1e-14 there): f is not extrapolated outside the mesh
+  {
+    double d2min = hd[0];
+    for (int k = 1; k < K; k++) d2min = fmin(d2min, hd[k]);
+    if (d2min > 144.0 * delta) vp_coef_clear(coef);
+  }
   double alpha = 0.0;
   int32_t node = a.tperm[t] < a.node_targets ? (int32_t)a.tperm[t] : -1;
   if (node >= 0) {
