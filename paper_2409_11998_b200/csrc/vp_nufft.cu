@@ -90,19 +90,16 @@ __global__ void k_tile_heads(const uint64_t *__restrict__ k1, int64_t n, int32_t
 // footprint origin (res = (row * nw + col) mod 16, 16 slots of 8 B per 128 B wavefront): a chunk of
 // 32 consecutive points holds at most 2 points per slot when the slots are evenly populated, so the
 // row-step LDS/STS of a batch need ~2 wavefronts instead of the ~4-5 of random columns.
-#define PK_B 16
-#define PK_ROWS 36
+#define PK_B 32
+#define PK_ROWS 48
 __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restrict__ tstart, int64_t ntile,
                          int64_t n, int W, int nw, uint64_t *__restrict__ k2, int *__restrict__ overflow_flag) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= ntile) return;
   const int64_t s0 = tstart[t], s1 = (t + 1 < ntile) ? tstart[t + 1] : n;
   const uint64_t tile = k1[s0] >> 32;
-  // sparse tile (every row has few points): greedy packing into <= PK_B open batches of <= 32 points.  Points
-  // are visited in a pseudo-random order (stride coprime to the count) and each goes to the FULLEST open batch
-  // where (hard) its W columns are free in its footprint row and (soft) its bank slot holds < 2 points, so
-  // batches close at 32 instead of all staying partly filled (row order + first fit left ~68% lane fill,
-  // this ~90%, by simulation on config-2-like tiles).
+  // sparse tile (every row has few points): greedy packing into <= PK_B open batches of <= 32 points, first
+  // batch whose row is free at these columns and whose bank slot holds < 2 points -> full batches
   int64_t maxrow = 0;
   for (int64_t r0 = s0; r0 < s1;) {
     int64_t r1 = r0;
@@ -111,59 +108,44 @@ __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restr
     if (r1 - r0 > maxrow) maxrow = r1 - r0;
     r0 = r1;
   }
-  const int64_t nt = s1 - s0;
-  if (maxrow <= 3 * PK_B && nt <= 65536) {
-    uint64_t occ[PK_B][PK_ROWS];  // occupied footprint columns per batch and row
+  if (maxrow <= 2 * PK_B && s1 - s0 <= 8192) {
+    uint8_t rowend[PK_B][PK_ROWS];
     uint8_t slot[PK_B][16];
     uint8_t cnt[PK_B];
     uint32_t bid[PK_B];
     int nopen = 0;
     uint32_t next_id = 0;
     bool ok = true;
-    int64_t stride = 1;
-    {
-      const int64_t cand[6] = {7919, 104729, 1299709, 15485863, 3, 1};
-      for (int c = 0; c < 6; c++) {
-        int64_t x = cand[c] % nt, y = nt;  // gcd
-        while (y) { int64_t tmp = x % y; x = y; y = tmp; }
-        if (x == 1 && cand[c] % nt != 0) { stride = cand[c] % nt; break; }
-      }
-    }
-    const uint64_t wmask = (W >= 64) ? ~0ull : ((1ull << W) - 1);
-    for (int64_t q = 0; q < nt && ok; q++) {
-      const int64_t i = s0 + (q * stride) % nt;
+    for (int64_t i = s0; i < s1 && ok; i++) {
       const int row = (int)((k1[i] >> 16) & 0xff), col = (int)(k1[i] & 0xff);
-      if (row >= PK_ROWS || col + W > 64) { ok = false; break; }
+      if (row >= PK_ROWS || col + W > 255) { ok = false; break; }
       const int res = (row * nw + col) & 15;
-      const uint64_t need = wmask << col;
-      int best = -1, bestc = -1, soft = -1, softc = -1;
+      int best = -1, soft = -1;
       for (int b = 0; b < nopen; b++) {
-        if (occ[b][row] & need) continue;
-        if (slot[b][res] < 2) {
-          if (cnt[b] > bestc) { best = b; bestc = cnt[b]; }
-        } else if (cnt[b] > softc) {
-          soft = b;
-          softc = cnt[b];
+        if (rowend[b][row] <= col) {
+          if (slot[b][res] < 2) { best = b; break; }
+          if (soft < 0) soft = b;
         }
       }
-      if (best < 0) best = soft;
       if (best < 0) {
-        if (nopen < PK_B) {
+        if (soft >= 0) {
+          best = soft;  // a bank-slot repeat costs one extra wavefront; a new batch costs a whole row sweep
+        } else if (nopen < PK_B) {
           best = nopen++;
-          for (int r = 0; r < PK_ROWS; r++) occ[best][r] = 0;
+          for (int r = 0; r < PK_ROWS; r++) rowend[best][r] = 0;
           for (int r = 0; r < 16; r++) slot[best][r] = 0;
           cnt[best] = 0;
           bid[best] = next_id++;
-        } else {  // every open batch is taken at these columns: use the level scheme for this tile
+        } else {  // every open batch is taken on this row: use the level scheme for this tile
           ok = false;
           break;
         }
       }
       k2[i] = (tile << 40) | ((uint64_t)(bid[best] & 0xFFFFF) << 20) | (uint64_t)res;
-      occ[best][row] |= need;
+      rowend[best][row] = (uint8_t)(col + W);
       slot[best][res]++;
       if (++cnt[best] == 32) {  // closed: reopen the slot as a fresh batch
-        for (int r = 0; r < PK_ROWS; r++) occ[best][r] = 0;
+        for (int r = 0; r < PK_ROWS; r++) rowend[best][r] = 0;
         for (int r = 0; r < 16; r++) slot[best][r] = 0;
         cnt[best] = 0;
         bid[best] = next_id++;
@@ -247,20 +229,41 @@ __global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items
   const int64_t ox = (int64_t)it.x * TS - (W / 2 + 1), oy = (int64_t)it.y * TS - (W / 2 + 1);
   for (int i = lane; i < nw * nw; i += 32) tile[i] = 0.0;
   __syncwarp();
+  // software pipeline over batches: the next batch's point data (x, y, w, node index, then f) is loaded while
+  // the current batch's row steps run, so the global-memory latency is not exposed once per batch
+  int jn = -1;
+  double xn = 0.0, yn = 0.0, wn = 0.0, fn = 0.0;
+  {
+    const int s0 = bstart[it.z];
+    if (lane < bstart[it.z + 1] - s0) {
+      jn = s0 + lane;
+      xn = sx[jn]; yn = sy[jn]; wn = sw[jn];
+      fn = f[sperm[jn]];
+    }
+  }
   for (int b = it.z; b < it.w; b++) {
-    const int s = bstart[b], n = bstart[b + 1] - s;
-    const bool act = lane < n;
+    const int j = jn;
+    const bool act = j >= 0;
+    const double x = xn, y = yn, fj = fn, wj = wn;
+    int pn = -1;
+    jn = -1;
+    if (b + 1 < it.w) {
+      const int s1 = bstart[b + 1];
+      if (lane < bstart[b + 2] - s1) {
+        jn = s1 + lane;
+        xn = sx[jn]; yn = sy[jn]; wn = sw[jn];
+        pn = sperm[jn];
+      }
+    }
     double wx[W], wy[W], c = 0.0;
     int lx = 0, ly = 0;
     if (act) {
-      const int j = s + lane;
-      const double x = sx[j], y = sy[j];
-      const double fj = f[sperm[j]];
       if (fs_out) fs_out[j] = fj;  // f in spreading order: spatially coherent copy for the stencil gathers
-      c = fj * sw[j];
+      c = fj * wj;
       lx = (int)(es_horner<W, D>(gcoord(x, g.ox, g.inv_h), wx) - ox);
       ly = (int)(es_horner<W, D>(gcoord(y, g.oy, g.inv_h), wy) - oy);
     }
+    if (pn >= 0) fn = f[pn];
 #pragma unroll
     for (int r = 0; r < W; r++) {
       if (act) {
@@ -749,9 +752,9 @@ void vp_launch_multiply(vp_plan_s *P, VpGrid &G) {
 // interpolation (NH grid, which also carries the prolongated FH field) + local part + scatter.
 // One CTA of 256 threads per work item (tile_x, tile_y, t0, t1): the (TSI+W+3)^2 grid window of a
 // TSI x TSI tile is staged once in shared memory (coalesced rows), then every thread interpolates
-// targets t0 + tid, t0 + tid + 256, ... from shared memory.  Targets were ordered at plan time by
-// footprint origin inside the tile (vp_build_interp_order): sparse tiles read consecutive columns,
-// dense cells read the same addresses (broadcasts).
+// targets t0 + tid, t0 + tid + 256, ... from shared memory.  Targets were ordered at plan time
+// rank-major over the bank slot of their footprint origin (vp_build_interp_order), so the 32
+// row-reads of a warp spread over the 16 8-byte bank slots.
 template <int W, int D>
 __global__ void __launch_bounds__(256, 4) k_interp_local(const int4 *__restrict__ items, int TSI,
                                                       const double *__restrict__ tx, const double *__restrict__ ty,
@@ -1028,7 +1031,7 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// plan-time: order the targets by (TSI-tile, footprint row, footprint column) and cut the tiles into
+// plan-time: order the targets by (TSI-tile, rank within bank slot, bank slot) and cut the tiles into
 // work items of <= VP_INTERP_CHUNK targets
 #define VP_INTERP_CHUNK 16384  // targets per work item: dense tiles reload the grid window once per item
 __global__ void k_interp_keys1(const double *__restrict__ xy, int64_t n, GridArgs g, int TSI, int W, int64_t ntx,
@@ -1039,15 +1042,26 @@ __global__ void k_interp_keys1(const double *__restrict__ xy, int64_t n, GridArg
   int64_t tx = (int64_t)floor(gx / TSI), ty = (int64_t)floor(gy / TSI);
   tx = tx < 0 ? 0 : (tx >= ntx ? ntx - 1 : tx);
   ty = ty < 0 ? 0 : (ty >= nty ? nty - 1 : ty);
-  // order inside a tile: by footprint origin (row, column).  Consecutive targets of a sparse tile then read
-  // consecutive columns (distinct bank slots), and the many targets of one dense cell (config-5 clusters) read
-  // the same addresses -- shared-memory broadcasts, one wavefront per instruction
+  const int nw = TSI + W + 3;
   int64_t lrow = (int64_t)ceil(gy - 0.5 * W) - (ty * TSI - (W / 2 + 1));
   int64_t lcol = (int64_t)ceil(gx - 0.5 * W) - (tx * TSI - (W / 2 + 1));
-  lrow = lrow < 0 ? 0 : (lrow > 255 ? 255 : lrow);
-  lcol = lcol < 0 ? 0 : (lcol > 255 ? 255 : lcol);
-  keys[i] = ((uint64_t)(ty * ntx + tx) << 16) | ((uint64_t)lrow << 8) | (uint64_t)lcol;
+  const int res = (int)((((lrow * nw + lcol) % 16) + 16) % 16);
+  keys[i] = ((uint64_t)(ty * ntx + tx) << 4) | (uint64_t)res;
   idx[i] = (int32_t)i;
+}
+
+__global__ void k_interp_keys2(const uint64_t *__restrict__ k1, int64_t n, uint64_t *__restrict__ k2) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t key = k1[i];
+  int64_t lo = 0, hi = i;
+  while (lo < hi) {  // first index of this (tile, slot) group
+    int64_t mid = (lo + hi) >> 1;
+    if (k1[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  uint64_t rank = (uint64_t)(i - lo);
+  if (rank > 0xFFFFF) rank = 0xFFFFF;
+  k2[i] = ((key >> 4) << 24) | (rank << 4) | (key & 15);
 }
 
 // TRIANGLE mode: node targets ordered by (tile, triangle, node) so that the per-node V_L reads of a warp are
@@ -1099,8 +1113,10 @@ void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
   } else {
     k_interp_keys1<<<nb, 256, 0, s>>>(xy, n, g, TSI, P->w, ntx, nty, k1, i1);
     VP_CHECK_LAUNCH();
-    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k2s, i1, i2s, (int)n, 0, 64, s));
-    tile_shift = 16;
+    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
+    k_interp_keys2<<<nb, 256, 0, s>>>(k1s, n, k2);
+    VP_CHECK_LAUNCH();
+    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
   }
   P->tx = vp_alloc<double>(P, n);
   P->ty = vp_alloc<double>(P, n);
