@@ -295,7 +295,7 @@ static void setup_horner(vp_plan_s *P) {
   }
   P->horner_err = maxerr;
   vp_upload_horner(W, P->horner);
-  if (!(maxerr < 1e-6)) {
+  if (!(maxerr <= 0.6 * P->eps)) {  // the fit error floor is the truncated kernel's edge value, ~0.16 eps
     vp_set_last_error("Horner fit of the ES kernel failed");
     throw VpError{VP_ERR_CUDA};
   }
@@ -521,10 +521,12 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     if (P->dmode != VP_DERIV_KNN && P->dmode != VP_DERIV_TRIANGLE) throw VpError{VP_ERR_ARG};
     P->deg = o.deriv_degree > 0 ? o.deriv_degree : (N > 1000000 ? 4 : 6);
     if (P->deg > VP_MAXDEG) throw VpError{VP_ERR_ARG};
+    while (P->deg > 0 && 2 * vp_ncoef(P->deg) > N && o.deriv_degree <= 0) P->deg--;  // tiny inputs
     int nc = vp_ncoef(P->deg);
     // K: 2 x #monomials at degree >= 5; degree 4 needs fewer (config 2: 1.30e-9 at K = 17, 20, 24 and 30)
     P->K = o.deriv_k > 0 ? o.deriv_k : (P->deg >= 5 ? 2 * nc : nc + 6);
     if (P->K > 64) P->K = 64;
+    if (P->K > N && o.deriv_k <= 0) P->K = (int)N;
     if (P->K < nc) throw VpError{VP_ERR_ARG};
     if (P->K > N) throw VpError{VP_ERR_ARG};
     if (parts & VP_PART_LOCAL) {

@@ -41,7 +41,7 @@ void vp_set_last_error(const std::string &s);
 // ---------------------------------------------------------------------------------------------
 // ES kernel taps as Horner polynomials: psi(z_k(t)), z_k = (k + (t+1)/2 - W/2) 2/W, t in [-1, 1]
 #define VP_HORNER_MAXW 16
-#define VP_HORNER_DEG(W) ((W) <= 8 ? (W) : ((W)-1))
+#define VP_HORNER_DEG(W) ((W) <= 8 ? ((W) + 1) : ((W)-1))  // fit error ~0.16 x 10^-(W-1): the kernel's edge value
 struct VpHorner {
   double c[VP_HORNER_MAXW][VP_HORNER_MAXW];  // c[k][j]: coefficient of t^j for tap k
 };
