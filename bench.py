@@ -218,7 +218,6 @@ def main():
     plan = vp.Plan(nodes, wts, tg, w.tol, boundary=w.boundary, targets_are_nodes=w.targets_are_nodes, stream=stream,
                    ref_nodes=rule.BARY[:, 1:3], levels=levels)
     info = plan.info()
-    plan.set_profiling(True)
     out = torch.empty(w.T, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -241,9 +240,8 @@ def main():
         for s in range(args.steps):
             flush.zero_()                       # L2 flush outside the timed events
             evs[s][0].record(stream)
-            plan.eval(f, out)
+            plan.eval(f, out)                   # fork/join across three streams; joined on `stream`
             evs[s][1].record(stream)
-            phases.append(plan.phase_times())   # syncs on this step's last event
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
         if world > 1:
@@ -256,8 +254,17 @@ def main():
     value = aggregate_rate(world, pts, ms_max)
     kern, ffts = plan.launch_count()
 
-    # ---- roofline of the dominant kernel (algorithmic bytes, DESIGN.md §Roofline)
+    # ---- per-phase times: separate profiled evals (serial on one stream so that the CUDA events bracket each
+    # phase; the timed steps above overlap the far-history chain and the local part with the near-history FFTs)
+    plan.set_profiling(True)
+    for s in range(max(3, min(args.steps, 10))):
+        flush.zero_()
+        plan.eval(f, out)
+        phases.append(plan.phase_times())
+    plan.set_profiling(False)
     ph = {k: float(np.mean([p[k] for p in phases])) for k in phases[0]}
+    serial_ms = float(sum(ph.values()))
+    # ---- roofline of the dominant kernel (algorithmic bytes, DESIGN.md §Roofline)
     # algorithmic bytes: spread reads x, y, w, f per source and writes the NH grid once;
     # interp_local reads the NH grid once, x, y per target, writes out, reads the target's own f, and the
     # stencil (int32 + fp64 per entry) for stencil targets or the triangle metric (24 B / 12 targets) otherwise
@@ -307,7 +314,7 @@ def main():
                            "deriv": f"{['auto', 'knn', 'triangle'][info['deriv_mode']]} (knn deg {info['deriv_degree']} K {K} "
                                     f"on {S} targets)", "levels": info["n_levels"], "plan_ms": info["plan_ms"],
                            "spread_batches": info["n_batches"], "spread_lane_fill": w.N / max(1, info["n_batches"]) / 32.0},
-                "phase_ms": ph, "wall_ms_per_step": t_wall * 1e3 / args.steps,
+                "phase_ms": ph, "serial_ms_per_step": serial_ms, "wall_ms_per_step": t_wall * 1e3 / args.steps,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk.summary(), "gpu_launches": kern * args.steps,
                 "cufft_execs": ffts * args.steps}

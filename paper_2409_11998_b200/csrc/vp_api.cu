@@ -385,14 +385,15 @@ static void make_fft_plans(vp_plan_s *P) {
                                  &ws[2 * g + 1]));
     G.has_plans = true;
   }
-  for (int i = 0; i < 4; i++) wmax = std::max(wmax, ws[i]);
-  void *work = vp_alloc<char>(P, wmax + 256);
+  // separate work areas: the NH and FH transforms run concurrently on different streams
   for (int g = 0; g < 2; g++) {
+    void *work = vp_alloc<char>(P, std::max(ws[2 * g], ws[2 * g + 1]) + 256);
     VP_CUFFT(cufftSetWorkArea(gs[g]->fwd, work));
     VP_CUFFT(cufftSetWorkArea(gs[g]->inv, work));
     VP_CUFFT(cufftSetStream(gs[g]->fwd, P->stream));
     VP_CUFFT(cufftSetStream(gs[g]->inv, P->stream));
   }
+  (void)wmax;
 }
 
 
@@ -419,6 +420,10 @@ static void free_plan(vp_plan_s *P) {
     cufftDestroy(P->bands.fwd);
     cufftDestroy(P->bands.inv);
   }
+  if (P->s_fh) cudaStreamDestroy(P->s_fh);
+  if (P->s_loc) cudaStreamDestroy(P->s_loc);
+  for (cudaEvent_t e : {P->ev_fork, P->ev_fh, P->ev_loc})
+    if (e) cudaEventDestroy(e);
   for (void *p : P->allocs) cudaFree(p);
   if (P->ev_init)
     for (int i = 0; i < 10; i++) cudaEventDestroy(P->ev[i]);
@@ -544,8 +549,13 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
       P->lw = vp_alloc<double>(P, 1);
       P->lptr = vp_alloc<int32_t>(P, 1);
     }
-    // ---- FFT plans
+    // ---- FFT plans, forked streams
     make_fft_plans(P);
+    VP_CUDA(cudaStreamCreateWithFlags(&P->s_fh, cudaStreamNonBlocking));
+    VP_CUDA(cudaStreamCreateWithFlags(&P->s_loc, cudaStreamNonBlocking));
+    VP_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+    VP_CUDA(cudaEventCreateWithFlags(&P->ev_fh, cudaEventDisableTiming));
+    VP_CUDA(cudaEventCreateWithFlags(&P->ev_loc, cudaEventDisableTiming));
     VP_CUDA(cudaStreamSynchronize(P->stream));
     VP_CUDA(cudaGetLastError());
   } catch (VpError &e) {
@@ -566,6 +576,56 @@ static void record(vp_plan_s *P, int i) {
   if (P->profiling) cudaEventRecord(P->ev[i], P->stream);
 }
 
+// Fork/join eval (no profiling): after the spread, the far-history chain (restriction, FH transforms,
+// prolongation pass B^T) runs on stream B and the local part (stencils, triangle fits) on stream C while
+// the near-history transforms run on the caller's stream A; A joins both before the interpolation.
+// Cross-eval hazards: B and C start after A's spread of this eval, i.e. after A finished every read of
+// the previous eval's scratch (t2), V_L buffers and grids.
+struct StreamScope {
+  vp_plan_s *P;
+  cudaStream_t old;
+  StreamScope(vp_plan_s *p, cudaStream_t s) : P(p), old(p->stream) { P->stream = s; }
+  ~StreamScope() { P->stream = old; }
+};
+
+static void eval_concurrent(vp_plan_s *P, const double *f, double *out, int parts) {
+  cudaStream_t A = P->stream;
+  VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, A));
+  vp_launch_spread(P, P->sp, grid_args(P->nh), f);
+  VP_CUDA(cudaEventRecord(P->ev_fork, A));
+  {  // B: far history
+    StreamScope sc(P, P->s_fh);
+    VP_CUDA(cudaStreamWaitEvent(P->s_fh, P->ev_fork, 0));
+    VP_CUDA(cudaMemsetAsync(P->fh.data, 0, sizeof(double) * P->fh.nf * P->fh.row, P->s_fh));
+    vp_launch_restrict(P);
+    VP_CUFFT(cufftSetStream(P->fh.fwd, P->s_fh));
+    VP_CUFFT(cufftSetStream(P->fh.inv, P->s_fh));
+    VP_CUFFT(cufftExecD2Z(P->fh.fwd, P->fh.data, (cufftDoubleComplex *)P->fh.cdata));
+    vp_launch_multiply(P, P->fh);
+    VP_CUFFT(cufftExecZ2D(P->fh.inv, (cufftDoubleComplex *)P->fh.cdata, P->fh.data));
+    vp_launch_prolong(P, 1);
+    VP_CUDA(cudaEventRecord(P->ev_fh, P->s_fh));
+  }
+  bool local_forked = false;
+  if (parts & VP_PART_LOCAL) {  // C: local part
+    StreamScope sc(P, P->s_loc);
+    VP_CUDA(cudaStreamWaitEvent(P->s_loc, P->ev_fork, 0));
+    vp_launch_tri_local(P, f);
+    VP_CUDA(cudaEventRecord(P->ev_loc, P->s_loc));
+    local_forked = true;
+  }
+  // A: near history, join, interpolation
+  VP_CUFFT(cufftExecD2Z(P->nh.fwd, P->nh.data, (cufftDoubleComplex *)P->nh.cdata));
+  vp_launch_multiply(P, P->nh);
+  VP_CUFFT(cufftExecZ2D(P->nh.inv, (cufftDoubleComplex *)P->nh.cdata, P->nh.data));
+  VP_CUDA(cudaStreamWaitEvent(A, P->ev_fh, 0));
+  vp_launch_prolong(P, 2);
+  if (local_forked) VP_CUDA(cudaStreamWaitEvent(A, P->ev_loc, 0));
+  P->n_ffts = 4;
+  vp_launch_interp_local(P, f, out, false);
+  if (parts & VP_PART_LOCAL) vp_launch_bands(P, f, out);
+}
+
 extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
   if (!P || !f || !out) return VP_ERR_ARG;
   try {
@@ -576,6 +636,12 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
       for (int i = 0; i < 10; i++) VP_CUDA(cudaEventCreate(&P->ev[i]));
       P->ev_init = true;
     }
+    if (!P->profiling && P->concurrent && (parts & VP_PART_HISTORY)) {
+      eval_concurrent(P, f, out, parts);
+      return VP_OK;
+    }
+    VP_CUFFT(cufftSetStream(P->fh.fwd, P->stream));
+    VP_CUFFT(cufftSetStream(P->fh.inv, P->stream));
     record(P, 0);
     if (parts & VP_PART_HISTORY) {
       VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, P->stream));
@@ -594,13 +660,13 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
       VP_CUFFT(cufftExecZ2D(P->nh.inv, (cufftDoubleComplex *)P->nh.cdata, P->nh.data));
       VP_CUFFT(cufftExecZ2D(P->fh.inv, (cufftDoubleComplex *)P->fh.cdata, P->fh.data));
       record(P, 6);
-      vp_launch_prolong(P);
+      vp_launch_prolong(P, 3);
       P->n_ffts = 4;
       record(P, 7);
     } else {
       for (int i = 1; i <= 7; i++) record(P, i);
     }
-    vp_launch_interp_local(P, f, out);
+    vp_launch_interp_local(P, f, out, true);
     record(P, 8);
     if (parts & VP_PART_LOCAL) vp_launch_bands(P, f, out);
     record(P, 9);

@@ -123,7 +123,10 @@ struct vp_plan_s {
   int32_t p = 0;
   double tol = 0, eps = 0;
   vp_opts opts{};
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;       // the caller's stream (A): spread, NH chain, interpolation
+  cudaStream_t s_fh = nullptr, s_loc = nullptr;  // forked streams: FH chain (B), local part (C)
+  cudaEvent_t ev_fork = nullptr, ev_fh = nullptr, ev_loc = nullptr;
+  bool concurrent = true;              // fork/join eval (off while profiling: phases need serial order)
   // parameters
   double dx2 = 0, delta1 = 0, delta2 = 0, kmax_nh = 0, kmax_fh = 0, R = 0, S = 0, cx = 0, cy = 0;
   int w = 0;
@@ -207,9 +210,10 @@ int64_t vp_next_smooth(int64_t n);
 void vp_es_deconv_table(const vp_plan_s *P, double h, double L, int64_t nhalf, std::vector<double> &out);
 void vp_upload_horner(int W, const VpHorner &h);
 void vp_launch_restrict(vp_plan_s *P);
-void vp_launch_prolong(vp_plan_s *P);
+void vp_launch_prolong(vp_plan_s *P, int pass);
+void vp_launch_tri_local(vp_plan_s *P, const double *f);
 void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
-void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out);
+void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out, bool local_kernels);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n);
 void vp_remap_stencils(vp_plan_s *P);
 void vp_build_local(vp_plan_s *P, const double *nodes_dev);

@@ -634,22 +634,22 @@ static void launch_restrict_int(vp_plan_s *P, const RestrictArgs &a, const TapAr
 }
 
 template <int M>
-static void launch_prolong_int(vp_plan_s *P, const RestrictArgs &a, const TapArgs &tp, bool fuse_x) {
+static void launch_prolong_int(vp_plan_s *P, const RestrictArgs &a, const TapArgs &tp, bool fuse_x, int pass) {
   // NH index i = M c + k - j covers [0, n1) for c in [c_lo, c_hi]
   const int64_t c_lo = (tp.j >= 0) ? tp.j / M : -((-tp.j + M - 1) / M);
   const int64_t c_hi = (a.n1 - 1 + tp.j) / M;
   const int64_t nc = c_hi - c_lo + 1;
-  dim3 gB((unsigned)((a.ne + 127) / 128), (unsigned)nc);
-  k_prolong_y_int<M><<<gB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a, tp, c_lo);
-  VP_CHECK_LAUNCH();
-  if (fuse_x) {  // pass A^T is applied by k_interp_local while it stages its grid windows
+  if (pass & 1) {
+    dim3 gB((unsigned)((a.ne + 127) / 128), (unsigned)nc);
+    k_prolong_y_int<M><<<gB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a, tp, c_lo);
+    VP_CHECK_LAUNCH();
     P->n_kernels++;
-    return;
   }
+  if (fuse_x || !(pass & 2)) return;  // fused: pass A^T is applied by k_interp_local while staging windows
   dim3 gA((unsigned)((nc + 127) / 128), (unsigned)a.n1);
   k_prolong_x_int<M><<<gA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a, tp, c_lo, nc);
   VP_CHECK_LAUNCH();
-  P->n_kernels += 2;
+  P->n_kernels++;
 }
 
 static RestrictArgs restrict_args(vp_plan_s *P) {
@@ -685,30 +685,36 @@ void vp_launch_restrict(vp_plan_s *P) {
   P->n_kernels += 2;
 }
 
-void vp_launch_prolong(vp_plan_s *P) {
+// pass: 1 = FH rows -> t2 (pass B^T, reads the FH grid), 2 = t2 -> NH grid (pass A^T), 3 = both
+void vp_launch_prolong(vp_plan_s *P, int pass) {
   RestrictArgs a = restrict_args(P);
-  P->prolong_fused = false;
+  if (pass & 1) P->prolong_fused = false;
   if (P->tap_qh > 0) {
     TapArgs tp = tap_args(P);
     const bool fuse = !P->no_fuse_prolong;
     switch (P->fh_ratio) {
-      case 2: launch_prolong_int<2>(P, a, tp, fuse); P->prolong_fused = fuse; return;
-      case 3: launch_prolong_int<3>(P, a, tp, fuse); P->prolong_fused = fuse; return;
-      case 4: launch_prolong_int<4>(P, a, tp, fuse); P->prolong_fused = fuse; return;
-      case 5: launch_prolong_int<5>(P, a, tp, fuse); P->prolong_fused = fuse; return;
-      case 6: launch_prolong_int<6>(P, a, tp, fuse); P->prolong_fused = fuse; return;
-      case 7: launch_prolong_int<7>(P, a, tp, fuse); P->prolong_fused = fuse; return;
-      case 8: launch_prolong_int<8>(P, a, tp, fuse); P->prolong_fused = fuse; return;
+      case 2: launch_prolong_int<2>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
+      case 3: launch_prolong_int<3>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
+      case 4: launch_prolong_int<4>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
+      case 5: launch_prolong_int<5>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
+      case 6: launch_prolong_int<6>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
+      case 7: launch_prolong_int<7>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
+      case 8: launch_prolong_int<8>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
       default: break;
     }
   }
-  dim3 bB((unsigned)((a.ne + 127) / 128), (unsigned)a.n1);
-  k_prolong_y<<<bB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a);
-  VP_CHECK_LAUNCH();
-  dim3 bA((unsigned)((a.n1 + 127) / 128), (unsigned)a.n1);
-  k_prolong_x<<<bA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a);
-  VP_CHECK_LAUNCH();
-  P->n_kernels += 2;
+  if (pass & 1) {
+    dim3 bB((unsigned)((a.ne + 127) / 128), (unsigned)a.n1);
+    k_prolong_y<<<bB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a);
+    VP_CHECK_LAUNCH();
+    P->n_kernels++;
+  }
+  if (pass & 2) {
+    dim3 bA((unsigned)((a.n1 + 127) / 128), (unsigned)a.n1);
+    k_prolong_x<<<bA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a);
+    VP_CHECK_LAUNCH();
+    P->n_kernels++;
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1143,9 +1149,9 @@ void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
     VP_CUDA(cudaFreeAsync(q, s));
 }
 
-void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out) {
+void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out, bool local_kernels) {
   int parts_ = P->opts.parts ? P->opts.parts : VP_PART_ALL;
-  if (parts_ & VP_PART_LOCAL) vp_launch_tri_local(P, f);
+  if (local_kernels && (parts_ & VP_PART_LOCAL)) vp_launch_tri_local(P, f);
   switch (P->w) {
 #define CASE(W) \
   case W: launch_interp_w<W>(P, f, out); break;
