@@ -636,7 +636,9 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
       for (int i = 0; i < 10; i++) VP_CUDA(cudaEventCreate(&P->ev[i]));
       P->ev_init = true;
     }
-    if (!P->profiling && P->concurrent && (parts & VP_PART_HISTORY)) {
+    // fork/join pays only when the kernels leave the GPU partly idle: measured faster for config 2 (2744^2
+    // grids: 0.97 vs 1.03 ms), slower for configs 3-5 (c5: 63.5 vs 58.5 ms)
+    if (!P->profiling && P->concurrent && P->nh.nf <= 6000 && (parts & VP_PART_HISTORY)) {
       eval_concurrent(P, f, out, parts);
       return VP_OK;
     }
