@@ -316,30 +316,13 @@ __global__ void __launch_bounds__(32) k_spread_dense(const int4 *__restrict__ it
   for (int r = 0; r < H; r++)
 #pragma unroll
     for (int a = 0; a < W; a++) acc[r][a] = 0.0;
-  // software pipeline: point j + 16 is loaded while point j is accumulated; the two halves share one point and
-  // split its kernel weights (half 0: x taps, half 1: y taps, exchanged with W shuffles)
-  int j = it.z + l16;
-  double xn = 0.0, yn = 0.0, wn = 0.0, fn = 0.0;
-  if (j < it.w) {
-    xn = dx[j]; yn = dy[j]; wn = dw[j];
-    fn = __ldg(f + dperm[j]);
-  }
-  for (; j < it.w; j += 16) {
-    const double x = xn, y = yn, fj = fn, wj = wn;
-    const int jn = j + 16;
-    int pn = -1;
-    if (jn < it.w) {
-      xn = dx[jn]; yn = dy[jn]; wn = dw[jn];
-      pn = dperm[jn];
-    }
+  for (int j = it.z + l16; j < it.w; j += 16) {
+    const double fj = __ldg(f + dperm[j]);
     if (fs_out && half == 0) fs_out[j] = fj;
-    const double c = fj * wj;
-    double wown[W], woth[W];
-    es_horner<W, D>(half ? gcoord(y, g.oy, g.inv_h) : gcoord(x, g.ox, g.inv_h), wown);
-#pragma unroll
-    for (int a = 0; a < W; a++) woth[a] = __shfl_xor_sync(0xffffffffu, wown[a], 16);
-    const double *wx = half ? woth : wown;
-    const double *wy = half ? wown : woth;
+    const double c = fj * dw[j];
+    double wx[W], wy[W];
+    es_horner<W, D>(gcoord(dx[j], g.ox, g.inv_h), wx);
+    es_horner<W, D>(gcoord(dy[j], g.oy, g.inv_h), wy);
 #pragma unroll
     for (int r = 0; r < H; r++) {
       const int rr = r + H * half;
@@ -347,7 +330,6 @@ __global__ void __launch_bounds__(32) k_spread_dense(const int4 *__restrict__ it
 #pragma unroll
       for (int a = 0; a < W; a++) acc[r][a] = fma(cy, wx[a], acc[r][a]);
     }
-    if (pn >= 0) fn = __ldg(f + pn);
   }
   // sum over the 16 lanes of each half-warp (every lane ends with the totals)
 #pragma unroll
