@@ -1466,12 +1466,10 @@ void vp_build_spread_split(vp_plan_s *P, const double *xy, const double *weights
   const unsigned nb = (unsigned)((n + 255) / 256);
   k_origin_keys<<<nb, 256, 0, s>>>(xy, n, g, P->w, k, ix);
   VP_CHECK_LAUNCH();
-  size_t tb = 0, tb2 = 0, tb3 = 0;
+  size_t tb = 0, tb2 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, k, ks, ix, ixs, (int)n, 0, 64, s);
   cub::CountingInputIterator<int32_t> cnt0(0);
   cub::DeviceSelect::Flagged(nullptr, tb2, ixs, fd, sel, d_cnt, (int)n, s);
-  cub::DeviceSelect::Flagged(nullptr, tb3, ks, fd, k, d_cnt, (int)n, s);
-  tb2 = std::max(tb2, tb3);
   void *tmp;
   VP_CUDA(cudaMallocAsync(&tmp, std::max(tb, tb2) + 16, s));
   VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k, ks, ix, ixs, (int)n, 0, 64, s));
