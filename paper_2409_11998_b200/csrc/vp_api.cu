@@ -508,7 +508,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     // ---- sources and targets sorted by NH tile
     P->sp.det = o.deterministic ? 1 : 0;
     P->bands.sp.det = P->sp.det;
-    vp_build_spread_split(P, tri_nodes, weights, grid_args(P->nh));
+    vp_build_spread_order(P, P->sp, tri_nodes, weights, nullptr, N, grid_args(P->nh));
     P->dmode = o.deriv_mode;
     if (P->dmode == VP_DERIV_AUTO) P->dmode = (o.ref_nodes && N > 10000000) ? VP_DERIV_TRIANGLE : VP_DERIV_KNN;
     vp_build_interp_order(P, targets, T);
@@ -592,7 +592,6 @@ static void eval_concurrent(vp_plan_s *P, const double *f, double *out, int part
   cudaStream_t A = P->stream;
   VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, A));
   vp_launch_spread(P, P->sp, grid_args(P->nh), f);
-  vp_launch_spread_dense(P, grid_args(P->nh), f);
   VP_CUDA(cudaEventRecord(P->ev_fork, A));
   {  // B: far history
     StreamScope sc(P, P->s_fh);
@@ -651,7 +650,6 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
       VP_CUDA(cudaMemsetAsync(P->fh.data, 0, sizeof(double) * P->fh.nf * P->fh.row, P->stream));
       record(P, 1);
       vp_launch_spread(P, P->sp, grid_args(P->nh), f);
-      vp_launch_spread_dense(P, grid_args(P->nh), f);
       record(P, 2);
       vp_launch_restrict(P);
       record(P, 3);

@@ -94,16 +94,6 @@ struct VpSpreadSet {
   double *fs_out = nullptr;    // if set, the spread also writes f in this sorted order
 };
 
-// Dense footprint-origin cells spread by register accumulation (vp_nufft.cu k_spread_dense)
-struct VpDense {
-  int64_t n = 0;                   // points
-  double *dx = nullptr, *dy = nullptr, *dw = nullptr;
-  int32_t *dperm = nullptr;        // -> user node index
-  int4 *items = nullptr;           // (ix0, iy0, first, end)
-  int64_t nitems = 0;
-  int64_t fs_off = 0;              // offset of these points in the spreading-order f copy
-};
-
 // Level-band corrections for graded meshes: per-target level
 // l(x) in 0..nlev, bands B_l (l = 1..l(x)) by box-local NUFFTs on one "virtual" grid of nbox boxes
 // (box b = rows [b nfb, (b+1) nfb)), V_L evaluated with delta_{l(x)} = delta_1 / 4^{l(x)}.
@@ -152,8 +142,6 @@ struct vp_plan_s {
   double horner_err = 0;
   // sources, sorted by (NH tile, row rank, row) into batches of <= 32 points with distinct rows
   VpSpreadSet sp;
-  int64_t sp_n = 0;            // points on the tile path (the rest are in `dense`)
-  VpDense dense;
   // graded-mesh level bands (a12)
   VpBands bands;
   // FH <- NH restriction tables
@@ -216,8 +204,6 @@ void vp_launch_spread(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, con
 void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const double *w, const int32_t *node_of,
                            int64_t n, const GridArgs &g);
 void vp_build_levels(vp_plan_s *P, const double *nodes, const double *weights);
-void vp_build_spread_split(vp_plan_s *P, const double *xy, const double *weights, const GridArgs &g);
-void vp_launch_spread_dense(vp_plan_s *P, const GridArgs &g, const double *f);
 void vp_launch_bands(vp_plan_s *P, const double *f, double *out);
 double vp_solve_e1(double eps);
 int64_t vp_next_smooth(int64_t n);

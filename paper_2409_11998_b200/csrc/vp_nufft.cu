@@ -296,92 +296,6 @@ __global__ void __launch_bounds__(32) k_spread_nh(const int4 *__restrict__ items
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// Dense cells (plan: >= VP_DENSE_MIN points share one footprint-origin cell, e.g. the config-5 clusters with
-// ~1700 nodes per NH cell).  All points of a cell share the same w x w footprint, so their contributions are
-// summed in REGISTERS first: B[r][a] = sum_p c_p psi_y,p[r] psi_x,p[a].  One warp per work item (cell, <= CH
-// points): the two half-warps own rows [0, H) and [H, W) of B (H = ceil(W/2)), each lane accumulates its
-// share of the points, the 16 lanes of a half are summed with xor shuffles, and the W x W block goes to the
-// grid with W^2 fp64 REDs -- no shared memory at all (fp64-issue bound instead of LSU bound).
-template <int W, int D>
-__global__ void __launch_bounds__(32) k_spread_dense(const int4 *__restrict__ items, const double *__restrict__ dx,
-                                                     const double *__restrict__ dy, const double *__restrict__ dw,
-                                                     const int32_t *__restrict__ dperm, const double *__restrict__ f,
-                                                     GridArgs g, double *__restrict__ fs_out) {
-  constexpr int H = (W + 1) / 2;
-  const int lane = threadIdx.x, half = lane >> 4, l16 = lane & 15;
-  const int4 it = items[blockIdx.x];  // (ix0, iy0, first point, end point)
-  double acc[H][W];
-#pragma unroll
-  for (int r = 0; r < H; r++)
-#pragma unroll
-    for (int a = 0; a < W; a++) acc[r][a] = 0.0;
-  for (int j = it.z + l16; j < it.w; j += 16) {
-    const double fj = __ldg(f + dperm[j]);
-    if (fs_out && half == 0) fs_out[j] = fj;
-    const double c = fj * dw[j];
-    double wx[W], wy[W];
-    es_horner<W, D>(gcoord(dx[j], g.ox, g.inv_h), wx);
-    es_horner<W, D>(gcoord(dy[j], g.oy, g.inv_h), wy);
-#pragma unroll
-    for (int r = 0; r < H; r++) {
-      const int rr = r + H * half;
-      const double cy = rr < W ? c * (half ? wy[(r + H) < W ? r + H : 0] : wy[r]) : 0.0;
-#pragma unroll
-      for (int a = 0; a < W; a++) acc[r][a] = fma(cy, wx[a], acc[r][a]);
-    }
-  }
-  // sum over the 16 lanes of each half-warp (every lane ends with the totals)
-#pragma unroll
-  for (int r = 0; r < H; r++)
-#pragma unroll
-    for (int a = 0; a < W; a++) {
-      double v = acc[r][a];
-#pragma unroll
-      for (int o = 8; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, 16);
-      acc[r][a] = v;
-    }
-  const bool interior = it.x >= 0 && it.y >= 0 && it.x + W <= g.nfx && it.y + W <= g.nfy;
-#pragma unroll
-  for (int r = 0; r < H; r++) {
-    const int rr = r + H * half;
-    if (rr >= W) continue;
-#pragma unroll
-    for (int a = 0; a < W; a++) {
-      if (((r * W + a) & 15) != l16) continue;
-      const double v = acc[r][a];
-      if (v == 0.0) continue;
-      int64_t gx = (int64_t)it.x + a, gy = (int64_t)it.y + rr;
-      if (!interior) {
-        gx = wrapi(gx, g.nfx);
-        gy = wrapi(gy, g.nfy);
-      }
-      atomicAdd(g.data + gy * g.row + gx, v);
-    }
-  }
-}
-
-template <int W>
-static void launch_spread_dense_w(vp_plan_s *P, const GridArgs &g, const double *f) {
-  constexpr int D = VP_HORNER_DEG(W);
-  const VpDense &Dn = P->dense;
-  if (Dn.nitems == 0) return;
-  k_spread_dense<W, D><<<(unsigned)Dn.nitems, 32, 0, P->stream>>>(Dn.items, Dn.dx, Dn.dy, Dn.dw, Dn.dperm, f, g,
-                                                                  P->fs ? P->fs + Dn.fs_off : nullptr);
-  VP_CHECK_LAUNCH();
-  P->n_kernels++;
-}
-
-void vp_launch_spread_dense(vp_plan_s *P, const GridArgs &g, const double *f) {
-  switch (P->w) {
-#define CASE(W) \
-  case W: launch_spread_dense_w<W>(P, g, f); break;
-    CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
-#undef CASE
-    default: throw VpError{VP_ERR_UNSUPPORTED};
-  }
-}
-
 template <int W>
 static void launch_spread_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *f) {
   constexpr int D = VP_HORNER_DEG(W);
@@ -1036,9 +950,9 @@ __global__ void __launch_bounds__(256) k_local_stencil(const int32_t *__restrict
   vL_st[s] = acc;
 }
 
-__global__ void k_invert_perm(const int32_t *__restrict__ perm, int64_t n, int32_t *__restrict__ inv, int64_t off) {
+__global__ void k_invert_perm(const int32_t *__restrict__ perm, int64_t n, int32_t *__restrict__ inv) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) inv[perm[i]] = (int32_t)(off + i);
+  if (i < n) inv[perm[i]] = (int32_t)i;
 }
 
 __global__ void k_remap_idx(int32_t *__restrict__ idx, int64_t n, const int32_t *__restrict__ inv) {
@@ -1051,13 +965,8 @@ void vp_remap_stencils(vp_plan_s *P) {
   if (P->n_stencil == 0 || P->K == 0) return;
   int32_t *inv = nullptr;
   VP_CUDA(cudaMallocAsync(&inv, sizeof(int32_t) * P->N, P->stream));
-  k_invert_perm<<<(unsigned)((P->sp_n + 255) / 256 + 1), 256, 0, P->stream>>>(P->sp.sperm, P->sp_n, inv, 0);
+  k_invert_perm<<<(unsigned)((P->N + 255) / 256), 256, 0, P->stream>>>(P->sp.sperm, P->N, inv);
   VP_CHECK_LAUNCH();
-  if (P->dense.n > 0) {
-    k_invert_perm<<<(unsigned)((P->dense.n + 255) / 256), 256, 0, P->stream>>>(P->dense.dperm, P->dense.n, inv,
-                                                                               P->dense.fs_off);
-    VP_CHECK_LAUNCH();
-  }
   const int64_t ne = P->n_stencil * (int64_t)P->K;
   k_remap_idx<<<(unsigned)((ne + 255) / 256), 256, 0, P->stream>>>(P->lidx, ne, inv);
   VP_CHECK_LAUNCH();
@@ -1076,15 +985,8 @@ void vp_launch_tri_local(vp_plan_s *P, const double *f) {
     // when the history part is off)
     int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
     if (!(parts & VP_PART_HISTORY)) {
-      if (P->sp_n > 0) {
-        k_gather_f<<<(unsigned)((P->sp_n + 255) / 256), 256, 0, P->stream>>>(f, P->sp.sperm, P->sp_n, P->fs);
-        VP_CHECK_LAUNCH();
-      }
-      if (P->dense.n > 0) {
-        k_gather_f<<<(unsigned)((P->dense.n + 255) / 256), 256, 0, P->stream>>>(f, P->dense.dperm, P->dense.n,
-                                                                                P->fs + P->dense.fs_off);
-        VP_CHECK_LAUNCH();
-      }
+      k_gather_f<<<(unsigned)((P->N + 255) / 256), 256, 0, P->stream>>>(f, P->sp.sperm, P->N, P->fs);
+      VP_CHECK_LAUNCH();
       P->n_kernels++;
     }
     k_local_stencil<<<(unsigned)((P->n_stencil + 255) / 256), 256, 0, P->stream>>>(P->lidx, P->lw, P->K, P->n_stencil,
@@ -1391,148 +1293,6 @@ void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const
   for (void *p : {(void *)k1, (void *)k1s, (void *)k2, (void *)k2s, (void *)i1, (void *)i1s, (void *)i2s, (void *)head,
                   tmp})
     VP_CUDA(cudaFreeAsync(p, s));
-}
-
-// ---------------------------------------------------------------------------------------------
-// plan-time split of the sources into dense footprint-origin cells (register path) and the rest (tiles)
-#define VP_DENSE_MIN 48
-#define VP_DENSE_CHUNK 256
-__global__ void k_origin_keys(const double *__restrict__ xy, int64_t n, GridArgs g, int W,
-                              uint64_t *__restrict__ keys, int32_t *__restrict__ idx) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t ix0 = (int64_t)ceil(gcoord(xy[2 * i], g.ox, g.inv_h) - 0.5 * W);
-  const int64_t iy0 = (int64_t)ceil(gcoord(xy[2 * i + 1], g.oy, g.inv_h) - 0.5 * W);
-  keys[i] = ((uint64_t)(iy0 + (1 << 24)) << 32) | (uint64_t)(ix0 + (1 << 24));
-  idx[i] = (int32_t)i;
-}
-
-__global__ void k_dense_flags(const uint64_t *__restrict__ ks, int64_t n, int min_run, int32_t *__restrict__ dense,
-                              int32_t *__restrict__ sparse) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint64_t k = ks[i];
-  int64_t lo = 0, hi = i;
-  while (lo < hi) {  // first of the run
-    int64_t mid = (lo + hi) >> 1;
-    if (ks[mid] < k) lo = mid + 1; else hi = mid;
-  }
-  int64_t lo2 = i, hi2 = n;
-  while (lo2 < hi2) {  // one past the run
-    int64_t mid = (lo2 + hi2) >> 1;
-    if (ks[mid] <= k) lo2 = mid + 1; else hi2 = mid;
-  }
-  const int d = (lo2 - lo) >= min_run ? 1 : 0;
-  dense[i] = d;
-  sparse[i] = 1 - d;
-}
-
-__global__ void k_gather_pts(const double *__restrict__ xy, const double *__restrict__ w,
-                             const int32_t *__restrict__ sel, int64_t n, double *__restrict__ ox,
-                             double *__restrict__ oy, double *__restrict__ oxy, double *__restrict__ ow,
-                             int32_t *__restrict__ onode) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int32_t j = sel[i];
-  const double x = xy[2 * (int64_t)j], y = xy[2 * (int64_t)j + 1];
-  if (ox) ox[i] = x;
-  if (oy) oy[i] = y;
-  if (oxy) { oxy[2 * i] = x; oxy[2 * i + 1] = y; }
-  ow[i] = w[j];
-  onode[i] = j;
-}
-
-// Builds P->dense (dense cells, register path) and P->sp (the remaining points, tile path).
-void vp_build_spread_split(vp_plan_s *P, const double *xy, const double *weights, const GridArgs &g) {
-  cudaStream_t s = P->stream;
-  const int64_t n = P->N;
-  VpDense &Dn = P->dense;
-  if (P->sp.det || P->opts.deterministic) {  // the register path uses atomics: deterministic mode keeps tiles only
-    vp_build_spread_order(P, P->sp, xy, weights, nullptr, n, g);
-    P->sp_n = n;
-    Dn.fs_off = n;
-    return;
-  }
-  uint64_t *k, *ks;
-  int32_t *ix, *ixs, *fd, *fsp, *sel, *d_cnt;
-  VP_CUDA(cudaMallocAsync(&k, 8 * (n + 1), s));
-  VP_CUDA(cudaMallocAsync(&ks, 8 * (n + 1), s));
-  VP_CUDA(cudaMallocAsync(&ix, 4 * (n + 1), s));
-  VP_CUDA(cudaMallocAsync(&ixs, 4 * (n + 1), s));
-  VP_CUDA(cudaMallocAsync(&fd, 4 * (n + 1), s));
-  VP_CUDA(cudaMallocAsync(&fsp, 4 * (n + 1), s));
-  VP_CUDA(cudaMallocAsync(&sel, 4 * (n + 1), s));
-  VP_CUDA(cudaMallocAsync(&d_cnt, 8, s));
-  const unsigned nb = (unsigned)((n + 255) / 256);
-  k_origin_keys<<<nb, 256, 0, s>>>(xy, n, g, P->w, k, ix);
-  VP_CHECK_LAUNCH();
-  size_t tb = 0, tb2 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb, k, ks, ix, ixs, (int)n, 0, 64, s);
-  cub::CountingInputIterator<int32_t> cnt0(0);
-  cub::DeviceSelect::Flagged(nullptr, tb2, ixs, fd, sel, d_cnt, (int)n, s);
-  void *tmp;
-  VP_CUDA(cudaMallocAsync(&tmp, std::max(tb, tb2) + 16, s));
-  VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k, ks, ix, ixs, (int)n, 0, 64, s));
-  k_dense_flags<<<nb, 256, 0, s>>>(ks, n, VP_DENSE_MIN, fd, fsp);
-  VP_CHECK_LAUNCH();
-  // dense points, grouped by cell (sorted order kept)
-  VP_CUDA(cub::DeviceSelect::Flagged(tmp, tb2, ixs, fd, sel, d_cnt, (int)n, s));
-  int32_t nd = 0;
-  VP_CUDA(cudaMemcpyAsync(&nd, d_cnt, 4, cudaMemcpyDeviceToHost, s));
-  VP_CUDA(cudaStreamSynchronize(s));
-  Dn.n = nd;
-  Dn.dx = vp_alloc<double>(P, std::max(1, nd));
-  Dn.dy = vp_alloc<double>(P, std::max(1, nd));
-  Dn.dw = vp_alloc<double>(P, std::max(1, nd));
-  Dn.dperm = vp_alloc<int32_t>(P, std::max(1, nd));
-  if (nd > 0) {
-    k_gather_pts<<<(unsigned)((nd + 255) / 256), 256, 0, s>>>(xy, weights, sel, nd, Dn.dx, Dn.dy, nullptr, Dn.dw,
-                                                              Dn.dperm);
-    VP_CHECK_LAUNCH();
-    // items: runs of equal keys among the dense points, cut into chunks
-    uint64_t *dk;
-    VP_CUDA(cudaMallocAsync(&dk, 8 * (size_t)nd, s));
-    // keys of the dense points: select from ks with the same flags
-    VP_CUDA(cub::DeviceSelect::Flagged(tmp, tb2, ks, fd, dk, d_cnt, (int)n, s));
-    std::vector<uint64_t> hk(nd);
-    VP_CUDA(cudaMemcpyAsync(hk.data(), dk, 8 * (size_t)nd, cudaMemcpyDeviceToHost, s));
-    VP_CUDA(cudaStreamSynchronize(s));
-    VP_CUDA(cudaFreeAsync(dk, s));
-    std::vector<int4> items;
-    for (int64_t i = 0; i < nd;) {
-      int64_t e = i;
-      while (e < nd && hk[e] == hk[i]) e++;
-      const int ix0 = (int)((int64_t)(hk[i] & 0xffffffffull) - (1 << 24));
-      const int iy0 = (int)((int64_t)(hk[i] >> 32) - (1 << 24));
-      for (int64_t c = i; c < e; c += VP_DENSE_CHUNK)
-        items.push_back(make_int4(ix0, iy0, (int)c, (int)std::min<int64_t>(e, c + VP_DENSE_CHUNK)));
-      i = e;
-    }
-    Dn.nitems = (int64_t)items.size();
-    Dn.items = vp_alloc<int4>(P, items.size());
-    VP_CUDA(cudaMemcpy(Dn.items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
-  }
-  // sparse points -> tile path
-  VP_CUDA(cub::DeviceSelect::Flagged(tmp, tb2, ixs, fsp, sel, d_cnt, (int)n, s));
-  int32_t ns = 0;
-  VP_CUDA(cudaMemcpyAsync(&ns, d_cnt, 4, cudaMemcpyDeviceToHost, s));
-  VP_CUDA(cudaStreamSynchronize(s));
-  double *sxy, *sw;
-  int32_t *snode;
-  VP_CUDA(cudaMallocAsync(&sxy, 16 * ((size_t)ns + 1), s));
-  VP_CUDA(cudaMallocAsync(&sw, 8 * ((size_t)ns + 1), s));
-  VP_CUDA(cudaMallocAsync(&snode, 4 * ((size_t)ns + 1), s));
-  if (ns > 0) {
-    k_gather_pts<<<(unsigned)((ns + 255) / 256), 256, 0, s>>>(xy, weights, sel, ns, nullptr, nullptr, sxy, sw, snode);
-    VP_CHECK_LAUNCH();
-  }
-  vp_build_spread_order(P, P->sp, sxy, sw, snode, ns, g);
-  P->sp_n = ns;
-  Dn.fs_off = ns;
-  for (void *q : {(void *)k, (void *)ks, (void *)ix, (void *)ixs, (void *)fd, (void *)fsp, (void *)sel, (void *)d_cnt,
-                  tmp, (void *)sxy, (void *)sw, (void *)snode})
-    VP_CUDA(cudaFreeAsync(q, s));
-  (void)cnt0;
 }
 
 // ---------------------------------------------------------------------------------------------
