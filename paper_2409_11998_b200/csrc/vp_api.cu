@@ -446,6 +446,9 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     vp_opts &o = P->opts;
     if (o.targets_are_nodes && T < N) throw VpError{VP_ERR_ARG};
     if (o.parts < 0 || o.parts > 3) throw VpError{VP_ERR_ARG};
+    if (o.spread_tile < 0 || o.spread_tile > 64 || (o.spread_tile > 0 && o.spread_tile < 8)) throw VpError{VP_ERR_ARG};
+    if (o.interp_tile < 0 || o.interp_tile > 128 || (o.interp_tile > 0 && o.interp_tile < 16)) throw VpError{VP_ERR_ARG};
+    if (o.interp_tile > 0) P->TSI = o.interp_tile;
     if (o.boundary.kind == VP_BDRY_CIRCLE && !(o.boundary.p[2] > 0)) throw VpError{VP_ERR_GEOMETRY};
     if (o.boundary.kind == VP_BDRY_RECT && !(o.boundary.p[2] > o.boundary.p[0] && o.boundary.p[3] > o.boundary.p[1]))
       throw VpError{VP_ERR_GEOMETRY};

@@ -91,7 +91,7 @@ __global__ void k_tile_heads(const uint64_t *__restrict__ k1, int64_t n, int32_t
 // 32 consecutive points holds at most 2 points per slot when the slots are evenly populated, so the
 // row-step LDS/STS of a batch need ~2 wavefronts instead of the ~4-5 of random columns.
 #define PK_B 32
-#define PK_ROWS 48
+#define PK_ROWS 72  // footprint start rows of a tile: TS + 2 (TS <= 64)
 __global__ void k_levels(const uint64_t *__restrict__ k1, const int32_t *__restrict__ tstart, int64_t ntile,
                          int64_t n, int W, int nw, uint64_t *__restrict__ k2, int *__restrict__ overflow_flag) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -302,6 +302,11 @@ static void launch_spread_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &
   int nw = S.tiles.TS + W + 3;
   size_t sm = sizeof(double) * (size_t)nw * nw;
   if (S.tiles.nsub == 0) return;
+  static int attr_set = 0;
+  if ((int)sm > attr_set && sm > 48 * 1024) {
+    VP_CUDA(cudaFuncSetAttribute(k_spread_nh<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr_set = (int)sm;
+  }
   if (!S.det) {
     k_spread_nh<W, D><<<(unsigned)S.tiles.nsub, 32, sm, P->stream>>>(S.tiles.sub, S.bstart, S.sx, S.sy, S.sw,
                                                                      S.sperm, f, g, S.tiles.TS, 0, S.fs_out);
@@ -1019,11 +1024,10 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
   const int TSI = P->TSI, nw = TSI + W + 3;
   const int do_hist = (parts & VP_PART_HISTORY) ? 1 : 0;
   size_t sm = do_hist ? sizeof(double) * (size_t)nw * nw : 0;
-  static bool attr_set[17] = {};
-  if (!attr_set[W]) {
-    VP_CUDA(cudaFuncSetAttribute(k_interp_local<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(double) * (TSI + W + 3) * (TSI + W + 3))));
-    attr_set[W] = true;
+  static int attr_set[17] = {};  // largest dynamic shared memory enabled so far for this W
+  if ((int)sm > attr_set[W]) {
+    VP_CUDA(cudaFuncSetAttribute(k_interp_local<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr_set[W] = (int)sm;
   }
   const bool fused = do_hist && P->prolong_fused;
   RestrictArgs ra = restrict_args(P);
@@ -1181,7 +1185,7 @@ void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const
                            const int32_t *node_of, int64_t n, const GridArgs &g) {
   cudaStream_t s = P->stream;
   VpTiles &Tl = S.tiles;
-  Tl.TS = 32;
+  Tl.TS = P->opts.spread_tile > 0 ? P->opts.spread_tile : 32;
   Tl.ntx = (g.nfx + Tl.TS - 1) / Tl.TS;
   Tl.nty = (g.nfy + Tl.TS - 1) / Tl.TS;
   if (n == 0) {
