@@ -108,10 +108,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def oracle_rate(w, n_targets, seed=99):
-    """Time the CPU oracle (as it stands) on a bounded target sample; extrapolate to all targets."""
+def oracle_rate(w, n_targets, seed=99, budget_s=None):
+    """Time the CPU oracle (as it stands) on a bounded target sample; extrapolate to all targets.
+    budget_s: size the sample so that it takes about this long (a 16-target probe sets the rate)."""
     import oracle
     from workloads import configs
+    if budget_s is not None:
+        probe = configs.sample_targets(w.T, 16, seed=seed + 7)
+        t0 = time.perf_counter()
+        oracle.workload_potential(w, probe)
+        per = (time.perf_counter() - t0) / len(probe)
+        n_targets = int(max(16, min(4096, budget_s / max(per, 1e-9))))
     idx = configs.sample_targets(w.T, n_targets, seed=seed)
     t0 = time.perf_counter()
     oracle.workload_potential(w, idx)
@@ -186,8 +193,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("VP_BENCH_CONFIG", "c2"))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-targets", type=int, default=32)
+    ap.add_argument("--ref-targets", type=int, default=384)
     ap.add_argument("--cpu-targets", type=int, default=96)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline sample sized to ~this many seconds")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
@@ -302,7 +310,7 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            cpu = oracle_rate(w, args.cpu_targets)
+            cpu = oracle_rate(w, args.cpu_targets, budget_s=args.cpu_seconds)
             cpu.pop("seconds")
         line = {"metric": METRIC, "value": value, "unit": "pts/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
