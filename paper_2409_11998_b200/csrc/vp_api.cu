@@ -421,9 +421,6 @@ static void free_plan(vp_plan_s *P) {
     cufftDestroy(P->bands.inv);
   }
   if (P->s_fh) cudaStreamDestroy(P->s_fh);
-  if (P->s_copy) cudaStreamDestroy(P->s_copy);
-  for (cudaEvent_t e : P->ev_copy)
-    if (e) cudaEventDestroy(e);
   if (P->s_loc) cudaStreamDestroy(P->s_loc);
   for (cudaEvent_t e : {P->ev_fork, P->ev_fh, P->ev_loc})
     if (e) cudaEventDestroy(e);
@@ -596,10 +593,8 @@ struct StreamScope {
 
 static void eval_concurrent(vp_plan_s *P, const double *f, double *out, int parts) {
   cudaStream_t A = P->stream;
-  if (!P->prespread) {
-    VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, A));
-    vp_launch_spread(P, P->sp, grid_args(P->nh), f);
-  }
+  VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, A));
+  vp_launch_spread(P, P->sp, grid_args(P->nh), f);
   VP_CUDA(cudaEventRecord(P->ev_fork, A));
   {  // B: far history
     StreamScope sc(P, P->s_fh);
@@ -654,10 +649,10 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
     VP_CUFFT(cufftSetStream(P->fh.inv, P->stream));
     record(P, 0);
     if (parts & VP_PART_HISTORY) {
-      if (!P->prespread) VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, P->stream));
+      VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, P->stream));
       VP_CUDA(cudaMemsetAsync(P->fh.data, 0, sizeof(double) * P->fh.nf * P->fh.row, P->stream));
       record(P, 1);
-      if (!P->prespread) vp_launch_spread(P, P->sp, grid_args(P->nh), f);
+      vp_launch_spread(P, P->sp, grid_args(P->nh), f);
       record(P, 2);
       vp_launch_restrict(P);
       record(P, 3);
@@ -692,33 +687,8 @@ extern "C" vp_status vp_eval_host(vp_handle P, const double *f_host, double *out
   try {
     if (!P->f_dev) P->f_dev = vp_alloc<double>(P, P->N);
     if (!P->out_dev) P->out_dev = vp_alloc<double>(P, P->T);
-    const int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
-    vp_status s;
-    if ((parts & VP_PART_HISTORY) && !P->profiling) {
-      // f arrives in 4 chunks on a copy stream; each chunk is spread as soon as it lands, so the host->device
-      // copy overlaps the spreading (the rest of the eval needs all of f)
-      vp_build_host_chunks(P);
-      VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, P->stream));
-      VP_CUDA(cudaEventRecord(P->ev_fork, P->stream));  // the previous eval's reads of f_dev are done
-      VP_CUDA(cudaStreamWaitEvent(P->s_copy, P->ev_fork, 0));
-      for (int c = 0; c < 4; c++) {
-        const int64_t lo = P->chunk_lo[c], hi = P->chunk_lo[c + 1];
-        if (hi > lo)
-          VP_CUDA(cudaMemcpyAsync(P->f_dev + lo, f_host + lo, sizeof(double) * (hi - lo), cudaMemcpyHostToDevice,
-                                  P->s_copy));
-        VP_CUDA(cudaEventRecord(P->ev_copy[c], P->s_copy));
-      }
-      for (int c = 0; c < 4; c++) {
-        VP_CUDA(cudaStreamWaitEvent(P->stream, P->ev_copy[c], 0));
-        vp_launch_spread(P, P->spc[c], grid_args(P->nh), P->f_dev);
-      }
-      P->prespread = true;
-      s = vp_eval(P, P->f_dev, P->out_dev);
-      P->prespread = false;
-    } else {
-      VP_CUDA(cudaMemcpyAsync(P->f_dev, f_host, sizeof(double) * P->N, cudaMemcpyHostToDevice, P->stream));
-      s = vp_eval(P, P->f_dev, P->out_dev);
-    }
+    VP_CUDA(cudaMemcpyAsync(P->f_dev, f_host, sizeof(double) * P->N, cudaMemcpyHostToDevice, P->stream));
+    vp_status s = vp_eval(P, P->f_dev, P->out_dev);
     if (s != VP_OK) return s;
     VP_CUDA(cudaMemcpyAsync(out_host, P->out_dev, sizeof(double) * P->T, cudaMemcpyDeviceToHost, P->stream));
     VP_CUDA(cudaStreamSynchronize(P->stream));

@@ -173,15 +173,8 @@ struct vp_plan_s {
   double *tri_vL = nullptr;    // [N] TRIANGLE-mode V_L per node (eval scratch; null outside TRIANGLE mode)
   double *st_vL = nullptr;     // [n_stencil] stencil part of V_L per stencil slot (eval scratch)
   double *fs = nullptr;        // [N] f in spreading order (eval scratch; stencil indices point into it)
-  // host-side eval staging (vp_eval_host): f arrives in VP_HOST_CHUNKS user-index chunks, each spread as soon
-  // as its copy lands (spc[c] holds the chunk's points in spreading order)
+  // host-side eval staging (vp_eval_host)
   double *f_dev = nullptr, *out_dev = nullptr;
-  VpSpreadSet spc[4];
-  int64_t chunk_lo[5] = {};
-  bool spc_built = false;
-  bool prespread = false;      // this eval: grids zeroed and spread already (host path)
-  cudaStream_t s_copy = nullptr;
-  cudaEvent_t ev_copy[4] = {};
   // profiling
   bool profiling = false;
   cudaEvent_t ev[12] = {};
@@ -223,7 +216,6 @@ void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out, bool local_kernels);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n);
 void vp_remap_stencils(vp_plan_s *P);
-void vp_build_host_chunks(vp_plan_s *P);
 void vp_build_local(vp_plan_s *P, const double *nodes_dev);
 void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop);
 int64_t vp_sort_points(vp_plan_s *P, const double *xy, int64_t n, double ox, double oy, double cell,

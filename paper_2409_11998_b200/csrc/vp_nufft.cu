@@ -989,7 +989,7 @@ void vp_launch_tri_local(vp_plan_s *P, const double *f) {
     // stencil entries index f in spreading order (P->fs, written by the spread of this eval; gathered here
     // when the history part is off)
     int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
-    if (!(parts & VP_PART_HISTORY) || P->prespread) {
+    if (!(parts & VP_PART_HISTORY)) {
       k_gather_f<<<(unsigned)((P->N + 255) / 256), 256, 0, P->stream>>>(f, P->sp.sperm, P->N, P->fs);
       VP_CHECK_LAUNCH();
       P->n_kernels++;
@@ -1297,70 +1297,6 @@ void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const
   for (void *p : {(void *)k1, (void *)k1s, (void *)k2, (void *)k2s, (void *)i1, (void *)i1s, (void *)i2s, (void *)head,
                   tmp})
     VP_CUDA(cudaFreeAsync(p, s));
-}
-
-// ---------------------------------------------------------------------------------------------
-// host path: the plan's points split by user-index chunk (so each chunk can be spread as soon as its part of f
-// has been copied), each chunk in its own spreading order
-__global__ void k_chunk_flag(const int32_t *__restrict__ sperm, int64_t n, int64_t lo, int64_t hi,
-                             int32_t *__restrict__ flag) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) flag[i] = (sperm[i] >= lo && sperm[i] < hi) ? 1 : 0;
-}
-__global__ void k_chunk_gather(const double *__restrict__ sx, const double *__restrict__ sy,
-                               const double *__restrict__ sw, const int32_t *__restrict__ sperm,
-                               const int32_t *__restrict__ sel, int64_t n, double *__restrict__ xy,
-                               double *__restrict__ w, int32_t *__restrict__ node) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int32_t j = sel[i];
-  xy[2 * i] = sx[j];
-  xy[2 * i + 1] = sy[j];
-  w[i] = sw[j];
-  node[i] = sperm[j];
-}
-
-void vp_build_host_chunks(vp_plan_s *P) {
-  if (P->spc_built) return;
-  cudaStream_t s = P->stream;
-  const int64_t n = P->N, C = 4, cs = (n + C - 1) / C;
-  int32_t *flag, *sel, *d_n, *node;
-  double *xy, *w;
-  VP_CUDA(cudaMallocAsync(&flag, 4 * (n + 1), s));
-  VP_CUDA(cudaMallocAsync(&sel, 4 * (n + 1), s));
-  VP_CUDA(cudaMallocAsync(&d_n, 4, s));
-  VP_CUDA(cudaMallocAsync(&node, 4 * (n + 1), s));
-  VP_CUDA(cudaMallocAsync(&xy, 16 * (n + 1), s));
-  VP_CUDA(cudaMallocAsync(&w, 8 * (n + 1), s));
-  size_t tb = 0;
-  cub::DeviceSelect::Flagged(nullptr, tb, cub::CountingInputIterator<int32_t>(0), flag, sel, d_n, (int)n, s);
-  void *tmp;
-  VP_CUDA(cudaMallocAsync(&tmp, tb + 16, s));
-  const unsigned nb = (unsigned)((n + 255) / 256);
-  for (int c = 0; c < C; c++) {
-    const int64_t lo = std::min(n, c * cs), hi = std::min(n, (c + 1) * cs);
-    P->chunk_lo[c] = lo;
-    P->chunk_lo[c + 1] = hi;
-    k_chunk_flag<<<nb, 256, 0, s>>>(P->sp.sperm, n, lo, hi, flag);
-    VP_CHECK_LAUNCH();
-    VP_CUDA(cub::DeviceSelect::Flagged(tmp, tb, cub::CountingInputIterator<int32_t>(0), flag, sel, d_n, (int)n, s));
-    int32_t m = 0;
-    VP_CUDA(cudaMemcpyAsync(&m, d_n, 4, cudaMemcpyDeviceToHost, s));
-    VP_CUDA(cudaStreamSynchronize(s));
-    if (m > 0) {
-      k_chunk_gather<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(P->sp.sx, P->sp.sy, P->sp.sw, P->sp.sperm, sel, m,
-                                                                 xy, w, node);
-      VP_CHECK_LAUNCH();
-    }
-    P->spc[c].det = P->sp.det;
-    vp_build_spread_order(P, P->spc[c], xy, w, node, m, grid_args(P->nh));
-  }
-  for (void *q : {(void *)flag, (void *)sel, (void *)d_n, (void *)node, (void *)xy, (void *)w, tmp})
-    VP_CUDA(cudaFreeAsync(q, s));
-  VP_CUDA(cudaStreamCreateWithFlags(&P->s_copy, cudaStreamNonBlocking));
-  for (int c = 0; c < C; c++) VP_CUDA(cudaEventCreateWithFlags(&P->ev_copy[c], cudaEventDisableTiming));
-  VP_CUDA(cudaStreamSynchronize(s));
-  P->spc_built = true;
 }
 
 // ---------------------------------------------------------------------------------------------
