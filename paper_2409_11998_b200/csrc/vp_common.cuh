@@ -114,6 +114,12 @@ struct VpBands {
   double *ent_x = nullptr, *ent_y = nullptr;  // [n_ent] virtual-grid coordinates
   int64_t n_pairs = 0;            // (box, source) pairs spread
   int8_t *tlev = nullptr;         // [T] level per sorted target
+  // staged interpolation of the entries (k_interp_local on the virtual grid): entries in (tile, bank) order
+  double *e_x = nullptr, *e_y = nullptr;
+  int64_t *e_perm = nullptr;      // staged order -> entry index
+  int4 *e_items = nullptr;
+  int64_t e_n_items = 0;
+  double *ent_val = nullptr;      // [n_ent] band value per entry
   int64_t lev_count[16] = {};     // targets per level
 };
 
@@ -215,6 +221,8 @@ void vp_launch_tri_local(vp_plan_s *P, const double *f);
 void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out, bool local_kernels);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n);
+void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, bool allow_tri,
+                             double **otx, double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items);
 void vp_remap_stencils(vp_plan_s *P);
 void vp_build_local(vp_plan_s *P, const double *nodes_dev);
 void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop);

@@ -204,6 +204,15 @@ __global__ void k_src_pairs(const double *__restrict__ xy, const double *__restr
   if (!FILL) count[j] = c;
 }
 
+__global__ void k_interleave(const double *__restrict__ x, const double *__restrict__ y, int64_t n,
+                             double *__restrict__ xy) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    xy[2 * i] = x[i];
+    xy[2 * i + 1] = y[i];
+  }
+}
+
 __global__ void k_lev_flag(const int8_t *__restrict__ tlev, int64_t T, int32_t *__restrict__ flag,
                            int32_t *__restrict__ val) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -395,6 +404,7 @@ void vp_build_levels(vp_plan_s *P, const double *nodes, const double *weights) {
                                                                  ekeys, ubox, B.nbox, bg, B.ent_x, B.ent_y);
   VP_CHECK_LAUNCH();
   for (void *q : {(void *)ekeys, (void *)ekeys2, (void *)ubox_t}) VP_CUDA(cudaFreeAsync(q, s));
+  // (the staged entry order is built below, once the virtual grid exists)
   // ---- (box, source) pairs
   int64_t *cnt = tmp_alloc<int64_t>(N + 1, s), *off = tmp_alloc<int64_t>(N + 1, s);
   VP_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (N + 1), s));
@@ -418,6 +428,14 @@ void vp_build_levels(vp_plan_s *P, const double *nodes, const double *weights) {
   // ---- virtual grid, spreading order, FFT plans, multiplier tables
   B.grid = vp_alloc<double>(P, (size_t)B.nbox * B.nfb * B.rowb);
   GridArgs gb{B.grid, B.nfb, B.nbox * B.nfb, B.rowb, 0.0, 0.0, 1.0, 1.0};
+  {  // entries ordered for the shared-memory-staged interpolation on the virtual grid
+    double *exy = tmp_alloc<double>(2 * B.n_ent, s);
+    k_interleave<<<(unsigned)((B.n_ent + 255) / 256), 256, 0, s>>>(B.ent_x, B.ent_y, B.n_ent, exy);
+    VP_CHECK_LAUNCH();
+    vp_build_interp_order_g(P, exy, B.n_ent, gb, false, &B.e_x, &B.e_y, &B.e_perm, &B.e_items, &B.e_n_items);
+    B.ent_val = vp_alloc<double>(P, B.n_ent);
+    VP_CUDA(cudaFreeAsync(exy, s));
+  }
   vp_build_spread_order(P, B.sp, pxy, pw, pnode, B.n_pairs, gb);
   for (void *q : {(void *)cnt, (void *)off, (void *)pxy, (void *)pw, (void *)pnode}) VP_CUDA(cudaFreeAsync(q, s));
   B.lev_par = vp_alloc<double>(P, lp.size());

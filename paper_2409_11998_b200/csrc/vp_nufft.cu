@@ -1091,9 +1091,18 @@ __global__ void k_interp_keys_tri(const double *__restrict__ xy, int64_t n, Grid
   idx[i] = (int32_t)i;
 }
 
+void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, bool allow_tri,
+                             double **otx, double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
+  vp_build_interp_order_g(P, xy, n, grid_args(P->nh), P->dmode == VP_DERIV_TRIANGLE, &P->tx, &P->ty, &P->tperm,
+                          &P->items, &P->n_items);
+}
+
+// targets (xy interleaved, n) of grid g ordered for k_interp_local: *tx, *ty, *tperm (sorted -> input index),
+// work items; allow_tri enables the (tile, triangle, node) order (off by default, see below)
+void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, bool allow_tri,
+                             double **otx, double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items) {
   cudaStream_t s = P->stream;
-  const GridArgs g = grid_args(P->nh);
   const int TSI = P->TSI;
   const int64_t ntx = (g.nfx + TSI - 1) / TSI, nty = (g.nfy + TSI - 1) / TSI;
   uint64_t *k1, *k1s, *k2, *k2s;
@@ -1108,7 +1117,7 @@ void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
   unsigned nb = (unsigned)((n + 255) / 256);
   // (tile, triangle, node) order coalesces the per-node V_L reads but costs more shared-memory bank conflicts
   // than it saves (config 5: interp 9.7 -> 11.8 ms); off
-  const bool tri_order = false;
+  const bool tri_order = false && allow_tri;
   size_t tb = 0, tb2 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s);
   cub::DeviceRadixSort::SortPairs(nullptr, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s);
@@ -1128,10 +1137,10 @@ void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
     VP_CHECK_LAUNCH();
     VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
   }
-  P->tx = vp_alloc<double>(P, n);
-  P->ty = vp_alloc<double>(P, n);
-  P->tperm = vp_alloc<int64_t>(P, n);
-  k_gather_xy<<<nb, 256, 0, s>>>(xy, i2s, n, P->tx, P->ty, P->tperm, nullptr);
+  *otx = vp_alloc<double>(P, n);
+  *oty = vp_alloc<double>(P, n);
+  *otperm = vp_alloc<int64_t>(P, n);
+  k_gather_xy<<<nb, 256, 0, s>>>(xy, i2s, n, *otx, *oty, *otperm, nullptr);
   VP_CHECK_LAUNCH();
   std::vector<uint64_t> hk(n);
   VP_CUDA(cudaMemcpyAsync(hk.data(), k2s, 8 * n, cudaMemcpyDeviceToHost, s));
@@ -1145,10 +1154,10 @@ void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
       items.push_back(make_int4((int)(tile % ntx), (int)(tile / ntx), (int)c, (int)std::min<int64_t>(e, c + VP_INTERP_CHUNK)));
     i = e;
   }
-  P->n_items = (int64_t)items.size();
-  P->items = vp_alloc<int4>(P, std::max<size_t>(items.size(), 1));
+  *on_items = (int64_t)items.size();
+  *oitems = vp_alloc<int4>(P, std::max<size_t>(items.size(), 1));
   if (!items.empty())
-    VP_CUDA(cudaMemcpy(P->items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
+    VP_CUDA(cudaMemcpy(*oitems, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
   for (void *q : {(void *)k1, (void *)k1s, (void *)k2, (void *)k2s, (void *)i1, (void *)i1s, (void *)i2s, tmp})
     VP_CUDA(cudaFreeAsync(q, s));
 }
@@ -1441,6 +1450,37 @@ static void launch_interp_bands_w(vp_plan_s *P, const GridArgs &g, double *out) 
   P->n_kernels++;
 }
 
+// per-target sum of its band entries (CSR by target) into out
+__global__ void k_band_sum(const int32_t *__restrict__ lt_t, const int32_t *__restrict__ lt_off, int64_t n_lt,
+                           const double *__restrict__ ent_val, const int64_t *__restrict__ tperm,
+                           double *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_lt) return;
+  double v = 0.0;
+  for (int32_t e = lt_off[i]; e < lt_off[i + 1]; e++) v += ent_val[e];
+  out[tperm[lt_t[i]]] += v;
+}
+
+template <int W>
+static void launch_band_entries_w(vp_plan_s *P, const GridArgs &g) {
+  constexpr int D = VP_HORNER_DEG(W);
+  VpBands &B = P->bands;
+  const int TSI = P->TSI, nw = TSI + W + 3;
+  const size_t sm = sizeof(double) * (size_t)nw * nw;
+  static int attr = 0;
+  if ((int)sm > attr) {
+    VP_CUDA(cudaFuncSetAttribute(k_interp_local<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = (int)sm;
+  }
+  RestrictArgs ra{};
+  TapArgs tp{};
+  k_interp_local<W, D><<<(unsigned)B.e_n_items, 256, sm, P->stream>>>(
+      B.e_items, TSI, B.e_x, B.e_y, B.e_perm, g, 1, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, 0, nullptr,
+      nullptr, nullptr, B.ent_val, nullptr, ra, tp, 1);
+  VP_CHECK_LAUNCH();
+  P->n_kernels++;
+}
+
 void vp_launch_bands(vp_plan_s *P, const double *f, double *out) {
   VpBands &B = P->bands;
   if (B.nlev == 0 || B.nbox == 0) return;
@@ -1456,6 +1496,20 @@ void vp_launch_bands(vp_plan_s *P, const double *f, double *out) {
   P->n_kernels++;
   VP_CUFFT(cufftExecZ2D(B.inv, (cufftDoubleComplex *)B.grid, B.grid));
   P->n_ffts += 2;
+  if (B.e_items) {  // staged interpolation of the (target, level) entries, then the per-target sums
+    switch (P->w) {
+#define CASE(W) \
+  case W: launch_band_entries_w<W>(P, g); break;
+      CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+      default: throw VpError{VP_ERR_UNSUPPORTED};
+    }
+    k_band_sum<<<(unsigned)((B.n_lt + 255) / 256), 256, 0, P->stream>>>(B.lt_t, B.lt_off, B.n_lt, B.ent_val, P->tperm,
+                                                                         out);
+    VP_CHECK_LAUNCH();
+    P->n_kernels++;
+    return;
+  }
   switch (P->w) {
 #define CASE(W) \
   case W: launch_interp_bands_w<W>(P, g, out); break;
