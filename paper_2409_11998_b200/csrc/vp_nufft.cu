@@ -1414,42 +1414,6 @@ __global__ void k_multiply_bands(double *__restrict__ data, int64_t nbox, int64_
   }
 }
 
-// bands at their targets: out[user(t)] += sum over the target's levels of the box interpolant
-template <int W, int D>
-__global__ void __launch_bounds__(256) k_interp_bands(const int32_t *__restrict__ lt_t,
-                                                      const int32_t *__restrict__ lt_off, int64_t n_lt,
-                                                      const double *__restrict__ ex, const double *__restrict__ ey,
-                                                      GridArgs g, const int64_t *__restrict__ tperm,
-                                                      double *__restrict__ out) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n_lt) return;
-  double v = 0.0;
-  for (int32_t e = lt_off[i]; e < lt_off[i + 1]; e++) {
-    double wx[W], wy[W];
-    int ix = es_horner<W, D>(ex[e], wx);
-    int iy = es_horner<W, D>(ey[e], wy);
-#pragma unroll
-    for (int b = 0; b < W; b++) {
-      const double *rp = g.data + (int64_t)(iy + b) * g.row + ix;
-      double racc = 0.0;
-#pragma unroll
-      for (int a = 0; a < W; a++) racc = fma(wx[a], __ldg(rp + a), racc);
-      v = fma(wy[b], racc, v);
-    }
-  }
-  out[tperm[lt_t[i]]] += v;
-}
-
-template <int W>
-static void launch_interp_bands_w(vp_plan_s *P, const GridArgs &g, double *out) {
-  constexpr int D = VP_HORNER_DEG(W);
-  VpBands &B = P->bands;
-  k_interp_bands<W, D><<<(unsigned)((B.n_lt + 255) / 256), 256, 0, P->stream>>>(B.lt_t, B.lt_off, B.n_lt, B.ent_x,
-                                                                               B.ent_y, g, P->tperm, out);
-  VP_CHECK_LAUNCH();
-  P->n_kernels++;
-}
-
 // per-target sum of its band entries (CSR by target) into out
 __global__ void k_band_sum(const int32_t *__restrict__ lt_t, const int32_t *__restrict__ lt_off, int64_t n_lt,
                            const double *__restrict__ ent_val, const int64_t *__restrict__ tperm,
@@ -1496,25 +1460,16 @@ void vp_launch_bands(vp_plan_s *P, const double *f, double *out) {
   P->n_kernels++;
   VP_CUFFT(cufftExecZ2D(B.inv, (cufftDoubleComplex *)B.grid, B.grid));
   P->n_ffts += 2;
-  if (B.e_items) {  // staged interpolation of the (target, level) entries, then the per-target sums
-    switch (P->w) {
-#define CASE(W) \
-  case W: launch_band_entries_w<W>(P, g); break;
-      CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
-#undef CASE
-      default: throw VpError{VP_ERR_UNSUPPORTED};
-    }
-    k_band_sum<<<(unsigned)((B.n_lt + 255) / 256), 256, 0, P->stream>>>(B.lt_t, B.lt_off, B.n_lt, B.ent_val, P->tperm,
-                                                                         out);
-    VP_CHECK_LAUNCH();
-    P->n_kernels++;
-    return;
-  }
+  // staged interpolation of the (target, level) entries, then the per-target sums
   switch (P->w) {
 #define CASE(W) \
-  case W: launch_interp_bands_w<W>(P, g, out); break;
+  case W: launch_band_entries_w<W>(P, g); break;
     CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
     default: throw VpError{VP_ERR_UNSUPPORTED};
   }
+  k_band_sum<<<(unsigned)((B.n_lt + 255) / 256), 256, 0, P->stream>>>(B.lt_t, B.lt_off, B.n_lt, B.ent_val, P->tperm,
+                                                                       out);
+  VP_CHECK_LAUNCH();
+  P->n_kernels++;
 }
