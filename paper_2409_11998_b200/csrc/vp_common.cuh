@@ -141,8 +141,6 @@ struct vp_plan_s {
   int fh_ratio = 1;         // h_FH = fh_ratio * h_NH
   int64_t fh_shift = 0;     // FH node i' sits on NH node fh_ratio * i' - fh_shift
   int tap_qh = 0;           // integer-ratio restriction taps w[q + QH], |q| <= QH (0: general tables)
-  bool prolong_fused = false;   // this eval: prolongation pass A^T applied inside k_interp_local
-  bool no_fuse_prolong = true;  // fusing pass A^T into the interpolation windows measured slower (c5 +7.5 ms)
   double tap_w[192] = {};
   VpHorner horner{};
   double horner_err = 0;
@@ -221,8 +219,8 @@ void vp_launch_tri_local(vp_plan_s *P, const double *f);
 void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out, bool local_kernels);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n);
-void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, bool allow_tri,
-                             double **otx, double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items);
+void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx,
+                             double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items);
 void vp_remap_stencils(vp_plan_s *P);
 void vp_build_local(vp_plan_s *P, const double *nodes_dev);
 void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop);

@@ -432,7 +432,7 @@ void vp_build_levels(vp_plan_s *P, const double *nodes, const double *weights) {
     double *exy = tmp_alloc<double>(2 * B.n_ent, s);
     k_interleave<<<(unsigned)((B.n_ent + 255) / 256), 256, 0, s>>>(B.ent_x, B.ent_y, B.n_ent, exy);
     VP_CHECK_LAUNCH();
-    vp_build_interp_order_g(P, exy, B.n_ent, gb, false, &B.e_x, &B.e_y, &B.e_perm, &B.e_items, &B.e_n_items);
+    vp_build_interp_order_g(P, exy, B.n_ent, gb, &B.e_x, &B.e_y, &B.e_perm, &B.e_items, &B.e_n_items);
     B.ent_val = vp_alloc<double>(P, B.n_ent);
     VP_CUDA(cudaFreeAsync(exy, s));
   }

@@ -639,7 +639,7 @@ static void launch_restrict_int(vp_plan_s *P, const RestrictArgs &a, const TapAr
 }
 
 template <int M>
-static void launch_prolong_int(vp_plan_s *P, const RestrictArgs &a, const TapArgs &tp, bool fuse_x, int pass) {
+static void launch_prolong_int(vp_plan_s *P, const RestrictArgs &a, const TapArgs &tp, int pass) {
   // NH index i = M c + k - j covers [0, n1) for c in [c_lo, c_hi]
   const int64_t c_lo = (tp.j >= 0) ? tp.j / M : -((-tp.j + M - 1) / M);
   const int64_t c_hi = (a.n1 - 1 + tp.j) / M;
@@ -650,7 +650,7 @@ static void launch_prolong_int(vp_plan_s *P, const RestrictArgs &a, const TapArg
     VP_CHECK_LAUNCH();
     P->n_kernels++;
   }
-  if (fuse_x || !(pass & 2)) return;  // fused: pass A^T is applied by k_interp_local while staging windows
+  if (!(pass & 2)) return;
   dim3 gA((unsigned)((nc + 127) / 128), (unsigned)a.n1);
   k_prolong_x_int<M><<<gA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a, tp, c_lo, nc);
   VP_CHECK_LAUNCH();
@@ -693,18 +693,16 @@ void vp_launch_restrict(vp_plan_s *P) {
 // pass: 1 = FH rows -> t2 (pass B^T, reads the FH grid), 2 = t2 -> NH grid (pass A^T), 3 = both
 void vp_launch_prolong(vp_plan_s *P, int pass) {
   RestrictArgs a = restrict_args(P);
-  if (pass & 1) P->prolong_fused = false;
   if (P->tap_qh > 0) {
     TapArgs tp = tap_args(P);
-    const bool fuse = !P->no_fuse_prolong;
     switch (P->fh_ratio) {
-      case 2: launch_prolong_int<2>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
-      case 3: launch_prolong_int<3>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
-      case 4: launch_prolong_int<4>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
-      case 5: launch_prolong_int<5>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
-      case 6: launch_prolong_int<6>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
-      case 7: launch_prolong_int<7>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
-      case 8: launch_prolong_int<8>(P, a, tp, fuse, pass); P->prolong_fused = fuse; return;
+      case 2: launch_prolong_int<2>(P, a, tp, pass); return;
+      case 3: launch_prolong_int<3>(P, a, tp, pass); return;
+      case 4: launch_prolong_int<4>(P, a, tp, pass); return;
+      case 5: launch_prolong_int<5>(P, a, tp, pass); return;
+      case 6: launch_prolong_int<6>(P, a, tp, pass); return;
+      case 7: launch_prolong_int<7>(P, a, tp, pass); return;
+      case 8: launch_prolong_int<8>(P, a, tp, pass); return;
       default: break;
     }
   }
@@ -771,22 +769,17 @@ __global__ void __launch_bounds__(256, 4) k_interp_local(const int4 *__restrict_
                                                       const double *__restrict__ tx, const double *__restrict__ ty,
                                                       const int64_t *__restrict__ tperm, GridArgs g, int do_hist,
                                                       const double *__restrict__ f, const double *__restrict__ lalpha,
-                                                      const int32_t *__restrict__ lnode,
-                                                      const int32_t *__restrict__ lidx, const double *__restrict__ lw,
-                                                      int K, int64_t n_sten, int do_local, const int32_t *__restrict__ lptr,
+                                                      const int32_t *__restrict__ lnode, int do_local,
+                                                      const int32_t *__restrict__ lptr,
                                                       const double *__restrict__ vL_tri,
-                                                      const double *__restrict__ vL_st,
-                                                      double *__restrict__ out, const double *__restrict__ t2,
-                                                      RestrictArgs ra, TapArgs tp, int M) {
+                                                      const double *__restrict__ vL_st, double *__restrict__ out) {
   extern __shared__ double tile[];
   const int nw = TSI + W + 3;
   const int4 it = items[blockIdx.x];
   const int64_t ox = (int64_t)it.x * TSI - (W / 2 + 1), oy = (int64_t)it.y * TSI - (W / 2 + 1);
   if (do_hist) {
     const bool interior = ox >= 0 && oy >= 0 && ox + nw <= g.nfx && oy + nw <= g.nfy;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int QH = tp.QH, dlo = -(QH / M), dhi = (M - 1 + QH) / M;
-    if (!t2 && interior) {  // common case: flat copy with 4 independent loads in flight per thread
+    if (interior) {  // common case: flat copy with 4 independent loads in flight per thread
       const int ncell = nw * nw;
       const double *base = g.data + oy * g.row + ox;
       for (int i0 = threadIdx.x; i0 < ncell; i0 += 4 * 256) {
@@ -803,25 +796,11 @@ __global__ void __launch_bounds__(256, 4) k_interp_local(const int4 *__restrict_
         for (int u = 0; u < 4; u++)
           if (i0 + u * 256 < ncell) tile[i0 + u * 256] = v[u];
       }
-    } else
-    for (int r = warp; r < nw; r += 8) {
-      const int64_t gy = interior ? oy + r : wrapi(oy + r, g.nfy);
-      const double *src = g.data + gy * g.row;
-      for (int c = lane; c < nw; c += 32) {
-        const int64_t gx = interior ? ox + c : wrapi(ox + c, g.nfx);
-        double v = __ldg(src + gx);
-        if (t2) {  // fused prolongation pass A^T: + sum_{i'} w[gx + j - M i'] t2[gy][i' - e_lo]
-          const int64_t q = gx + tp.j;
-          const int64_t cc = q >= 0 ? q / M : -((-q + M - 1) / M);
-          const int k = (int)(q - cc * M);
-          const double *trow = t2 + gy * ra.ne - ra.e_lo;
-          for (int d = dlo; d <= dhi; d++) {
-            const int64_t ip = cc + d;
-            const int qq = k - M * d;
-            if (ip >= ra.e_lo && ip < ra.e_lo + ra.ne && qq >= -QH && qq <= QH) v = fma(tp.w[qq + QH], __ldg(trow + ip), v);
-          }
-        }
-        tile[r * nw + c] = v;
+    } else {  // window wraps around the periodic grid
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      for (int r = warp; r < nw; r += 8) {
+        const double *src = g.data + wrapi(oy + r, g.nfy) * g.row;
+        for (int c = lane; c < nw; c += 32) tile[r * nw + c] = __ldg(src + wrapi(ox + c, g.nfx));
       }
     }
     __syncthreads();
@@ -1029,13 +1008,9 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
     VP_CUDA(cudaFuncSetAttribute(k_interp_local<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr_set[W] = (int)sm;
   }
-  const bool fused = do_hist && P->prolong_fused;
-  RestrictArgs ra = restrict_args(P);
-  TapArgs tp = fused ? tap_args(P) : TapArgs{};
   k_interp_local<W, D><<<(unsigned)P->n_items, 256, sm, P->stream>>>(
-      P->items, TSI, P->tx, P->ty, P->tperm, grid_args(P->nh), do_hist, f, P->lalpha, P->lnode, P->lidx, P->lw, P->K,
-      P->n_stencil, (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr, P->tri_vL, P->st_vL, out, fused ? P->scratch : nullptr,
-      ra, tp, P->fh_ratio);
+      P->items, TSI, P->tx, P->ty, P->tperm, grid_args(P->nh), do_hist, f, P->lalpha, P->lnode,
+      (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr, P->tri_vL, P->st_vL, out);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
@@ -1074,34 +1049,16 @@ __global__ void k_interp_keys2(const uint64_t *__restrict__ k1, int64_t n, uint6
   k2[i] = ((key >> 4) << 24) | (rank << 4) | (key & 15);
 }
 
-// TRIANGLE mode: node targets ordered by (tile, triangle, node) so that the per-node V_L reads of a warp are
-// runs of p consecutive nodes (coalesced); other targets follow inside their tile
-__global__ void k_interp_keys_tri(const double *__restrict__ xy, int64_t n, GridArgs g, int TSI, int64_t ntx,
-                                  int64_t nty, int64_t node_targets, int p, uint64_t *__restrict__ keys,
-                                  int32_t *__restrict__ idx) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double gx = gcoord(xy[2 * i], g.ox, g.inv_h), gy = gcoord(xy[2 * i + 1], g.oy, g.inv_h);
-  int64_t tx = (int64_t)floor(gx / TSI), ty = (int64_t)floor(gy / TSI);
-  tx = tx < 0 ? 0 : (tx >= ntx ? ntx - 1 : tx);
-  ty = ty < 0 ? 0 : (ty >= nty ? nty - 1 : ty);
-  const uint64_t tri = i < node_targets ? (uint64_t)(i / p) : 0xFFFFFFFFull;
-  const uint64_t k = i < node_targets ? (uint64_t)(i % p) : 0;
-  keys[i] = ((uint64_t)(ty * ntx + tx) << 36) | (tri << 4) | k;
-  idx[i] = (int32_t)i;
-}
-
-void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, bool allow_tri,
-                             double **otx, double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items);
+void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx,
+                             double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
-  vp_build_interp_order_g(P, xy, n, grid_args(P->nh), P->dmode == VP_DERIV_TRIANGLE, &P->tx, &P->ty, &P->tperm,
-                          &P->items, &P->n_items);
+  vp_build_interp_order_g(P, xy, n, grid_args(P->nh), &P->tx, &P->ty, &P->tperm, &P->items, &P->n_items);
 }
 
 // targets (xy interleaved, n) of grid g ordered for k_interp_local: *tx, *ty, *tperm (sorted -> input index),
-// work items; allow_tri enables the (tile, triangle, node) order (off by default, see below)
-void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, bool allow_tri,
-                             double **otx, double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items) {
+// work items.  (A (tile, triangle, node) order that coalesces the per-node V_L reads cost more bank
+// conflicts than it saved: config 5 interp 9.7 -> 11.8 ms.)
+void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx, double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items) {
   cudaStream_t s = P->stream;
   const int TSI = P->TSI;
   const int64_t ntx = (g.nfx + TSI - 1) / TSI, nty = (g.nfy + TSI - 1) / TSI;
@@ -1117,26 +1074,18 @@ void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const Gr
   unsigned nb = (unsigned)((n + 255) / 256);
   // (tile, triangle, node) order coalesces the per-node V_L reads but costs more shared-memory bank conflicts
   // than it saves (config 5: interp 9.7 -> 11.8 ms); off
-  const bool tri_order = false && allow_tri;
   size_t tb = 0, tb2 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s);
   cub::DeviceRadixSort::SortPairs(nullptr, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s);
   void *tmp;
   VP_CUDA(cudaMallocAsync(&tmp, std::max(tb, tb2) + 16, s));
-  int tile_shift = 24;
-  if (tri_order) {
-    k_interp_keys_tri<<<nb, 256, 0, s>>>(xy, n, g, TSI, ntx, nty, P->N, P->p, k1, i1);
-    VP_CHECK_LAUNCH();
-    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k2s, i1, i2s, (int)n, 0, 64, s));
-    tile_shift = 36;
-  } else {
-    k_interp_keys1<<<nb, 256, 0, s>>>(xy, n, g, TSI, P->w, ntx, nty, k1, i1);
-    VP_CHECK_LAUNCH();
-    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
-    k_interp_keys2<<<nb, 256, 0, s>>>(k1s, n, k2);
-    VP_CHECK_LAUNCH();
-    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
-  }
+  const int tile_shift = 24;
+  k_interp_keys1<<<nb, 256, 0, s>>>(xy, n, g, TSI, P->w, ntx, nty, k1, i1);
+  VP_CHECK_LAUNCH();
+  VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
+  k_interp_keys2<<<nb, 256, 0, s>>>(k1s, n, k2);
+  VP_CHECK_LAUNCH();
+  VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
   *otx = vp_alloc<double>(P, n);
   *oty = vp_alloc<double>(P, n);
   *otperm = vp_alloc<int64_t>(P, n);
@@ -1436,11 +1385,9 @@ static void launch_band_entries_w(vp_plan_s *P, const GridArgs &g) {
     VP_CUDA(cudaFuncSetAttribute(k_interp_local<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr = (int)sm;
   }
-  RestrictArgs ra{};
-  TapArgs tp{};
   k_interp_local<W, D><<<(unsigned)B.e_n_items, 256, sm, P->stream>>>(
-      B.e_items, TSI, B.e_x, B.e_y, B.e_perm, g, 1, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, 0, nullptr,
-      nullptr, nullptr, B.ent_val, nullptr, ra, tp, 1);
+      B.e_items, TSI, B.e_x, B.e_y, B.e_perm, g, 1, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr,
+      B.ent_val);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
