@@ -93,7 +93,9 @@ typedef struct {
    * spreading-tile halos into the grid; this mode launches the spreading once per tile colour (tx & 1, ty & 1)
    * with one work item per tile and plain read-add-write (slower on dense tiles). */
   int32_t deterministic;
-  /* tuning: spreading tile side in NH cells (0 -> 32, 8..64) and interpolation tile side (0 -> 64, 16..128) */
+  /* tuning: spread_tile 0 -> register strips (k_spread_strip), 8..64 -> shared-memory tile
+   * batches of that side (k_spread_nh; always used in deterministic mode, tile side 32 when 0);
+   * interp_tile: interpolation tile side (0 -> 64, 16..128) */
   int32_t spread_tile;
   int32_t interp_tile;
 } vp_opts;

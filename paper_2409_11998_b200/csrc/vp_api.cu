@@ -511,7 +511,10 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     // ---- sources and targets sorted by NH tile
     P->sp.det = o.deterministic ? 1 : 0;
     P->bands.sp.det = P->sp.det;
-    vp_build_spread_order(P, P->sp, tri_nodes, weights, nullptr, N, grid_args(P->nh));
+    if (P->sp.det || o.spread_tile > 0)  // tile batches: deterministic colouring, or explicitly requested
+      vp_build_spread_order(P, P->sp, tri_nodes, weights, nullptr, N, grid_args(P->nh));
+    else
+      vp_build_strip_order(P, P->sp, tri_nodes, weights, nullptr, N, grid_args(P->nh));
     P->dmode = o.deriv_mode;
     if (P->dmode == VP_DERIV_AUTO) P->dmode = (o.ref_nodes && N > 10000000) ? VP_DERIV_TRIANGLE : VP_DERIV_KNN;
     vp_build_interp_order(P, targets, T);

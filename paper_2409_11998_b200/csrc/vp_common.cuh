@@ -92,6 +92,9 @@ struct VpSpreadSet {
   int det = 0;                 // deterministic mode: items sorted by tile colour, colour_off[c]..colour_off[c+1]
   int64_t color_off[5] = {};
   double *fs_out = nullptr;    // if set, the spread also writes f in this sorted order
+  int strip = 0;               // 1: strip order for k_spread_strip (sitems), 0: tile batches (tiles, bstart)
+  int4 *sitems = nullptr;      // (strip_x, strip_y, first point, end point)
+  int64_t n_sitems = 0;
 };
 
 // Level-band corrections for graded meshes: per-target level
@@ -219,6 +222,8 @@ void vp_launch_tri_local(vp_plan_s *P, const double *f);
 void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out, bool local_kernels);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n);
+void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const double *weights,
+                          const int32_t *node_of, int64_t n, const GridArgs &g);
 void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx,
                              double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items);
 void vp_remap_stencils(vp_plan_s *P);

@@ -24,8 +24,13 @@
 #include "vp_math.cuh"
 
 
-// fractional grid coordinate of x (identical expression in binning, spreading and interpolation)
-__device__ __forceinline__ double gcoord(double x, double o, double inv_h) { return (x - o) * inv_h; }
+// fractional grid coordinate of x (identical expression in binning, spreading and interpolation; the _rn
+// intrinsics keep the compiler from contracting it differently in different kernels, so plan-time keys and
+// eval-time footprints agree bit for bit)
+__device__ __forceinline__ double gcoord(double x, double o, double inv_h) { return __dmul_rn(__dsub_rn(x, o), inv_h); }
+
+// first grid index of the W-point footprint around fractional coordinate g
+__device__ __forceinline__ int es_origin(double g, int W) { return (int)ceil(__dsub_rn(g, 0.5 * W)); }
 
 // Horner tables of the ES taps for every width W (beta = 2.30 W fixed, so the table depends on W only)
 __constant__ double c_horner[VP_HORNER_MAXW - 3][VP_HORNER_MAXW][VP_HORNER_MAXW];
@@ -38,9 +43,9 @@ void vp_upload_horner(int W, const VpHorner &h) {
 // t = 2u - 1, u = i0 - (g - W/2) in [0, 1)
 template <int W, int D>
 __device__ __forceinline__ int es_horner(double g, double *wts) {
-  double s = g - 0.5 * W;
-  int i0 = (int)ceil(s);
-  double t = 2.0 * (i0 - s) - 1.0;
+  const double s = __dsub_rn(g, 0.5 * W);
+  const int i0 = (int)ceil(s);
+  const double t = 2.0 * (i0 - s) - 1.0;
 #pragma unroll
   for (int k = 0; k < W; k++) wts[k] = c_horner[W - 4][k][D];
 #pragma unroll
@@ -70,8 +75,8 @@ __global__ void k_spread_keys(const double *__restrict__ xy, int64_t n, GridArgs
   int64_t tx = (int64_t)floor(gx / TS), ty = (int64_t)floor(gy / TS);
   tx = tx < 0 ? 0 : (tx >= ntx ? ntx - 1 : tx);
   ty = ty < 0 ? 0 : (ty >= nty ? nty - 1 : ty);
-  int64_t lrow = (int64_t)ceil(gy - 0.5 * W) - (ty * TS - (W / 2 + 1));
-  int64_t lcol = (int64_t)ceil(gx - 0.5 * W) - (tx * TS - (W / 2 + 1));
+  int64_t lrow = (int64_t)es_origin(gy, W) - (ty * TS - (W / 2 + 1));
+  int64_t lcol = (int64_t)es_origin(gx, W) - (tx * TS - (W / 2 + 1));
   lrow = lrow < 0 ? 0 : (lrow > 255 ? 255 : lrow);
   lcol = lcol < 0 ? 0 : (lcol > 255 ? 255 : lcol);
   keys[i] = ((uint64_t)(ty * ntx + tx) << 32) | ((uint64_t)lrow << 16) | (uint64_t)lcol;
@@ -326,10 +331,139 @@ static void launch_spread_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// NH spreading, strip form (default for the NH grid).  A warp owns a 32-column x (SH + W - 1)-row window
+// of the grid in REGISTERS: lane = column, acc[r] = window row r.  The points of a work item are the
+// points whose footprint origin lies in an SW x SH "strip" (SW = 33 - W, so every footprint fits the 32
+// lanes), sorted by origin row.  Per chunk of CH points:
+//   phase A (lane per point): ES weights by Horner, wx -> shared (odd stride), c wy -> shared (16-B rows),
+//            origin (row, col) -> shared;
+//   phase B (warp per point, in row order): lane l takes wx[l - col] (0 outside the footprint) and adds
+//            wx * (c wy[b]) to acc[row + b], b < W: W DFMA per point, no shared-memory writes, no atomics.
+// The row loop is unrolled so acc[] indices are compile-time (registers).  One fp64 RED per non-zero window
+// cell at the end.  Compared with the shared-memory tile scatter (k_spread_nh), this replaces 2 W^2
+// shared-memory accesses per point by W + 2 broadcast loads.
+#define VP_STRIP_WARPS 4
+#define VP_STRIP_MAXP 2048  // points per work item: dense strips are split (each part writes its own window)
+template <int W>
+struct StripCfg {
+  static constexpr int SW = 33 - W;             // footprint-origin columns per strip
+  static constexpr int SH = 32;                 // footprint-origin rows per strip
+  static constexpr int NR = SH + W - 1;         // window rows (registers per lane)
+  static constexpr int CH = W <= 10 ? 64 : 32;  // points staged per chunk
+  static constexpr int WXS = W | 1;             // odd stride: conflict-free lane-per-point stores
+  static constexpr int WYS = (W + 1) & ~1;      // even stride: 16-byte aligned rows for double2 broadcasts
+  static constexpr size_t smem_warp = (size_t)CH * (WXS + WYS) * 8 + (size_t)CH * 4;
+};
+
+template <int W, int D>
+__global__ void __launch_bounds__(32 * VP_STRIP_WARPS, W <= 9 ? 4 : (W <= 13 ? 3 : 2))
+    k_spread_strip(const int4 *__restrict__ items, int64_t n_items, const double *__restrict__ sx,
+                   const double *__restrict__ sy, const double *__restrict__ sw, const int32_t *__restrict__ sperm,
+                   const double *__restrict__ f, GridArgs g, double *__restrict__ fs_out) {
+  using C = StripCfg<W>;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * VP_STRIP_WARPS + warp;
+  if (item >= n_items) return;
+  double *s_wy = smem + (size_t)warp * C::CH * (C::WXS + C::WYS);
+  double *s_wx = s_wy + C::CH * C::WYS;
+  int *s_key = (int *)(smem + (size_t)VP_STRIP_WARPS * C::CH * (C::WXS + C::WYS)) + warp * C::CH;
+  const int4 it = items[item];
+  const int64_t ox = (int64_t)it.x * C::SW - (W / 2 + 1), oy = (int64_t)it.y * C::SH - (W / 2 + 1);
+  double acc[C::NR];
+#pragma unroll
+  for (int r = 0; r < C::NR; r++) acc[r] = 0.0;
+  for (int c0 = it.z; c0 < it.w; c0 += C::CH) {
+    const int n = min(C::CH, it.w - c0);
+#pragma unroll
+    for (int h = 0; h < C::CH / 32; h++) {
+      const int q = lane + 32 * h;
+      if (q < n) {
+        const int j = c0 + q;
+        const double fj = __ldg(f + sperm[j]);
+        if (fs_out) fs_out[j] = fj;  // f in spreading order: spatially coherent copy for the stencil gathers
+        const double c = fj * sw[j];
+        int lc, lr;
+        {  // one weight vector live at a time (acc[] holds NR registers)
+          double wx[W];
+          lc = (int)(es_horner<W, D>(gcoord(sx[j], g.ox, g.inv_h), wx) - ox);
+#pragma unroll
+          for (int a = 0; a < W; a++) s_wx[q * C::WXS + a] = wx[a];
+        }
+        double wy[W];
+        lr = (int)(es_horner<W, D>(gcoord(sy[j], g.oy, g.inv_h), wy) - oy);
+        double2 *wyp = (double2 *)(s_wy + q * C::WYS);
+#pragma unroll
+        for (int b = 0; b + 1 < W; b += 2) wyp[b >> 1] = make_double2(c * wy[b], c * wy[b + 1]);
+        if (W & 1) s_wy[q * C::WYS + W - 1] = c * wy[W - 1];
+        s_key[q] = (lr << 8) | lc;
+      }
+    }
+    __syncwarp();
+    int q = 0;
+    int key = s_key[0];
+#pragma unroll
+    for (int r = 0; r < C::SH; r++) {
+      while ((key >> 8) == r) {
+        const int a = lane - (key & 0xff);
+        const double wv = s_wx[q * C::WXS + min(max(a, 0), W - 1)];
+        const double wxl = (a >= 0 && a < W) ? wv : 0.0;
+        const double2 *wyp = (const double2 *)(s_wy + q * C::WYS);
+#pragma unroll
+        for (int b = 0; b + 1 < W; b += 2) {
+          const double2 v = wyp[b >> 1];
+          acc[r + b] = fma(v.x, wxl, acc[r + b]);
+          acc[r + b + 1] = fma(v.y, wxl, acc[r + b + 1]);
+        }
+        if (W & 1) acc[r + W - 1] = fma(s_wy[q * C::WYS + W - 1], wxl, acc[r + W - 1]);
+        q++;
+        key = q < n ? s_key[q] : 0x7fffffff;
+      }
+    }
+    __syncwarp();
+  }
+  const bool interior = ox >= 0 && oy >= 0 && ox + 32 <= g.nfx && oy + C::NR <= g.nfy;
+  const int64_t gx = interior ? ox + lane : wrapi(ox + lane, g.nfx);
+#pragma unroll
+  for (int r = 0; r < C::NR; r++) {
+    if (acc[r] != 0.0) {
+      const int64_t gy = interior ? oy + r : wrapi(oy + r, g.nfy);
+      atomicAdd(g.data + gy * g.row + gx, acc[r]);
+    }
+  }
+}
+
+template <int W>
+static void launch_spread_strip_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *f) {
+  constexpr int D = VP_HORNER_DEG(W);
+  if (S.n_sitems == 0) return;
+  const size_t sm = StripCfg<W>::smem_warp * VP_STRIP_WARPS;
+  static size_t attr_set = 0;
+  if (sm > attr_set && sm > 48 * 1024) {
+    VP_CUDA(cudaFuncSetAttribute(k_spread_strip<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr_set = sm;
+  }
+  const unsigned nb = (unsigned)((S.n_sitems + VP_STRIP_WARPS - 1) / VP_STRIP_WARPS);
+  k_spread_strip<W, D><<<nb, 32 * VP_STRIP_WARPS, sm, P->stream>>>(S.sitems, S.n_sitems, S.sx, S.sy, S.sw, S.sperm,
+                                                                   f, g, S.fs_out);
+  VP_CHECK_LAUNCH();
+  P->n_kernels++;
+}
+
+// strip geometry of width W (host side of StripCfg)
+void vp_strip_dims(int W, int *SW, int *SH) {
+  *SW = 33 - W;
+  *SH = 32;
+}
+
 void vp_launch_spread(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *f) {
   switch (P->w) {
-#define CASE(W) \
-  case W: launch_spread_w<W>(P, S, g, f); break;
+#define CASE(W)                                      \
+  case W:                                            \
+    if (S.strip) launch_spread_strip_w<W>(P, S, g, f); \
+    else launch_spread_w<W>(P, S, g, f);              \
+    break;
     CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
     default: throw VpError{VP_ERR_UNSUPPORTED};
@@ -1254,6 +1388,121 @@ void vp_build_spread_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const
   if (!items.empty()) VP_CUDA(cudaMemcpy(Tl.sub, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
   for (void *p : {(void *)k1, (void *)k1s, (void *)k2, (void *)k2s, (void *)i1, (void *)i1s, (void *)i2s, (void *)head,
                   tmp})
+    VP_CUDA(cudaFreeAsync(p, s));
+}
+
+// ---------------------------------------------------------------------------------------------
+// plan-time: strip order for k_spread_strip.  Key = (strip, origin row in strip, origin column in strip);
+// the same es_origin() as the kernel's es_horner, so the kernel's rows agree with the sort.
+__global__ void k_strip_keys(const double *__restrict__ xy, int64_t n, GridArgs g, int W, int SW, int SH,
+                             int64_t nsx, int64_t nsy, uint64_t *__restrict__ keys, int32_t *__restrict__ idx,
+                             int *__restrict__ bad) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t cx = (int64_t)es_origin(gcoord(xy[2 * i], g.ox, g.inv_h), W) + (W / 2 + 1);
+  const int64_t cy = (int64_t)es_origin(gcoord(xy[2 * i + 1], g.oy, g.inv_h), W) + (W / 2 + 1);
+  const int64_t bx = cx >= 0 ? cx / SW : -1, by = cy >= 0 ? cy / SH : -1;
+  if (bx < 0 || by < 0 || bx >= nsx || by >= nsy) {  // outside the grid frame (not produced by the plan's grid)
+    *bad = 1;
+    keys[i] = 0;
+  } else {
+    keys[i] = ((uint64_t)(by * nsx + bx) << 16) | ((uint64_t)(cy - by * SH) << 8) | (uint64_t)(cx - bx * SW);
+  }
+  idx[i] = (int32_t)i;
+}
+
+__global__ void k_strip_heads(const uint64_t *__restrict__ k, int64_t n, int32_t *__restrict__ head) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  head[i] = (i == 0 || (k[i - 1] >> 16) != (k[i] >> 16)) ? 1 : 0;
+}
+
+__global__ void k_strip_ids(const uint64_t *__restrict__ k, const int32_t *__restrict__ pos, int64_t m,
+                            int64_t *__restrict__ sid) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) sid[i] = (int64_t)(k[pos[i]] >> 16);
+}
+
+void vp_strip_dims(int W, int *SW, int *SH);
+
+void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const double *weights,
+                          const int32_t *node_of, int64_t n, const GridArgs &g) {
+  cudaStream_t s = P->stream;
+  S.strip = 1;
+  int SW, SH;
+  vp_strip_dims(P->w, &SW, &SH);
+  const int64_t nsx = (g.nfx + P->w + 2) / SW + 1, nsy = (g.nfy + P->w + 2) / SH + 1;
+  if (n == 0) {
+    S.sx = vp_alloc<double>(P, 1); S.sy = vp_alloc<double>(P, 1); S.sw = vp_alloc<double>(P, 1);
+    S.sperm = vp_alloc<int32_t>(P, 1); S.sitems = vp_alloc<int4>(P, 1);
+    S.n_sitems = 0; S.n_batches = 0;
+    return;
+  }
+  if (nsx * nsy >= (int64_t)1 << 47) throw VpError{VP_ERR_UNSUPPORTED};
+  uint64_t *k1, *k1s;
+  int32_t *i1, *i1s, *head, *hpos, *d_nh;
+  int *d_bad;
+  VP_CUDA(cudaMallocAsync(&k1, 8 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&k1s, 8 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&i1, 4 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&i1s, 4 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&head, 4 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&hpos, 4 * (n + 1), s));
+  VP_CUDA(cudaMallocAsync(&d_nh, 4, s));
+  VP_CUDA(cudaMallocAsync(&d_bad, 4, s));
+  VP_CUDA(cudaMemsetAsync(d_bad, 0, 4, s));
+  const unsigned nb = (unsigned)((n + 255) / 256);
+  k_strip_keys<<<nb, 256, 0, s>>>(xy, n, g, P->w, SW, SH, nsx, nsy, k1, i1, d_bad);
+  VP_CHECK_LAUNCH();
+  size_t tb = 0, tb3 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s);
+  cub::CountingInputIterator<int32_t> cnt(0);
+  cub::DeviceSelect::Flagged(nullptr, tb3, cnt, head, hpos, d_nh, (int)n, s);
+  void *tmp;
+  VP_CUDA(cudaMallocAsync(&tmp, std::max(tb, tb3) + 16, s));
+  VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
+  k_strip_heads<<<nb, 256, 0, s>>>(k1s, n, head);
+  VP_CHECK_LAUNCH();
+  VP_CUDA(cub::DeviceSelect::Flagged(tmp, tb3, cnt, head, hpos, d_nh, (int)n, s));
+  int32_t nh = 0;
+  int bad = 0;
+  VP_CUDA(cudaMemcpyAsync(&nh, d_nh, 4, cudaMemcpyDeviceToHost, s));
+  VP_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, s));
+  VP_CUDA(cudaStreamSynchronize(s));
+  if (bad) {
+    vp_set_last_error("a source lies outside the spreading grid's frame");
+    throw VpError{VP_ERR_GEOMETRY};
+  }
+  int64_t *d_sid;
+  VP_CUDA(cudaMallocAsync(&d_sid, 8 * (size_t)nh, s));
+  k_strip_ids<<<(unsigned)((nh + 255) / 256), 256, 0, s>>>(k1s, hpos, nh, d_sid);
+  VP_CHECK_LAUNCH();
+  std::vector<int32_t> hp(nh);
+  std::vector<int64_t> hs(nh);
+  VP_CUDA(cudaMemcpyAsync(hp.data(), hpos, 4 * (size_t)nh, cudaMemcpyDeviceToHost, s));
+  VP_CUDA(cudaMemcpyAsync(hs.data(), d_sid, 8 * (size_t)nh, cudaMemcpyDeviceToHost, s));
+  S.sx = vp_alloc<double>(P, n);
+  S.sy = vp_alloc<double>(P, n);
+  S.sw = vp_alloc<double>(P, n);
+  S.sperm = vp_alloc<int32_t>(P, n);
+  k_gather_src<<<nb, 256, 0, s>>>(xy, weights, i1s, node_of, n, S.sx, S.sy, S.sw, S.sperm);
+  VP_CHECK_LAUNCH();
+  VP_CUDA(cudaStreamSynchronize(s));
+  // work items: every strip, dense strips cut into <= VP_STRIP_MAXP points; largest first (load balance)
+  std::vector<int4> items;
+  for (int64_t h = 0; h < nh; h++) {
+    const int64_t p0 = hp[h], p1 = (h + 1 < nh) ? hp[h + 1] : n;
+    const int bx = (int)(hs[h] % nsx), by = (int)(hs[h] / nsx);
+    for (int64_t a = p0; a < p1; a += VP_STRIP_MAXP)
+      items.push_back(make_int4(bx, by, (int)a, (int)std::min<int64_t>(p1, a + VP_STRIP_MAXP)));
+  }
+  std::stable_sort(items.begin(), items.end(), [](const int4 &a, const int4 &b) { return a.w - a.z > b.w - b.z; });
+  S.n_sitems = (int64_t)items.size();
+  S.n_batches = S.n_sitems;
+  S.sitems = vp_alloc<int4>(P, items.size());
+  VP_CUDA(cudaMemcpy(S.sitems, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
+  for (void *p : {(void *)k1, (void *)k1s, (void *)i1, (void *)i1s, (void *)head, (void *)hpos, (void *)d_nh,
+                  (void *)d_bad, (void *)d_sid, tmp})
     VP_CUDA(cudaFreeAsync(p, s));
 }
 
