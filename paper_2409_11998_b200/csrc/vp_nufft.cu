@@ -332,32 +332,31 @@ static void launch_spread_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &
 }
 
 // ---------------------------------------------------------------------------------------------
-// NH spreading, strip form (default for the NH grid).  A warp owns a 32-column x (SH + W - 1)-row window
-// of the grid in REGISTERS: lane = column, acc[r] = window row r.  The points of a work item are the
-// points whose footprint origin lies in an SW x SH "strip" (SW = 33 - W, so every footprint fits the 32
-// lanes), sorted by origin row.  Per chunk of CH points:
-//   phase A (lane per point): ES weights by Horner, wx -> shared (odd stride), c wy -> shared (16-B rows),
-//            origin (row, col) -> shared;
-//   phase B (warp per point, in row order): lane l takes wx[l - col] (0 outside the footprint) and adds
-//            wx * (c wy[b]) to acc[row + b], b < W: W DFMA per point, no shared-memory writes, no atomics.
-// The row loop is unrolled so acc[] indices are compile-time (registers).  One fp64 RED per non-zero window
-// cell at the end.  Compared with the shared-memory tile scatter (k_spread_nh), this replaces 2 W^2
-// shared-memory accesses per point by W + 2 broadcast loads.
+// NH spreading, strip form (default for the NH grid).  A warp owns a 32-column strip of the grid: lane =
+// column.  The points of a work item are those whose footprint origin lies in an SW x SH "strip" (SW = 33 - W,
+// so every footprint fits the 32 lanes), sorted by origin row.  The warp walks the rows in order and keeps the
+// W rows r .. r + W - 1 in REGISTERS as a ring (row rho in acc[rho mod W]); a point with origin row r adds
+// wxrow[lane] * (c wy[b]) to row r + b (W DFMA, no shared-memory writes, no atomics), and leaving row r flushes
+// acc[r mod W] (one coalesced fp64 RED per lane, skipped when zero).  The ring phase k = r mod W is a
+// compile-time constant in each of the W unrolled phases (switch + fall-through), so acc[] stays in registers.
+// Points are staged 32 at a time (lane per point): the x weights as a zero-padded 32-wide row (the lane's
+// column weight is then one conflict-free load), c wy as 16-byte rows read by double2 broadcasts, origin
+// (row, col) as a key.  Compared with the shared-memory tile scatter (k_spread_nh) this replaces 2 W^2
+// shared-memory accesses per point by ~W/2 + 2 loads.
 #define VP_STRIP_WARPS 4
-#define VP_STRIP_MAXP 2048  // points per work item: dense strips are split (each part writes its own window)
+#define VP_STRIP_MAXP 2048  // points per work item: dense strips are split (each part flushes its own rows)
 template <int W>
 struct StripCfg {
-  static constexpr int SW = 33 - W;             // footprint-origin columns per strip
-  static constexpr int SH = 32;                 // footprint-origin rows per strip
-  static constexpr int NR = SH + W - 1;         // window rows (registers per lane)
-  static constexpr int CH = W <= 10 ? 64 : 32;  // points staged per chunk
-  static constexpr int WXS = W | 1;             // odd stride: conflict-free lane-per-point stores
-  static constexpr int WYS = (W + 1) & ~1;      // even stride: 16-byte aligned rows for double2 broadcasts
+  static constexpr int SW = 33 - W;         // footprint-origin columns per strip
+  static constexpr int SH = 32;             // footprint-origin rows per strip
+  static constexpr int CH = 32;             // points staged per chunk (one per lane)
+  static constexpr int WXS = 33;            // padded x-weight rows (32 columns)
+  static constexpr int WYS = (W + 1) & ~1;  // even stride: 16-byte aligned rows for double2 broadcasts
   static constexpr size_t smem_warp = (size_t)CH * (WXS + WYS) * 8 + (size_t)CH * 4;
 };
 
 template <int W, int D>
-__global__ void __launch_bounds__(32 * VP_STRIP_WARPS, W <= 9 ? 4 : (W <= 13 ? 3 : 2))
+__global__ void __launch_bounds__(32 * VP_STRIP_WARPS, W <= 10 ? 5 : 4)
     k_spread_strip(const int4 *__restrict__ items, int64_t n_items, const double *__restrict__ sx,
                    const double *__restrict__ sy, const double *__restrict__ sw, const int32_t *__restrict__ sperm,
                    const double *__restrict__ f, GridArgs g, double *__restrict__ fs_out) {
@@ -371,65 +370,84 @@ __global__ void __launch_bounds__(32 * VP_STRIP_WARPS, W <= 9 ? 4 : (W <= 13 ? 3
   int *s_key = (int *)(smem + (size_t)VP_STRIP_WARPS * C::CH * (C::WXS + C::WYS)) + warp * C::CH;
   const int4 it = items[item];
   const int64_t ox = (int64_t)it.x * C::SW - (W / 2 + 1), oy = (int64_t)it.y * C::SH - (W / 2 + 1);
-  double acc[C::NR];
+  const bool interior = ox >= 0 && oy >= 0 && ox + 32 <= g.nfx && oy + C::SH + W - 1 <= g.nfy;
+  double *col = g.data + (interior ? ox + lane : wrapi(ox + lane, g.nfx));
+  double acc[W];
 #pragma unroll
-  for (int r = 0; r < C::NR; r++) acc[r] = 0.0;
-  for (int c0 = it.z; c0 < it.w; c0 += C::CH) {
-    const int n = min(C::CH, it.w - c0);
+  for (int b = 0; b < W; b++) acc[b] = 0.0;
+  int c0 = it.z, n = 0, q = 0, r = 0;
+  bool first = true;
+stage:
+  n = min(C::CH, it.w - c0);
+  if (lane < n) {
+    const int j = c0 + lane;
+    const double fj = __ldg(f + sperm[j]);
+    if (fs_out) fs_out[j] = fj;  // f in spreading order: spatially coherent copy for the stencil gathers
+    const double c = fj * sw[j];
+    double *wrow = s_wx + lane * C::WXS;
 #pragma unroll
-    for (int h = 0; h < C::CH / 32; h++) {
-      const int q = lane + 32 * h;
-      if (q < n) {
-        const int j = c0 + q;
-        const double fj = __ldg(f + sperm[j]);
-        if (fs_out) fs_out[j] = fj;  // f in spreading order: spatially coherent copy for the stencil gathers
-        const double c = fj * sw[j];
-        int lc, lr;
-        {  // one weight vector live at a time (acc[] holds NR registers)
-          double wx[W];
-          lc = (int)(es_horner<W, D>(gcoord(sx[j], g.ox, g.inv_h), wx) - ox);
+    for (int a = 0; a < 32; a++) wrow[a] = 0.0;
+    int lc, lr;
+    {
+      double wx[W];
+      lc = (int)(es_horner<W, D>(gcoord(sx[j], g.ox, g.inv_h), wx) - ox);
 #pragma unroll
-          for (int a = 0; a < W; a++) s_wx[q * C::WXS + a] = wx[a];
-        }
-        double wy[W];
-        lr = (int)(es_horner<W, D>(gcoord(sy[j], g.oy, g.inv_h), wy) - oy);
-        double2 *wyp = (double2 *)(s_wy + q * C::WYS);
-#pragma unroll
-        for (int b = 0; b + 1 < W; b += 2) wyp[b >> 1] = make_double2(c * wy[b], c * wy[b + 1]);
-        if (W & 1) s_wy[q * C::WYS + W - 1] = c * wy[W - 1];
-        s_key[q] = (lr << 8) | lc;
-      }
+      for (int a = 0; a < W; a++) wrow[lc + a] = wx[a];
     }
-    __syncwarp();
-    int q = 0;
-    int key = s_key[0];
+    double wy[W];
+    lr = (int)(es_horner<W, D>(gcoord(sy[j], g.oy, g.inv_h), wy) - oy);
+    double2 *wyp = (double2 *)(s_wy + lane * C::WYS);
 #pragma unroll
-    for (int r = 0; r < C::SH; r++) {
-      while ((key >> 8) == r) {
-        const int a = lane - (key & 0xff);
-        const double wv = s_wx[q * C::WXS + min(max(a, 0), W - 1)];
-        const double wxl = (a >= 0 && a < W) ? wv : 0.0;
-        const double2 *wyp = (const double2 *)(s_wy + q * C::WYS);
-#pragma unroll
-        for (int b = 0; b + 1 < W; b += 2) {
-          const double2 v = wyp[b >> 1];
-          acc[r + b] = fma(v.x, wxl, acc[r + b]);
-          acc[r + b + 1] = fma(v.y, wxl, acc[r + b + 1]);
-        }
-        if (W & 1) acc[r + W - 1] = fma(s_wy[q * C::WYS + W - 1], wxl, acc[r + W - 1]);
-        q++;
-        key = q < n ? s_key[q] : 0x7fffffff;
-      }
-    }
-    __syncwarp();
+    for (int b = 0; b + 1 < W; b += 2) wyp[b >> 1] = make_double2(c * wy[b], c * wy[b + 1]);
+    if (W & 1) s_wy[lane * C::WYS + W - 1] = c * wy[W - 1];
+    s_key[lane] = lr;
   }
-  const bool interior = ox >= 0 && oy >= 0 && ox + 32 <= g.nfx && oy + C::NR <= g.nfy;
-  const int64_t gx = interior ? ox + lane : wrapi(ox + lane, g.nfx);
+  __syncwarp();
+  q = 0;
+  if (first) {
+    r = s_key[0];
+    first = false;
+  }
+  for (;;) {
+    switch (r % W) {
+#define VP_STRIP_PHASE(k)                                                              \
+  case k:                                                                              \
+    if ((k) < W) {                                                                     \
+      while (q < n && s_key[q] == r) {                                                 \
+        const double wxl = s_wx[q * C::WXS + lane];                                    \
+        const double2 *wyp = (const double2 *)(s_wy + q * C::WYS);                     \
+        _Pragma("unroll") for (int b = 0; b + 1 < W; b += 2) {                         \
+          const double2 v = wyp[b >> 1];                                               \
+          acc[((k) + b) % W] = fma(v.x, wxl, acc[((k) + b) % W]);                      \
+          acc[((k) + b + 1) % W] = fma(v.y, wxl, acc[((k) + b + 1) % W]);              \
+        }                                                                              \
+        if (W & 1) acc[((k) + W - 1) % W] = fma(s_wy[q * C::WYS + W - 1], wxl, acc[((k) + W - 1) % W]); \
+        q++;                                                                           \
+      }                                                                                \
+      if (q == n) goto next_chunk;                                                     \
+      if (acc[(k) % W] != 0.0) {                                                       \
+        atomicAdd(col + (interior ? oy + r : wrapi(oy + r, g.nfy)) * g.row, acc[(k) % W]); \
+        acc[(k) % W] = 0.0;                                                            \
+      }                                                                                \
+      r++;                                                                             \
+    }
+      VP_STRIP_PHASE(0) VP_STRIP_PHASE(1) VP_STRIP_PHASE(2) VP_STRIP_PHASE(3) VP_STRIP_PHASE(4)
+      VP_STRIP_PHASE(5) VP_STRIP_PHASE(6) VP_STRIP_PHASE(7) VP_STRIP_PHASE(8) VP_STRIP_PHASE(9)
+      VP_STRIP_PHASE(10) VP_STRIP_PHASE(11) VP_STRIP_PHASE(12) VP_STRIP_PHASE(13) VP_STRIP_PHASE(14)
+      VP_STRIP_PHASE(15)
+#undef VP_STRIP_PHASE
+    }
+  }
+next_chunk:
+  __syncwarp();
+  c0 += C::CH;
+  if (c0 < it.w) goto stage;
+  // flush the ring: acc[j] holds row r + ((j - r) mod W)
 #pragma unroll
-  for (int r = 0; r < C::NR; r++) {
-    if (acc[r] != 0.0) {
-      const int64_t gy = interior ? oy + r : wrapi(oy + r, g.nfy);
-      atomicAdd(g.data + gy * g.row + gx, acc[r]);
+  for (int j = 0; j < W; j++) {
+    if (acc[j] != 0.0) {
+      const int rr = r + ((j - r % W) + W) % W;
+      atomicAdd(col + (interior ? oy + rr : wrapi(oy + rr, g.nfy)) * g.row, acc[j]);
     }
   }
 }
