@@ -65,6 +65,17 @@ __device__ __forceinline__ int64_t wrapi(int64_t i, int64_t n) {
   return i < 0 ? i + n : i;
 }
 
+// fp64 RED of v into grid row gy (periodic) at column pointer col; the wrapped case out of line (small code
+// in unrolled loops)
+__device__ __noinline__ void red_row_wrapped(double *col, int64_t gy, int64_t nfy, int64_t row, double v) {
+  atomicAdd(col + wrapi(gy, nfy) * row, v);
+}
+__device__ __forceinline__ void red_row(double *col, int64_t gy, bool interior, const GridArgs &g, double v) {
+  if (v == 0.0) return;
+  if (interior) atomicAdd(col + gy * g.row, v);
+  else red_row_wrapped(col, gy, g.nfy, g.row, v);
+}
+
 // ---------------------------------------------------------------------------------------------
 // plan-time keys for the batch ordering: (tile, footprint row, footprint column) of each point
 __global__ void k_spread_keys(const double *__restrict__ xy, int64_t n, GridArgs g, int TS, int W, int64_t ntx,
@@ -375,18 +386,21 @@ __global__ void __launch_bounds__(32 * VP_STRIP_WARPS, W <= 10 ? 5 : 4)
   double acc[W];
 #pragma unroll
   for (int b = 0; b < W; b++) acc[b] = 0.0;
-  int c0 = it.z, n = 0, q = 0, r = 0;
+  int c0 = it.z, n = 0, q = 0, r = 0, mylr = 0x7fffffff, prev_lc = 0;
   bool first = true;
+  double *wrow = s_wx + lane * C::WXS;
+#pragma unroll
+  for (int a = 0; a < 32; a++) wrow[a] = 0.0;
 stage:
   n = min(C::CH, it.w - c0);
+  mylr = 0x7fffffff;
   if (lane < n) {
     const int j = c0 + lane;
     const double fj = __ldg(f + sperm[j]);
     if (fs_out) fs_out[j] = fj;  // f in spreading order: spatially coherent copy for the stencil gathers
     const double c = fj * sw[j];
-    double *wrow = s_wx + lane * C::WXS;
 #pragma unroll
-    for (int a = 0; a < 32; a++) wrow[a] = 0.0;
+    for (int a = 0; a < W; a++) wrow[prev_lc + a] = 0.0;  // the row is zero outside the footprint
     int lc, lr;
     {
       double wx[W];
@@ -394,18 +408,19 @@ stage:
 #pragma unroll
       for (int a = 0; a < W; a++) wrow[lc + a] = wx[a];
     }
+    prev_lc = lc;
     double wy[W];
     lr = (int)(es_horner<W, D>(gcoord(sy[j], g.oy, g.inv_h), wy) - oy);
     double2 *wyp = (double2 *)(s_wy + lane * C::WYS);
 #pragma unroll
     for (int b = 0; b + 1 < W; b += 2) wyp[b >> 1] = make_double2(c * wy[b], c * wy[b + 1]);
     if (W & 1) s_wy[lane * C::WYS + W - 1] = c * wy[W - 1];
-    s_key[lane] = lr;
+    mylr = lr;
   }
   __syncwarp();
   q = 0;
   if (first) {
-    r = s_key[0];
+    r = __shfl_sync(0xffffffffu, mylr, 0);
     first = false;
   }
   for (;;) {
@@ -413,7 +428,7 @@ stage:
 #define VP_STRIP_PHASE(k)                                                              \
   case k:                                                                              \
     if ((k) < W) {                                                                     \
-      while (q < n && s_key[q] == r) {                                                 \
+      _Pragma("unroll 2") for (const int e = __popc(__ballot_sync(0xffffffffu, mylr <= r)); q < e; q++) { \
         const double wxl = s_wx[q * C::WXS + lane];                                    \
         const double2 *wyp = (const double2 *)(s_wy + q * C::WYS);                     \
         _Pragma("unroll") for (int b = 0; b + 1 < W; b += 2) {                         \
@@ -422,13 +437,10 @@ stage:
           acc[((k) + b + 1) % W] = fma(v.y, wxl, acc[((k) + b + 1) % W]);              \
         }                                                                              \
         if (W & 1) acc[((k) + W - 1) % W] = fma(s_wy[q * C::WYS + W - 1], wxl, acc[((k) + W - 1) % W]); \
-        q++;                                                                           \
       }                                                                                \
       if (q == n) goto next_chunk;                                                     \
-      if (acc[(k) % W] != 0.0) {                                                       \
-        atomicAdd(col + (interior ? oy + r : wrapi(oy + r, g.nfy)) * g.row, acc[(k) % W]); \
-        acc[(k) % W] = 0.0;                                                            \
-      }                                                                                \
+      red_row(col, oy + r, interior, g, acc[(k) % W]);                                 \
+      acc[(k) % W] = 0.0;                                                              \
       r++;                                                                             \
     }
       VP_STRIP_PHASE(0) VP_STRIP_PHASE(1) VP_STRIP_PHASE(2) VP_STRIP_PHASE(3) VP_STRIP_PHASE(4)
@@ -445,10 +457,7 @@ next_chunk:
   // flush the ring: acc[j] holds row r + ((j - r) mod W)
 #pragma unroll
   for (int j = 0; j < W; j++) {
-    if (acc[j] != 0.0) {
-      const int rr = r + ((j - r % W) + W) % W;
-      atomicAdd(col + (interior ? oy + rr : wrapi(oy + rr, g.nfy)) * g.row, acc[j]);
-    }
+    red_row(col, oy + r + ((j - r % W) + W) % W, interior, g, acc[j]);
   }
 }
 
