@@ -321,7 +321,7 @@ def main():
                            "nf_nh": info["nf_nh"], "nf_fh": info["nf_fh"], "w_es": info["w_es"],
                            "deriv": f"{['auto', 'knn', 'triangle'][info['deriv_mode']]} (knn deg {info['deriv_degree']} K {K} "
                                     f"on {S} targets)", "levels": info["n_levels"], "plan_ms": info["plan_ms"],
-                           "spread_batches": info["n_batches"], "spread_lane_fill": w.N / max(1, info["n_batches"]) / 32.0},
+                           "spread": "register strips (k_spread_strip)", "spread_items": info["n_batches"]},
                 "phase_ms": ph, "serial_ms_per_step": serial_ms, "wall_ms_per_step": t_wall * 1e3 / args.steps,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk.summary(), "gpu_launches": kern * args.steps,

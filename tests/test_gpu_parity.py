@@ -251,3 +251,26 @@ def test_loose_tolerance_parity():
     idx = configs.sample_targets(w.T, 96, seed=71)
     ref = oracle.workload_potential(w, idx)
     assert rel_l2(V[idx], ref) <= 1e-3
+
+
+@pytest.mark.parametrize("tol", [1e-4, 1e-7, 1e-9, 1e-11, 1e-13])
+def test_strip_spread_matches_tile_spread(tol):
+    """Register-strip spreading (default) vs the shared-memory tile batches (spread_tile=32) on the same plan
+    inputs: same grid, so the history parts agree to rounding.  Mixed density: a uniform background, a dense
+    clump (thousands of nodes in a few NH cells -> strips split into several work items) and nodes along the
+    box edge (footprints wrapping around the periodic grid)."""
+    rng = np.random.default_rng(91)
+    bg = rng.uniform(0.0, 1.0, (3000, 12, 2))
+    clump = 0.5 + 1e-4 * rng.standard_normal((800, 12, 2))
+    edge = np.stack([rng.uniform(0, 1, (200, 12)), rng.choice([0.0, 1.0], (200, 12))], axis=-1)
+    nodes_np = np.concatenate([bg, clump, edge])
+    wts_np = rng.uniform(0.5, 1.5, nodes_np.shape[:2]) / nodes_np.shape[0]
+    f_np = rng.standard_normal(nodes_np.shape[:2])
+    tg_np = rng.uniform(0.0, 1.0, (2000, 2))
+    nodes, wts, tg, f = (torch.from_numpy(np.ascontiguousarray(a)).to(DEV) for a in (nodes_np, wts_np, tg_np, f_np))
+    out = []
+    for st in (0, 32):
+        plan = vp.Plan(nodes, wts, tg, tol, parts=vp.PART_HISTORY, spread_tile=st)
+        out.append(plan.eval(f).cpu().numpy())
+    scale = np.max(np.abs(out[1]))
+    assert np.max(np.abs(out[0] - out[1])) <= 1e-13 * scale
