@@ -436,7 +436,10 @@ void vp_build_levels(vp_plan_s *P, const double *nodes, const double *weights) {
     B.ent_val = vp_alloc<double>(P, B.n_ent);
     VP_CUDA(cudaFreeAsync(exy, s));
   }
-  vp_build_spread_order(P, B.sp, pxy, pw, pnode, B.n_pairs, gb);
+  if (B.sp.det || P->opts.spread_tile > 0)
+    vp_build_spread_order(P, B.sp, pxy, pw, pnode, B.n_pairs, gb);
+  else
+    vp_build_strip_order(P, B.sp, pxy, pw, pnode, B.n_pairs, gb);
   for (void *q : {(void *)cnt, (void *)off, (void *)pxy, (void *)pw, (void *)pnode}) VP_CUDA(cudaFreeAsync(q, s));
   B.lev_par = vp_alloc<double>(P, lp.size());
   VP_CUDA(cudaMemcpyAsync(B.lev_par, lp.data(), sizeof(double) * lp.size(), cudaMemcpyHostToDevice, s));
