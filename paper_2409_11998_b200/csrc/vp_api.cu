@@ -372,6 +372,8 @@ static void make_fft_plans(vp_plan_s *P) {
   VpGrid *gs[2] = {&P->nh, &P->fh};
   for (int g = 0; g < 2; g++) {
     VpGrid &G = *gs[g];
+    vp_fft_setup(P, G);
+    if (G.own_fft) continue;
     long long n[2] = {G.nf, G.nf};
     long long rin[2] = {G.nf, G.row};         // real layout
     long long cin[2] = {G.nf, G.crow / 2};    // complex layout
@@ -387,6 +389,7 @@ static void make_fft_plans(vp_plan_s *P) {
   }
   // separate work areas: the NH and FH transforms run concurrently on different streams
   for (int g = 0; g < 2; g++) {
+    if (!gs[g]->has_plans) continue;
     void *work = vp_alloc<char>(P, std::max(ws[2 * g], ws[2 * g + 1]) + 256);
     VP_CUFFT(cufftSetWorkArea(gs[g]->fwd, work));
     VP_CUFFT(cufftSetWorkArea(gs[g]->inv, work));
@@ -449,6 +452,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     if (o.spread_tile < 0 || o.spread_tile > 64 || (o.spread_tile > 0 && o.spread_tile < 8)) throw VpError{VP_ERR_ARG};
     if (o.interp_tile < 0 || o.interp_tile > 128 || (o.interp_tile > 0 && o.interp_tile < 16)) throw VpError{VP_ERR_ARG};
     if (o.interp_tile > 0) P->TSI = o.interp_tile;
+    if (o.fft_mode < 0 || o.fft_mode > 1) throw VpError{VP_ERR_ARG};
     if (o.boundary.kind == VP_BDRY_CIRCLE && !(o.boundary.p[2] > 0)) throw VpError{VP_ERR_GEOMETRY};
     if (o.boundary.kind == VP_BDRY_RECT && !(o.boundary.p[2] > o.boundary.p[0] && o.boundary.p[3] > o.boundary.p[1]))
       throw VpError{VP_ERR_GEOMETRY};
@@ -578,6 +582,24 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
   return VP_OK;
 }
 
+// the three transform steps of one history grid: fused kernels (vp_fft.cu) or cuFFT + k_multiply
+static void grid_fft_fwd(vp_plan_s *P, VpGrid &G) {
+  if (G.own_fft) return vp_fft_forward(P, G);
+  VP_CUFFT(cufftSetStream(G.fwd, P->stream));
+  VP_CUFFT(cufftExecD2Z(G.fwd, G.data, (cufftDoubleComplex *)G.cdata));
+  P->n_ffts++;
+}
+static void grid_multiply(vp_plan_s *P, VpGrid &G) {
+  if (G.own_fft) return vp_fft_columns(P, G);
+  vp_launch_multiply(P, G);
+}
+static void grid_fft_inv(vp_plan_s *P, VpGrid &G) {
+  if (G.own_fft) return vp_fft_inverse(P, G);
+  VP_CUFFT(cufftSetStream(G.inv, P->stream));
+  VP_CUFFT(cufftExecZ2D(G.inv, (cufftDoubleComplex *)G.cdata, G.data));
+  P->n_ffts++;
+}
+
 static void record(vp_plan_s *P, int i) {
   if (P->profiling) cudaEventRecord(P->ev[i], P->stream);
 }
@@ -604,11 +626,9 @@ static void eval_concurrent(vp_plan_s *P, const double *f, double *out, int part
     VP_CUDA(cudaStreamWaitEvent(P->s_fh, P->ev_fork, 0));
     VP_CUDA(cudaMemsetAsync(P->fh.data, 0, sizeof(double) * P->fh.nf * P->fh.row, P->s_fh));
     vp_launch_restrict(P);
-    VP_CUFFT(cufftSetStream(P->fh.fwd, P->s_fh));
-    VP_CUFFT(cufftSetStream(P->fh.inv, P->s_fh));
-    VP_CUFFT(cufftExecD2Z(P->fh.fwd, P->fh.data, (cufftDoubleComplex *)P->fh.cdata));
-    vp_launch_multiply(P, P->fh);
-    VP_CUFFT(cufftExecZ2D(P->fh.inv, (cufftDoubleComplex *)P->fh.cdata, P->fh.data));
+    grid_fft_fwd(P, P->fh);
+    grid_multiply(P, P->fh);
+    grid_fft_inv(P, P->fh);
     vp_launch_prolong(P, 1);
     VP_CUDA(cudaEventRecord(P->ev_fh, P->s_fh));
   }
@@ -621,13 +641,12 @@ static void eval_concurrent(vp_plan_s *P, const double *f, double *out, int part
     local_forked = true;
   }
   // A: near history, join, interpolation
-  VP_CUFFT(cufftExecD2Z(P->nh.fwd, P->nh.data, (cufftDoubleComplex *)P->nh.cdata));
-  vp_launch_multiply(P, P->nh);
-  VP_CUFFT(cufftExecZ2D(P->nh.inv, (cufftDoubleComplex *)P->nh.cdata, P->nh.data));
+  grid_fft_fwd(P, P->nh);
+  grid_multiply(P, P->nh);
+  grid_fft_inv(P, P->nh);
   VP_CUDA(cudaStreamWaitEvent(A, P->ev_fh, 0));
   vp_launch_prolong(P, 2);
   if (local_forked) VP_CUDA(cudaStreamWaitEvent(A, P->ev_loc, 0));
-  P->n_ffts = 4;
   vp_launch_interp_local(P, f, out, false);
   if (parts & VP_PART_LOCAL) vp_launch_bands(P, f, out);
 }
@@ -648,8 +667,6 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
       eval_concurrent(P, f, out, parts);
       return VP_OK;
     }
-    VP_CUFFT(cufftSetStream(P->fh.fwd, P->stream));
-    VP_CUFFT(cufftSetStream(P->fh.inv, P->stream));
     record(P, 0);
     if (parts & VP_PART_HISTORY) {
       VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, P->stream));
@@ -659,17 +676,16 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
       record(P, 2);
       vp_launch_restrict(P);
       record(P, 3);
-      VP_CUFFT(cufftExecD2Z(P->nh.fwd, P->nh.data, (cufftDoubleComplex *)P->nh.cdata));
-      VP_CUFFT(cufftExecD2Z(P->fh.fwd, P->fh.data, (cufftDoubleComplex *)P->fh.cdata));
+      grid_fft_fwd(P, P->nh);
+      grid_fft_fwd(P, P->fh);
       record(P, 4);
-      vp_launch_multiply(P, P->nh);
-      vp_launch_multiply(P, P->fh);
+      grid_multiply(P, P->nh);
+      grid_multiply(P, P->fh);
       record(P, 5);
-      VP_CUFFT(cufftExecZ2D(P->nh.inv, (cufftDoubleComplex *)P->nh.cdata, P->nh.data));
-      VP_CUFFT(cufftExecZ2D(P->fh.inv, (cufftDoubleComplex *)P->fh.cdata, P->fh.data));
+      grid_fft_inv(P, P->nh);
+      grid_fft_inv(P, P->fh);
       record(P, 6);
       vp_launch_prolong(P, 3);
-      P->n_ffts = 4;
       record(P, 7);
     } else {
       for (int i = 1; i <= 7; i++) record(P, i);

@@ -63,6 +63,12 @@ struct VpGrid {
   double mult_scale = 0;            // h^2 / nf^2 (NH);  h2^2 h1^4 / nf2^2 (FH, two-stage kernel)
   cufftHandle fwd = 0, inv = 0;
   bool has_plans = false;
+  // fused transform (vp_fft.cu): row pass, column pass with the multiply, inverse row pass
+  bool own_fft = false;
+  int fft_ncs = 0, fft_cb = 1;                     // kept columns (nmode/2 + 1), columns per CTA
+  double2 *tw_r = nullptr, *tw_c = nullptr;        // W_{nf/2}^j, W_nf^j
+  int32_t *pos_r = nullptr, *sig_c = nullptr;      // digit-reversal maps (row: frequency -> position)
+  alignas(8) char fft_st_r[160] = {}, fft_st_c[160] = {};  // FftStages (row length nf/2, column length nf)
 };
 
 struct VpTiles {          // sorted points binned into TS x TS tiles of a fine grid
@@ -222,6 +228,10 @@ void vp_launch_tri_local(vp_plan_s *P, const double *f);
 void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out, bool local_kernels);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n);
+void vp_fft_setup(vp_plan_s *P, VpGrid &G);
+void vp_fft_forward(vp_plan_s *P, VpGrid &G);
+void vp_fft_columns(vp_plan_s *P, VpGrid &G);
+void vp_fft_inverse(vp_plan_s *P, VpGrid &G);
 void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const double *weights,
                           const int32_t *node_of, int64_t n, const GridArgs &g);
 void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx,

@@ -274,3 +274,23 @@ def test_strip_spread_matches_tile_spread(tol):
         out.append(plan.eval(f).cpu().numpy())
     scale = np.max(np.abs(out[1]))
     assert np.max(np.abs(out[0] - out[1])) <= 1e-13 * scale
+
+
+@pytest.mark.parametrize("which", ["c1", "c2small", "c2loose"])
+def test_fused_fft_matches_cufft(which):
+    """Fused row/column transforms with the multiply in the column pass (default) vs cuFFT D2Z + k_multiply +
+    Z2D (fft_mode=1) on the same plan inputs: the full V agrees to rounding."""
+    if which == "c1":
+        w, tol = configs.config1(), None
+    elif which == "c2small":
+        w, tol = configs.config2(n=60), None
+    else:
+        w, tol = configs.config2(n=60), 1e-4
+    out = []
+    for mode in (0, 1):
+        kw = {"fft_mode": mode}
+        if tol:
+            kw["tol"] = tol
+        plan, f = make_plan(w, **kw)
+        out.append(plan.eval(f).cpu().numpy())
+    assert np.max(np.abs(out[0] - out[1])) <= 1e-12 * np.max(np.abs(out[1]))
