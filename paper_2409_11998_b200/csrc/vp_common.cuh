@@ -65,10 +65,10 @@ struct VpGrid {
   bool has_plans = false;
   // fused transform (vp_fft.cu): row pass, column pass with the multiply, inverse row pass
   bool own_fft = false;
-  int fft_ncs = 0, fft_cb = 1;                     // kept columns (nmode/2 + 1), columns per CTA
+  int fft_ncs = 0;                                 // kept columns (nmode/2 + 1)
   double2 *tw_r = nullptr, *tw_c = nullptr;        // W_{nf/2}^j, W_nf^j
   int32_t *pos_r = nullptr, *sig_c = nullptr;      // digit-reversal maps (row: frequency -> position)
-  alignas(8) char fft_st_r[160] = {}, fft_st_c[160] = {};  // FftStages (row length nf/2, column length nf)
+  alignas(8) char fft_st_r[256] = {}, fft_st_c[256] = {};  // FftStages (row length nf/2, column length nf)
 };
 
 struct VpTiles {          // sorted points binned into TS x TS tiles of a fine grid

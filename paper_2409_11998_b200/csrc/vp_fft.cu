@@ -27,7 +27,8 @@
 struct FftStages {
   int n, S;
   int r[VP_FFT_MAXS];
-  int Lp[VP_FFT_MAXS];  // L_{s-1}
+  int Lp[VP_FFT_MAXS];      // L_{s-1}
+  float invLp[VP_FFT_MAXS];  // 1 / L_{s-1} (butterfly index split without integer division)
 };
 
 __constant__ double c_dft_c[9][8];  // cos(2 pi j / R), R = 2..8
@@ -40,11 +41,11 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 // in-place R-point DFT, sign DIR (-1 forward, +1 inverse)
 template <int R, int DIR>
 __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
-  if (R == 2) {
+  if constexpr (R == 2) {
     const double2 a = v[0], b = v[1];
     v[0] = make_double2(a.x + b.x, a.y + b.y);
     v[1] = make_double2(a.x - b.x, a.y - b.y);
-  } else if (R == 4) {
+  } else if constexpr (R == 4) {
     const double2 a0 = make_double2(v[0].x + v[2].x, v[0].y + v[2].y);
     const double2 a1 = make_double2(v[0].x - v[2].x, v[0].y - v[2].y);
     const double2 b0 = make_double2(v[1].x + v[3].x, v[1].y + v[3].y);
@@ -55,80 +56,119 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
     v[2] = make_double2(a0.x - b0.x, a0.y - b0.y);
     v[1] = make_double2(a1.x + jb1.x, a1.y + jb1.y);
     v[3] = make_double2(a1.x - jb1.x, a1.y - jb1.y);
-  } else {
+  } else if constexpr (R == 8) {  // two radix-4 halves (even, odd inputs) and W_8^q
+    double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+    dft_small<4, DIR>(e);
+    dft_small<4, DIR>(o);
+    const double h = 0.70710678118654752440;
+    // W_8^q o[q], W_8 = (1 + DIR i) / sqrt 2
+    const double2 o1 = make_double2(h * (o[1].x - DIR * o[1].y), h * (o[1].y + DIR * o[1].x));
+    const double2 o2 = DIR < 0 ? make_double2(o[2].y, -o[2].x) : make_double2(-o[2].y, o[2].x);
+    const double2 o3 = make_double2(h * (-o[3].x - DIR * o[3].y), h * (-o[3].y + DIR * o[3].x));
+    v[0] = make_double2(e[0].x + o[0].x, e[0].y + o[0].y);
+    v[4] = make_double2(e[0].x - o[0].x, e[0].y - o[0].y);
+    v[1] = make_double2(e[1].x + o1.x, e[1].y + o1.y);
+    v[5] = make_double2(e[1].x - o1.x, e[1].y - o1.y);
+    v[2] = make_double2(e[2].x + o2.x, e[2].y + o2.y);
+    v[6] = make_double2(e[2].x - o2.x, e[2].y - o2.y);
+    v[3] = make_double2(e[3].x + o3.x, e[3].y + o3.y);
+    v[7] = make_double2(e[3].x - o3.x, e[3].y - o3.y);
+  } else {  // odd R: pair t with R - t (a_t = v_t + v_{R-t}, b_t = v_t - v_{R-t})
+    constexpr int H = (R - 1) / 2;
+    double2 sa[H], sb[H];
+    double2 o0 = v[0];
+#pragma unroll
+    for (int t = 1; t <= H; t++) {
+      sa[t - 1] = make_double2(v[t].x + v[R - t].x, v[t].y + v[R - t].y);
+      sb[t - 1] = make_double2(v[t].x - v[R - t].x, v[t].y - v[R - t].y);
+      o0.x += sa[t - 1].x;
+      o0.y += sa[t - 1].y;
+    }
     double2 out[R];
+    out[0] = o0;
 #pragma unroll
-    for (int q = 0; q < R; q++) {
-      double2 acc = v[0];
+    for (int q = 1; q <= H; q++) {
+      double2 re = v[0], im = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int t = 1; t < R; t++) {
+      for (int t = 1; t <= H; t++) {
         const int j = (t * q) % R;
-        const double c = c_dft_c[R][j], s = DIR * c_dft_s[R][j];
-        acc.x = fma(v[t].x, c, fma(-v[t].y, s, acc.x));
-        acc.y = fma(v[t].x, s, fma(v[t].y, c, acc.y));
+        const double c = c_dft_c[R][j], sn = c_dft_s[R][j];
+        re.x = fma(sa[t - 1].x, c, re.x);
+        re.y = fma(sa[t - 1].y, c, re.y);
+        im.x = fma(sb[t - 1].x, sn, im.x);
+        im.y = fma(sb[t - 1].y, sn, im.y);
       }
-      out[q] = acc;
+      // out[q] = re + DIR i im, out[R - q] = re - DIR i im
+      out[q] = make_double2(re.x - DIR * im.y, re.y + DIR * im.x);
+      out[R - q] = make_double2(re.x + DIR * im.y, re.y - DIR * im.x);
     }
 #pragma unroll
     for (int q = 0; q < R; q++) v[q] = out[q];
   }
 }
 
-// one stage over `batch` independent transforms of length n stored at a + b n
+// one stage of a length-n transform at a
 template <int R, int DIR, bool DIT>
-__device__ __forceinline__ void fft_stage(double2 *a, int n, int batch, int Lp, const double2 *__restrict__ tw) {
+__device__ __forceinline__ void fft_stage(double2 *a, int n, int Lp, float invLp, const double2 *__restrict__ tw) {
   const int L = Lp * R;
   const int nb = n / R;
   const int tstride = n / L;
-  for (int j = threadIdx.x; j < batch * nb; j += blockDim.x) {
-    const int col = j / nb, jj = j - col * nb;
-    const int b = jj / Lp, k1 = jj - b * Lp;
-    double2 *base = a + (size_t)col * n + b * L + k1;
+  for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+    int b = __float2int_rz((float)j * invLp), k1 = j - b * Lp;
+    if (k1 < 0) {
+      b--;
+      k1 += Lp;
+    } else if (k1 >= Lp) {
+      b++;
+      k1 -= Lp;
+    }
+    double2 *base = a + b * L + k1;
     double2 v[R];
 #pragma unroll
     for (int t = 0; t < R; t++) v[t] = base[t * Lp];
-    if (DIT) {
+    // twiddles W_L^{t k1}: one table load (t = 1), higher powers by multiplication (error ~ t eps)
+    double2 w1 = make_double2(1.0, 0.0);
+    if (k1) {
+      w1 = __ldg(tw + k1 * tstride);
+      if (DIR > 0) w1.y = -w1.y;
+    }
+    if (!DIT) dft_small<R, DIR>(v);
+    if (k1) {
+      double2 w = w1;
 #pragma unroll
       for (int t = 1; t < R; t++) {
-        double2 w = __ldg(tw + t * k1 * tstride);
-        if (DIR > 0) w.y = -w.y;
         v[t] = cmul(v[t], w);
-      }
-      dft_small<R, DIR>(v);
-    } else {
-      dft_small<R, DIR>(v);
-#pragma unroll
-      for (int t = 1; t < R; t++) {
-        double2 w = __ldg(tw + t * k1 * tstride);
-        if (DIR > 0) w.y = -w.y;
-        v[t] = cmul(v[t], w);
+        if (t + 1 < R) w = cmul(w, w1);
       }
     }
+    if (DIT) dft_small<R, DIR>(v);
 #pragma unroll
     for (int t = 0; t < R; t++) base[t * Lp] = v[t];
   }
 }
 
 template <int DIR, bool DIT>
-__device__ void fft_run(double2 *a, const FftStages &st, int batch, const double2 *__restrict__ tw) {
+__device__ void fft_run(double2 *a, const FftStages &st, const double2 *__restrict__ tw) {
   for (int i = 0; i < st.S; i++) {
     const int s = DIT ? i : st.S - 1 - i;
     switch (st.r[s]) {
-      case 2: fft_stage<2, DIR, DIT>(a, st.n, batch, st.Lp[s], tw); break;
-      case 3: fft_stage<3, DIR, DIT>(a, st.n, batch, st.Lp[s], tw); break;
-      case 4: fft_stage<4, DIR, DIT>(a, st.n, batch, st.Lp[s], tw); break;
-      case 5: fft_stage<5, DIR, DIT>(a, st.n, batch, st.Lp[s], tw); break;
-      case 7: fft_stage<7, DIR, DIT>(a, st.n, batch, st.Lp[s], tw); break;
-      case 8: fft_stage<8, DIR, DIT>(a, st.n, batch, st.Lp[s], tw); break;
+      case 2: fft_stage<2, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 3: fft_stage<3, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 4: fft_stage<4, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 5: fft_stage<5, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 7: fft_stage<7, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 8: fft_stage<8, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
       default: break;
     }
     __syncthreads();
   }
 }
 
-// ---- row pass, forward: grid row (real, nf) -> kept half-spectrum columns 0..ncs-1
+// ---- row pass, forward: grid row (real, nf) -> kept half-spectrum columns 0..ncs-1, stored column-major
+// (spec[k nf + row]: the column pass then reads contiguous columns; neighbouring rows' CTAs run together, so
+// their 16-byte writes meet in L2 sectors)
 __global__ void __launch_bounds__(256) k_fft_row_fwd(const double *__restrict__ grid, int64_t row_pitch,
-                                                     double2 *__restrict__ spec, int ncs, FftStages st,
+                                                     double2 *__restrict__ spec, int ncs, int nf, FftStages st,
                                                      const double2 *__restrict__ tw_r,
                                                      const double2 *__restrict__ tw_c,
                                                      const int32_t *__restrict__ pos_r) {
@@ -137,8 +177,8 @@ __global__ void __launch_bounds__(256) k_fft_row_fwd(const double *__restrict__ 
   const double2 *src = (const double2 *)(grid + (int64_t)blockIdx.x * row_pitch);
   for (int i = threadIdx.x; i < nr; i += blockDim.x) a2[i] = src[i];
   __syncthreads();
-  fft_run<-1, false>(a2, st, 1, tw_r);
-  double2 *dst = spec + (int64_t)blockIdx.x * ncs;
+  fft_run<-1, false>(a2, st, tw_r);
+  double2 *dst = spec + blockIdx.x;
   for (int k = threadIdx.x; k < ncs; k += blockDim.x) {
     const double2 zk = a2[pos_r[k % nr]], zm = a2[pos_r[(nr - k) % nr]];
     // Ze = (Z[k] + conj Z[nr-k]) / 2, Zo = -i (Z[k] - conj Z[nr-k]) / 2, X = Ze + W_nf^k Zo
@@ -146,59 +186,53 @@ __global__ void __launch_bounds__(256) k_fft_row_fwd(const double *__restrict__ 
     const double2 zo = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
     const double2 w = __ldg(tw_c + k);  // W_nf^k, k <= nr < nf
     const double2 t = cmul(w, zo);
-    dst[k] = make_double2(ze.x + t.x, ze.y + t.y);
+    dst[(int64_t)k * nf] = make_double2(ze.x + t.x, ze.y + t.y);
   }
 }
 
-// ---- column pass: forward DIF, multiply, inverse DIT on CB kept columns
-__global__ void __launch_bounds__(256) k_fft_col(double2 *__restrict__ spec, int ncs, int CB, FftStages st,
+// ---- column pass: forward DIF, multiply, inverse DIT on one kept column (contiguous in spec)
+__global__ void __launch_bounds__(256) k_fft_col(double2 *__restrict__ spec, FftStages st,
                                                  const double2 *__restrict__ tw_c, const int32_t *__restrict__ sig_c,
                                                  int64_t half_modes, const double *__restrict__ deconv, double dk,
                                                  double scale, int kind, double da, double db) {
   extern __shared__ double2 a2[];
   const int nc = st.n;
-  const int c0 = blockIdx.x * CB;
-  const int cb_n = min(CB, ncs - c0);
-  for (int id = threadIdx.x; id < nc * CB; id += blockDim.x) {
-    const int i = id / CB, cb = id - i * CB;
-    if (cb < cb_n) a2[cb * nc + i] = spec[(int64_t)i * ncs + c0 + cb];
-  }
+  const int64_t m1 = blockIdx.x;
+  double2 *col = spec + m1 * nc;
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) a2[i] = col[i];
   __syncthreads();
-  fft_run<-1, false>(a2, st, cb_n, tw_c);
-  for (int id = threadIdx.x; id < nc * cb_n; id += blockDim.x) {
-    const int cb = id / nc, p = id - cb * nc;
-    const int64_t m1 = c0 + cb;
+  fft_run<-1, false>(a2, st, tw_c);
+  const double d1 = deconv[m1];
+  for (int p = threadIdx.x; p < nc; p += blockDim.x) {
     const int f = sig_c[p];
     const int64_t m2 = f <= nc / 2 ? f : f - nc;
     const int64_t a2m = m2 < 0 ? -m2 : m2;
     double fac = 0.0;
-    if (m1 <= half_modes && a2m <= half_modes) {
+    if (a2m <= half_modes) {
       const double k2 = dk * dk * ((double)m1 * m1 + (double)m2 * m2);
       const double mk = kind == 0 ? vp_mult_nh(k2, da, db) : vp_mult_fh(k2, da, db);
-      fac = mk * scale * deconv[m1] * deconv[a2m];
+      fac = mk * scale * d1 * deconv[a2m];
     }
-    double2 v = a2[cb * nc + p];
-    a2[cb * nc + p] = make_double2(v.x * fac, v.y * fac);
+    const double2 v = a2[p];
+    a2[p] = make_double2(v.x * fac, v.y * fac);
   }
   __syncthreads();
-  fft_run<1, true>(a2, st, cb_n, tw_c);
-  for (int id = threadIdx.x; id < nc * CB; id += blockDim.x) {
-    const int i = id / CB, cb = id - i * CB;
-    if (cb < cb_n) spec[(int64_t)i * ncs + c0 + cb] = a2[cb * nc + i];
-  }
+  fft_run<1, true>(a2, st, tw_c);
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) col[i] = a2[i];
 }
 
 // ---- row pass, inverse: kept half-spectrum columns -> real grid row (unnormalised, as cuFFT Z2D)
-__global__ void __launch_bounds__(256) k_fft_row_inv(const double2 *__restrict__ spec, int ncs, double *__restrict__ grid,
+__global__ void __launch_bounds__(256) k_fft_row_inv(const double2 *__restrict__ spec, int ncs, int nf,
+                                                     double *__restrict__ grid,
                                                      int64_t row_pitch, FftStages st, const double2 *__restrict__ tw_r,
                                                      const double2 *__restrict__ tw_c,
                                                      const int32_t *__restrict__ pos_r) {
   extern __shared__ double2 a2[];
   const int nr = st.n;
-  const double2 *src = spec + (int64_t)blockIdx.x * ncs;
+  const double2 *src = spec + blockIdx.x;
   for (int k = threadIdx.x; k < nr; k += blockDim.x) {
-    const double2 xk = k < ncs ? src[k] : make_double2(0.0, 0.0);
-    const double2 xm = (nr - k) < ncs ? src[nr - k] : make_double2(0.0, 0.0);
+    const double2 xk = k < ncs ? src[(int64_t)k * nf] : make_double2(0.0, 0.0);
+    const double2 xm = (nr - k) < ncs ? src[(int64_t)(nr - k) * nf] : make_double2(0.0, 0.0);
     // Ze = (X[k] + conj X[nr-k]) / 2, Zo = W_nf^{-k} (X[k] - conj X[nr-k]) / 2, Z = Ze + i Zo
     const double2 ze = make_double2(0.5 * (xk.x + xm.x), 0.5 * (xk.y - xm.y));
     double2 w = __ldg(tw_c + k);
@@ -207,7 +241,7 @@ __global__ void __launch_bounds__(256) k_fft_row_inv(const double2 *__restrict__
     a2[pos_r[k]] = make_double2(ze.x - zo.y, ze.y + zo.x);
   }
   __syncthreads();
-  fft_run<1, true>(a2, st, 1, tw_r);
+  fft_run<1, true>(a2, st, tw_r);
   double2 *dst = (double2 *)(grid + (int64_t)blockIdx.x * row_pitch);
   for (int i = threadIdx.x; i < nr; i += blockDim.x) {
     const double2 z = a2[i];
@@ -242,6 +276,7 @@ static bool factor_stages(int n, FftStages &st) {
   for (int s = 0; s < st.S; s++) {
     st.r[s] = rs[s];
     st.Lp[s] = L;
+    st.invLp[s] = 1.0f / (float)L;
     L *= rs[s];
   }
   return true;
@@ -311,22 +346,23 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
   static_assert(sizeof(FftStages) <= sizeof(G.fft_st_r), "stage buffer");
   memcpy(G.fft_st_r, &sr, sizeof(sr));
   memcpy(G.fft_st_c, &sc, sizeof(sc));
-  // columns per CTA: keep two CTAs per SM where the column block fits ~100 KB
-  const size_t col_bytes = sizeof(double2) * (size_t)nf;
-  G.fft_cb = (int)std::max<size_t>(1, std::min<size_t>(4, (100 * 1024) / col_bytes));
-  const size_t sm_c = col_bytes * G.fft_cb, sm_r = sizeof(double2) * (size_t)(nf / 2);
+  const size_t sm_c = sizeof(double2) * (size_t)nf, sm_r = sizeof(double2) * (size_t)(nf / 2);
   VP_CUDA(cudaFuncSetAttribute(k_fft_col, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   VP_CUDA(cudaFuncSetAttribute(k_fft_row_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   VP_CUDA(cudaFuncSetAttribute(k_fft_row_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  for (const void *k : {(const void *)k_fft_col, (const void *)k_fft_row_fwd, (const void *)k_fft_row_inv})
+    VP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   if (sm_c > 227 * 1024 || sm_r > 227 * 1024) return;
   G.own_fft = true;
 }
 
+static int fft_threads(int n) { return n <= 2048 ? 128 : 256; }
+
 void vp_fft_forward(vp_plan_s *P, VpGrid &G) {
   FftStages sr;
   memcpy(&sr, G.fft_st_r, sizeof(sr));
-  k_fft_row_fwd<<<(unsigned)G.nf, 256, sizeof(double2) * (G.nf / 2), P->stream>>>(
-      G.data, G.row, (double2 *)G.cdata, G.fft_ncs, sr, G.tw_r, G.tw_c, G.pos_r);
+  k_fft_row_fwd<<<(unsigned)G.nf, fft_threads(sr.n), sizeof(double2) * (G.nf / 2), P->stream>>>(
+      G.data, G.row, (double2 *)G.cdata, G.fft_ncs, (int)G.nf, sr, G.tw_r, G.tw_c, G.pos_r);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
@@ -334,10 +370,9 @@ void vp_fft_forward(vp_plan_s *P, VpGrid &G) {
 void vp_fft_columns(vp_plan_s *P, VpGrid &G) {
   FftStages sc;
   memcpy(&sc, G.fft_st_c, sizeof(sc));
-  const int nblk = (G.fft_ncs + G.fft_cb - 1) / G.fft_cb;
-  k_fft_col<<<(unsigned)nblk, 256, sizeof(double2) * G.nf * G.fft_cb, P->stream>>>(
-      (double2 *)G.cdata, G.fft_ncs, G.fft_cb, sc, G.tw_c, G.sig_c, G.nmode / 2, G.deconv, 2.0 * VP_PI / G.L,
-      G.mult_scale, G.kind, G.delta_a, G.delta_b);
+  k_fft_col<<<(unsigned)G.fft_ncs, fft_threads(sc.n), sizeof(double2) * G.nf, P->stream>>>(
+      (double2 *)G.cdata, sc, G.tw_c, G.sig_c, G.nmode / 2, G.deconv, 2.0 * VP_PI / G.L, G.mult_scale, G.kind,
+      G.delta_a, G.delta_b);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
@@ -345,8 +380,8 @@ void vp_fft_columns(vp_plan_s *P, VpGrid &G) {
 void vp_fft_inverse(vp_plan_s *P, VpGrid &G) {
   FftStages sr;
   memcpy(&sr, G.fft_st_r, sizeof(sr));
-  k_fft_row_inv<<<(unsigned)G.nf, 256, sizeof(double2) * (G.nf / 2), P->stream>>>(
-      (const double2 *)G.cdata, G.fft_ncs, G.data, G.row, sr, G.tw_r, G.tw_c, G.pos_r);
+  k_fft_row_inv<<<(unsigned)G.nf, fft_threads(sr.n), sizeof(double2) * (G.nf / 2), P->stream>>>(
+      (const double2 *)G.cdata, G.fft_ncs, (int)G.nf, G.data, G.row, sr, G.tw_r, G.tw_c, G.pos_r);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
