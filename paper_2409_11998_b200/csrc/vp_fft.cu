@@ -164,6 +164,24 @@ __device__ void fft_run(double2 *a, const FftStages &st, const double2 *__restri
   }
 }
 
+// copy n double2 from global (stride gs) to shared memory with U loads in flight per thread
+template <int U>
+__device__ __forceinline__ void load_g2s(double2 *dst, const double2 *__restrict__ src, int n, int64_t gs) {
+  for (int i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {
+    double2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int i = i0 + u * blockDim.x;
+      if (i < n) v[u] = src[(int64_t)i * gs];
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int i = i0 + u * blockDim.x;
+      if (i < n) dst[i] = v[u];
+    }
+  }
+}
+
 // ---- row pass, forward: grid row (real, nf) -> kept half-spectrum columns 0..ncs-1, stored column-major
 // (spec[k nf + row]: the column pass then reads contiguous columns; neighbouring rows' CTAs run together, so
 // their 16-byte writes meet in L2 sectors)
@@ -174,8 +192,7 @@ __global__ void __launch_bounds__(256) k_fft_row_fwd(const double *__restrict__ 
                                                      const int32_t *__restrict__ pos_r) {
   extern __shared__ double2 a2[];
   const int nr = st.n;
-  const double2 *src = (const double2 *)(grid + (int64_t)blockIdx.x * row_pitch);
-  for (int i = threadIdx.x; i < nr; i += blockDim.x) a2[i] = src[i];
+  load_g2s<8>(a2, (const double2 *)(grid + (int64_t)blockIdx.x * row_pitch), nr, 1);
   __syncthreads();
   fft_run<-1, false>(a2, st, tw_r);
   double2 *dst = spec + blockIdx.x;
@@ -199,7 +216,7 @@ __global__ void __launch_bounds__(256) k_fft_col(double2 *__restrict__ spec, Fft
   const int nc = st.n;
   const int64_t m1 = blockIdx.x;
   double2 *col = spec + m1 * nc;
-  for (int i = threadIdx.x; i < nc; i += blockDim.x) a2[i] = col[i];
+  load_g2s<8>(a2, col, nc, 1);
   __syncthreads();
   fft_run<-1, false>(a2, st, tw_c);
   const double d1 = deconv[m1];
@@ -229,10 +246,15 @@ __global__ void __launch_bounds__(256) k_fft_row_inv(const double2 *__restrict__
                                                      const int32_t *__restrict__ pos_r) {
   extern __shared__ double2 a2[];
   const int nr = st.n;
-  const double2 *src = spec + blockIdx.x;
+  // stage the kept columns of this row (strided, several loads in flight), zero above
+  const int nk = min(ncs, nr + 1);
+  double2 *xs = a2 + nr;  // nr + 1 scratch entries after the transform buffer
+  load_g2s<8>(xs, spec + blockIdx.x, nk, nf);
+  for (int k = nk + threadIdx.x; k <= nr; k += blockDim.x) xs[k] = make_double2(0.0, 0.0);
+  __syncthreads();
   for (int k = threadIdx.x; k < nr; k += blockDim.x) {
-    const double2 xk = k < ncs ? src[(int64_t)k * nf] : make_double2(0.0, 0.0);
-    const double2 xm = (nr - k) < ncs ? src[(int64_t)(nr - k) * nf] : make_double2(0.0, 0.0);
+    const double2 xk = xs[k];
+    const double2 xm = xs[nr - k];
     // Ze = (X[k] + conj X[nr-k]) / 2, Zo = W_nf^{-k} (X[k] - conj X[nr-k]) / 2, Z = Ze + i Zo
     const double2 ze = make_double2(0.5 * (xk.x + xm.x), 0.5 * (xk.y - xm.y));
     double2 w = __ldg(tw_c + k);
@@ -316,7 +338,9 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
   G.own_fft = false;
   if (P->opts.fft_mode == 1) return;
   const int nf = (int)G.nf;
-  if (nf % 2 || nf > 12800) return;  // column of nf complex values must fit one CTA's shared memory
+  // measured (profiles/r1/probe_fft_*.json): faster than cuFFT + k_multiply for grids up to 2744 (configs 1-2), even at 4000,
+  // slower at 6048-12500 (config 4: few CTAs per SM hold a whole column, load and transform serialise)
+  if (nf % 2 || nf > 3072) return;
   FftStages sr, sc;
   if (!factor_stages(nf / 2, sr) || !factor_stages(nf, sc)) return;
   if (!g_dft_uploaded) {
@@ -346,7 +370,7 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
   static_assert(sizeof(FftStages) <= sizeof(G.fft_st_r), "stage buffer");
   memcpy(G.fft_st_r, &sr, sizeof(sr));
   memcpy(G.fft_st_c, &sc, sizeof(sc));
-  const size_t sm_c = sizeof(double2) * (size_t)nf, sm_r = sizeof(double2) * (size_t)(nf / 2);
+  const size_t sm_c = sizeof(double2) * (size_t)nf, sm_r = sizeof(double2) * (size_t)(nf + 1);
   VP_CUDA(cudaFuncSetAttribute(k_fft_col, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   VP_CUDA(cudaFuncSetAttribute(k_fft_row_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   VP_CUDA(cudaFuncSetAttribute(k_fft_row_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -380,7 +404,7 @@ void vp_fft_columns(vp_plan_s *P, VpGrid &G) {
 void vp_fft_inverse(vp_plan_s *P, VpGrid &G) {
   FftStages sr;
   memcpy(&sr, G.fft_st_r, sizeof(sr));
-  k_fft_row_inv<<<(unsigned)G.nf, fft_threads(sr.n), sizeof(double2) * (G.nf / 2), P->stream>>>(
+  k_fft_row_inv<<<(unsigned)G.nf, fft_threads(sr.n), sizeof(double2) * (G.nf + 1), P->stream>>>(
       (const double2 *)G.cdata, G.fft_ncs, (int)G.nf, G.data, G.row, sr, G.tw_r, G.tw_c, G.pos_r);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
