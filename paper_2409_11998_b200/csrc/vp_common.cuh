@@ -68,6 +68,8 @@ struct VpGrid {
   int fft_ncs = 0;                                 // kept columns (nmode/2 + 1)
   double2 *tw_r = nullptr, *tw_c = nullptr;        // W_{nf/2}^j, W_nf^j
   int32_t *pos_r = nullptr, *sig_c = nullptr;      // digit-reversal maps (row: frequency -> position)
+  double2 *spec2 = nullptr;                        // column-pass output, row-major [nf][ncs]
+  double *fft_mult = nullptr;                      // multiplier table [ncs][nf] in DIF output order
   alignas(8) char fft_st_r[256] = {}, fft_st_c[256] = {};  // FftStages (row length nf/2, column length nf)
 };
 

@@ -207,49 +207,62 @@ __global__ void __launch_bounds__(256) k_fft_row_fwd(const double *__restrict__ 
   }
 }
 
-// ---- column pass: forward DIF, multiply, inverse DIT on one kept column (contiguous in spec)
-__global__ void __launch_bounds__(256) k_fft_col(double2 *__restrict__ spec, FftStages st,
-                                                 const double2 *__restrict__ tw_c, const int32_t *__restrict__ sig_c,
-                                                 int64_t half_modes, const double *__restrict__ deconv, double dk,
-                                                 double scale, int kind, double da, double db) {
+// multiplier of k_multiply (NH or FH kernel, ES deconvolution, trapezoid and 1/nf^2 scale, truncation) for
+// column m1 at DIF output position p (frequency sig_c[p]); tabulated at plan time
+__global__ void k_fft_mult_table(double *__restrict__ tab, int ncs, int nc, const int32_t *__restrict__ sig_c,
+                                 int64_t half_modes, const double *__restrict__ deconv, double dk, double scale,
+                                 int kind, double da, double db) {
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= (int64_t)ncs * nc) return;
+  const int64_t m1 = id / nc;
+  const int p = (int)(id - m1 * nc);
+  const int f = sig_c[p];
+  const int64_t m2 = f <= nc / 2 ? f : f - nc;
+  const int64_t a2m = m2 < 0 ? -m2 : m2;
+  double fac = 0.0;
+  if (m1 <= half_modes && a2m <= half_modes) {
+    const double k2 = dk * dk * ((double)m1 * m1 + (double)m2 * m2);
+    const double mk = kind == 0 ? vp_mult_nh(k2, da, db) : vp_mult_fh(k2, da, db);
+    fac = mk * scale * deconv[m1] * deconv[a2m];
+  }
+  tab[id] = fac;
+}
+
+// ---- column pass: forward DIF, multiply, inverse DIT on one kept column.  Reads the column-major spectrum
+// (contiguous column), writes the result row-major (spec_out[row ncs + m1]; concurrent columns' 16-byte writes
+// meet in L2 sectors) so that the inverse row pass reads contiguous rows.
+__global__ void __launch_bounds__(256) k_fft_col(const double2 *__restrict__ spec, double2 *__restrict__ spec_out,
+                                                 int ncs, FftStages st, const double2 *__restrict__ tw_c,
+                                                 const double *__restrict__ mult) {
   extern __shared__ double2 a2[];
   const int nc = st.n;
   const int64_t m1 = blockIdx.x;
-  double2 *col = spec + m1 * nc;
-  load_g2s<8>(a2, col, nc, 1);
+  load_g2s<8>(a2, spec + m1 * nc, nc, 1);
   __syncthreads();
   fft_run<-1, false>(a2, st, tw_c);
-  const double d1 = deconv[m1];
+  const double *mc = mult + m1 * nc;
   for (int p = threadIdx.x; p < nc; p += blockDim.x) {
-    const int f = sig_c[p];
-    const int64_t m2 = f <= nc / 2 ? f : f - nc;
-    const int64_t a2m = m2 < 0 ? -m2 : m2;
-    double fac = 0.0;
-    if (a2m <= half_modes) {
-      const double k2 = dk * dk * ((double)m1 * m1 + (double)m2 * m2);
-      const double mk = kind == 0 ? vp_mult_nh(k2, da, db) : vp_mult_fh(k2, da, db);
-      fac = mk * scale * d1 * deconv[a2m];
-    }
+    const double fac = __ldg(mc + p);
     const double2 v = a2[p];
     a2[p] = make_double2(v.x * fac, v.y * fac);
   }
   __syncthreads();
   fft_run<1, true>(a2, st, tw_c);
-  for (int i = threadIdx.x; i < nc; i += blockDim.x) col[i] = a2[i];
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) spec_out[(int64_t)i * ncs + m1] = a2[i];
 }
 
-// ---- row pass, inverse: kept half-spectrum columns -> real grid row (unnormalised, as cuFFT Z2D)
-__global__ void __launch_bounds__(256) k_fft_row_inv(const double2 *__restrict__ spec, int ncs, int nf,
+// ---- row pass, inverse: kept half-spectrum columns (row-major) -> real grid row (unnormalised, as cuFFT Z2D)
+__global__ void __launch_bounds__(256) k_fft_row_inv(const double2 *__restrict__ spec, int ncs,
                                                      double *__restrict__ grid,
                                                      int64_t row_pitch, FftStages st, const double2 *__restrict__ tw_r,
                                                      const double2 *__restrict__ tw_c,
                                                      const int32_t *__restrict__ pos_r) {
   extern __shared__ double2 a2[];
   const int nr = st.n;
-  // stage the kept columns of this row (strided, several loads in flight), zero above
+  // stage the kept columns of this row, zero above
   const int nk = min(ncs, nr + 1);
   double2 *xs = a2 + nr;  // nr + 1 scratch entries after the transform buffer
-  load_g2s<8>(xs, spec + blockIdx.x, nk, nf);
+  load_g2s<8>(xs, spec + (int64_t)blockIdx.x * ncs, nk, 1);
   for (int k = nk + threadIdx.x; k <= nr; k += blockDim.x) xs[k] = make_double2(0.0, 0.0);
   __syncthreads();
   for (int k = threadIdx.x; k < nr; k += blockDim.x) {
@@ -377,6 +390,14 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
   for (const void *k : {(const void *)k_fft_col, (const void *)k_fft_row_fwd, (const void *)k_fft_row_inv})
     VP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   if (sm_c > 227 * 1024 || sm_r > 227 * 1024) return;
+  // second spectrum buffer (row-major column-pass output) and the multiplier table (in DIF output order)
+  G.spec2 = vp_alloc<double2>(P, (size_t)G.fft_ncs * nf);
+  G.fft_mult = vp_alloc<double>(P, (size_t)G.fft_ncs * nf);
+  const int64_t nt = (int64_t)G.fft_ncs * nf;
+  k_fft_mult_table<<<(unsigned)((nt + 255) / 256), 256, 0, P->stream>>>(G.fft_mult, G.fft_ncs, nf, G.sig_c,
+                                                                        G.nmode / 2, G.deconv, 2.0 * VP_PI / G.L,
+                                                                        G.mult_scale, G.kind, G.delta_a, G.delta_b);
+  VP_CHECK_LAUNCH();
   G.own_fft = true;
 }
 
@@ -395,8 +416,7 @@ void vp_fft_columns(vp_plan_s *P, VpGrid &G) {
   FftStages sc;
   memcpy(&sc, G.fft_st_c, sizeof(sc));
   k_fft_col<<<(unsigned)G.fft_ncs, fft_threads(sc.n), sizeof(double2) * G.nf, P->stream>>>(
-      (double2 *)G.cdata, sc, G.tw_c, G.sig_c, G.nmode / 2, G.deconv, 2.0 * VP_PI / G.L, G.mult_scale, G.kind,
-      G.delta_a, G.delta_b);
+      (const double2 *)G.cdata, G.spec2, G.fft_ncs, sc, G.tw_c, G.fft_mult);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
@@ -405,7 +425,7 @@ void vp_fft_inverse(vp_plan_s *P, VpGrid &G) {
   FftStages sr;
   memcpy(&sr, G.fft_st_r, sizeof(sr));
   k_fft_row_inv<<<(unsigned)G.nf, fft_threads(sr.n), sizeof(double2) * (G.nf + 1), P->stream>>>(
-      (const double2 *)G.cdata, G.fft_ncs, (int)G.nf, G.data, G.row, sr, G.tw_r, G.tw_c, G.pos_r);
+      G.spec2, G.fft_ncs, G.data, G.row, sr, G.tw_r, G.tw_c, G.pos_r);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
