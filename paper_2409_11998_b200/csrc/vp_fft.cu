@@ -353,7 +353,7 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
   const int nf = (int)G.nf;
   // measured (profiles/r1/probe_fft_*.json): faster than cuFFT + k_multiply for grids up to 2744 (configs 1-2), even at 4000,
   // slower at 6048-12500 (config 4: few CTAs per SM hold a whole column, load and transform serialise)
-  if (nf % 2 || nf > 3072) return;
+  if (nf % 2 || nf > 6400) return;
   FftStages sr, sc;
   if (!factor_stages(nf / 2, sr) || !factor_stages(nf, sc)) return;
   if (!g_dft_uploaded) {
