@@ -19,6 +19,8 @@
 #include <cmath>
 #include <vector>
 
+#include <cuda_pipeline.h>
+
 #include "vp_common.cuh"
 #include "vp_math.cuh"
 
@@ -109,7 +111,7 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
 
 // one stage of a length-n transform at a
 template <int R, int DIR, bool DIT>
-__device__ __forceinline__ void fft_stage(double2 *a, int n, int Lp, float invLp, const double2 *__restrict__ tw) {
+__device__ __forceinline__ void fft_stage(double2 *a, int n, int Lp, float invLp, const double2 *tw) {
   const int L = Lp * R;
   const int nb = n / R;
   const int tstride = n / L;
@@ -129,7 +131,7 @@ __device__ __forceinline__ void fft_stage(double2 *a, int n, int Lp, float invLp
     // twiddles W_L^{t k1}: one table load (t = 1), higher powers by multiplication (error ~ t eps)
     double2 w1 = make_double2(1.0, 0.0);
     if (k1) {
-      w1 = __ldg(tw + k1 * tstride);
+      w1 = tw[k1 * tstride];  // shared-memory or global table
       if (DIR > 0) w1.y = -w1.y;
     }
     if (!DIT) dft_small<R, DIR>(v);
@@ -148,7 +150,7 @@ __device__ __forceinline__ void fft_stage(double2 *a, int n, int Lp, float invLp
 }
 
 template <int DIR, bool DIT>
-__device__ void fft_run(double2 *a, const FftStages &st, const double2 *__restrict__ tw) {
+__device__ void fft_run(double2 *a, const FftStages &st, const double2 *tw) {
   for (int i = 0; i < st.S; i++) {
     const int s = DIT ? i : st.S - 1 - i;
     switch (st.r[s]) {
@@ -182,28 +184,50 @@ __device__ __forceinline__ void load_g2s(double2 *dst, const double2 *__restrict
   }
 }
 
-// ---- row pass, forward: grid row (real, nf) -> kept half-spectrum columns 0..ncs-1, stored column-major
-// (spec[k nf + row]: the column pass then reads contiguous columns; neighbouring rows' CTAs run together, so
-// their 16-byte writes meet in L2 sectors)
+// asynchronous copy of n double2 (16-byte aligned, contiguous) global -> shared (cp.async, 16 B per thread-op)
+__device__ __forceinline__ void prefetch_g2s(double2 *dst, const double2 *src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) __pipeline_memcpy_async(dst + i, src + i, sizeof(double2));
+}
+
+// ---- row pass, forward: grid rows (real, nf) -> kept half-spectrum columns 0..ncs-1, stored column-major
+// (spec[k nf + row]: the column pass then reads contiguous columns; concurrent rows' 16-byte writes meet in
+// L2 sectors).  Persistent CTAs: the row twiddles and the digit-reversal map are staged once, and the next
+// row is prefetched (cp.async) into a second buffer while the current one is transformed.
 __global__ void __launch_bounds__(256) k_fft_row_fwd(const double *__restrict__ grid, int64_t row_pitch,
                                                      double2 *__restrict__ spec, int ncs, int nf, FftStages st,
                                                      const double2 *__restrict__ tw_r,
                                                      const double2 *__restrict__ tw_c,
                                                      const int32_t *__restrict__ pos_r) {
-  extern __shared__ double2 a2[];
+  extern __shared__ double2 sm2[];
   const int nr = st.n;
-  load_g2s<8>(a2, (const double2 *)(grid + (int64_t)blockIdx.x * row_pitch), nr, 1);
-  __syncthreads();
-  fft_run<-1, false>(a2, st, tw_r);
-  double2 *dst = spec + blockIdx.x;
-  for (int k = threadIdx.x; k < ncs; k += blockDim.x) {
-    const double2 zk = a2[pos_r[k % nr]], zm = a2[pos_r[(nr - k) % nr]];
-    // Ze = (Z[k] + conj Z[nr-k]) / 2, Zo = -i (Z[k] - conj Z[nr-k]) / 2, X = Ze + W_nf^k Zo
-    const double2 ze = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-    const double2 zo = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
-    const double2 w = __ldg(tw_c + k);  // W_nf^k, k <= nr < nf
-    const double2 t = cmul(w, zo);
-    dst[(int64_t)k * nf] = make_double2(ze.x + t.x, ze.y + t.y);
+  double2 *twr = sm2, *buf0 = sm2 + nr, *buf1 = sm2 + 2 * nr;
+  int *pos = (int *)(sm2 + 3 * nr);
+  for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+    twr[i] = tw_r[i];
+    pos[i] = pos_r[i];
+  }
+  int r = blockIdx.x;
+  if (r < nf) prefetch_g2s(buf0, (const double2 *)(grid + (int64_t)r * row_pitch), nr);
+  __pipeline_commit();
+  for (int cur = 0; r < nf; r += gridDim.x, cur ^= 1) {
+    double2 *a2 = cur ? buf1 : buf0;
+    const int rn = r + gridDim.x;
+    if (rn < nf) prefetch_g2s(cur ? buf0 : buf1, (const double2 *)(grid + (int64_t)rn * row_pitch), nr);
+    __pipeline_commit();
+    __pipeline_wait_prior(1);
+    __syncthreads();
+    fft_run<-1, false>(a2, st, twr);
+    double2 *dst = spec + r;
+    for (int k = threadIdx.x; k < ncs; k += blockDim.x) {
+      const double2 zk = a2[pos[k % nr]], zm = a2[pos[(nr - k) % nr]];
+      // Ze = (Z[k] + conj Z[nr-k]) / 2, Zo = -i (Z[k] - conj Z[nr-k]) / 2, X = Ze + W_nf^k Zo
+      const double2 ze = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+      const double2 zo = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+      const double2 w = __ldg(tw_c + k);  // W_nf^k, k <= nr < nf
+      const double2 t = cmul(w, zo);
+      dst[(int64_t)k * nf] = make_double2(ze.x + t.x, ze.y + t.y);
+    }
+    __syncthreads();  // buffer a2 is refilled in the next iteration's prefetch of row rn + gridDim.x
   }
 }
 
@@ -251,36 +275,51 @@ __global__ void __launch_bounds__(256) k_fft_col(const double2 *__restrict__ spe
   for (int i = threadIdx.x; i < nc; i += blockDim.x) spec_out[(int64_t)i * ncs + m1] = a2[i];
 }
 
-// ---- row pass, inverse: kept half-spectrum columns (row-major) -> real grid row (unnormalised, as cuFFT Z2D)
-__global__ void __launch_bounds__(256) k_fft_row_inv(const double2 *__restrict__ spec, int ncs,
+// ---- row pass, inverse: kept half-spectrum columns (row-major) -> real grid rows (unnormalised, as cuFFT
+// Z2D).  Persistent CTAs with staged row twiddles / digit-reversal map and a prefetched next spectrum row.
+__global__ void __launch_bounds__(256) k_fft_row_inv(const double2 *__restrict__ spec, int ncs, int nf,
                                                      double *__restrict__ grid,
                                                      int64_t row_pitch, FftStages st, const double2 *__restrict__ tw_r,
                                                      const double2 *__restrict__ tw_c,
                                                      const int32_t *__restrict__ pos_r) {
-  extern __shared__ double2 a2[];
+  extern __shared__ double2 sm2[];
   const int nr = st.n;
-  // stage the kept columns of this row, zero above
   const int nk = min(ncs, nr + 1);
-  double2 *xs = a2 + nr;  // nr + 1 scratch entries after the transform buffer
-  load_g2s<8>(xs, spec + (int64_t)blockIdx.x * ncs, nk, 1);
-  for (int k = nk + threadIdx.x; k <= nr; k += blockDim.x) xs[k] = make_double2(0.0, 0.0);
-  __syncthreads();
-  for (int k = threadIdx.x; k < nr; k += blockDim.x) {
-    const double2 xk = xs[k];
-    const double2 xm = xs[nr - k];
-    // Ze = (X[k] + conj X[nr-k]) / 2, Zo = W_nf^{-k} (X[k] - conj X[nr-k]) / 2, Z = Ze + i Zo
-    const double2 ze = make_double2(0.5 * (xk.x + xm.x), 0.5 * (xk.y - xm.y));
-    double2 w = __ldg(tw_c + k);
-    w.y = -w.y;
-    const double2 zo = cmul(w, make_double2(0.5 * (xk.x - xm.x), 0.5 * (xk.y + xm.y)));
-    a2[pos_r[k]] = make_double2(ze.x - zo.y, ze.y + zo.x);
-  }
-  __syncthreads();
-  fft_run<1, true>(a2, st, tw_r);
-  double2 *dst = (double2 *)(grid + (int64_t)blockIdx.x * row_pitch);
+  const int nkp = (nk + 1) & ~1;
+  double2 *twr = sm2, *a2 = sm2 + nr, *xs0 = sm2 + 2 * nr, *xs1 = xs0 + nkp;
+  int *pos = (int *)(xs1 + nkp);
   for (int i = threadIdx.x; i < nr; i += blockDim.x) {
-    const double2 z = a2[i];
-    dst[i] = make_double2(2.0 * z.x, 2.0 * z.y);
+    twr[i] = tw_r[i];
+    pos[i] = pos_r[i];
+  }
+  int r = blockIdx.x;
+  if (r < nf) prefetch_g2s(xs0, spec + (int64_t)r * ncs, nk);
+  __pipeline_commit();
+  for (int cur = 0; r < nf; r += gridDim.x, cur ^= 1) {
+    const double2 *xs = cur ? xs1 : xs0;
+    const int rn = r + gridDim.x;
+    if (rn < nf) prefetch_g2s(cur ? xs0 : xs1, spec + (int64_t)rn * ncs, nk);
+    __pipeline_commit();
+    __pipeline_wait_prior(1);
+    __syncthreads();
+    for (int k = threadIdx.x; k < nr; k += blockDim.x) {
+      const double2 xk = k < nk ? xs[k] : make_double2(0.0, 0.0);
+      const double2 xm = (nr - k) < nk ? xs[nr - k] : make_double2(0.0, 0.0);
+      // Ze = (X[k] + conj X[nr-k]) / 2, Zo = W_nf^{-k} (X[k] - conj X[nr-k]) / 2, Z = Ze + i Zo
+      const double2 ze = make_double2(0.5 * (xk.x + xm.x), 0.5 * (xk.y - xm.y));
+      double2 w = __ldg(tw_c + k);
+      w.y = -w.y;
+      const double2 zo = cmul(w, make_double2(0.5 * (xk.x - xm.x), 0.5 * (xk.y + xm.y)));
+      a2[pos[k]] = make_double2(ze.x - zo.y, ze.y + zo.x);
+    }
+    __syncthreads();
+    fft_run<1, true>(a2, st, twr);
+    double2 *dst = (double2 *)(grid + (int64_t)r * row_pitch);
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+      const double2 z = a2[i];
+      dst[i] = make_double2(2.0 * z.x, 2.0 * z.y);
+    }
+    __syncthreads();
   }
 }
 
@@ -344,6 +383,15 @@ static double2 *twiddle_table(vp_plan_s *P, int n) {
   return d;
 }
 
+// shared memory of the persistent row kernels: twiddles + 2 buffers (forward) / twiddles + transform buffer +
+// 2 staged spectrum rows (inverse), plus the digit-reversal map; the larger of the two
+static size_t fft_row_smem(int nr, int ncs) {
+  const int nk = std::min(ncs, nr + 1), nkp = (nk + 1) & ~1;
+  const size_t fwd = sizeof(double2) * 3 * (size_t)nr + sizeof(int) * nr;
+  const size_t inv = sizeof(double2) * (2 * (size_t)nr + 2 * (size_t)nkp) + sizeof(int) * nr;
+  return std::max(fwd, inv);
+}
+
 static bool g_dft_uploaded = false;
 
 // decide and build the fused transform for grid G (opts.fft_mode 0: where it fits shared memory)
@@ -383,7 +431,7 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
   static_assert(sizeof(FftStages) <= sizeof(G.fft_st_r), "stage buffer");
   memcpy(G.fft_st_r, &sr, sizeof(sr));
   memcpy(G.fft_st_c, &sc, sizeof(sc));
-  const size_t sm_c = sizeof(double2) * (size_t)nf, sm_r = sizeof(double2) * (size_t)(nf + 1);
+  const size_t sm_c = sizeof(double2) * (size_t)nf, sm_r = fft_row_smem(nf / 2, G.fft_ncs);
   VP_CUDA(cudaFuncSetAttribute(k_fft_col, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   VP_CUDA(cudaFuncSetAttribute(k_fft_row_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   VP_CUDA(cudaFuncSetAttribute(k_fft_row_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -403,10 +451,27 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
 
 static int fft_threads(int n) { return n <= 2048 ? 128 : 256; }
 
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    VP_CUDA(cudaGetDevice(&dev));
+    VP_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return g_num_sms;
+}
+// persistent row kernels: CTAs per SM that the shared memory (227 KB) allows, at most 4
+static unsigned row_grid(size_t smem, int64_t rows) {
+  int per = (int)std::min<size_t>(4, (227 * 1024) / (smem + 1024));
+  if (per < 1) per = 1;
+  return (unsigned)std::min<int64_t>(rows, (int64_t)per * num_sms());
+}
+
 void vp_fft_forward(vp_plan_s *P, VpGrid &G) {
   FftStages sr;
   memcpy(&sr, G.fft_st_r, sizeof(sr));
-  k_fft_row_fwd<<<(unsigned)G.nf, fft_threads(sr.n), sizeof(double2) * (G.nf / 2), P->stream>>>(
+  const size_t sm = fft_row_smem(sr.n, G.fft_ncs);
+  k_fft_row_fwd<<<row_grid(sm, G.nf), 256, sm, P->stream>>>(
       G.data, G.row, (double2 *)G.cdata, G.fft_ncs, (int)G.nf, sr, G.tw_r, G.tw_c, G.pos_r);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
@@ -424,8 +489,9 @@ void vp_fft_columns(vp_plan_s *P, VpGrid &G) {
 void vp_fft_inverse(vp_plan_s *P, VpGrid &G) {
   FftStages sr;
   memcpy(&sr, G.fft_st_r, sizeof(sr));
-  k_fft_row_inv<<<(unsigned)G.nf, fft_threads(sr.n), sizeof(double2) * (G.nf + 1), P->stream>>>(
-      G.spec2, G.fft_ncs, G.data, G.row, sr, G.tw_r, G.tw_c, G.pos_r);
+  const size_t sm = fft_row_smem(sr.n, G.fft_ncs);
+  k_fft_row_inv<<<row_grid(sm, G.nf), 256, sm, P->stream>>>(G.spec2, G.fft_ncs, (int)G.nf, G.data, G.row, sr, G.tw_r,
+                                                              G.tw_c, G.pos_r);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
