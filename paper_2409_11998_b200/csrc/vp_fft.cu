@@ -252,27 +252,38 @@ __global__ void k_fft_mult_table(double *__restrict__ tab, int ncs, int nc, cons
   tab[id] = fac;
 }
 
-// ---- column pass: forward DIF, multiply, inverse DIT on one kept column.  Reads the column-major spectrum
-// (contiguous column), writes the result row-major (spec_out[row ncs + m1]; concurrent columns' 16-byte writes
-// meet in L2 sectors) so that the inverse row pass reads contiguous rows.
+// ---- column pass: forward DIF, multiply, inverse DIT on kept columns.  Reads the column-major spectrum
+// (contiguous columns), writes the result row-major (spec_out[row ncs + m1]; concurrent columns' 16-byte writes
+// meet in L2 sectors) so that the inverse row pass reads contiguous rows.  Persistent CTAs, next column
+// prefetched (cp.async) while the current one is transformed.
 __global__ void __launch_bounds__(256) k_fft_col(const double2 *__restrict__ spec, double2 *__restrict__ spec_out,
                                                  int ncs, FftStages st, const double2 *__restrict__ tw_c,
                                                  const double *__restrict__ mult) {
-  extern __shared__ double2 a2[];
+  extern __shared__ double2 sm2[];
   const int nc = st.n;
-  const int64_t m1 = blockIdx.x;
-  load_g2s<8>(a2, spec + m1 * nc, nc, 1);
-  __syncthreads();
-  fft_run<-1, false>(a2, st, tw_c);
-  const double *mc = mult + m1 * nc;
-  for (int p = threadIdx.x; p < nc; p += blockDim.x) {
-    const double fac = __ldg(mc + p);
-    const double2 v = a2[p];
-    a2[p] = make_double2(v.x * fac, v.y * fac);
+  double2 *buf0 = sm2, *buf1 = sm2 + nc;
+  int m1 = blockIdx.x;
+  if (m1 < ncs) prefetch_g2s(buf0, spec + (int64_t)m1 * nc, nc);
+  __pipeline_commit();
+  for (int cur = 0; m1 < ncs; m1 += gridDim.x, cur ^= 1) {
+    double2 *a2 = cur ? buf1 : buf0;
+    const int mn = m1 + gridDim.x;
+    if (mn < ncs) prefetch_g2s(cur ? buf0 : buf1, spec + (int64_t)mn * nc, nc);
+    __pipeline_commit();
+    __pipeline_wait_prior(1);
+    __syncthreads();
+    fft_run<-1, false>(a2, st, tw_c);
+    const double *mc = mult + (int64_t)m1 * nc;
+    for (int p = threadIdx.x; p < nc; p += blockDim.x) {
+      const double fac = __ldg(mc + p);
+      const double2 v = a2[p];
+      a2[p] = make_double2(v.x * fac, v.y * fac);
+    }
+    __syncthreads();
+    fft_run<1, true>(a2, st, tw_c);
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) spec_out[(int64_t)i * ncs + m1] = a2[i];
+    __syncthreads();
   }
-  __syncthreads();
-  fft_run<1, true>(a2, st, tw_c);
-  for (int i = threadIdx.x; i < nc; i += blockDim.x) spec_out[(int64_t)i * ncs + m1] = a2[i];
 }
 
 // ---- row pass, inverse: kept half-spectrum columns (row-major) -> real grid rows (unnormalised, as cuFFT
@@ -431,7 +442,7 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
   static_assert(sizeof(FftStages) <= sizeof(G.fft_st_r), "stage buffer");
   memcpy(G.fft_st_r, &sr, sizeof(sr));
   memcpy(G.fft_st_c, &sc, sizeof(sc));
-  const size_t sm_c = sizeof(double2) * (size_t)nf, sm_r = fft_row_smem(nf / 2, G.fft_ncs);
+  const size_t sm_c = 2 * sizeof(double2) * (size_t)nf, sm_r = fft_row_smem(nf / 2, G.fft_ncs);
   VP_CUDA(cudaFuncSetAttribute(k_fft_col, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   VP_CUDA(cudaFuncSetAttribute(k_fft_row_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   VP_CUDA(cudaFuncSetAttribute(k_fft_row_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -480,7 +491,8 @@ void vp_fft_forward(vp_plan_s *P, VpGrid &G) {
 void vp_fft_columns(vp_plan_s *P, VpGrid &G) {
   FftStages sc;
   memcpy(&sc, G.fft_st_c, sizeof(sc));
-  k_fft_col<<<(unsigned)G.fft_ncs, fft_threads(sc.n), sizeof(double2) * G.nf, P->stream>>>(
+  const size_t sm = 2 * sizeof(double2) * G.nf;
+  k_fft_col<<<row_grid(sm, G.fft_ncs), 256, sm, P->stream>>>(
       (const double2 *)G.cdata, G.spec2, G.fft_ncs, sc, G.tw_c, G.fft_mult);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
