@@ -99,7 +99,7 @@ typedef struct {
   int32_t spread_tile;
   int32_t interp_tile;
   /* transforms: 0 -> fused row/column FFT with the spectral multiply in the column pass (vp_fft.cu) for
-   * grids with nf <= 3072, cuFFT D2Z + multiply + Z2D otherwise; 1 -> cuFFT for every grid */
+   * grids with nf <= 6400, cuFFT D2Z + multiply + Z2D otherwise; 1 -> cuFFT for every grid */
   int32_t fft_mode;
 } vp_opts;
 
