@@ -410,8 +410,8 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
   G.own_fft = false;
   if (P->opts.fft_mode == 1) return;
   const int nf = (int)G.nf;
-  // measured (profiles/r1/probe_fft_*.json): faster than cuFFT + k_multiply for grids up to 2744 (configs 1-2), even at 4000,
-  // slower at 6048-12500 (config 4: few CTAs per SM hold a whole column, load and transform serialise)
+  // measured (profiles/r1/probe_fft_*.json): faster than cuFFT + k_multiply up to 6048 (configs 1-2, FH grids of
+  // configs 3-4), slower at 12500 (one column fills a CTA's shared memory; load and transform serialise)
   if (nf % 2 || nf > 6400) return;
   FftStages sr, sc;
   if (!factor_stages(nf / 2, sr) || !factor_stages(nf, sc)) return;
