@@ -197,6 +197,8 @@ def main():
     ap.add_argument("--cpu-targets", type=int, default=96)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline sample sized to ~this many seconds")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch", type=int, default=4,
+                    help="also time vp_eval_batch with this many fields (SURVEY §8(f) f3); 0 or 1 to skip")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -307,6 +309,28 @@ def main():
     e2e = {"value": aggregate_rate(world, pts, e2e_max), "unit": "pts/s", "h2d_bytes_per_step": 8 * w.N,
            "d2h_bytes_per_step": 8 * w.T, "ms_per_step": e2e_max}
 
+    # ---- batched fields (vp_eval_batch): K scaled copies of f, same plan; device-timed like the steps
+    batch = None
+    if args.batch and args.batch > 1:
+        K = args.batch
+        F = torch.stack([f * (1.0 + 0.25 * k) for k in range(K)]).contiguous()
+        OB = torch.empty(K, w.T, dtype=torch.float64, device=dev)
+        plan.eval_batch(F, OB)
+        bms = []
+        for s in range(max(3, args.steps // 2)):
+            flush.zero_()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            b0.record(stream)
+            plan.eval_batch(F, OB)
+            b1.record(stream)
+            torch.cuda.synchronize()
+            bms.append(b0.elapsed_time(b1))
+        bmax = max_over_ranks(float(np.mean(bms)), dev)
+        batch = {"K": K, "ms_per_batch": bmax, "value": aggregate_rate(world, K * pts, bmax), "unit": "pts/s",
+                 "note": "K fields per vp_eval_batch; value counts K * (N_src + N_tgt) points"}
+        del F, OB
+
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
@@ -323,7 +347,7 @@ def main():
                                     f"on {S} targets)", "levels": info["n_levels"], "plan_ms": info["plan_ms"],
                            "spread": "register strips (k_spread_strip)", "spread_items": info["n_batches"]},
                 "phase_ms": ph, "serial_ms_per_step": serial_ms, "wall_ms_per_step": t_wall * 1e3 / args.steps,
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "batch": batch,
                 "clocks": clk.summary(), "gpu_launches": kern * args.steps,
                 "cufft_execs": ffts * args.steps}
         print(json.dumps(line))

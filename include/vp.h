@@ -161,6 +161,19 @@ vp_status vp_eval(vp_handle plan, const double *f, double *out);
  * synchronises.  Pinned host memory is recommended. */
 vp_status vp_eval_host(vp_handle plan, const double *f_host, double *out_host);
 
+/* Evaluate K fields on the same plan ("batched multi-f vp_eval"; PAPER.md Steps 2-4,
+ * lines 848-850, are linear in the strengths c_j = f_j w_j).
+ *   K    number of fields, >= 1
+ *   f    [K][M][p] fp64 source values (device, read only), field k at f + k M p
+ *   out  [K][T]    fp64 (device), field k at out + k T, fully overwritten
+ * The spreading of up to four fields shares one pass over the sorted nodes (geometry, ES weights and their
+ * shared-memory broadcasts are computed once per node); transforms, interpolation and the local part run per
+ * field.  The first call with a given K allocates K-1 extra NH grids (and K spreading-order copies of f for
+ * KNN stencils), owned by the plan.  Same stream and concurrency rules as vp_eval; serial schedule.
+ * Errors: VP_ERR_ARG (null pointer, K < 1), VP_ERR_OOM (extra grids beyond the device), VP_ERR_UNSUPPORTED
+ * (deterministic mode or spread_tile > 0, which use the tile-batch spreading), VP_ERR_CUDA / VP_ERR_CUFFT. */
+vp_status vp_eval_batch(vp_handle plan, int32_t K, const double *f, double *out);
+
 /* Release all device memory and cuFFT plans owned by the plan.  NULL is accepted. */
 vp_status vp_destroy(vp_handle plan);
 

@@ -22,7 +22,7 @@ BDRY = {None: 0, "none": 0, "circle": 1, "rect": 2}
 DERIV = {"auto": 0, "knn": 1, "triangle": 2}
 PART_HISTORY, PART_LOCAL, PART_ALL = 1, 2, 3
 
-EXPORTED = ["vp_plan", "vp_eval", "vp_eval_host", "vp_destroy", "vp_strerror", "vp_get_info", "vp_set_profiling",
+EXPORTED = ["vp_plan", "vp_eval", "vp_eval_host", "vp_eval_batch", "vp_destroy", "vp_strerror", "vp_get_info", "vp_set_profiling",
             "vp_get_phase_times", "vp_eval_launch_count", "vp_check_finite", "vp_last_error_detail", "vp_version"]
 
 
@@ -76,6 +76,7 @@ def lib():
         L.vp_plan.argtypes = [vp, vp, i64, i32, vp, i64, d, ctypes.POINTER(VpOpts), ctypes.POINTER(vp)]
         L.vp_eval.argtypes = [vp, vp, vp]
         L.vp_eval_host.argtypes = [vp, vp, vp]
+        L.vp_eval_batch.argtypes = [vp, i32, vp, vp]
         L.vp_destroy.argtypes = [vp]
         L.vp_strerror.argtypes = [ctypes.c_int]
         L.vp_strerror.restype = ctypes.c_char_p
@@ -171,6 +172,18 @@ class Plan:
         if out is None:
             out = torch.empty(self.T, dtype=torch.float64, device=f.device)
         _check(lib().vp_eval(self.h, f.data_ptr(), out.data_ptr()), "vp_eval")
+        return out
+
+    def eval_batch(self, F, out=None):
+        """K fields at once (C ABI vp_eval_batch): F [K, M, p] or [K, M*p] device fp64 -> [K, T]."""
+        import torch
+        F = _dev_f64(F)
+        if F.numel() % self.N:
+            raise ValueError("F must hold K x M*p entries")
+        K = F.numel() // self.N
+        if out is None:
+            out = torch.empty(K, self.T, dtype=torch.float64, device=F.device)
+        _check(lib().vp_eval_batch(self.h, K, F.data_ptr(), out.data_ptr()), "vp_eval_batch")
         return out
 
     def eval_host(self, f_host, out_host=None):

@@ -701,6 +701,64 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
   return VP_OK;
 }
 
+extern "C" vp_status vp_eval_batch(vp_handle P, int32_t K, const double *f, double *out) {
+  if (!P || !f || !out || K < 1) return VP_ERR_ARG;
+  if (K == 1) return vp_eval(P, f, out);
+  try {
+    if (!P->sp.strip) throw VpError{VP_ERR_UNSUPPORTED};
+    const int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
+    const size_t gcells = (size_t)P->nh.nf * P->nh.row;
+    if (P->bcap < K) {  // plan-owned extra grids (released with the plan)
+      P->bgrid = vp_alloc<double>(P, gcells * (size_t)(K - 1));
+      if (P->fs) P->fs_batch = vp_alloc<double>(P, (size_t)P->N * K);
+      P->bcap = K;
+    }
+    P->n_kernels = 0;
+    P->n_ffts = 0;
+    std::vector<const double *> fk(K);
+    std::vector<double *> gk(K), fsk(K, nullptr);
+    for (int k = 0; k < K; k++) {
+      fk[k] = f + (size_t)k * P->N;
+      gk[k] = k == 0 ? P->nh.data : P->bgrid + gcells * (size_t)(k - 1);
+      if (P->fs) fsk[k] = P->fs_batch + (size_t)k * P->N;
+    }
+    double *const data0 = P->nh.data, *const fs0 = P->fs;
+    if (parts & VP_PART_HISTORY) {
+      for (int k = 0; k < K; k++) VP_CUDA(cudaMemsetAsync(gk[k], 0, sizeof(double) * gcells, P->stream));
+      vp_launch_spread_batch(P, P->sp, grid_args(P->nh), K, fk.data(), gk.data(), P->fs ? fsk.data() : nullptr);
+    }
+    try {
+      for (int k = 0; k < K; k++) {
+        P->nh.data = gk[k];
+        if (P->fs) P->fs = fsk[k];
+        if (parts & VP_PART_HISTORY) {
+          VP_CUDA(cudaMemsetAsync(P->fh.data, 0, sizeof(double) * P->fh.nf * P->fh.row, P->stream));
+          vp_launch_restrict(P);
+          grid_fft_fwd(P, P->nh);
+          grid_fft_fwd(P, P->fh);
+          grid_multiply(P, P->nh);
+          grid_multiply(P, P->fh);
+          grid_fft_inv(P, P->nh);
+          grid_fft_inv(P, P->fh);
+          vp_launch_prolong(P, 3);
+        }
+        vp_launch_interp_local(P, fk[k], out + (size_t)k * P->T, true);
+        if (parts & VP_PART_LOCAL) vp_launch_bands(P, fk[k], out + (size_t)k * P->T);
+      }
+    } catch (...) {
+      P->nh.data = data0;
+      P->fs = fs0;
+      throw;
+    }
+    P->nh.data = data0;
+    P->fs = fs0;
+    P->n_phase = 0;
+  } catch (VpError &e) {
+    return e.s;
+  }
+  return VP_OK;
+}
+
 extern "C" vp_status vp_eval_host(vp_handle P, const double *f_host, double *out_host) {
   if (!P || !f_host || !out_host) return VP_ERR_ARG;
   try {

@@ -188,6 +188,9 @@ struct vp_plan_s {
   double *tri_vL = nullptr;    // [N] TRIANGLE-mode V_L per node (eval scratch; null outside TRIANGLE mode)
   double *st_vL = nullptr;     // [n_stencil] stencil part of V_L per stencil slot (eval scratch)
   double *fs = nullptr;        // [N] f in spreading order (eval scratch; stencil indices point into it)
+  double *bgrid = nullptr;     // vp_eval_batch: (bcap - 1) extra NH grids
+  double *fs_batch = nullptr;  // vp_eval_batch: [bcap][N] spreading-order copies of the fields (KNN stencils)
+  int bcap = 1;
   // host-side eval staging (vp_eval_host)
   double *f_dev = nullptr, *out_dev = nullptr;
   // profiling
@@ -234,6 +237,8 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G);
 void vp_fft_forward(vp_plan_s *P, VpGrid &G);
 void vp_fft_columns(vp_plan_s *P, VpGrid &G);
 void vp_fft_inverse(vp_plan_s *P, VpGrid &G);
+void vp_launch_spread_batch(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, int K, const double *const *f,
+                            double *const *grids, double *const *fs);
 void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const double *weights,
                           const int32_t *node_of, int64_t n, const GridArgs &g);
 void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx,

@@ -499,6 +499,187 @@ void vp_launch_spread(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, con
 }
 
 // ---------------------------------------------------------------------------------------------
+// Batched strip spreading: KB fields f_0 .. f_{KB-1} on the same nodes, KB NH grids.  The
+// footprint geometry, the Horner weights and the shared-memory broadcasts of wx / wy are shared by the KB
+// fields; per point and lane the kernel adds wx * c_k * wy[b] to KB register rings (KB * W DFMA for one set
+// of loads), so the shared-memory delivery that bounds k_spread_strip is paid once per KB fields.
+template <int KB>
+struct BatchPtrs {
+  const double *f[KB];
+  double *grid[KB];
+  double *fs[KB];  // spreading-order copies of the fields (null: not written)
+};
+
+template <int W, int D, int KB>
+__global__ void __launch_bounds__(32 * VP_STRIP_WARPS, KB <= 2 ? 4 : 3)
+    k_spread_strip_b(const int4 *__restrict__ items, int64_t n_items, const double *__restrict__ sx,
+                     const double *__restrict__ sy, const double *__restrict__ sw, const int32_t *__restrict__ sperm,
+                     BatchPtrs<KB> bp, GridArgs g) {
+  using C = StripCfg<W>;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * VP_STRIP_WARPS + warp;
+  if (item >= n_items) return;
+  constexpr size_t per_warp = (size_t)C::CH * (C::WXS + C::WYS + KB);
+  double *s_wy = smem + (size_t)warp * per_warp;
+  double *s_wx = s_wy + C::CH * C::WYS;
+  double *s_c = s_wx + C::CH * C::WXS;  // [CH][KB], 16-byte aligned rows (KB even)
+  const int4 it = items[item];
+  const int64_t ox = (int64_t)it.x * C::SW - (W / 2 + 1), oy = (int64_t)it.y * C::SH - (W / 2 + 1);
+  const bool interior = ox >= 0 && oy >= 0 && ox + 32 <= g.nfx && oy + C::SH + W - 1 <= g.nfy;
+  const int64_t colx = interior ? ox + lane : wrapi(ox + lane, g.nfx);
+  double acc[KB][W];
+#pragma unroll
+  for (int k = 0; k < KB; k++)
+#pragma unroll
+    for (int b = 0; b < W; b++) acc[k][b] = 0.0;
+  int c0 = it.z, n = 0, q = 0, r = 0, mylr = 0x7fffffff, prev_lc = 0;
+  bool first = true;
+  double *wrow = s_wx + lane * C::WXS;
+#pragma unroll
+  for (int a = 0; a < 32; a++) wrow[a] = 0.0;
+stage:
+  n = min(C::CH, it.w - c0);
+  mylr = 0x7fffffff;
+  if (lane < n) {
+    const int j = c0 + lane;
+    const int32_t node = sperm[j];
+    const double wj = sw[j];
+#pragma unroll
+    for (int k = 0; k < KB; k++) {
+      const double fj = __ldg(bp.f[k] + node);
+      if (bp.fs[k]) bp.fs[k][j] = fj;
+      s_c[lane * KB + k] = fj * wj;
+    }
+#pragma unroll
+    for (int a = 0; a < W; a++) wrow[prev_lc + a] = 0.0;
+    int lc, lr;
+    {
+      double wx[W];
+      lc = (int)(es_horner<W, D>(gcoord(sx[j], g.ox, g.inv_h), wx) - ox);
+#pragma unroll
+      for (int a = 0; a < W; a++) wrow[lc + a] = wx[a];
+    }
+    prev_lc = lc;
+    double wy[W];
+    lr = (int)(es_horner<W, D>(gcoord(sy[j], g.oy, g.inv_h), wy) - oy);
+    double2 *wyp = (double2 *)(s_wy + lane * C::WYS);
+#pragma unroll
+    for (int b = 0; b + 1 < W; b += 2) wyp[b >> 1] = make_double2(wy[b], wy[b + 1]);
+    if (W & 1) s_wy[lane * C::WYS + W - 1] = wy[W - 1];
+    mylr = lr;
+  }
+  __syncwarp();
+  q = 0;
+  if (first) {
+    r = __shfl_sync(0xffffffffu, mylr, 0);
+    first = false;
+  }
+  for (;;) {
+    switch (r % W) {
+#define VP_STRIPB_PHASE(ph)                                                                     \
+  case ph:                                                                                      \
+    if ((ph) < W) {                                                                             \
+      for (const int e = __popc(__ballot_sync(0xffffffffu, mylr <= r)); q < e; q++) {           \
+        const double wxl = s_wx[q * C::WXS + lane];                                             \
+        double t[KB];                                                                           \
+        _Pragma("unroll") for (int k = 0; k < KB; k += 2) {                                     \
+          const double2 cc = *(const double2 *)(s_c + q * KB + k);                              \
+          t[k] = wxl * cc.x;                                                                    \
+          t[k + 1] = wxl * cc.y;                                                                \
+        }                                                                                       \
+        const double2 *wyp = (const double2 *)(s_wy + q * C::WYS);                              \
+        _Pragma("unroll") for (int b = 0; b + 1 < W; b += 2) {                                  \
+          const double2 v = wyp[b >> 1];                                                        \
+          _Pragma("unroll") for (int k = 0; k < KB; k++) {                                      \
+            acc[k][((ph) + b) % W] = fma(v.x, t[k], acc[k][((ph) + b) % W]);                    \
+            acc[k][((ph) + b + 1) % W] = fma(v.y, t[k], acc[k][((ph) + b + 1) % W]);            \
+          }                                                                                     \
+        }                                                                                       \
+        if (W & 1) {                                                                            \
+          const double v = s_wy[q * C::WYS + W - 1];                                            \
+          _Pragma("unroll") for (int k = 0; k < KB; k++) acc[k][((ph) + W - 1) % W] =           \
+              fma(v, t[k], acc[k][((ph) + W - 1) % W]);                                         \
+        }                                                                                       \
+      }                                                                                         \
+      if (q == n) goto next_chunk;                                                              \
+      _Pragma("unroll") for (int k = 0; k < KB; k++) {                                          \
+        red_row(bp.grid[k] + colx, oy + r, interior, g, acc[k][(ph) % W]);                      \
+        acc[k][(ph) % W] = 0.0;                                                                 \
+      }                                                                                         \
+      r++;                                                                                      \
+    }
+      VP_STRIPB_PHASE(0) VP_STRIPB_PHASE(1) VP_STRIPB_PHASE(2) VP_STRIPB_PHASE(3) VP_STRIPB_PHASE(4)
+      VP_STRIPB_PHASE(5) VP_STRIPB_PHASE(6) VP_STRIPB_PHASE(7) VP_STRIPB_PHASE(8) VP_STRIPB_PHASE(9)
+      VP_STRIPB_PHASE(10) VP_STRIPB_PHASE(11) VP_STRIPB_PHASE(12) VP_STRIPB_PHASE(13) VP_STRIPB_PHASE(14)
+      VP_STRIPB_PHASE(15)
+#undef VP_STRIPB_PHASE
+    }
+  }
+next_chunk:
+  __syncwarp();
+  c0 += C::CH;
+  if (c0 < it.w) goto stage;
+#pragma unroll
+  for (int k = 0; k < KB; k++)
+#pragma unroll
+    for (int jj = 0; jj < W; jj++) red_row(bp.grid[k] + colx, oy + r + ((jj - r % W) + W) % W, interior, g, acc[k][jj]);
+}
+
+template <int W, int KB>
+static void launch_spread_strip_b_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *const *f,
+                                    double *const *grids, double *const *fs) {
+  constexpr int D = VP_HORNER_DEG(W);
+  if (S.n_sitems == 0) return;
+  const size_t sm = (size_t)StripCfg<W>::CH * (StripCfg<W>::WXS + StripCfg<W>::WYS + KB) * 8 * VP_STRIP_WARPS;
+  static size_t attr_set = 0;
+  if (sm > attr_set && sm > 48 * 1024) {
+    VP_CUDA(cudaFuncSetAttribute(k_spread_strip_b<W, D, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr_set = sm;
+  }
+  BatchPtrs<KB> bp;
+  for (int k = 0; k < KB; k++) {
+    bp.f[k] = f[k];
+    bp.grid[k] = grids[k];
+    bp.fs[k] = fs ? fs[k] : nullptr;
+  }
+  const unsigned nb = (unsigned)((S.n_sitems + VP_STRIP_WARPS - 1) / VP_STRIP_WARPS);
+  k_spread_strip_b<W, D, KB><<<nb, 32 * VP_STRIP_WARPS, sm, P->stream>>>(S.sitems, S.n_sitems, S.sx, S.sy, S.sw,
+                                                                         S.sperm, bp, g);
+  VP_CHECK_LAUNCH();
+  P->n_kernels++;
+}
+
+// spread K fields (K = 1 uses k_spread_strip; pairs and quadruples share one strip pass)
+void vp_launch_spread_batch(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, int K, const double *const *f,
+                            double *const *grids, double *const *fs) {
+  if (!S.strip) throw VpError{VP_ERR_UNSUPPORTED};
+  for (int k0 = 0; k0 < K;) {
+    const int kb = K - k0 >= 4 ? 4 : (K - k0 >= 2 ? 2 : 1);
+    if (kb == 1) {
+      VpSpreadSet S1 = S;
+      S1.fs_out = fs ? fs[k0] : nullptr;
+      GridArgs g1 = g;
+      g1.data = grids[k0];
+      vp_launch_spread(P, S1, g1, f[k0]);
+    } else {
+      switch (P->w) {
+#define CASEB(W)                                                                                     \
+  case W:                                                                                            \
+    if (kb == 4) launch_spread_strip_b_w<W, 4>(P, S, g, f + k0, grids + k0, fs ? fs + k0 : nullptr); \
+    else launch_spread_strip_b_w<W, 2>(P, S, g, f + k0, grids + k0, fs ? fs + k0 : nullptr);         \
+    break;
+        CASEB(4) CASEB(5) CASEB(6) CASEB(7) CASEB(8) CASEB(9) CASEB(10) CASEB(11) CASEB(12) CASEB(13) CASEB(14)
+        CASEB(15) CASEB(16)
+#undef CASEB
+        default: throw VpError{VP_ERR_UNSUPPORTED};
+      }
+    }
+    k0 += kb;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // FH restriction / prolongation (separable, gather form).  Tap table for FH index i':
 // NH indices rlo[i'] .. rlo[i'] + ntap-1, weights rw[i'][t] = psi_FH(X1(i) - X2(i')).
 // Transposed table for NH index i: FH indices tlo[i] .. tlo[i] + ntt-1, weights tw[i][t].

@@ -294,3 +294,21 @@ def test_fused_fft_matches_cufft(which):
         plan, f = make_plan(w, **kw)
         out.append(plan.eval(f).cpu().numpy())
     assert np.max(np.abs(out[0] - out[1])) <= 1e-12 * np.max(np.abs(out[1]))
+
+
+@pytest.mark.parametrize("K", [2, 3, 5])
+def test_eval_batch_matches_single_evals(K):
+    """vp_eval_batch: K fields through the shared strip pass (pairs / quadruples + a single)
+    equal K separate vp_eval calls to rounding, and field 0 of the batch matches the oracle."""
+    w = configs.config2(n=80)
+    plan, f0 = make_plan(w)
+    rng = np.random.default_rng(101 + K)
+    F = torch.stack([f0] + [f0 * float(rng.uniform(0.5, 2.0)) + torch.from_numpy(
+        rng.standard_normal(w.f.shape)).to(DEV) * 1e-3 for _ in range(K - 1)]).contiguous()
+    VB = plan.eval_batch(F).cpu().numpy()
+    for k in range(K):
+        Vk = plan.eval(F[k]).cpu().numpy()
+        assert np.max(np.abs(VB[k] - Vk)) <= 1e-13 * np.max(np.abs(Vk)), k
+    idx = configs.sample_targets(w.T, 48, seed=111)
+    ref = oracle.workload_potential(w, idx)
+    assert rel_l2(VB[0][idx], ref) <= 1e-4  # n = 80 under-resolves f (as test_deterministic_mode_bit_identical)
