@@ -580,7 +580,7 @@ stage:
 #define VP_STRIPB_PHASE(ph)                                                                     \
   case ph:                                                                                      \
     if ((ph) < W) {                                                                             \
-      for (const int e = __popc(__ballot_sync(0xffffffffu, mylr <= r)); q < e; q++) {           \
+      _Pragma("unroll 2") for (const int e = __popc(__ballot_sync(0xffffffffu, mylr <= r)); q < e; q++) { \
         const double wxl = s_wx[q * C::WXS + lane];                                             \
         double t[KB];                                                                           \
         _Pragma("unroll") for (int k = 0; k < KB; k += 2) {                                     \
