@@ -45,6 +45,8 @@ def test_argument_errors_without_gpu():
     assert L.vp_plan(1, 1, 10, 12, 1, 10, 1e-20, ctypes.byref(o), ctypes.byref(h)) == vp.VP_ERR_TOL
     assert L.vp_plan(1, 1, 10, 12, 1, 10, 0.5, ctypes.byref(o), ctypes.byref(h)) == vp.VP_ERR_TOL
     assert L.vp_eval(None, None, None) == vp.VP_ERR_ARG
+    assert L.vp_eval_batch(None, 4, None, None) == vp.VP_ERR_ARG
+    assert L.vp_eval_batch(1, 0, 1, 1) == vp.VP_ERR_ARG  # K < 1 is rejected before the handle is used
     assert L.vp_destroy(None) == vp.VP_OK
 
 
