@@ -118,6 +118,7 @@ struct VpBands {
   double *deconv = nullptr;       // [nmode/2 + 1] grid-unit 1/Phi^2
   cufftHandle fwd = 0, inv = 0;
   bool has_plans = false;
+  VpGrid fg;                      // fused-transform tables and spectra (fg.own_fft) instead of the cuFFT plans
   VpSpreadSet sp;
   int64_t n_lt = 0, n_ent = 0;    // targets with level >= 1; (target, level) entries
   int32_t *lt_t = nullptr;        // [n_lt] sorted target index
@@ -239,6 +240,8 @@ void vp_fft_columns(vp_plan_s *P, VpGrid &G);
 void vp_fft_inverse(vp_plan_s *P, VpGrid &G);
 void vp_launch_spread_batch(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, int K, const double *const *f,
                             double *const *grids, double *const *fs);
+bool vp_fft_setup_bands(vp_plan_s *P);
+void vp_fft_bands(vp_plan_s *P);
 void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const double *weights,
                           const int32_t *node_of, int64_t n, const GridArgs &g);
 void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx,

@@ -256,24 +256,33 @@ __global__ void k_fft_mult_table(double *__restrict__ tab, int ncs, int nc, cons
 // (contiguous columns), writes the result row-major (spec_out[row ncs + m1]; concurrent columns' 16-byte writes
 // meet in L2 sectors) so that the inverse row pass reads contiguous rows.  Persistent CTAs, next column
 // prefetched (cp.async) while the current one is transformed.
+// Several boxes (level bands, §5.6): nbox grids of nc rows stacked (NR = nbox nc spectrum rows), unit u = (box
+// b, column m1) with the column at spec + m1 NR + b nc and the multiplier row of the box's level.
 __global__ void __launch_bounds__(256) k_fft_col(const double2 *__restrict__ spec, double2 *__restrict__ spec_out,
-                                                 int ncs, FftStages st, const double2 *__restrict__ tw_c,
-                                                 const double *__restrict__ mult) {
+                                                 int ncs, int nbox, int64_t NR, FftStages st,
+                                                 const double2 *__restrict__ tw_c, const double *__restrict__ mult,
+                                                 const int32_t *__restrict__ box_level) {
   extern __shared__ double2 sm2[];
   const int nc = st.n;
+  const int nu = ncs * nbox;
   double2 *buf0 = sm2, *buf1 = sm2 + nc;
-  int m1 = blockIdx.x;
-  if (m1 < ncs) prefetch_g2s(buf0, spec + (int64_t)m1 * nc, nc);
+  auto col_of = [&](int u) {
+    const int b = u / ncs, m1 = u - b * ncs;
+    return spec + (int64_t)m1 * NR + (int64_t)b * nc;
+  };
+  int u = blockIdx.x;
+  if (u < nu) prefetch_g2s(buf0, col_of(u), nc);
   __pipeline_commit();
-  for (int cur = 0; m1 < ncs; m1 += gridDim.x, cur ^= 1) {
+  for (int cur = 0; u < nu; u += gridDim.x, cur ^= 1) {
     double2 *a2 = cur ? buf1 : buf0;
-    const int mn = m1 + gridDim.x;
-    if (mn < ncs) prefetch_g2s(cur ? buf0 : buf1, spec + (int64_t)mn * nc, nc);
+    const int un = u + gridDim.x;
+    if (un < nu) prefetch_g2s(cur ? buf0 : buf1, col_of(un), nc);
     __pipeline_commit();
     __pipeline_wait_prior(1);
     __syncthreads();
+    const int b = u / ncs, m1 = u - b * ncs;
     fft_run<-1, false>(a2, st, tw_c);
-    const double *mc = mult + (int64_t)m1 * nc;
+    const double *mc = mult + ((int64_t)(box_level ? box_level[b] : 0) * ncs + m1) * nc;
     for (int p = threadIdx.x; p < nc; p += blockDim.x) {
       const double fac = __ldg(mc + p);
       const double2 v = a2[p];
@@ -281,9 +290,31 @@ __global__ void __launch_bounds__(256) k_fft_col(const double2 *__restrict__ spe
     }
     __syncthreads();
     fft_run<1, true>(a2, st, tw_c);
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) spec_out[(int64_t)i * ncs + m1] = a2[i];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) spec_out[((int64_t)b * nc + i) * ncs + m1] = a2[i];
     __syncthreads();
   }
+}
+
+// band multiplier per level l: (e^{-k^2 delta_l} - e^{-k^2 delta_{l-1}}) / k^2, k = dk_l m,
+// ES deconvolution and scale_l, in DIF order; level 0 rows are unused (zero)
+__global__ void k_fft_mult_table_bands(double *__restrict__ tab, int nlev1, int ncs, int nc,
+                                       const int32_t *__restrict__ sig_c, int64_t half_modes,
+                                       const double *__restrict__ deconv, const double *__restrict__ lev_par) {
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= (int64_t)nlev1 * ncs * nc) return;
+  const int64_t l = id / ((int64_t)ncs * nc), rem = id - l * ncs * nc;
+  const int64_t m1 = rem / nc;
+  const int p = (int)(rem - m1 * nc);
+  const int f = sig_c[p];
+  const int64_t m2 = f <= nc / 2 ? f : f - nc;
+  const int64_t a2m = m2 < 0 ? -m2 : m2;
+  double fac = 0.0;
+  if (l > 0 && m1 <= half_modes && a2m <= half_modes) {
+    const double *lp = lev_par + 4 * l;
+    const double k2 = lp[2] * lp[2] * ((double)m1 * m1 + (double)m2 * m2);
+    fac = vp_mult_nh(k2, lp[0], lp[1]) * lp[3] * deconv[m1] * deconv[a2m];
+  }
+  tab[id] = fac;
 }
 
 // ---- row pass, inverse: kept half-spectrum columns (row-major) -> real grid rows (unnormalised, as cuFFT
@@ -406,15 +437,14 @@ static size_t fft_row_smem(int nr, int ncs) {
 static bool g_dft_uploaded = false;
 
 // decide and build the fused transform for grid G (opts.fft_mode 0: where it fits shared memory)
-void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
-  G.own_fft = false;
-  if (P->opts.fft_mode == 1) return;
+// stage plans, twiddles and digit maps of an nf x nf transform (false: size not supported)
+static bool fft_tables(vp_plan_s *P, VpGrid &G) {
   const int nf = (int)G.nf;
   // measured (profiles/r1/probe_fft_*.json): faster than cuFFT + k_multiply up to 6048 (configs 1-2, FH grids of
   // configs 3-4), slower at 12500 (one column fills a CTA's shared memory; load and transform serialise)
-  if (nf % 2 || nf > 6400) return;
+  if (nf % 2 || nf > 6400) return false;
   FftStages sr, sc;
-  if (!factor_stages(nf / 2, sr) || !factor_stages(nf, sc)) return;
+  if (!factor_stages(nf / 2, sr) || !factor_stages(nf, sc)) return false;
   if (!g_dft_uploaded) {
     double hc[9][8] = {}, hs[9][8] = {};
     for (int R = 2; R <= 8; R++)
@@ -448,7 +478,13 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
   VP_CUDA(cudaFuncSetAttribute(k_fft_row_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   for (const void *k : {(const void *)k_fft_col, (const void *)k_fft_row_fwd, (const void *)k_fft_row_inv})
     VP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  if (sm_c > 227 * 1024 || sm_r > 227 * 1024) return;
+  return sm_c <= 227 * 1024 && sm_r <= 227 * 1024;
+}
+
+void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
+  G.own_fft = false;
+  if (P->opts.fft_mode == 1 || !fft_tables(P, G)) return;
+  const int nf = (int)G.nf;
   // second spectrum buffer (row-major column-pass output) and the multiplier table (in DIF output order)
   G.spec2 = vp_alloc<double2>(P, (size_t)G.fft_ncs * nf);
   G.fft_mult = vp_alloc<double>(P, (size_t)G.fft_ncs * nf);
@@ -493,7 +529,7 @@ void vp_fft_columns(vp_plan_s *P, VpGrid &G) {
   memcpy(&sc, G.fft_st_c, sizeof(sc));
   const size_t sm = 2 * sizeof(double2) * G.nf;
   k_fft_col<<<row_grid(sm, G.fft_ncs), 256, sm, P->stream>>>(
-      (const double2 *)G.cdata, G.spec2, G.fft_ncs, sc, G.tw_c, G.fft_mult);
+      (const double2 *)G.cdata, G.spec2, G.fft_ncs, 1, G.nf, sc, G.tw_c, G.fft_mult, nullptr);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
@@ -506,4 +542,46 @@ void vp_fft_inverse(vp_plan_s *P, VpGrid &G) {
                                                               G.tw_c, G.pos_r);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
+}
+
+// ---- level bands (vp_levels.cu): nbox boxes of nfb^2 on one virtual grid, same three passes
+bool vp_fft_setup_bands(vp_plan_s *P) {
+  VpBands &B = P->bands;
+  VpGrid &G = B.fg;
+  G.nf = B.nfb;
+  G.nmode = B.nmode;
+  G.row = B.rowb;
+  if (P->opts.fft_mode == 1 || !fft_tables(P, G)) return false;
+  const int nf = (int)G.nf;
+  const int64_t NR = B.nbox * B.nfb;
+  G.cdata = (double *)vp_alloc<double2>(P, (size_t)G.fft_ncs * NR);
+  G.spec2 = vp_alloc<double2>(P, (size_t)G.fft_ncs * NR);
+  const int nlev1 = B.nlev + 1;
+  G.fft_mult = vp_alloc<double>(P, (size_t)nlev1 * G.fft_ncs * nf);
+  const int64_t nt = (int64_t)nlev1 * G.fft_ncs * nf;
+  k_fft_mult_table_bands<<<(unsigned)((nt + 255) / 256), 256, 0, P->stream>>>(G.fft_mult, nlev1, G.fft_ncs, nf, G.sig_c,
+                                                                              B.nmode / 2, B.deconv, B.lev_par);
+  VP_CHECK_LAUNCH();
+  G.own_fft = true;
+  return true;
+}
+
+void vp_fft_bands(vp_plan_s *P) {
+  VpBands &B = P->bands;
+  VpGrid &G = B.fg;
+  const int64_t NR = B.nbox * B.nfb;
+  FftStages sr, sc;
+  memcpy(&sr, G.fft_st_r, sizeof(sr));
+  memcpy(&sc, G.fft_st_c, sizeof(sc));
+  const size_t smr = fft_row_smem(sr.n, G.fft_ncs), smc = 2 * sizeof(double2) * G.nf;
+  k_fft_row_fwd<<<row_grid(smr, NR), 256, smr, P->stream>>>(B.grid, B.rowb, (double2 *)G.cdata, G.fft_ncs, (int)NR, sr,
+                                                             G.tw_r, G.tw_c, G.pos_r);
+  VP_CHECK_LAUNCH();
+  k_fft_col<<<row_grid(smc, (int64_t)G.fft_ncs * B.nbox), fft_threads(sc.n), smc, P->stream>>>(
+      (const double2 *)G.cdata, G.spec2, G.fft_ncs, (int)B.nbox, NR, sc, G.tw_c, G.fft_mult, B.box_level);
+  VP_CHECK_LAUNCH();
+  k_fft_row_inv<<<row_grid(smr, NR), 256, smr, P->stream>>>(G.spec2, G.fft_ncs, (int)NR, B.grid, B.rowb, sr, G.tw_r,
+                                                             G.tw_c, G.pos_r);
+  VP_CHECK_LAUNCH();
+  P->n_kernels += 3;
 }

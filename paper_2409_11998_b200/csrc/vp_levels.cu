@@ -447,7 +447,7 @@ void vp_build_levels(vp_plan_s *P, const double *nodes, const double *weights) {
   vp_es_deconv_table(P, 1.0, (double)B.nfb, B.nmode / 2, dg);
   B.deconv = vp_alloc<double>(P, dg.size());
   VP_CUDA(cudaMemcpyAsync(B.deconv, dg.data(), sizeof(double) * dg.size(), cudaMemcpyHostToDevice, s));
-  {
+  if (!vp_fft_setup_bands(P)) {  // cuFFT batched over the boxes where the fused transform does not apply
     long long n[2] = {B.nfb, B.nfb};
     long long rin[2] = {B.nfb, B.rowb}, cin[2] = {B.nfb, B.rowb / 2};
     size_t w1 = 0, w2 = 0;

@@ -1857,15 +1857,21 @@ void vp_launch_bands(vp_plan_s *P, const double *f, double *out) {
   GridArgs g{B.grid, B.nfb, B.nbox * B.nfb, B.rowb, 0.0, 0.0, 1.0, 1.0};
   VP_CUDA(cudaMemsetAsync(B.grid, 0, sizeof(double) * B.nbox * B.nfb * B.rowb, P->stream));
   vp_launch_spread(P, B.sp, g, f);
-  VP_CUFFT(cufftExecD2Z(B.fwd, B.grid, (cufftDoubleComplex *)B.grid));
-  int64_t total = B.nbox * B.nfb * (B.nfb / 2 + 1);
-  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  k_multiply_bands<<<blocks, 256, 0, P->stream>>>(B.grid, B.nbox, B.nfb, B.rowb, B.nmode / 2, B.box_level, B.lev_par,
-                                                  B.deconv);
-  VP_CHECK_LAUNCH();
-  P->n_kernels++;
-  VP_CUFFT(cufftExecZ2D(B.inv, (cufftDoubleComplex *)B.grid, B.grid));
-  P->n_ffts += 2;
+  if (B.fg.own_fft) {
+    vp_fft_bands(P);
+  } else {
+    VP_CUFFT(cufftSetStream(B.fwd, P->stream));
+    VP_CUFFT(cufftSetStream(B.inv, P->stream));
+    VP_CUFFT(cufftExecD2Z(B.fwd, B.grid, (cufftDoubleComplex *)B.grid));
+    int64_t total = B.nbox * B.nfb * (B.nfb / 2 + 1);
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    k_multiply_bands<<<blocks, 256, 0, P->stream>>>(B.grid, B.nbox, B.nfb, B.rowb, B.nmode / 2, B.box_level,
+                                                    B.lev_par, B.deconv);
+    VP_CHECK_LAUNCH();
+    P->n_kernels++;
+    VP_CUFFT(cufftExecZ2D(B.inv, (cufftDoubleComplex *)B.grid, B.grid));
+    P->n_ffts += 2;
+  }
   // staged interpolation of the (target, level) entries, then the per-target sums
   switch (P->w) {
 #define CASE(W) \
