@@ -616,10 +616,17 @@ struct StreamScope {
   ~StreamScope() { P->stream = old; }
 };
 
+// everything after the spread (the NH grid already holds this field's spread)
+static void eval_concurrent_after_spread(vp_plan_s *P, const double *f, double *out, int parts);
+
 static void eval_concurrent(vp_plan_s *P, const double *f, double *out, int parts) {
-  cudaStream_t A = P->stream;
-  VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, A));
+  VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, P->stream));
   vp_launch_spread(P, P->sp, grid_args(P->nh), f);
+  eval_concurrent_after_spread(P, f, out, parts);
+}
+
+static void eval_concurrent_after_spread(vp_plan_s *P, const double *f, double *out, int parts) {
+  cudaStream_t A = P->stream;
   VP_CUDA(cudaEventRecord(P->ev_fork, A));
   {  // B: far history
     StreamScope sc(P, P->s_fh);
@@ -727,10 +734,17 @@ extern "C" vp_status vp_eval_batch(vp_handle P, int32_t K, const double *f, doub
       for (int k = 0; k < K; k++) VP_CUDA(cudaMemsetAsync(gk[k], 0, sizeof(double) * gcells, P->stream));
       vp_launch_spread_batch(P, P->sp, grid_args(P->nh), K, fk.data(), gk.data(), P->fs ? fsk.data() : nullptr);
     }
+    // per field: the fork/join schedule of vp_eval where it pays (small grids), else serial; a field's far-
+    // history and local streams start after the caller's stream finished the previous field (ev_fork)
+    const bool conc = P->concurrent && P->nh.nf <= 6000 && (parts & VP_PART_HISTORY);
     try {
       for (int k = 0; k < K; k++) {
         P->nh.data = gk[k];
         if (P->fs) P->fs = fsk[k];
+        if (conc) {
+          eval_concurrent_after_spread(P, fk[k], out + (size_t)k * P->T, parts);
+          continue;
+        }
         if (parts & VP_PART_HISTORY) {
           VP_CUDA(cudaMemsetAsync(P->fh.data, 0, sizeof(double) * P->fh.nf * P->fh.row, P->stream));
           vp_launch_restrict(P);

@@ -6,4 +6,4 @@ timeout 900 python bench.py --steps 5 --warmup 3 --config c5 > gpurun_out/bench_
 timeout 600 python bench.py --steps 5 --warmup 3 --config c3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo bench3=$?
 timeout 600 python bench.py --steps 5 --warmup 3 --config c4 --no-cpu-baseline > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo bench4=$?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --batch 0 > gpurun_out/ncu_launch_c2.log 2>&1; echo l2=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_spread_strip|k_interp_local|k_local_stencil|k_fft" -s 6 -c 8 -o gpurun_out/prof_c2_e3 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --batch 0 > gpurun_out/ncu_c2.log 2>&1; echo ncu2=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_spread_strip|k_interp_local|k_local_stencil|k_fft" -s 6 -c 8 -o gpurun_out/prof_c2_e4 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --batch 0 > gpurun_out/ncu_c2.log 2>&1; echo ncu2=$?
