@@ -312,3 +312,27 @@ def test_eval_batch_matches_single_evals(K):
     idx = configs.sample_targets(w.T, 48, seed=111)
     ref = oracle.workload_potential(w, idx)
     assert rel_l2(VB[0][idx], ref) <= 1e-4  # n = 80 under-resolves f (as test_deterministic_mode_bit_identical)
+
+
+def test_strip_spread_lattice_nodes():
+    """Nodes on a dyadic lattice (coordinates k/256, many of them exactly on NH cell boundaries for power-of-two
+    related grids): strip spreading (plan-time strip keys and eval-time footprints use the same rounding) agrees
+    with the tile batches and with the direct G_H sum of the smooth part."""
+    xs = (np.arange(8, 248, 2) / 256.0)
+    X, Y = np.meshgrid(xs, xs, indexing="ij")
+    pts = np.stack([X.ravel(), Y.ravel()], axis=-1)
+    pts = pts[: (len(pts) // 12) * 12]
+    nodes_np = pts.reshape(-1, 12, 2)
+    rng = np.random.default_rng(121)
+    wts_np = rng.uniform(0.5, 1.5, nodes_np.shape[:2]) / pts.shape[0]
+    f_np = rng.standard_normal(nodes_np.shape[:2])
+    tg_np = np.concatenate([pts[::7], rng.uniform(0.05, 0.95, (300, 2))])
+    nodes, wts, tg, f = (torch.from_numpy(np.ascontiguousarray(a)).to(DEV) for a in (nodes_np, wts_np, tg_np, f_np))
+    d1 = 3.0 * float(wts_np.mean())
+    out = []
+    for st in (0, 32):
+        plan = vp.Plan(nodes, wts, tg, 1e-13, parts=vp.PART_HISTORY, delta1_override=d1, spread_tile=st)
+        out.append(plan.eval(f).cpu().numpy())
+    assert np.max(np.abs(out[0] - out[1])) <= 1e-13 * np.max(np.abs(out[1]))
+    ref = oracle.smooth_direct(pts, (f_np * wts_np).ravel(), tg_np, d1)
+    assert rel_l2(out[0], ref) < 1e-12
