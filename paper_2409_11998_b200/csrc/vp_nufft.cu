@@ -358,10 +358,13 @@ static void launch_spread_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &
 // W = 10, against ~40 for the tile scatter).
 #define VP_STRIP_WARPS 4
 #define VP_STRIP_MAXP 2048  // points per work item: dense strips are split (each part flushes its own rows)
+#ifndef VP_STRIP_SH
+#define VP_STRIP_SH 64  // footprint-origin rows per strip (the register ring is W rows whatever the height)
+#endif
 template <int W>
 struct StripCfg {
   static constexpr int SW = 33 - W;         // footprint-origin columns per strip
-  static constexpr int SH = 32;             // footprint-origin rows per strip
+  static constexpr int SH = VP_STRIP_SH;    // footprint-origin rows per strip
   static constexpr int CH = 32;             // points staged per chunk (one per lane)
   static constexpr int WXS = 33;            // padded x-weight rows (32 columns)
   static constexpr int WYS = (W + 1) & ~1;  // even stride: 16-byte aligned rows for double2 broadcasts
@@ -482,7 +485,7 @@ static void launch_spread_strip_w(vp_plan_s *P, const VpSpreadSet &S, const Grid
 // strip geometry of width W (host side of StripCfg)
 void vp_strip_dims(int W, int *SW, int *SH) {
   *SW = 33 - W;
-  *SH = 32;
+  *SH = VP_STRIP_SH;
 }
 
 void vp_launch_spread(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *f) {
