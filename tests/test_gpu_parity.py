@@ -336,3 +336,25 @@ def test_strip_spread_lattice_nodes():
     assert np.max(np.abs(out[0] - out[1])) <= 1e-13 * np.max(np.abs(out[1]))
     ref = oracle.smooth_direct(pts, (f_np * wts_np).ravel(), tg_np, d1)
     assert rel_l2(out[0], ref) < 1e-12
+
+
+def test_fused_fft_grid_sizes():
+    """Fused transforms vs cuFFT over a sweep of grid sizes (delta_1 varied: n_f runs through 2,3,5,7-smooth
+    sizes, including ones with odd n_f / 2): the smooth part agrees to rounding for every size."""
+    rng = np.random.default_rng(131)
+    src = rng.uniform(0.1, 0.9, (600, 2))
+    nodes = torch.from_numpy(src.reshape(50, 12, 2).copy()).to(DEV)
+    wts = torch.from_numpy(rng.uniform(0.5, 1.5, (50, 12)) / 600).to(DEV)
+    fv = torch.from_numpy(rng.standard_normal((50, 12))).to(DEV)
+    tg = torch.from_numpy(rng.uniform(0.05, 0.95, (200, 2))).to(DEV)
+    sizes = set()
+    for d1 in np.geomspace(2e-3, 2e-5, 9):
+        out = []
+        for mode in (0, 1):
+            plan = vp.Plan(nodes, wts, tg, 1e-10, parts=vp.PART_HISTORY, delta1_override=float(d1), fft_mode=mode)
+            out.append(plan.eval(fv).cpu().numpy())
+            nf = plan.info()["nf_nh"]
+            plan.destroy()
+        sizes.add(nf)
+        assert np.max(np.abs(out[0] - out[1])) <= 1e-12 * np.max(np.abs(out[1])), nf
+    assert any((n // 2) % 2 == 1 for n in sizes), sorted(sizes)
