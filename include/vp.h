@@ -118,7 +118,7 @@ typedef struct {
   double plan_ms;
   int64_t device_bytes;      /* device memory owned by the plan */
   int64_t n_stencil_targets; /* targets whose local part uses a stored KNN stencil */
-  int64_t n_batches;         /* spreading batches (<= 32 points each) */
+  int64_t n_batches;         /* spreading work units: strip items (<= 2048 points) or tile batches (<= 32) */
   double horner_err;         /* max |Horner - ES| over the kernel taps */
   int32_t n_levels;          /* finest band level present (0: no level bands) */
   int64_t n_boxes;           /* band boxes (all levels) */
