@@ -60,6 +60,16 @@ __global__ void k_gather_xy(const double *__restrict__ xy, const int32_t *__rest
                             double *__restrict__ xs, double *__restrict__ ys, int64_t *__restrict__ p64,
                             int32_t *__restrict__ p32);
 
+// ES weight of tap k at t (one Horner chain; register-lean form of es_horner for kernels that keep many
+// accumulators live)
+template <int W, int D>
+__device__ __forceinline__ double es_tap(double t, int k) {
+  double v = c_horner[W - 4][k][D];
+#pragma unroll
+  for (int j = D - 1; j >= 0; j--) v = fma(v, t, c_horner[W - 4][k][j]);
+  return v;
+}
+
 __device__ __forceinline__ int64_t wrapi(int64_t i, int64_t n) {
   i %= n;
   return i < 0 ? i + n : i;
@@ -514,7 +524,7 @@ struct BatchPtrs {
 };
 
 template <int W, int D, int KB>
-__global__ void __launch_bounds__(32 * VP_STRIP_WARPS, KB <= 2 ? 4 : 3)
+__global__ void __launch_bounds__(32 * VP_STRIP_WARPS, 4)
     k_spread_strip_b(const int4 *__restrict__ items, int64_t n_items, const double *__restrict__ sx,
                      const double *__restrict__ sy, const double *__restrict__ sw, const int32_t *__restrict__ sperm,
                      BatchPtrs<KB> bp, GridArgs g) {
@@ -556,20 +566,17 @@ stage:
     }
 #pragma unroll
     for (int a = 0; a < W; a++) wrow[prev_lc + a] = 0.0;
-    int lc, lr;
-    {
-      double wx[W];
-      lc = (int)(es_horner<W, D>(gcoord(sx[j], g.ox, g.inv_h), wx) - ox);
-#pragma unroll
-      for (int a = 0; a < W; a++) wrow[lc + a] = wx[a];
-    }
+    // taps one Horner chain at a time (the KB register rings stay live through the staging)
+    const double gx = gcoord(sx[j], g.ox, g.inv_h), gy = gcoord(sy[j], g.oy, g.inv_h);
+    const double sxw = __dsub_rn(gx, 0.5 * W), syw = __dsub_rn(gy, 0.5 * W);
+    const int ix = (int)ceil(sxw), iy = (int)ceil(syw);
+    const double txh = 2.0 * (ix - sxw) - 1.0, tyh = 2.0 * (iy - syw) - 1.0;
+    const int lc = (int)(ix - ox), lr = (int)(iy - oy);
+#pragma unroll 1
+    for (int a = 0; a < W; a++) wrow[lc + a] = es_tap<W, D>(txh, a);
     prev_lc = lc;
-    double wy[W];
-    lr = (int)(es_horner<W, D>(gcoord(sy[j], g.oy, g.inv_h), wy) - oy);
-    double2 *wyp = (double2 *)(s_wy + lane * C::WYS);
-#pragma unroll
-    for (int b = 0; b + 1 < W; b += 2) wyp[b >> 1] = make_double2(wy[b], wy[b + 1]);
-    if (W & 1) s_wy[lane * C::WYS + W - 1] = wy[W - 1];
+#pragma unroll 1
+    for (int b = 0; b < W; b++) s_wy[lane * C::WYS + b] = es_tap<W, D>(tyh, b);
     mylr = lr;
   }
   __syncwarp();
