@@ -524,7 +524,7 @@ struct BatchPtrs {
 };
 
 template <int W, int D, int KB>
-__global__ void __launch_bounds__(32 * VP_STRIP_WARPS, 4)
+__global__ void __launch_bounds__(32 * VP_STRIP_WARPS, (KB <= 2 || W <= 10) ? 4 : 3)
     k_spread_strip_b(const int4 *__restrict__ items, int64_t n_items, const double *__restrict__ sx,
                      const double *__restrict__ sy, const double *__restrict__ sw, const int32_t *__restrict__ sperm,
                      BatchPtrs<KB> bp, GridArgs g) {
