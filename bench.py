@@ -6,7 +6,10 @@ cuFFT Z2D x2 -> interpolation + local part (all of SURVEY §8(a) rows a4-a11; pl
 are not timed).  Inputs are resident in HBM when the timed region starts; L2 is flushed (256 MiB
 write) between timed steps, outside the per-step CUDA events.
 
-  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config c5] [--impl ours|reference]
+
+Default workload: config 5 (BASELINE.json configs[4], the 16M-triangle config the north star's roofline target
+names; it fits one B200).  --config c1..c4 for the others.
 
 N > 1 (torchrun): every rank evaluates its own replica of the workload (the north star fixes one
 GPU per problem), value = total points of all ranks / max-over-ranks time.
@@ -108,38 +111,60 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def oracle_rate(w, n_targets, seed=99, budget_s=None):
-    """Time the CPU oracle (as it stands) on a bounded target sample; extrapolate to all targets.
-    budget_s: size the sample so that it takes about this long (a 16-target probe sets the rate)."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def oracle_rate(w, budget_s=15.0, seed=99, prep=None):
+    """Time the CPU oracle (as it stands) on a bounded seeded target sample: the per-triangle setup once (timed),
+    then a target batch sized (by a 4-target probe) to take about budget_s.  Full-job estimate
+    t_full = t_setup + t_batch * T / n (direct summation is linear in T up to near-field variation)."""
     import oracle
     from workloads import configs
-    if budget_s is not None:
-        probe = configs.sample_targets(w.T, 16, seed=seed + 7)
-        t0 = time.perf_counter()
-        oracle.workload_potential(w, probe)
-        per = (time.perf_counter() - t0) / len(probe)
-        n_targets = int(max(16, min(4096, budget_s / max(per, 1e-9))))
-    idx = configs.sample_targets(w.T, n_targets, seed=seed)
     t0 = time.perf_counter()
-    oracle.workload_potential(w, idx)
+    own = prep is None
+    if own:
+        prep = oracle.Prepared(w)
+    t_setup = time.perf_counter() - t0
+    probe = configs.sample_targets(w.T, 4, seed=seed + 7)
+    t0 = time.perf_counter()
+    prep.eval(w.targets[probe])
+    per = (time.perf_counter() - t0) / len(probe)
+    n = int(max(4, min(4096, budget_s / max(per, 1e-9))))
+    idx = configs.sample_targets(w.T, n, seed=seed)
+    t0 = time.perf_counter()
+    prep.eval(w.targets[idx])
     dt = time.perf_counter() - t0
-    t_full = dt * w.T / len(idx)
+    if own:
+        prep.close()
+    t_full = t_setup + dt * w.T / len(idx)
     return {"value": (w.N + w.T) / t_full, "unit": "pts/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{len(idx)} of {w.T} targets (seeded uniform) against all {w.M} triangles, "
-                      f"{dt:.2f} s measured, extrapolated linearly in T", "seconds": dt}
+            "cpu": cpu_model(),
+            "sample": f"{len(idx)} of {w.T} targets (seeded uniform) against all {w.M} triangles: {dt:.2f} s, "
+                      f"plus the per-triangle setup {t_setup:.2f} s; t_full = setup + batch * T / {len(idx)}",
+            "seconds": dt, "setup_s": t_setup, "t_full_s": t_full, "n": len(idx)}
 
 
 def ncu_traffic(workload, phase):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the phase's kernels, from the committed ncu
-    --set full captures (profiles/r1/ncu_traffic.json); None if that workload/phase was not captured."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")) as fh:
-            tab = json.load(fh)
-    except Exception:
-        return None, None
-    for prefix, phases in tab.get("workloads", {}).items():
-        if workload.startswith(prefix) and phase in phases:
-            return phases[phase]["bytes"], phases[phase]["source"]
+    --set full captures (profiles/r2/ncu_traffic.json, else r1's); None if that workload/phase was not captured."""
+    for rnd in ("r2", "r1"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "ncu_traffic.json")) as fh:
+                tab = json.load(fh)
+        except Exception:
+            continue
+        for prefix, phases in tab.get("workloads", {}).items():
+            if workload.startswith(prefix) and phase in phases:
+                return phases[phase]["bytes"], phases[phase]["source"]
     return None, None
 
 
@@ -160,22 +185,31 @@ def aggregate_rate(world, pts_per_rank, ms_max):
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the oracle (the method's definition, oracle/) timed on the host cores, rank 0 only.  The
+    per-triangle setup is paid once; every step evaluates a fresh seeded target batch sized so that the whole
+    run stays within a few minutes (per-step budget min(10 s, 120 s / (steps + warmup)))."""
     if rank != 0:
         return
+    import oracle
     w = make_workload(args.config)
-    per_step = args.ref_targets
-    for _ in range(args.warmup):
-        oracle_rate(w, per_step)
-    times = []
+    t0 = time.perf_counter()
+    prep = oracle.Prepared(w)
+    t_setup = time.perf_counter() - t0
+    budget = args.ref_seconds or min(10.0, 120.0 / max(1, args.steps + args.warmup))
+    for s in range(args.warmup):
+        oracle_rate(w, budget_s=min(budget, 2.0), seed=500 + s, prep=prep)
+    fulls = []
     last = None
     for s in range(args.steps):
-        last = oracle_rate(w, per_step, seed=1000 + s)
-        times.append(last["seconds"] * w.T / per_step)
-    t_full = float(np.mean(times))
+        last = oracle_rate(w, budget_s=budget, seed=1000 + s, prep=prep)
+        fulls.append(t_setup + last["seconds"] * w.T / last["n"])
+    prep.close()
+    t_full = float(np.mean(fulls))
     val = (w.N + w.T) / t_full
-    cpu = dict(last)
-    cpu.pop("seconds")
+    cpu = {k: v for k, v in last.items() if k not in ("seconds", "setup_s", "t_full_s", "n")}
     cpu["value"] = val
+    cpu["sample"] = (f"per step {last['sample'].split(' against')[0]} against all {w.M} triangles; setup "
+                     f"{t_setup:.2f} s once; t_full = setup + batch time * T / n, mean over {args.steps} steps")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "pts/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -191,12 +225,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=os.environ.get("VP_BENCH_CONFIG", "c2"))
+    ap.add_argument("--config", default=os.environ.get("VP_BENCH_CONFIG", "c5"))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-targets", type=int, default=384)
-    ap.add_argument("--cpu-targets", type=int, default=96)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline sample sized to ~this many seconds")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=None, help="--impl reference: per-step oracle budget (s)")
     ap.add_argument("--batch", type=int, default=4,
                     help="also time vp_eval_batch with this many fields (SURVEY §8(f) f3); 0 or 1 to skip")
     args = ap.parse_args()
@@ -274,24 +307,37 @@ def main():
     plan.set_profiling(False)
     ph = {k: float(np.mean([p[k] for p in phases])) for k in phases[0]}
     serial_ms = float(sum(ph.values()))
-    # ---- roofline of the dominant kernel (algorithmic bytes)
-    # algorithmic bytes: spread reads x, y, w, f per source and writes the NH grid once;
-    # interp_local reads the NH grid once, x, y per target, writes out, reads the target's own f, and the
-    # stencil (int32 + fp64 per entry) for stencil targets or the triangle metric (24 B / 12 targets) otherwise
-    cells = info["nf_nh"] ** 2
-    K = info["deriv_k"]
-    S = info["n_stencil_targets"]
-    bytes_spread = 32.0 * w.N + 8.0 * cells
-    bytes_interp = 24.0 * w.T + 8.0 * cells + 8.0 * w.T + 12.0 * K * S + 2.0 * (w.T - S)
-    dom = "spread" if ph["spread"] >= ph["interp_local"] else "interp_local"
-    dom_bytes = bytes_spread if dom == "spread" else bytes_interp
+    # ---- roofline (SURVEY §8(d) bytes model): per unit, spread reads x, y, w, f (32 B per source)
+    # and writes the NH grid once (8 B per cell); interp_local reads x, y and writes out (24 B per target), reads
+    # the NH grid once (8 B per cell) and the node target's own f or V_L word (8 B per node target).  KNN
+    # stencil entries (12 B each) are reported separately as overhead, not as algorithmic bytes.
+    cells = float(info["nf_nh"]) ** 2
+    K_st = info["deriv_k"]
+    S_st = info["n_stencil_targets"]
+    T_node = w.N if w.targets_are_nodes or w.name.startswith("c5") else 0
+    alg = {"spread": 32.0 * w.N + 8.0 * cells,
+           "interp_local": 24.0 * w.T + 8.0 * cells + 8.0 * T_node}
     peaks, peak_src = load_peaks()
-    achieved = dom_bytes / (ph[dom] * 1e-3) / 1e9
-    traffic, traffic_src = ncu_traffic(w.name, dom)
-    roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_src,
-            "peak_source": peak_src, "algorithmic_bytes": dom_bytes, "kernel_ms": ph[dom],
-            "co_bound": "shared memory (LSU wavefronts; DESIGN.md §5.1/§5.4)"}
+    hbm = peaks["hbm_gbs"]
+    kern = {}
+    for k in ("spread", "interp_local"):
+        a = alg[k] / (ph[k] * 1e-3) / 1e9
+        tr, trs = ncu_traffic(w.name, k)
+        kern[k] = {"ms": ph[k], "algorithmic_bytes": alg[k], "achieved": a, "frac": a / hbm, "traffic": tr,
+                   "traffic_source": trs}
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    both_ms = ph["spread"] + ph["interp_local"]
+    roof = {"kernel": dom, "bound": "hbm", "achieved": kern[dom]["achieved"], "peak": hbm, "unit": "GB/s",
+            "frac": kern[dom]["frac"], "traffic": kern[dom]["traffic"], "traffic_source": kern[dom]["traffic_source"],
+            "peak_source": peak_src, "algorithmic_bytes": alg[dom], "kernel_ms": ph[dom],
+            "kernels": kern,
+            "spread_plus_interp": {"ms": both_ms, "algorithmic_bytes": alg["spread"] + alg["interp_local"],
+                                   "frac": (alg["spread"] + alg["interp_local"]) / (both_ms * 1e-3) / 1e9 / hbm,
+                                   "north_star_target_frac": 0.5},
+            "overhead_bytes": {"knn_stencil": 12.0 * K_st * S_st, "stencil_targets": S_st, "stencil_k": K_st},
+            "bytes_model": "SURVEY §8(d): spread 32 B/source + 8 B/NH cell; interp 24 B/target + 8 B/NH cell + "
+                           "8 B/node target; phase times from the serial profiled evals (phase_ms)",
+            "co_bound": "fp64 issue + shared-memory wavefronts (DESIGN.md §5.1/§5.4, profiles/r2/microbench)"}
 
     # ---- end-to-end through the public API with host buffers (pinned)
     f_pin = torch.from_numpy(w.f).pin_memory()
@@ -312,9 +358,9 @@ def main():
     # ---- batched fields (vp_eval_batch): K scaled copies of f, same plan; device-timed like the steps
     batch = None
     if args.batch and args.batch > 1:
-        K = args.batch
-        F = torch.stack([f * (1.0 + 0.25 * k) for k in range(K)]).contiguous()
-        OB = torch.empty(K, w.T, dtype=torch.float64, device=dev)
+        KB = args.batch
+        F = torch.stack([f * (1.0 + 0.25 * k) for k in range(KB)]).contiguous()
+        OB = torch.empty(KB, w.T, dtype=torch.float64, device=dev)
         plan.eval_batch(F, OB)
         bms = []
         for s in range(max(3, args.steps // 2)):
@@ -327,15 +373,16 @@ def main():
             torch.cuda.synchronize()
             bms.append(b0.elapsed_time(b1))
         bmax = max_over_ranks(float(np.mean(bms)), dev)
-        batch = {"K": K, "ms_per_batch": bmax, "value": aggregate_rate(world, K * pts, bmax), "unit": "pts/s",
+        batch = {"K": KB, "ms_per_batch": bmax, "value": aggregate_rate(world, KB * pts, bmax), "unit": "pts/s",
                  "note": "K fields per vp_eval_batch; value counts K * (N_src + N_tgt) points"}
         del F, OB
 
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            cpu = oracle_rate(w, args.cpu_targets, budget_s=args.cpu_seconds)
-            cpu.pop("seconds")
+            cpu = oracle_rate(w, budget_s=args.cpu_seconds)
+            for k in ("seconds", "setup_s", "t_full_s", "n"):
+                cpu.pop(k)
         line = {"metric": METRIC, "value": value, "unit": "pts/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -343,8 +390,8 @@ def main():
                            "parallelism": f"replicas x{world}" if world > 1 else "single-gpu",
                            "l2": "flushed between steps (256 MiB write outside the step events)",
                            "nf_nh": info["nf_nh"], "nf_fh": info["nf_fh"], "w_es": info["w_es"],
-                           "deriv": f"{['auto', 'knn', 'triangle'][info['deriv_mode']]} (knn deg {info['deriv_degree']} K {K} "
-                                    f"on {S} targets)", "levels": info["n_levels"], "plan_ms": info["plan_ms"],
+                           "deriv": f"{['auto', 'knn', 'triangle'][info['deriv_mode']]} (knn deg {info['deriv_degree']} "
+                                    f"K {K_st} on {S_st} targets)", "levels": info["n_levels"], "plan_ms": info["plan_ms"],
                            "spread": "register strips (k_spread_strip)", "spread_items": info["n_batches"]},
                 "phase_ms": ph, "serial_ms_per_step": serial_ms, "wall_ms_per_step": t_wall * 1e3 / args.steps,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "batch": batch,

@@ -62,6 +62,19 @@ def lib():
         _lib.orc_smooth_direct.argtypes = [i64, p, p, i64, p, d, p]
         _lib.orc_smooth_dft.argtypes = [i64, p, p, i64, p, d, d, d, i64, d, i64, d, d, d, p]
         _lib.orc_num_threads.restype = ctypes.c_int
+        _lib.orc_prepare.argtypes = [i64, p, p, p, ctypes.POINTER(_Field), ctypes.POINTER(_Opts)]
+        _lib.orc_prepare.restype = p
+        _lib.orc_eval_prepared.argtypes = [p, i64, p, p]
+        _lib.orc_eval_prepared.restype = ctypes.c_int
+        _lib.orc_free.argtypes = [p]
+        _lib.orc_field_values.argtypes = [ctypes.POINTER(_Field), i64, p, p]
+        _lib.orc_set_gauss_legendre.argtypes = [ctypes.c_int, p, p]
+        _lib.orc_set_gauss_legendre.restype = ctypes.c_int
+        # Gauss-Legendre rules n = 1..40 from numpy (companion-matrix eigenvalues), handed to the C oracle
+        xs, ws = zip(*(np.polynomial.legendre.leggauss(n) for n in range(1, 41)))
+        _gl_keep = (np.ascontiguousarray(np.concatenate(xs)), np.ascontiguousarray(np.concatenate(ws)))
+        if _lib.orc_set_gauss_legendre(40, _ptr(_gl_keep[0]), _ptr(_gl_keep[1])) != 0:
+            raise RuntimeError("orc_set_gauss_legendre failed")
         _lib.orc_resolve_rules.argtypes = [i64, p, p, p, ctypes.POINTER(_Field), p]
         _lib.orc_resolve_rules.restype = ctypes.c_int
     return _lib
@@ -117,6 +130,46 @@ def volume_potential(tri, curved, circle, field, targets, eta_far=0.0, eta_polar
                                     _ptr(out), ctypes.byref(_opts(eta_far, eta_polar, nthreads, assume_resolved)))
     if rc != 0:
         raise RuntimeError(f"oracle failed rc={rc}")
+    return out
+
+
+class Prepared:
+    """A triangulation prepared once (per-triangle far-field rules, CSR of weighted points); eval(targets) then
+    costs only the per-target sums.  Same code path as volume_potential (which is prepare + eval + free)."""
+
+    def __init__(self, w, **kw):
+        if w.field["kind"] == "fourier":
+            kw.setdefault("assume_resolved", True)
+        self._keep = [np.ascontiguousarray(w.tri, np.float64),
+                      np.ascontiguousarray(w.curved, np.int8) if w.curved is not None else None,
+                      np.ascontiguousarray(w.circle, np.float64) if w.circle is not None else None]
+        self._F, self._fk = _field_struct(w.field)
+        self.h = lib().orc_prepare(self._keep[0].shape[0], _ptr(self._keep[0]), _ptr(self._keep[1]),
+                                   _ptr(self._keep[2]), ctypes.byref(self._F), ctypes.byref(_opts(**kw)))
+        if not self.h:
+            raise RuntimeError("oracle prepare failed (out of host memory)")
+
+    def eval(self, targets):
+        tg = np.ascontiguousarray(np.asarray(targets, np.float64).reshape(-1, 2))
+        out = np.empty(tg.shape[0])
+        lib().orc_eval_prepared(self.h, tg.shape[0], _ptr(tg), _ptr(out))
+        return out
+
+    def close(self):
+        if self.h:
+            lib().orc_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+def field_values(field, xy):
+    """The oracle's own evaluation of an analytic field spec at points xy [n, 2] (for pins)."""
+    xy = np.ascontiguousarray(np.asarray(xy, np.float64).reshape(-1, 2))
+    out = np.empty(xy.shape[0])
+    F, keep = _field_struct(field)
+    lib().orc_field_values(ctypes.byref(F), xy.shape[0], _ptr(xy), _ptr(out))
     return out
 
 

@@ -164,33 +164,46 @@ class Plan:
         self.h = h
         self.M, self.p, self.T, self.N = M, p, T, M * p
 
-    def eval(self, f, out=None):
+    def _out(self, out, n, dev, shape=None):
         import torch
+        if out is None:
+            return torch.empty(shape or (n,), dtype=torch.float64, device=dev)
+        out = _dev_f64(out)
+        if out.numel() != n or out.device != dev:
+            raise ValueError(f"out must be a contiguous float64 tensor of {n} entries on {dev}")
+        return out
+
+    def eval(self, f, out=None):
         f = _dev_f64(f)
         if f.numel() != self.N:
             raise ValueError("f must have M*p entries")
-        if out is None:
-            out = torch.empty(self.T, dtype=torch.float64, device=f.device)
+        out = self._out(out, self.T, f.device)
         _check(lib().vp_eval(self.h, f.data_ptr(), out.data_ptr()), "vp_eval")
         return out
 
     def eval_batch(self, F, out=None):
-        """K fields at once (C ABI vp_eval_batch): F [K, M, p] or [K, M*p] device fp64 -> [K, T]."""
-        import torch
+        """K fields at once (C ABI vp_eval_batch): F [K, M, p] or [K, M*p] device fp64 -> [K, T]
+        (a caller-supplied out must hold K*T contiguous float64 entries on F's device)."""
         F = _dev_f64(F)
         if F.numel() % self.N:
             raise ValueError("F must hold K x M*p entries")
         K = F.numel() // self.N
-        if out is None:
-            out = torch.empty(K, self.T, dtype=torch.float64, device=F.device)
+        if K < 1:
+            raise ValueError("F must hold at least one field")
+        out = self._out(out, K * self.T, F.device, (K, self.T))
         _check(lib().vp_eval_batch(self.h, K, F.data_ptr(), out.data_ptr()), "vp_eval_batch")
         return out
 
     def eval_host(self, f_host, out_host=None):
         """f_host: numpy float64 (ideally pinned, e.g. torch pinned tensor .numpy()); returns numpy [T]."""
         f_host = np.ascontiguousarray(f_host, dtype=np.float64).reshape(-1)
+        if f_host.size != self.N:
+            raise ValueError("f_host must have M*p entries")
         if out_host is None:
             out_host = np.empty(self.T)
+        if (not isinstance(out_host, np.ndarray) or out_host.dtype != np.float64 or out_host.size != self.T
+                or not out_host.flags.c_contiguous or not out_host.flags.writeable):
+            raise ValueError(f"out_host must be a writeable C-contiguous float64 array of {self.T} entries")
         _check(lib().vp_eval_host(self.h, f_host.ctypes.data, out_host.ctypes.data), "vp_eval_host")
         return out_host
 

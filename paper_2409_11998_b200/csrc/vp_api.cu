@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "vp_common.cuh"
@@ -22,6 +23,24 @@
 
 static thread_local std::string g_last_error;
 void vp_set_last_error(const std::string &s) { g_last_error = s; }
+
+int vp_current_device() {
+  int d = 0;
+  VP_CUDA(cudaGetDevice(&d));
+  return d;
+}
+
+void vp_smem_attr(const void *func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void *>, size_t> done;
+  if (bytes <= 48 * 1024) return;
+  const int dev = vp_current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  size_t &have = done[std::make_pair(dev, func)];
+  if (bytes <= have) return;
+  VP_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  have = bytes;
+}
 
 extern "C" const char *vp_strerror(vp_status s) {
   switch (s) {
@@ -425,7 +444,7 @@ static void free_plan(vp_plan_s *P) {
   }
   if (P->s_fh) cudaStreamDestroy(P->s_fh);
   if (P->s_loc) cudaStreamDestroy(P->s_loc);
-  for (cudaEvent_t e : {P->ev_fork, P->ev_fh, P->ev_loc})
+  for (cudaEvent_t e : {P->ev_fork, P->ev_fh, P->ev_loc, P->ev_restr})
     if (e) cudaEventDestroy(e);
   for (void *p : P->allocs) cudaFree(p);
   if (P->ev_init)
@@ -566,6 +585,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     VP_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
     VP_CUDA(cudaEventCreateWithFlags(&P->ev_fh, cudaEventDisableTiming));
     VP_CUDA(cudaEventCreateWithFlags(&P->ev_loc, cudaEventDisableTiming));
+    VP_CUDA(cudaEventCreateWithFlags(&P->ev_restr, cudaEventDisableTiming));
     VP_CUDA(cudaStreamSynchronize(P->stream));
     VP_CUDA(cudaGetLastError());
   } catch (VpError &e) {
@@ -633,6 +653,7 @@ static void eval_concurrent_after_spread(vp_plan_s *P, const double *f, double *
     VP_CUDA(cudaStreamWaitEvent(P->s_fh, P->ev_fork, 0));
     VP_CUDA(cudaMemsetAsync(P->fh.data, 0, sizeof(double) * P->fh.nf * P->fh.row, P->s_fh));
     vp_launch_restrict(P);
+    VP_CUDA(cudaEventRecord(P->ev_restr, P->s_fh));  // the restriction's last read of the spread NH grid
     grid_fft_fwd(P, P->fh);
     grid_multiply(P, P->fh);
     grid_fft_inv(P, P->fh);
@@ -650,6 +671,8 @@ static void eval_concurrent_after_spread(vp_plan_s *P, const double *f, double *
   // A: near history, join, interpolation
   grid_fft_fwd(P, P->nh);
   grid_multiply(P, P->nh);
+  // the NH inverse transform overwrites the NH grid that stream B's restriction reads: wait for it
+  VP_CUDA(cudaStreamWaitEvent(A, P->ev_restr, 0));
   grid_fft_inv(P, P->nh);
   VP_CUDA(cudaStreamWaitEvent(A, P->ev_fh, 0));
   vp_launch_prolong(P, 2);
@@ -715,7 +738,12 @@ extern "C" vp_status vp_eval_batch(vp_handle P, int32_t K, const double *f, doub
     if (!P->sp.strip) throw VpError{VP_ERR_UNSUPPORTED};
     const int parts = P->opts.parts ? P->opts.parts : VP_PART_ALL;
     const size_t gcells = (size_t)P->nh.nf * P->nh.row;
-    if (P->bcap < K) {  // plan-owned extra grids (released with the plan)
+    if (P->bcap < K) {  // plan-owned extra grids (released with the plan); the smaller set is freed first
+      VP_CUDA(cudaStreamSynchronize(P->stream));  // no queued work of a previous batch still uses them
+      vp_free(P, P->bgrid);
+      vp_free(P, P->fs_batch);
+      P->bgrid = P->fs_batch = nullptr;
+      P->bcap = 1;
       P->bgrid = vp_alloc<double>(P, gcells * (size_t)(K - 1));
       if (P->fs) P->fs_batch = vp_alloc<double>(P, (size_t)P->N * K);
       P->bcap = K;

@@ -38,6 +38,12 @@ struct VpError {
 
 void vp_set_last_error(const std::string &s);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel) and size; thread safe (a mutex-
+// guarded cache keyed by the current device, so a plan on a second device sets its own attribute)
+void vp_smem_attr(const void *func, size_t bytes);
+// current device (cached per call site is not safe across devices: always ask the runtime)
+int vp_current_device();
+
 // ---------------------------------------------------------------------------------------------
 // ES kernel taps as Horner polynomials: psi(z_k(t)), z_k = (k + (t+1)/2 - W/2) 2/W, t in [-1, 1]
 #define VP_HORNER_MAXW 16
@@ -143,7 +149,7 @@ struct vp_plan_s {
   vp_opts opts{};
   cudaStream_t stream = nullptr;       // the caller's stream (A): spread, NH chain, interpolation
   cudaStream_t s_fh = nullptr, s_loc = nullptr;  // forked streams: FH chain (B), local part (C)
-  cudaEvent_t ev_fork = nullptr, ev_fh = nullptr, ev_loc = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_fh = nullptr, ev_loc = nullptr, ev_restr = nullptr;
   bool concurrent = true;              // fork/join eval (off while profiling: phases need serial order)
   // parameters
   double dx2 = 0, delta1 = 0, delta2 = 0, kmax_nh = 0, kmax_fh = 0, R = 0, S = 0, cx = 0, cy = 0;
@@ -185,6 +191,7 @@ struct vp_plan_s {
   double *tri_M = nullptr;     // [M][3] A^-1 A^-T (M11, M12, M22)
   double *tri_H = nullptr;     // [3][p][p] reference cubic-fit Hessian operators
   std::vector<double> tri_H_host;
+  int trih_slot = -1;          // constant-bank slot of tri_H (p = 12), -1: shared-memory kernel
   double tri_c2 = 0;           // delta^2 / 2 (0 if series_order < 2)
   double *tri_vL = nullptr;    // [N] TRIANGLE-mode V_L per node (eval scratch; null outside TRIANGLE mode)
   double *st_vL = nullptr;     // [n_stencil] stencil part of V_L per stencil slot (eval scratch)
@@ -215,6 +222,17 @@ T *vp_alloc(vp_plan_s *P, size_t n) {
   P->allocs.push_back(p);
   P->device_bytes += (int64_t)(n * sizeof(T));
   return (T *)p;
+}
+
+// release one tracked allocation (nullptr accepted)
+inline void vp_free(vp_plan_s *P, void *p) {
+  if (!p) return;
+  for (size_t i = 0; i < P->allocs.size(); i++)
+    if (P->allocs[i] == p) {
+      P->allocs.erase(P->allocs.begin() + i);
+      cudaFree(p);
+      return;
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -249,6 +267,7 @@ void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const Gr
 void vp_remap_stencils(vp_plan_s *P);
 void vp_build_local(vp_plan_s *P, const double *nodes_dev);
 void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop);
+int vp_acquire_trih_slot(const double *hop432);
 int64_t vp_sort_points(vp_plan_s *P, const double *xy, int64_t n, double ox, double oy, double cell,
                        int64_t nbx, int64_t nby, double *xs, double *ys, int64_t *perm64, int32_t *perm32,
                        int64_t **bin_start_out);

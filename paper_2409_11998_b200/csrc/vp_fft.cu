@@ -21,6 +21,9 @@
 
 #include <cuda_pipeline.h>
 
+#include <mutex>
+#include <set>
+
 #include "vp_common.cuh"
 #include "vp_math.cuh"
 
@@ -434,7 +437,6 @@ static size_t fft_row_smem(int nr, int ncs) {
   return std::max(fwd, inv);
 }
 
-static bool g_dft_uploaded = false;
 
 // decide and build the fused transform for grid G (opts.fft_mode 0: where it fits shared memory)
 // stage plans, twiddles and digit maps of an nf x nf transform (false: size not supported)
@@ -445,7 +447,12 @@ static bool fft_tables(vp_plan_s *P, VpGrid &G) {
   if (nf % 2 || nf > 6400) return false;
   FftStages sr, sc;
   if (!factor_stages(nf / 2, sr) || !factor_stages(nf, sc)) return false;
-  if (!g_dft_uploaded) {
+  {  // DFT roots in the constant bank: uploaded once per device (same values for every plan)
+    static std::mutex mu;
+    static std::set<int> done;
+    const int dev = vp_current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(dev)) goto uploaded;
     double hc[9][8] = {}, hs[9][8] = {};
     for (int R = 2; R <= 8; R++)
       for (int j = 0; j < R; j++) {
@@ -455,8 +462,9 @@ static bool fft_tables(vp_plan_s *P, VpGrid &G) {
       }
     VP_CUDA(cudaMemcpyToSymbol(c_dft_c, hc, sizeof(hc)));
     VP_CUDA(cudaMemcpyToSymbol(c_dft_s, hs, sizeof(hs)));
-    g_dft_uploaded = true;
+    done.insert(dev);
   }
+uploaded:
   G.fft_ncs = (int)(G.nmode / 2 + 1);
   if (G.fft_ncs > nf / 2 + 1) G.fft_ncs = nf / 2 + 1;
   G.tw_r = twiddle_table(P, nf / 2);
@@ -498,14 +506,10 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G) {
 
 static int fft_threads(int n) { return n <= 2048 ? 128 : 256; }
 
-static int g_num_sms = 0;
-static int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    VP_CUDA(cudaGetDevice(&dev));
-    VP_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  return g_num_sms;
+static int num_sms() {  // of the current device (asked every time: plans may live on different devices)
+  int n = 0;
+  VP_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, vp_current_device()));
+  return n;
 }
 // persistent row kernels: CTAs per SM that the shared memory (227 KB) allows, at most 4
 static unsigned row_grid(size_t smem, int64_t rows) {

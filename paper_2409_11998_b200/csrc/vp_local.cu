@@ -397,6 +397,7 @@ void vp_build_local(vp_plan_s *P, const double *nodes_dev) {
     vp_cubic_hessian_ops(ref, p, Hop);
     P->tri_H = vp_alloc<double>(P, Hop.size());
     P->tri_H_host = Hop;
+    if (p == 12) P->trih_slot = vp_acquire_trih_slot(Hop.data());
     VP_CUDA(cudaMemcpy(P->tri_H, Hop.data(), sizeof(double) * Hop.size(), cudaMemcpyHostToDevice));
     double c1 = P->delta1;
     k_target_mode<<<tb_t, 256, 0, st>>>(P->tx, P->ty, P->tperm, P->T, p, P->tri_ok, P->opts.targets_are_nodes ? P->N : 0,

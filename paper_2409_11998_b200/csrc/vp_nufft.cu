@@ -19,6 +19,10 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
 
 #include "vp_common.cuh"
 #include "vp_math.cuh"
@@ -35,8 +39,16 @@ __device__ __forceinline__ int es_origin(double g, int W) { return (int)ceil(__d
 // Horner tables of the ES taps for every width W (beta = 2.30 W fixed, so the table depends on W only)
 __constant__ double c_horner[VP_HORNER_MAXW - 3][VP_HORNER_MAXW][VP_HORNER_MAXW];
 
+// The table of width W depends on W only (beta = 2.30 W, fixed degree), so every plan uploads identical bytes:
+// once per (device, W), synchronously at plan time, under a mutex.
 void vp_upload_horner(int W, const VpHorner &h) {
+  static std::mutex mu;
+  static std::set<std::pair<int, int>> done;
+  const int dev = vp_current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(std::make_pair(dev, W))) return;
   VP_CUDA(cudaMemcpyToSymbol(c_horner, &h.c[0][0], sizeof(h.c), sizeof(h.c) * (size_t)(W - 4)));
+  done.insert(std::make_pair(dev, W));
 }
 
 // ES weights for grid points i0 .. i0+W-1 around fractional coordinate g, by Horner polynomials in
@@ -328,11 +340,7 @@ static void launch_spread_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &
   int nw = S.tiles.TS + W + 3;
   size_t sm = sizeof(double) * (size_t)nw * nw;
   if (S.tiles.nsub == 0) return;
-  static int attr_set = 0;
-  if ((int)sm > attr_set && sm > 48 * 1024) {
-    VP_CUDA(cudaFuncSetAttribute(k_spread_nh<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr_set = (int)sm;
-  }
+  vp_smem_attr((const void *)k_spread_nh<W, D>, sm);
   if (!S.det) {
     k_spread_nh<W, D><<<(unsigned)S.tiles.nsub, 32, sm, P->stream>>>(S.tiles.sub, S.bstart, S.sx, S.sy, S.sw,
                                                                      S.sperm, f, g, S.tiles.TS, 0, S.fs_out);
@@ -480,11 +488,7 @@ static void launch_spread_strip_w(vp_plan_s *P, const VpSpreadSet &S, const Grid
   constexpr int D = VP_HORNER_DEG(W);
   if (S.n_sitems == 0) return;
   const size_t sm = StripCfg<W>::smem_warp * VP_STRIP_WARPS;
-  static size_t attr_set = 0;
-  if (sm > attr_set && sm > 48 * 1024) {
-    VP_CUDA(cudaFuncSetAttribute(k_spread_strip<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr_set = sm;
-  }
+  vp_smem_attr((const void *)k_spread_strip<W, D>, sm);
   const unsigned nb = (unsigned)((S.n_sitems + VP_STRIP_WARPS - 1) / VP_STRIP_WARPS);
   k_spread_strip<W, D><<<nb, 32 * VP_STRIP_WARPS, sm, P->stream>>>(S.sitems, S.n_sitems, S.sx, S.sy, S.sw, S.sperm,
                                                                    f, g, S.fs_out);
@@ -642,11 +646,7 @@ static void launch_spread_strip_b_w(vp_plan_s *P, const VpSpreadSet &S, const Gr
   constexpr int D = VP_HORNER_DEG(W);
   if (S.n_sitems == 0) return;
   const size_t sm = (size_t)StripCfg<W>::CH * (StripCfg<W>::WXS + StripCfg<W>::WYS + KB) * 8 * VP_STRIP_WARPS;
-  static size_t attr_set = 0;
-  if (sm > attr_set && sm > 48 * 1024) {
-    VP_CUDA(cudaFuncSetAttribute(k_spread_strip_b<W, D, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr_set = sm;
-  }
+  vp_smem_attr((const void *)k_spread_strip_b<W, D, KB>, sm);
   BatchPtrs<KB> bp;
   for (int k = 0; k < KB; k++) {
     bp.f[k] = f[k];
@@ -961,21 +961,12 @@ static void launch_restrict_int(vp_plan_s *P, const RestrictArgs &a, const TapAr
   constexpr int Q = 4;
   const int span = M * (128 * Q - 1) + 2 * tp.QH + 1;
   const size_t sm = sizeof(double) * (size_t)(span + span / (M * Q) + 2);
-  static bool attr = false;
-  if (!attr) {
-    VP_CUDA(cudaFuncSetAttribute(k_restrict_x_int<M, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    attr = true;
-  }
+  vp_smem_attr((const void *)k_restrict_x_int<M, Q>, 96 * 1024);
   dim3 gA((unsigned)((a.ne + 128 * Q - 1) / (128 * Q)), (unsigned)a.n1);
   bool fixed = false;
 #define VP_RFIX(QHV)                                                                                   \
   if (tp.QH == QHV) {                                                                                  \
-    static bool attr_fix = false;                                                                      \
-    if (!attr_fix) {                                                                                   \
-      VP_CUDA(cudaFuncSetAttribute(k_restrict_x_fix<M, Q, QHV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                   96 * 1024));                                                        \
-      attr_fix = true;                                                                                 \
-    }                                                                                                  \
+    vp_smem_attr((const void *)k_restrict_x_fix<M, Q, QHV>, 96 * 1024);                              \
     k_restrict_x_fix<M, Q, QHV><<<gA, 128, sm, P->stream>>>(P->nh.data, P->scratch, a, tp);           \
     fixed = true;                                                                                      \
   }
@@ -1237,10 +1228,28 @@ __global__ void __launch_bounds__(128) k_tri_local(const double *__restrict__ f,
 // p = 12 (the 12-point rule): reference Hessian operators in the constant bank (uniform, static offsets ->
 // DFMA constant operands, no shared-memory traffic), f and V_L staged through shared memory so that the
 // CTA's 128 x 12 values move as coalesced rows
-__constant__ double c_triH[3 * 12 * 12];
-static double g_triH_uploaded[432];
-static bool g_triH_valid = false;
+// Operators depend on the plan's reference rule, so distinct plans may need distinct tables: VP_TRIH_SLOTS
+// constant-bank slots per device, each written once (at plan time, synchronously) and never overwritten, so a
+// kernel queued by one plan can never see another plan's operators.  A plan whose rule finds no free slot
+// uses the shared-memory kernel k_tri_local<12>.
+#define VP_TRIH_SLOTS 4
+__constant__ double c_triH[VP_TRIH_SLOTS][3 * 12 * 12];
 
+int vp_acquire_trih_slot(const double *hop432) {
+  static std::mutex mu;
+  static std::map<int, std::vector<std::vector<double>>> slots;  // device -> uploaded tables
+  const int dev = vp_current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  std::vector<std::vector<double>> &v = slots[dev];
+  for (size_t i = 0; i < v.size(); i++)
+    if (memcmp(v[i].data(), hop432, sizeof(double) * 432) == 0) return (int)i;
+  if (v.size() >= VP_TRIH_SLOTS) return -1;
+  VP_CUDA(cudaMemcpyToSymbol(c_triH, hop432, sizeof(double) * 432, sizeof(double) * 432 * v.size()));
+  v.emplace_back(hop432, hop432 + 432);
+  return (int)v.size() - 1;
+}
+
+template <int SLOT>
 __global__ void __launch_bounds__(128) k_tri_local12(const double *__restrict__ f, const int8_t *__restrict__ tri_ok,
                                                      const double *__restrict__ tri_M, int64_t M, double c1, double c2,
                                                      double *__restrict__ vL) {
@@ -1261,7 +1270,8 @@ __global__ void __launch_bounds__(128) k_tri_local12(const double *__restrict__ 
       double lap = 0.0;
 #pragma unroll
       for (int j = 0; j < 12; j++)
-        lap = fma(fma(m11, c_triH[k * 12 + j], fma(m12x2, c_triH[144 + k * 12 + j], m22 * c_triH[288 + k * 12 + j])),
+        lap = fma(fma(m11, c_triH[SLOT][k * 12 + j],
+                      fma(m12x2, c_triH[SLOT][144 + k * 12 + j], m22 * c_triH[SLOT][288 + k * 12 + j])),
                   fb[j], lap);
       out[k] = fma(c2, lap, c1 * fb[k]);
     }
@@ -1333,15 +1343,20 @@ void vp_launch_tri_local(vp_plan_s *P, const double *f) {
   }
   if (!P->tri_vL || P->M == 0) return;
   const unsigned nb = (unsigned)((P->M + 127) / 128);
-  if (P->p == 12) {
-    // operators depend on the rule only; (re-)upload when this plan's differ from the last uploaded ones
-    if (!g_triH_valid || memcmp(g_triH_uploaded, P->tri_H_host.data(), sizeof(g_triH_uploaded)) != 0) {
-      memcpy(g_triH_uploaded, P->tri_H_host.data(), sizeof(g_triH_uploaded));
-      VP_CUDA(cudaMemcpyToSymbolAsync(c_triH, P->tri_H, sizeof(double) * 432, 0, cudaMemcpyDeviceToDevice, P->stream));
-      g_triH_valid = true;
+  if (P->p == 12 && P->trih_slot >= 0) {  // slot acquired at plan time (vp_build_local)
+    switch (P->trih_slot) {
+#define CASE(S)                                                                                                 \
+  case S:                                                                                                       \
+    k_tri_local12<S><<<nb, 128, 0, P->stream>>>(f, P->tri_ok, P->tri_M, P->M, P->delta1, P->tri_c2, P->tri_vL); \
+    break;
+      CASE(0) CASE(1) CASE(2) CASE(3)
+#undef CASE
+      default: throw VpError{VP_ERR_CUDA};
     }
-    k_tri_local12<<<nb, 128, 0, P->stream>>>(f, P->tri_ok, P->tri_M, P->M, P->delta1, P->tri_c2, P->tri_vL);
-  } else
+  } else if (P->p == 12)
+    k_tri_local<12><<<nb, 128, 0, P->stream>>>(f, P->tri_ok, P->tri_M, P->tri_H, 12, P->M, P->delta1, P->tri_c2,
+                                               P->tri_vL);
+  else
     k_tri_local<0><<<nb, 128, 0, P->stream>>>(f, P->tri_ok, P->tri_M, P->tri_H, P->p, P->M, P->delta1, P->tri_c2,
                                               P->tri_vL);
   VP_CHECK_LAUNCH();
@@ -1356,11 +1371,7 @@ static void launch_interp_w(vp_plan_s *P, const double *f, double *out) {
   const int TSI = P->TSI, nw = TSI + W + 3;
   const int do_hist = (parts & VP_PART_HISTORY) ? 1 : 0;
   size_t sm = do_hist ? sizeof(double) * (size_t)nw * nw : 0;
-  static int attr_set[17] = {};  // largest dynamic shared memory enabled so far for this W
-  if ((int)sm > attr_set[W]) {
-    VP_CUDA(cudaFuncSetAttribute(k_interp_local<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr_set[W] = (int)sm;
-  }
+  vp_smem_attr((const void *)k_interp_local<W, D>, sm);
   k_interp_local<W, D><<<(unsigned)P->n_items, 256, sm, P->stream>>>(
       P->items, TSI, P->tx, P->ty, P->tperm, grid_args(P->nh), do_hist, f, P->lalpha, P->lnode,
       (parts & VP_PART_LOCAL) ? 1 : 0, P->lptr, P->tri_vL, P->st_vL, out);
@@ -1849,11 +1860,7 @@ static void launch_band_entries_w(vp_plan_s *P, const GridArgs &g) {
   VpBands &B = P->bands;
   const int TSI = P->TSI, nw = TSI + W + 3;
   const size_t sm = sizeof(double) * (size_t)nw * nw;
-  static int attr = 0;
-  if ((int)sm > attr) {
-    VP_CUDA(cudaFuncSetAttribute(k_interp_local<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr = (int)sm;
-  }
+  vp_smem_attr((const void *)k_interp_local<W, D>, sm);
   k_interp_local<W, D><<<(unsigned)B.e_n_items, 256, sm, P->stream>>>(
       B.e_items, TSI, B.e_x, B.e_y, B.e_perm, g, 1, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr,
       B.ent_val);

@@ -59,7 +59,7 @@ def test_reference_arm_json_line():
     """bench.py --impl reference (the CPU oracle as the reference arm) prints one JSON line with the contract keys."""
     import json
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                        "--warmup", "1", "--config", "c2n40", "--ref-targets", "8"], capture_output=True, text=True,
+                        "--warmup", "1", "--config", "c2n40", "--ref-seconds", "0.5"], capture_output=True, text=True,
                        timeout=600, cwd=ROOT, env=dict(os.environ, RANK="0", WORLD_SIZE="1"))
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
