@@ -143,3 +143,33 @@ def test_circle_vs_rect_flat_limit():
         for idx in [_mono_index(0, 0), _mono_index(0, 1), _mono_index(2, 0), _mono_index(0, 2)]:
             # curvature terms kappa delta^{3/2} (kappa = 1/rho) and O(delta^{5/2}) remain
             assert abs(c1[idx] - c2[idx]) < 1e-3 * d ** 2 + 3 * d ** 1.5 / rho + 1e-9 * abs(c2[idx]), (cdist, idx)
+
+
+def _brute_vl_quadrant(x1, x2, delta, f):
+    """int_0^delta int_{y1 > 0, y2 > 0} K_t(x - y) f(y) dy dt for the quadrant (brute force, scipy)."""
+    def inner(t):
+        g = lambda y1, y2: np.exp(-((y1 - x1) ** 2 + (y2 - x2) ** 2) / (4 * t)) / (4 * np.pi * t) * f(y1, y2)
+        s = 12 * np.sqrt(t)
+        return si.dblquad(lambda y2, y1: g(y1, y2), max(0, x1 - s), x1 + s, max(0, x2 - s), x2 + s,
+                          epsabs=1e-16, epsrel=1e-11)[0]
+    return si.quad(inner, 0, delta, epsabs=1e-18, epsrel=1e-10, limit=100)[0]
+
+
+@pytest.mark.parametrize("pos", [(0.0, 0.0), (0.4, 1.3), (2.0, 0.2), (5.0, 4.0)])
+def test_rect_product_form_corner_vs_brute_force(pos):
+    """Quarter-plane corner of the unit square (R8; the paper is silent on corners): the product-form
+    coefficients of vp_coef_rect against a brute-force space-time integral over the quadrant, quadratic f with a
+    mixed term; positions in units of sqrt(delta) from the corner (0, 0)."""
+    d = 1e-3
+    sd = np.sqrt(d)
+    x, y = pos[0] * sd, pos[1] * sd
+    b, c = vp.debug_local_coef("rect", [0, 0, 1, 1], x, y, d, 3, 6)
+    assert b
+    a = {(0, 0): 0.7, (1, 0): -0.3, (0, 1): 1.1, (2, 0): 0.4, (1, 1): -0.8, (0, 2): 0.25}
+    jet = np.zeros(15)
+    for (p, q), v in a.items():
+        jet[_mono_index(p, q)] = v
+    f = lambda y1, y2: sum(v * (y1 - x) ** p * (y2 - y) ** q for (p, q), v in a.items())
+    ref = _brute_vl_quadrant(x, y, d, f)
+    got = _taylor_value(c, jet)
+    assert abs(got - ref) < 1e-9 * abs(ref), (got, ref)

@@ -244,3 +244,70 @@ def test_fourier_field_resolved():
     a = oracle.volume_potential(patch, None, None, fld, tg)
     b = oracle.volume_potential(patch, None, None, fld, tg, assume_resolved=True)
     assert np.max(np.abs(a - b)) < 1e-12 * np.max(np.abs(a))
+
+
+def test_WR_closed_form():
+    """The oracle evaluates W_R from its defining integral; the closed form (1 - J0(Rk))/k^2 - R log R J1(Rk)/k
+    (PAPER.md eq. (Wdef), general R) with scipy's Bessel functions must agree."""
+    for R in [0.7, 1.3, 2 * np.sqrt(2), 3.9]:
+        for k in [1e-3, 0.1, 1.0, 7.5, 40.0, 150.0]:
+            z = R * k
+            if z < 1.0:  # 1 - J0 and J1 by their full power series (no cancellation at small z)
+                m = np.arange(1, 30)
+                lg = sp.gammaln(m + 1)
+                one_m_j0 = np.sum((-1.0) ** (m + 1) * np.exp(2 * m * np.log(z / 2) - 2 * lg))
+                j1 = np.sum((-1.0) ** (m - 1) * np.exp((2 * m - 1) * np.log(z / 2) - lg - sp.gammaln(m)))
+            else:
+                one_m_j0, j1 = 1 - sp.j0(z), sp.j1(z)
+            ref = one_m_j0 / k ** 2 - R * np.log(R) * j1 / k
+            assert abs(oracle.WR(k, R) - ref) < 2e-13 * max(1.0, abs(ref)), (R, k)
+
+
+def test_e1_branches_and_recurrence():
+    """E1 on both sides of the oracle's series / quadrature switch (x = 2) and the exact recurrence-free identity
+    d/dx E1 = -e^{-x}/x checked by a 4th-order central difference (independent of scipy)."""
+    x = np.array([1.999999, 2.0, 2.000001, 3.7, 25.0, 300.0])
+    assert np.max(np.abs(oracle.e1(x) / sp.exp1(x) - 1)) < 3e-15
+    for x0 in [0.3, 1.9, 2.1, 6.0, 40.0]:
+        h = min(1e-3 * x0, 4e-3)
+        d = (-oracle.e1(x0 + 2 * h) + 8 * oracle.e1(x0 + h) - 8 * oracle.e1(x0 - h) + oracle.e1(x0 - 2 * h)) / (12 * h)
+        ex = -np.exp(-x0) / x0
+        assert abs(d - ex) < 1e-9 * abs(ex), x0
+
+
+def test_fourier_field_values_vs_numpy():
+    """The oracle's Fourier field evaluation (table + recurrences, vp_oracle.c field_eval) against a direct numpy
+    sum of a_k cos(2 pi k.x) + b_k sin(2 pi k.x) (config 4's field, |k| <= 64)."""
+    rng = np.random.default_rng(4)
+    fld = fields.random_fourier(rng, 64)
+    pts = np.random.default_rng(9).uniform(-0.2, 1.2, (300, 2))
+    got = oracle.field_values(fld, pts)
+    ph = 2 * np.pi * (pts[:, 0:1] * fld["k1"][None, :] + pts[:, 1:2] * fld["k2"][None, :])
+    ref = np.cos(ph) @ fld["a"] + np.sin(ph) @ fld["b"]
+    assert np.max(np.abs(got - ref)) < 1e-13 * np.max(np.abs(ref))
+    g = fields.gauss([1.3, -0.4], [0.2, 0.7], [0.5, 0.1], [0.01, 0.003])
+    ref = 1.3 * np.exp(-((pts[:, 0] - 0.2) ** 2 + (pts[:, 1] - 0.5) ** 2) / 0.01) - \
+        0.4 * np.exp(-((pts[:, 0] - 0.7) ** 2 + (pts[:, 1] - 0.1) ** 2) / 0.003)
+    assert np.max(np.abs(oracle.field_values(g, pts) - ref)) < 1e-15
+
+
+def test_narrow_gaussian_graded_mesh_closed_form():
+    """A config-3/5-like narrow source (width 1e-3, s = 1e-6) on a quadtree-graded square mesh: most triangles
+    see f < 1e-100, which exercises the oracle's resolution ladder with its absolute floor (O1).  The
+    R^2 closed form V = -(s/4)[log rho^2 + E1(rho^2/s)] applies (exterior mass e^{-0.2^2/1e-6} = 0)."""
+    c = np.array([0.5, 0.5])
+    leaves = configs.quadtree_leaves([c], 0.08, 4, 13)
+    x0, y0, h = leaves[:, 0], leaves[:, 1], leaves[:, 2]
+    a, b = np.stack([x0, y0], 1), np.stack([x0 + h, y0], 1)
+    cc, d = np.stack([x0 + h, y0 + h], 1), np.stack([x0, y0 + h], 1)
+    tri = np.concatenate([np.stack([a, b, cc], 1), np.stack([a, cc, d], 1)])
+    s = 1e-6
+    fld = fields.gauss([1.0], [c[0]], [c[1]], [s])
+    rng = np.random.default_rng(12)
+    tg = np.concatenate([c + 3e-3 * rng.standard_normal((12, 2)), c + [[0.0, 0.0], [1e-4, 0], [0.2, 0.3]]])
+    V = oracle.volume_potential(tri, None, None, fld, tg)
+    rho2 = ((tg - c) ** 2).sum(1)
+    with np.errstate(divide="ignore"):
+        ex = np.where(rho2 > 0, -(s / 4) * (np.log(np.where(rho2 > 0, rho2, 1)) + sp.exp1(np.where(rho2 > 0, rho2, 1) / s)),
+                      (s / 4) * (np.euler_gamma - np.log(s)))
+    assert np.max(np.abs(V - ex)) < 1e-12 * np.max(np.abs(ex)), np.max(np.abs(V - ex)) / np.max(np.abs(ex))
