@@ -319,18 +319,18 @@ def main():
            "interp_local": 24.0 * w.T + 8.0 * cells + 8.0 * T_node}
     peaks, peak_src = load_peaks()
     hbm = peaks["hbm_gbs"]
-    kern = {}
+    kstat = {}
     for k in ("spread", "interp_local"):
         a = alg[k] / (ph[k] * 1e-3) / 1e9
         tr, trs = ncu_traffic(w.name, k)
-        kern[k] = {"ms": ph[k], "algorithmic_bytes": alg[k], "achieved": a, "frac": a / hbm, "traffic": tr,
-                   "traffic_source": trs}
-    dom = max(kern, key=lambda k: kern[k]["ms"])
+        kstat[k] = {"ms": ph[k], "algorithmic_bytes": alg[k], "achieved": a, "frac": a / hbm, "traffic": tr,
+                    "traffic_source": trs}
+    dom = max(kstat, key=lambda k: kstat[k]["ms"])
     both_ms = ph["spread"] + ph["interp_local"]
-    roof = {"kernel": dom, "bound": "hbm", "achieved": kern[dom]["achieved"], "peak": hbm, "unit": "GB/s",
-            "frac": kern[dom]["frac"], "traffic": kern[dom]["traffic"], "traffic_source": kern[dom]["traffic_source"],
+    roof = {"kernel": dom, "bound": "hbm", "achieved": kstat[dom]["achieved"], "peak": hbm, "unit": "GB/s",
+            "frac": kstat[dom]["frac"], "traffic": kstat[dom]["traffic"], "traffic_source": kstat[dom]["traffic_source"],
             "peak_source": peak_src, "algorithmic_bytes": alg[dom], "kernel_ms": ph[dom],
-            "kernels": kern,
+            "kernels": kstat,
             "spread_plus_interp": {"ms": both_ms, "algorithmic_bytes": alg["spread"] + alg["interp_local"],
                                    "frac": (alg["spread"] + alg["interp_local"]) / (both_ms * 1e-3) / 1e9 / hbm,
                                    "north_star_target_frac": 0.5},

@@ -20,8 +20,9 @@
  * All array arguments are DEVICE pointers (CUDA global memory, e.g. from torch tensors) unless
  * the function name ends in _host.  Layouts are C-contiguous, fp64.  No exception crosses the
  * ABI: every entry point returns a vp_status; vp_strerror() gives a static message.
- * Thread safety: distinct plans may be used concurrently; one plan must not be evaluated
- * concurrently with itself (it owns scratch grids).
+ * Thread safety: distinct plans (also on distinct devices) may be used concurrently -- constant-bank tables are
+ * per device and never overwritten with different contents; one plan must not be evaluated concurrently with
+ * itself (it owns scratch grids).
  */
 #ifndef VP_H_
 #define VP_H_
@@ -44,13 +45,33 @@ typedef enum {
   VP_ERR_CUFFT = -8         /* cuFFT error */
 } vp_status;
 
-/* Boundary of Omega, needed by the boundary-aware local part V_L (PAPER.md §4, eq. (vplocO5);
- * §2.2 lines 657-674 closest point).  kind = NONE means "no boundary terms" (valid when f vanishes
- * within 12 sqrt(delta_1) of the boundary). */
-enum { VP_BDRY_NONE = 0, VP_BDRY_CIRCLE = 1, VP_BDRY_RECT = 2 };
+/* Boundary of Omega, needed by the boundary-aware local part V_L (PAPER.md §4, eq. (vplocO5) lines 1061-1087;
+ * §2.2: boundary chunks and the closest point b).  A target within 12 sqrt(delta_1) of the boundary
+ * gets the boundary form of V_L; others the interior series.
+ *   NONE    no boundary terms (valid when f vanishes within 12 sqrt(delta_1) of the boundary).
+ *   CHUNKS  a smooth closed curve, counter-clockwise (interior on the left), as n chunks of degree q = q_B in
+ *           [2, 32] ("a polynomial of degree q_B ... at least q_B + 1 points on each
+ *           segment"; reading R17: the q + 1 points of a chunk sample the curve at the Gauss-Legendre points of
+ *           the chunk's parameter interval [-1, 1], in increasing order, and consecutive chunks share their end
+ *           points).  pts = HOST array [n][q+1][2].  The closest point is the nearest node refined by Newton steps
+ *           (lines 668-674); an ambiguous closest point within 12 sqrt(delta_1) of a target (medial axis) is
+ *           VP_ERR_GEOMETRY; ends of consecutive chunks more than 1e-6 x chunk length apart, or a clockwise
+ *           curve, is VP_ERR_GEOMETRY.
+ *   POLYGON straight edges with right-angle corners (convex or reflex, any orientation; collinear vertices are
+ *           merged), counter-clockwise, simple.  pts = HOST array [n][2].  Exact product-form V_L over the local
+ *           half plane / quadrant / plane-minus-quadrant (R8; the paper is silent on corners).  A corner
+ *           that is not a right angle is VP_ERR_UNSUPPORTED; a target within 12 sqrt(delta_1) of two edges that do
+ *           not meet at a corner (a feature thinner than 24 sqrt(delta_1)) is VP_ERR_GEOMETRY.
+ *   CIRCLE  analytic circle: p = (cx, cy, radius).
+ *   RECT    analytic axis-aligned rectangle: p = (x0, y0, x1, y1) (all four sides and corners at once).
+ * pts is read during vp_plan only (the plan keeps device copies). */
+enum { VP_BDRY_NONE = 0, VP_BDRY_CIRCLE = 1, VP_BDRY_RECT = 2, VP_BDRY_POLYGON = 3, VP_BDRY_CHUNKS = 4 };
 typedef struct {
-  int32_t kind;
-  double p[4]; /* CIRCLE: cx, cy, radius.   RECT (axis-aligned): x0, y0, x1, y1 */
+  int32_t kind;       /* VP_BDRY_* */
+  int32_t q;          /* CHUNKS: degree q_B (q + 1 nodes per chunk) */
+  int64_t n;          /* POLYGON: vertices; CHUNKS: chunks */
+  const double *pts;  /* HOST.  POLYGON [n][2]; CHUNKS [n][q+1][2] */
+  double p[4];        /* CIRCLE: cx, cy, radius.   RECT: x0, y0, x1, y1 */
 } vp_boundary;
 
 /* How the Taylor jet of f at each target is estimated from nodal data (paper silent; DESIGN.md
@@ -142,7 +163,8 @@ typedef struct vp_plan_s *vp_handle;
  * device memory it allocates (released by vp_destroy).  Synchronises opts->cuda_stream.
  * Errors: VP_ERR_ARG (null pointer, M, p or T <= 0, sum of weights == 0, T < N with targets_are_nodes,
  * bad option), VP_ERR_TOL, VP_ERR_NONFINITE (NaN/Inf or negative weight in the inputs), VP_ERR_GEOMETRY
- * (invalid boundary descriptor), VP_ERR_UNSUPPORTED (N or T >= 2^31, TRIANGLE mode without ref_nodes,
+ * (invalid or ambiguous boundary, see vp_boundary), VP_ERR_UNSUPPORTED (N or T >= 2^31, TRIANGLE mode without ref_nodes,
+ * a polygon corner that is not a right angle,
  * or a spreading tile row with more than 2^20 points), VP_ERR_OOM (a grid beyond the device),
  * VP_ERR_CUDA / VP_ERR_CUFFT (runtime failures; vp_last_error_detail says which call). */
 vp_status vp_plan(const double *tri_nodes, const double *weights, int64_t M, int32_t p,
@@ -168,8 +190,10 @@ vp_status vp_eval_host(vp_handle plan, const double *f_host, double *out_host);
  *   out  [K][T]    fp64 (device), field k at out + k T, fully overwritten
  * The spreading of up to four fields shares one pass over the sorted nodes (geometry, ES weights and their
  * shared-memory broadcasts are computed once per node); transforms, interpolation and the local part run per
- * field.  The first call with a given K allocates K-1 extra NH grids (and K spreading-order copies of f for
- * KNN stencils), owned by the plan.  Same stream and concurrency rules as vp_eval; serial schedule.
+ * field, each with vp_eval's schedule (fork/join streams on small grids, serial otherwise).  The first call with a
+ * larger K than before synchronises the plan's stream, frees the previous extra buffers and allocates K-1 extra NH
+ * grids (and K spreading-order copies of f for KNN stencils), owned by the plan.  Same stream and concurrency rules
+ * as vp_eval.
  * Errors: VP_ERR_ARG (null pointer, K < 1), VP_ERR_OOM (extra grids beyond the device), VP_ERR_UNSUPPORTED
  * (deterministic mode or spread_tile > 0, which use the tile-batch spreading), VP_ERR_CUDA / VP_ERR_CUFFT. */
 vp_status vp_eval_batch(vp_handle plan, int32_t K, const double *f, double *out);

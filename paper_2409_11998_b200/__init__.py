@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libvp.so")
 
 VP_OK, VP_ERR_ARG, VP_ERR_TOL, VP_ERR_NONFINITE, VP_ERR_GEOMETRY, VP_ERR_UNSUPPORTED, VP_ERR_OOM, VP_ERR_CUDA, \
     VP_ERR_CUFFT = 0, -1, -2, -3, -4, -5, -6, -7, -8
-BDRY = {None: 0, "none": 0, "circle": 1, "rect": 2}
+BDRY = {None: 0, "none": 0, "circle": 1, "rect": 2, "polygon": 3, "chunks": 4}
 DERIV = {"auto": 0, "knn": 1, "triangle": 2}
 PART_HISTORY, PART_LOCAL, PART_ALL = 1, 2, 3
 
@@ -27,7 +27,8 @@ EXPORTED = ["vp_plan", "vp_eval", "vp_eval_host", "vp_eval_batch", "vp_destroy",
 
 
 class VpBoundary(ctypes.Structure):
-    _fields_ = [("kind", ctypes.c_int32), ("p", ctypes.c_double * 4)]
+    _fields_ = [("kind", ctypes.c_int32), ("q", ctypes.c_int32), ("n", ctypes.c_int64), ("pts", ctypes.c_void_p),
+                ("p", ctypes.c_double * 4)]
 
 
 class VpOpts(ctypes.Structure):
@@ -143,8 +144,18 @@ class Plan:
         o.parts, o.targets_are_nodes = parts, 1 if targets_are_nodes else 0
         if boundary is not None and boundary[0] not in (None, "none"):
             o.boundary.kind = BDRY[boundary[0]]
-            for i, v in enumerate(boundary[1:5]):
-                o.boundary.p[i] = float(v)
+            if boundary[0] == "polygon":      # ("polygon", pts [n, 2])
+                self._bpts = np.ascontiguousarray(boundary[1], np.float64).reshape(-1, 2)
+                o.boundary.n, o.boundary.pts = self._bpts.shape[0], self._bpts.ctypes.data
+            elif boundary[0] == "chunks":     # ("chunks", pts [n, q+1, 2])
+                self._bpts = np.ascontiguousarray(boundary[1], np.float64)
+                if self._bpts.ndim != 3 or self._bpts.shape[2] != 2:
+                    raise ValueError("chunks boundary: pts must be [n, q+1, 2]")
+                o.boundary.n, o.boundary.q = self._bpts.shape[0], self._bpts.shape[1] - 1
+                o.boundary.pts = self._bpts.ctypes.data
+            else:
+                for i, v in enumerate(boundary[1:5]):
+                    o.boundary.p[i] = float(v)
         if stream is None:
             stream = torch.cuda.current_stream()
         self.stream = stream

@@ -18,6 +18,7 @@
 #include <map>
 #include <mutex>
 
+#include "vp_boundary.cuh"
 #include "vp_common.cuh"
 #include "vp_math.cuh"
 
@@ -126,6 +127,15 @@ static void gauss_legendre01(int n, std::vector<double> &x, std::vector<double> 
     }
     x[i] = 0.5 * (1.0 - z);
     w[i] = 1.0 / ((1.0 - z * z) * pp * pp);
+  }
+}
+
+// Gauss-Legendre nodes (increasing) and weights on [-1, 1]
+void vp_gauss_legendre(int n, std::vector<double> &x, std::vector<double> &w) {
+  gauss_legendre01(n, x, w);
+  for (int i = 0; i < n; i++) {
+    x[i] = 2.0 * x[i] - 1.0;
+    w[i] *= 2.0;
   }
 }
 
@@ -475,7 +485,8 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     if (o.boundary.kind == VP_BDRY_CIRCLE && !(o.boundary.p[2] > 0)) throw VpError{VP_ERR_GEOMETRY};
     if (o.boundary.kind == VP_BDRY_RECT && !(o.boundary.p[2] > o.boundary.p[0] && o.boundary.p[3] > o.boundary.p[1]))
       throw VpError{VP_ERR_GEOMETRY};
-    if (o.boundary.kind < 0 || o.boundary.kind > 2) throw VpError{VP_ERR_GEOMETRY};
+    if (o.boundary.kind < VP_BDRY_NONE || o.boundary.kind > VP_BDRY_CHUNKS) throw VpError{VP_ERR_GEOMETRY};
+    o.boundary.pts = nullptr;  // host pointer valid during vp_plan only: read through opts->boundary below
     P->stream = (cudaStream_t)o.cuda_stream;
     P->eps = o.eps_nufft > 0 ? o.eps_nufft : tol;
     // ---- statistics
@@ -528,6 +539,17 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     P->nh.delta_a = P->delta1; P->nh.delta_b = P->delta2;
     setup_grid_fh(P, P->fh, L_fh, P->kmax_fh);
     P->fh.delta_a = P->delta2; P->fh.delta_b = P->R;
+    {  // boundary geometry of the local part (validated and uploaded; the caller's host array is read here only)
+      vp_opts tmp = P->opts;
+      if (opts) P->opts.boundary = opts->boundary;
+      try {
+        vp_build_boundary(P, P->bdev);
+      } catch (...) {
+        P->opts = tmp;
+        throw;
+      }
+      P->opts = tmp;
+    }
     setup_horner(P);
     setup_deconv(P);
     setup_restriction(P);

@@ -141,6 +141,28 @@ struct VpBands {
   int64_t lev_count[16] = {};     // targets per level
 };
 
+// Boundary geometry of the local part V_L on the device (vp_boundary.cuh, vp_boundary.cu)
+#define VP_CHUNK_MAXQ 32
+
+struct VpBdryDev {
+  int kind = VP_BDRY_NONE;
+  int q = 0;            // CHUNKS: degree
+  int64_t n = 0;        // POLYGON: vertices (after merging straight ones); CHUNKS: chunks
+  double p[4] = {0, 0, 0, 0};
+  const double *pts = nullptr;    // POLYGON [n][2] vertices; CHUNKS [n][q+1][2] nodes
+  const double *coef = nullptr;   // CHUNKS [n][q+1][2] Legendre coefficients of gamma on [-1, 1]
+  const double *snode = nullptr;  // CHUNKS [q+1] Gauss-Legendre points of [-1, 1] (node parameters)
+  const int8_t *vkind = nullptr;  // POLYGON [n]: 1 convex right angle, 2 reflex right angle
+  // uniform bins over the boundary's bounding box (+ reach): CHUNKS -> node ids (chunk * (q+1) + k),
+  // POLYGON -> edge ids (edge i joins vertex i and i+1)
+  double bx0 = 0, by0 = 0, bcell = 1;
+  int64_t nbx = 0, nby = 0;
+  const int32_t *bstart = nullptr, *bidx = nullptr;
+  double reach = 0;    // 12 sqrt(delta_1) (the largest delta used)
+  double gap = 0;      // CHUNKS: largest distance between consecutive nodes (incl. across chunk ends)
+  int *err = nullptr;  // device flag: set to 1 on an ambiguous closest point / unsupported local geometry
+};
+
 struct vp_plan_s {
   // sizes
   int64_t M = 0, N = 0, T = 0;
@@ -166,6 +188,7 @@ struct vp_plan_s {
   VpSpreadSet sp;
   // graded-mesh level bands (a12)
   VpBands bands;
+  VpBdryDev bdev;  // boundary geometry for V_L (plan-owned device copies; vp_build_boundary)
   // FH <- NH restriction tables
   int32_t *r_lo = nullptr, *t_lo = nullptr;
   double *r_w = nullptr, *t_w = nullptr;

@@ -15,6 +15,7 @@
 // pairs per target.
 #include <cub/cub.cuh>
 
+#include "vp_boundary.cuh"
 #include "vp_common.cuh"
 #include "vp_math.cuh"
 
@@ -34,7 +35,7 @@ struct LocalArgs {
   int K, deg, nterms;
   int64_t node_targets;           // targets with user index < node_targets are the nodes themselves
   double delta;
-  vp_boundary bd;
+  VpBdryDev bd;
   int32_t *lidx;                  // stencils, k-major: entry k of slot s at [k * stride + s]
   double *lw, *lalpha;
   int64_t slot0, stride;          // global slot of list entry 0; number of stencil slots
@@ -146,10 +147,7 @@ __global__ void k_build_local(LocalArgs a) {
   double coef[VP_NTAYLOR];
   bool bdry = false;
   const double delta = a.tlev ? a.delta * pow(0.25, (double)a.tlev[t]) : a.delta;
-  if (a.bd.kind == VP_BDRY_CIRCLE)
-    bdry = vp_coef_circle(x, y, a.bd.p[0], a.bd.p[1], a.bd.p[2], delta, a.nterms, a.deg, coef);
-  else if (a.bd.kind == VP_BDRY_RECT)
-    bdry = vp_coef_rect(x, y, a.bd.p[0], a.bd.p[1], a.bd.p[2], a.bd.p[3], delta, a.deg, coef);
+  bdry = vp_bdry_coef(a.bd, x, y, delta, a.nterms, a.deg, coef) == 1;  // -1 (geometry error) flags bd.err
   if (!bdry) vp_coef_interior(delta, a.nterms, a.deg, coef);
   a.is_bdry[t] = bdry ? 1 : 0;
   // a target farther than 12 sqrt(delta) from every node sees no local part (the short-time kernel is below
@@ -317,7 +315,7 @@ void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop) {
 
 // per sorted target: triangle mode (interior node of an ok triangle) or stencil
 __global__ void k_target_mode(const double *tx, const double *ty, const int64_t *tperm, int64_t T, int p,
-                              const int8_t *tri_ok, int64_t node_targets, vp_boundary bd, double delta, double c1,
+                              const int8_t *tri_ok, int64_t node_targets, VpBdryDev bd, double delta, double c1,
                               const int8_t *tlev, int32_t *need, double *lalpha, int32_t *lnode) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= T) return;
@@ -326,10 +324,7 @@ __global__ void k_target_mode(const double *tx, const double *ty, const int64_t 
   if (tri && bd.kind != VP_BDRY_NONE) {
     double coef[VP_NTAYLOR];
     double x = tx[t], y = ty[t];
-    bool b = false;
-    if (bd.kind == VP_BDRY_CIRCLE) b = vp_coef_circle(x, y, bd.p[0], bd.p[1], bd.p[2], delta, 1, 0, coef);
-    else if (bd.kind == VP_BDRY_RECT) b = vp_coef_rect(x, y, bd.p[0], bd.p[1], bd.p[2], bd.p[3], delta, 0, coef);
-    if (b) tri = false;
+    if (vp_bdry_coef(bd, x, y, delta, 1, 0, coef) != 0) tri = false;  // near the boundary: stencil path
   }
   need[t] = tri ? 0 : 1;
   if (tri) {
@@ -401,12 +396,12 @@ void vp_build_local(vp_plan_s *P, const double *nodes_dev) {
     VP_CUDA(cudaMemcpy(P->tri_H, Hop.data(), sizeof(double) * Hop.size(), cudaMemcpyHostToDevice));
     double c1 = P->delta1;
     k_target_mode<<<tb_t, 256, 0, st>>>(P->tx, P->ty, P->tperm, P->T, p, P->tri_ok, P->opts.targets_are_nodes ? P->N : 0,
-                                       P->opts.boundary, P->delta1, c1, P->bands.tlev, need, P->lalpha, P->lnode);
+                                       P->bdev, P->delta1, c1, P->bands.tlev, need, P->lalpha, P->lnode);
     VP_CHECK_LAUNCH();
     P->tri_c2 = nterms >= 2 ? 0.5 * P->delta1 * P->delta1 : 0.0;
     P->tri_vL = vp_alloc<double>(P, P->N);
   } else {
-    k_target_mode<<<tb_t, 256, 0, st>>>(P->tx, P->ty, P->tperm, P->T, 1, nullptr, 0, P->opts.boundary, P->delta1, 0.0,
+    k_target_mode<<<tb_t, 256, 0, st>>>(P->tx, P->ty, P->tperm, P->T, 1, nullptr, 0, P->bdev, P->delta1, 0.0,
                                        P->bands.tlev, need, P->lalpha, P->lnode);
     VP_CHECK_LAUNCH();
   }
@@ -465,7 +460,7 @@ void vp_build_local(vp_plan_s *P, const double *nodes_dev) {
       a.K = K; a.deg = deg; a.nterms = nterms;
       a.node_targets = P->opts.targets_are_nodes ? P->N : 0;
       a.delta = P->delta1;
-      a.bd = P->opts.boundary;
+      a.bd = P->bdev;
       a.lidx = P->lidx; a.lw = P->lw; a.slot0 = s0; a.stride = nst; a.lalpha = P->lalpha; a.lnode = P->lnode;
       a.is_bdry = isb;
       a.scratch = scratch;
@@ -484,7 +479,14 @@ void vp_build_local(vp_plan_s *P, const double *nodes_dev) {
   VP_CUDA(cudaMallocAsync(&tmp, tb + 16, st));
   VP_CUDA(cub::DeviceReduce::Sum(tmp, tb, isb, d_cnt, (int)P->T, st));
   VP_CUDA(cudaMemcpyAsync(&P->n_bdry, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  int gerr = 0;
+  if (P->bdev.err) VP_CUDA(cudaMemcpyAsync(&gerr, P->bdev.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   VP_CUDA(cudaStreamSynchronize(st));
+  if (gerr) {
+    vp_set_last_error("boundary: ambiguous closest point (medial axis) or unsupported local geometry within "
+                      "12 sqrt(delta_1) of a target");
+    throw VpError{VP_ERR_GEOMETRY};
+  }
   for (void *q : {(void *)tmp, (void *)d_cnt, (void *)need, (void *)list, (void *)d_n, (void *)isb})
     VP_CUDA(cudaFree(q));
 }

@@ -74,22 +74,15 @@ VP_HD void vp_coef_interior(double delta, int nterms, int deg, double *coef) {
   }
 }
 
-// near a circle of radius rho centred at (ccx, ccy); target inside at (x, y).
-// Returns false if the target is farther than 12 sqrt(delta) (caller uses the interior form).
-VP_HD bool vp_coef_circle(double x, double y, double ccx, double ccy, double rho, double delta, int nterms,
-                          int deg, double *coef) {
-  double dx = x - ccx, dy = y - ccy;
-  double rr = sqrt(dx * dx + dy * dy);
-  double r = rho - rr;
-  if (r < 0.0) r = 0.0;
+// eq. (vplocO5) in the frame of the closest boundary point b: r = |x - b| >= 0,
+// (nx, ny) the inward unit normal at b, kap the curvature at b (> 0 convex).  The caller has checked
+// r < 12 sqrt(delta).  Sign of the delta^{3/2} line: DESIGN.md R7.
+VP_HD void vp_coef_smooth(double r, double nx, double ny, double kap, double delta, int nterms, int deg,
+                          double *coef) {
   double sd = sqrt(delta);
   double c = r / sd;
-  if (c >= 12.0) return false;
   vp_coef_clear(coef);
-  // inward normal n (towards the centre) and tangent t
-  double nx = rr > 0 ? -dx / rr : 1.0, ny = rr > 0 ? -dy / rr : 0.0;
   double tx = -ny, ty = nx;
-  double kap = 1.0 / rho;
   const double sp = 1.7724538509055160273;  // sqrt(pi)
   double E = exp(-c * c / 4.0), ec = erfc(c / 2.0), ef = erf(c / 2.0);
   double c2 = c * c, c4 = c2 * c2;
@@ -115,6 +108,20 @@ VP_HD bool vp_coef_circle(double x, double y, double ccx, double ccy, double rho
     coef[vp_mono_index(2, 2)] = 4.0 * d3 / 3.0;
     coef[vp_mono_index(0, 4)] = 4.0 * d3;
   }
+}
+
+// near a circle of radius rho centred at (ccx, ccy); target inside at (x, y).
+// Returns false if the target is farther than 12 sqrt(delta) (caller uses the interior form).
+VP_HD bool vp_coef_circle(double x, double y, double ccx, double ccy, double rho, double delta, int nterms,
+                          int deg, double *coef) {
+  double dx = x - ccx, dy = y - ccy;
+  double rr = sqrt(dx * dx + dy * dy);
+  double r = rho - rr;
+  if (r < 0.0) r = 0.0;
+  if (r >= 12.0 * sqrt(delta)) return false;
+  // inward normal n (towards the centre)
+  double nx = rr > 0 ? -dx / rr : 1.0, ny = rr > 0 ? -dy / rr : 0.0;
+  vp_coef_smooth(r, nx, ny, 1.0 / rho, delta, nterms, deg, coef);
   return true;
 }
 
@@ -143,15 +150,15 @@ VP_HD double vp_gl12_w(int i) {
   return w[i];
 }
 
-// near an axis-aligned rectangle [x0,x1]x[y0,y1]: coef_ab = int_0^delta M_a(x-range, t) M_b(y-range, t) dt,
-// computed with Gauss-Legendre in tau = sqrt(t) on panels split at the edge distances.
-// Returns false when all edges are farther than 12 sqrt(delta).
-VP_HD bool vp_coef_rect(double x, double y, double x0, double y0, double x1, double y1, double delta, int deg,
-                        double *coef) {
+// local box integral: coef_ab = int_0^delta M_a([lo1, hi1], t) M_b([lo2, hi2], t) dt, bounds relative to the target
+// (infinite bounds allowed), by Gauss-Legendre in tau = sqrt(t) on panels split at the finite edge distances
+// (R8).  The exact local integral of the Taylor polynomial over the box (Taylor basis of the box frame).
+VP_HD void vp_coef_box(double lo1, double hi1, double lo2, double hi2, double delta, int deg, double *coef) {
   double sd = sqrt(delta);
-  double dist[4] = {x - x0, x1 - x, y - y0, y1 - y};
-  double dmin = fmin(fmin(dist[0], dist[1]), fmin(dist[2], dist[3]));
-  if (dmin >= 12.0 * sd) return false;
+  const double big = 60.0 * sd;  // exp(-big^2 / 4 delta) = e^{-900}: an infinite bound
+  lo1 = fmax(lo1, -big); lo2 = fmax(lo2, -big);
+  hi1 = fmin(hi1, big); hi2 = fmin(hi2, big);
+  double dist[4] = {-lo1, hi1, -lo2, hi2};
   vp_coef_clear(coef);
   double brk[20];
   int nb = 0;
@@ -181,11 +188,48 @@ VP_HD bool vp_coef_rect(double x, double y, double x0, double y0, double x1, dou
       double wt = h * vp_gl12_w(i) * 2.0 * tau;
       double t = tau * tau;
       double Mx[5], My[5];
-      vp_moments(x0 - x, x1 - x, t, Mx);
-      vp_moments(y0 - y, y1 - y, t, My);
+      vp_moments(lo1, hi1, t, Mx);
+      vp_moments(lo2, hi2, t, My);
       for (int d = 0; d <= dmax; d++)
         for (int a = d; a >= 0; a--) coef[vp_mono_index(a, d - a)] += wt * Mx[a] * My[d - a];
     }
   }
+}
+
+// Taylor-coefficient weights of a rotated frame -> the global frame: the local frame has orthonormal axes
+// (ax, ay), (bx, by); f(x + s1 a + s2 b) = sum a'_ij s1^i s2^j with a'_ij = sum_ab T[ab][ij] a_ab, T the
+// coefficients of (s1 ax + s2 bx)^a (s1 ay + s2 by)^b.  Returns coef_ab = sum_ij T[ab][ij] cloc_ij (degree <= 4).
+VP_HD void vp_coef_rotate(const double *cloc, double ax, double ay, double bx, double by, int deg, double *coef) {
+  vp_coef_clear(coef);
+  const int dmax = deg < 4 ? deg : 4;
+  for (int d = 0; d <= dmax; d++)
+    for (int a = d; a >= 0; a--) {
+      const int b = d - a;
+      double P[5] = {1.0, 0.0, 0.0, 0.0, 0.0};  // P[i]: coefficient of s1^i s2^(deg_so_far - i)
+      int n = 0;
+      for (int m = 0; m < d; m++) {
+        const double u = m < a ? ax : ay, v = m < a ? bx : by;  // factor (u s1 + v s2)
+        double Q[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int i = 0; i <= n; i++) {
+          Q[i + 1] += P[i] * u;
+          Q[i] += P[i] * v;
+        }
+        n++;
+        for (int i = 0; i <= n; i++) P[i] = Q[i];
+      }
+      double acc = 0.0;
+      for (int i = 0; i <= d; i++) acc += P[i] * cloc[vp_mono_index(i, d - i)];
+      coef[vp_mono_index(a, b)] = acc;
+    }
+}
+
+// near an axis-aligned rectangle [x0,x1]x[y0,y1]: coef_ab = int_0^delta M_a(x-range, t) M_b(y-range, t) dt.
+// Returns false when all edges are farther than 12 sqrt(delta).
+VP_HD bool vp_coef_rect(double x, double y, double x0, double y0, double x1, double y1, double delta, int deg,
+                        double *coef) {
+  double sd = sqrt(delta);
+  double dmin = fmin(fmin(x - x0, x1 - x), fmin(y - y0, y1 - y));
+  if (dmin >= 12.0 * sd) return false;
+  vp_coef_box(x0 - x, x1 - x, y0 - y, y1 - y, delta, deg, coef);
   return true;
 }

@@ -1,0 +1,129 @@
+"""GPU parity of the boundary descriptors (include/vp.h vp_boundary; §2.2):
+CHUNKS (smooth closed curve, closest point by nearest node + Newton) and POLYGON (right-angle corners, exact
+product form), against the analytic CIRCLE / RECT kinds and against the oracle at 10 x tol."""
+import numpy as np
+import pytest
+
+import oracle
+from strata import rel_l2
+from workloads import configs, geometry
+
+torch = pytest.importorskip("torch")
+import paper_2409_11998_b200 as vp  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def plan_eval(w, boundary, **kw):
+    nodes = torch.from_numpy(np.ascontiguousarray(w.nodes)).to(DEV)
+    wts = torch.from_numpy(w.weights).to(DEV)
+    tg = torch.from_numpy(np.ascontiguousarray(w.targets)).to(DEV)
+    f = torch.from_numpy(w.f).to(DEV)
+    tol = kw.pop("tol", w.tol)
+    plan = vp.Plan(nodes, wts, tg, tol, boundary=boundary, targets_are_nodes=w.targets_are_nodes, **kw)
+    V = plan.eval(f).cpu().numpy()
+    info = plan.info()
+    plan.destroy()
+    return V, info
+
+
+def test_disk_chunks_match_circle_and_oracle():
+    """Config 1 (unit disk, f = Gaussian, f != 0 on the boundary) with the circle given as 96 chunks of degree 16:
+    the chunk path (nearest node + Newton, curvature from the interpolant) reproduces the analytic circle and
+    matches the oracle at 10 x tol on all 24k targets."""
+    w = configs.config1(f="gauss")
+    Vc, ic = plan_eval(w, ("circle", 0.0, 0.0, 1.0))
+    Vk, ik = plan_eval(w, ("chunks", geometry.circle_chunks(0.0, 0.0, 1.0, 96, q=16, theta0=0.123)))
+    assert ik["n_boundary_targets"] == ic["n_boundary_targets"] > 1000
+    assert np.max(np.abs(Vk - Vc)) <= 1e-12 * np.max(np.abs(Vc))
+    ref = oracle.workload_potential(w)
+    e = rel_l2(Vk, ref)
+    print("disk chunks rel l2 vs oracle", e)
+    assert e <= 10 * w.tol
+
+
+def test_disk_low_degree_chunks():
+    """q = 4 chunks (the paper needs q_B >= 2): the interpolant of the circle is accurate to ~1e-10 at 256 chunks,
+    so V still matches the oracle at 10 x tol."""
+    w = configs.config1(f="gauss")
+    Vk, _ = plan_eval(w, ("chunks", geometry.circle_chunks(0.0, 0.0, 1.0, 256, q=4)))
+    ref_idx = configs.sample_targets(w.T, 4000, seed=3)
+    e = rel_l2(Vk[ref_idx], oracle.workload_potential(w, ref_idx))
+    assert e <= 10 * w.tol, e
+
+
+def test_star_chunks_config3_small():
+    """Config 3's star r = 1 + 0.3 cos 5 theta given as chunks (the north-star config's real boundary; f vanishes
+    there, so V equals the boundary-free evaluation) on the scaled config 3: parity with the oracle at 10 x tol."""
+    w = configs.config3(M_target=60000, lmin=7, lmax=13, g=0.1)
+    idx = configs.sample_targets(w.T, 1024, seed=5)
+    V0, _ = plan_eval(w, None)
+    Vs, info = plan_eval(w, ("chunks", geometry.star_chunks(200, q=16)))
+    assert info["n_boundary_targets"] > 0
+    assert np.max(np.abs(Vs - V0)) <= 1e-12 * np.max(np.abs(V0))
+    e = rel_l2(Vs[idx], oracle.workload_potential(w, idx))
+    assert e <= 10 * w.tol, e
+
+
+def test_square_polygon_matches_rect():
+    """The unit square as a 4-vertex polygon (+ a collinear vertex, merged) gives the RECT kind's values."""
+    w = configs.config2(n=80)
+    Vr, ir = plan_eval(w, ("rect", 0.0, 0.0, 1.0, 1.0))
+    sq = np.array([[0.0, 0.0], [0.5, 0.0], [1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
+    Vp, ip = plan_eval(w, ("polygon", sq))
+    assert ip["n_boundary_targets"] == ir["n_boundary_targets"] > 0
+    assert np.max(np.abs(Vp - Vr)) <= 1e-12 * np.max(np.abs(Vr))
+
+
+def test_lshape_polygon_vs_oracle():
+    """L-shaped domain (reflex right-angle corner at (1/2, 1/2); f != 0 on the boundary) as a polygon: per stratum
+    (reflex corner, convex corners, edges, uniform) relative l2 vs the oracle <= 10 x tol."""
+    w = configs.l_shape(n=100)
+    V, info = plan_eval(w, w.boundary)
+    band = 12 * np.sqrt(info["delta1"])
+    x, y = w.targets[:, 0], w.targets[:, 1]
+    rng = np.random.default_rng(4)
+    pick = lambda m, k: np.sort(rng.choice(np.nonzero(m)[0], size=min(k, int(m.sum())), replace=False))
+    d_reflex = np.hypot(x - 0.5, y - 0.5)
+    d_edge = np.min(np.stack([x, y, np.where(y <= 0.5, 1 - x, np.inf), np.where(x <= 0.5, 1 - y, np.inf),
+                              np.where(x >= 0.5, np.abs(y - 0.5), np.inf), np.where(y >= 0.5, np.abs(x - 0.5), np.inf)]),
+                   axis=0)
+    convex = np.array([[0, 0], [1, 0], [1, 0.5], [0.5, 1], [0, 1]])
+    d_conv = np.min(np.hypot(x[:, None] - convex[None, :, 0], y[:, None] - convex[None, :, 1]), axis=1)
+    st = {"reflex": pick(d_reflex < band, 256), "convex": pick(d_conv < band, 256),
+          "edge": pick((d_edge < band) & (d_reflex >= band) & (d_conv >= band), 512),
+          "uniform": configs.sample_targets(w.T, 1024, seed=9)}
+    prep = oracle.Prepared(w)
+    for k, idx in st.items():
+        e = rel_l2(V[idx], prep.eval(w.targets[idx]))
+        print("lshape", k, len(idx), e)
+        assert e <= 10 * w.tol, (k, e)
+    prep.close()
+
+
+def _status(w, boundary, **kw):
+    try:
+        plan_eval(w, boundary, **kw)
+    except vp.VpError as e:
+        return e.status
+    return vp.VP_OK
+
+
+def test_boundary_errors():
+    w = configs.config2(n=20)
+    # not a right angle
+    assert _status(w, ("polygon", np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]]))) == vp.VP_ERR_UNSUPPORTED
+    # clockwise
+    assert _status(w, ("polygon", np.array([[0.0, 0.0], [0.0, 1.0], [1.0, 1.0], [1.0, 0.0]]))) == vp.VP_ERR_GEOMETRY
+    # a feature thinner than 24 sqrt(delta_1): targets see two edges that do not meet
+    assert _status(w, ("polygon", np.array([[0.0, 0.0], [1.0, 0.0], [1.0, 0.01], [0.0, 0.01]]))) == vp.VP_ERR_GEOMETRY
+    d = configs.config1(M_target=600)
+    # chunks that do not close
+    ch = geometry.circle_chunks(0.0, 0.0, 1.0, 32)
+    ch[5] += 1e-3
+    assert _status(d, ("chunks", ch)) == vp.VP_ERR_GEOMETRY
+    # medial axis within reach: delta_1 so large that 12 sqrt(delta_1) exceeds the radius
+    assert _status(d, ("chunks", geometry.circle_chunks(0.0, 0.0, 1.0, 32)), delta1_override=1e-2) == vp.VP_ERR_GEOMETRY
+    # q out of range
+    assert _status(d, ("chunks", geometry.circle_chunks(0.0, 0.0, 1.0, 32, q=1))) == vp.VP_ERR_UNSUPPORTED

@@ -209,6 +209,21 @@ def config2(n=309, seed=2, split_frac=0.05, tol=1e-9):
                    ("rect", 0.0, 0.0, 1.0, 1.0), tol, meta={"seed": seed, "n": n})
 
 
+def l_shape(n=100, seed=6, tol=1e-8, jitter=0.0):
+    """L-shaped domain [0,1]^2 minus (1/2,1]^2 (a reflex right-angle corner at (1/2, 1/2)); n x n cells (n even),
+    f = 3 Gaussians of width 0.12-0.2 that do not vanish on the boundary.  Boundary: the 6-vertex CCW polygon."""
+    rng = np.random.default_rng(seed)
+    tri = square_grid(n, jitter=jitter, rng=rng if jitter else None)
+    c = tri.mean(1)
+    tri = tri[~((c[:, 0] > 0.5) & (c[:, 1] > 0.5))]
+    g = np.random.default_rng(seed + 1000)
+    fld = fields.gauss(g.uniform(0.5, 1.5, 3), g.uniform(0.1, 0.9, 3), g.uniform(0.1, 0.9, 3),
+                       g.uniform(0.12, 0.2, 3) ** 2)
+    poly = np.array([[0.0, 0.0], [1.0, 0.0], [1.0, 0.5], [0.5, 0.5], [0.5, 1.0], [0.0, 1.0]])
+    return _finish(f"lshape_n{n}", tri, np.zeros(tri.shape[0], np.int8), None, fld, ("polygon", poly), tol,
+                   meta={"seed": seed, "n": n})
+
+
 def config4(n=1414, seed=4, tol=1e-10, kmax=64, f_device=None):
     rng = np.random.default_rng(seed)
     tri = square_grid(n)

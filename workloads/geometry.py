@@ -125,3 +125,29 @@ def nodes_weights(tri, curved=None, circle=None, chunk=1 << 20):
         nodes[cur, :, 1] = y
         wts[cur] = rule.WEIGHTS[None, :] * 0.5 * np.abs(det)
     return nodes, wts
+
+
+# --------------------------------------------------------------------------- boundary descriptors
+def _gl_nodes(q):
+    """q + 1 Gauss-Legendre points of [-1, 1], increasing (numpy's leggauss)."""
+    return np.polynomial.legendre.leggauss(q + 1)[0]
+
+
+def circle_chunks(cx, cy, rho, n, q=16, theta0=0.0):
+    """CCW circle as n chunks of degree q: chunk c samples theta in [theta0 + 2 pi c / n, theta0 + 2 pi (c+1) / n]
+    at the Gauss-Legendre points (the vp_boundary CHUNKS convention, R17).  -> [n, q+1, 2]"""
+    s = _gl_nodes(q)
+    th = theta0 + 2 * np.pi * (np.arange(n)[:, None] + 0.5 * (s[None, :] + 1.0)) / n
+    return np.stack([cx + rho * np.cos(th), cy + rho * np.sin(th)], -1)
+
+
+def star_radius(th, a=0.3, m=5):
+    return 1.0 + a * np.cos(m * th)
+
+
+def star_chunks(n, q=16, a=0.3, m=5, cx=0.0, cy=0.0):
+    """CCW star r(theta) = 1 + a cos(m theta) (config 3's domain) as n chunks of degree q, uniform in theta."""
+    s = _gl_nodes(q)
+    th = 2 * np.pi * (np.arange(n)[:, None] + 0.5 * (s[None, :] + 1.0)) / n
+    r = star_radius(th, a, m)
+    return np.stack([cx + r * np.cos(th), cy + r * np.sin(th)], -1)
