@@ -157,13 +157,10 @@ __device__ inline int vp_bdry_coef(const VpBdryDev &B, double x, double y, doubl
     if (B.err) atomicExch(B.err, 1);
     return -1;
   }
-  // CHUNKS
-  // nearest node per chunk among the 3 x 3 bins (cell >= reach + gap)
-  const int NC = 8;
-  int64_t cc[NC];
-  double cs[NC], cd[NC];
-  int nc = 0;
+  // CHUNKS: nearest node in the 3 x 3 bins (cell >= reach + gap), then Newton from it
   const int qp = B.q + 1;
+  double dn = 1e300;
+  int64_t nid = -1;
   for (int64_t yy = by - 1; yy <= by + 1; yy++) {
     if (yy < 0 || yy >= B.nby) continue;
     for (int64_t xx = bx - 1; xx <= bx + 1; xx++) {
@@ -171,55 +168,51 @@ __device__ inline int vp_bdry_coef(const VpBdryDev &B, double x, double y, doubl
       const int64_t b = yy * B.nbx + xx;
       for (int32_t k = B.bstart[b]; k < B.bstart[b + 1]; k++) {
         const int64_t id = B.bidx[k];
-        const double px = B.pts[2 * id], py = B.pts[2 * id + 1];
-        const double d = sqrt((px - x) * (px - x) + (py - y) * (py - y));
-        if (d >= reach + B.gap) continue;
-        const int64_t ch = id / qp;
-        int j = 0;
-        while (j < nc && cc[j] != ch) j++;
-        if (j == nc) {
-          if (nc == NC) {  // too many boundary pieces within reach: unsupported local geometry
-            if (B.err) atomicExch(B.err, 1);
-            return -1;
-          }
-          cc[nc] = ch; cd[nc] = 1e300; nc++;
+        const double px = B.pts[2 * id] - x, py = B.pts[2 * id + 1] - y;
+        const double d = px * px + py * py;
+        if (d < dn) { dn = d; nid = id; }
+      }
+    }
+  }
+  if (nid < 0 || sqrt(dn) >= reach + B.gap) return 0;
+  int64_t bch;
+  double bs, bnx, bny, bkap;
+  double best = vp_chunk_closest(B, x, y, nid / qp, B.snode[nid % qp], &bch, &bs, &bnx, &bny, &bkap);
+  double g[2], g1[2], g2[2];
+  vp_chunk_eval(B, bch, bs, g, g1, g2);
+  double bpx = g[0], bpy = g[1];
+  // another piece of the curve nearly as close (a second local minimum of the distance: the medial axis)?  Newton
+  // from nodes of chunks not adjacent to the closest point's chunk that lie within best + gap
+  int tries = 0;
+  for (int64_t yy = by - 1; yy <= by + 1 && best < reach; yy++) {
+    if (yy < 0 || yy >= B.nby) continue;
+    for (int64_t xx = bx - 1; xx <= bx + 1; xx++) {
+      if (xx < 0 || xx >= B.nbx) continue;
+      const int64_t b = yy * B.nbx + xx;
+      for (int32_t k = B.bstart[b]; k < B.bstart[b + 1]; k++) {
+        const int64_t id = B.bidx[k];
+        if (vp_chunks_adjacent(id / qp, bch, B.n)) continue;
+        const double px = B.pts[2 * id] - x, py = B.pts[2 * id + 1] - y;
+        if (sqrt(px * px + py * py) >= best + B.gap) continue;
+        if (++tries > 16) {  // many distant pieces of the curve within reach: not a unique closest point
+          if (B.err) atomicExch(B.err, 1);
+          return -1;
         }
-        if (d < cd[j]) {
-          cd[j] = d;
-          cs[j] = B.snode[id % qp];  // the node's parameter: the k-th Gauss-Legendre point of [-1, 1]
+        int64_t c2;
+        double s2, nx2, ny2, k2;
+        const double d2 = vp_chunk_closest(B, x, y, id / qp, B.snode[id % qp], &c2, &s2, &nx2, &ny2, &k2);
+        double h[2], h1[2], h2[2];
+        vp_chunk_eval(B, c2, s2, h, h1, h2);
+        const double sep = sqrt((h[0] - bpx) * (h[0] - bpx) + (h[1] - bpy) * (h[1] - bpy));
+        if (sep <= B.gap) continue;  // converged to the same closest point
+        if (d2 <= best * (1.0 + 1e-6) + 1e-300) {  // a second, distinct minimiser as close (or closer)
+          if (B.err) atomicExch(B.err, 1);
+          return -1;
         }
       }
     }
   }
-  if (nc == 0) return 0;
-  // Newton from each candidate chunk's nearest node; s0 from the node's index (Chebyshev-like guess of the GL node)
-  double best = 1e300, bnx = 0, bny = 0, bkap = 0;
-  int64_t bch = -1;
-  double bpx = 0, bpy = 0;
-  double dist[NC], pxs[NC], pys[NC];
-  int64_t chs[NC];
-  for (int j = 0; j < nc; j++) {
-    const double s0 = cs[j];
-    int64_t c1;
-    double s1, nx, ny, kap;
-    dist[j] = vp_chunk_closest(B, x, y, cc[j], s0, &c1, &s1, &nx, &ny, &kap);
-    double g[2], g1[2], g2[2];
-    vp_chunk_eval(B, c1, s1, g, g1, g2);
-    pxs[j] = g[0]; pys[j] = g[1]; chs[j] = c1;
-    if (dist[j] < best) {
-      best = dist[j]; bnx = nx; bny = ny; bkap = kap; bch = c1; bpx = g[0]; bpy = g[1];
-    }
-  }
   if (best >= reach) return 0;
-  // ambiguity: another piece of the curve (not adjacent to the best one, its closest point elsewhere) as close
-  for (int j = 0; j < nc; j++) {
-    if (vp_chunks_adjacent(chs[j], bch, B.n)) continue;
-    const double sep = sqrt((pxs[j] - bpx) * (pxs[j] - bpx) + (pys[j] - bpy) * (pys[j] - bpy));
-    if (dist[j] < best + 1e-6 * reach && sep > B.gap) {
-      if (B.err) atomicExch(B.err, 1);
-      return -1;
-    }
-  }
   // inside / outside: the target lies on the interior side when (x - b) . n >= 0; outside -> on the boundary
   const double side = (x - bpx) * bnx + (y - bpy) * bny;
   const double r = side > 0 ? best : 0.0;

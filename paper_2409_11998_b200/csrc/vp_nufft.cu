@@ -52,18 +52,42 @@ void vp_upload_horner(int W, const VpHorner &h) {
 }
 
 // ES weights for grid points i0 .. i0+W-1 around fractional coordinate g, by Horner polynomials in
-// t = 2u - 1, u = i0 - (g - W/2) in [0, 1)
+// t = 2u - 1, u = i0 - (g - W/2) in [0, 1).  psi is even, so tap W-1-k at t equals tap k at -t: with
+// P_k(t) = E_k(t^2) + t O_k(t^2) one even and one odd Horner chain in t^2 give both taps of a pair
+// (about half the DFMA of W separate chains).
+// taps k and W-1-k at t (u = t^2): even and odd Horner chains of tap k's polynomial
 template <int W, int D>
-__device__ __forceinline__ int es_horner(double g, double *wts) {
+__device__ __forceinline__ void es_pair(int k, double t, double u, double *wk, double *wm) {
+  constexpr int DE = D / 2, DO = (D - 1) / 2;  // highest even / odd coefficient: 2 DE, 2 DO + 1 <= D
+  double e = c_horner[W - 4][k][2 * DE], o = c_horner[W - 4][k][2 * DO + 1];
+#pragma unroll
+  for (int j = DE - 1; j >= 0; j--) e = fma(e, u, c_horner[W - 4][k][2 * j]);
+#pragma unroll
+  for (int j = DO - 1; j >= 0; j--) o = fma(o, u, c_horner[W - 4][k][2 * j + 1]);
+  *wk = fma(t, o, e);
+  *wm = fma(-t, o, e);
+}
+
+// footprint origin and Horner argument of fractional grid coordinate g
+template <int W>
+__device__ __forceinline__ int es_arg(double g, double *t) {
   const double s = __dsub_rn(g, 0.5 * W);
   const int i0 = (int)ceil(s);
-  const double t = 2.0 * (i0 - s) - 1.0;
+  *t = 2.0 * (i0 - s) - 1.0;
+  return i0;
+}
+
+template <int W, int D>
+__device__ __forceinline__ int es_horner(double g, double *wts) {
+  double t;
+  const int i0 = es_arg<W>(g, &t);
+  const double u = t * t;
 #pragma unroll
-  for (int k = 0; k < W; k++) wts[k] = c_horner[W - 4][k][D];
-#pragma unroll
-  for (int j = D - 1; j >= 0; j--) {
-#pragma unroll
-    for (int k = 0; k < W; k++) wts[k] = fma(wts[k], t, c_horner[W - 4][k][j]);
+  for (int k = 0; k < (W + 1) / 2; k++) {
+    double wk, wm;
+    es_pair<W, D>(k, t, u, &wk, &wm);
+    wts[k] = wk;
+    if (W - 1 - k != k) wts[W - 1 - k] = wm;
   }
   return i0;
 }
@@ -80,6 +104,22 @@ __device__ __forceinline__ double es_tap(double t, int k) {
 #pragma unroll
   for (int j = D - 1; j >= 0; j--) v = fma(v, t, c_horner[W - 4][k][j]);
   return v;
+}
+
+// the same weights as es_horner by W separate Horner chains in t (lower register pressure in kernels that keep
+// a w x w window sweep live; the interpolation is bound by shared-memory reads, not by these DFMA)
+template <int W, int D>
+__device__ __forceinline__ int es_horner_chains(double g, double *wts) {
+  double t;
+  const int i0 = es_arg<W>(g, &t);
+#pragma unroll
+  for (int k = 0; k < W; k++) wts[k] = c_horner[W - 4][k][D];
+#pragma unroll
+  for (int j = D - 1; j >= 0; j--) {
+#pragma unroll
+    for (int k = 0; k < W; k++) wts[k] = fma(wts[k], t, c_horner[W - 4][k][j]);
+  }
+  return i0;
 }
 
 __device__ __forceinline__ int64_t wrapi(int64_t i, int64_t n) {
@@ -387,6 +427,7 @@ struct StripCfg {
   static constexpr int WXS = 33;            // padded x-weight rows (32 columns)
   static constexpr int WYS = (W + 1) & ~1;  // even stride: 16-byte aligned rows for double2 broadcasts
   static constexpr size_t smem_warp = (size_t)CH * (WXS + WYS) * 8;
+  static constexpr int NPMAX = (32 - W) / W + 1;  // column-disjoint W-wide footprints in one 32-lane window
 };
 
 template <int W, int D>
@@ -408,7 +449,8 @@ __global__ void __launch_bounds__(32 * VP_STRIP_WARPS, W <= 10 ? 5 : 4)
   double acc[W];
 #pragma unroll
   for (int b = 0; b < W; b++) acc[b] = 0.0;
-  int c0 = it.z, n = 0, q = 0, r = 0, mylr = 0x7fffffff, prev_lc = 0;
+  int c0 = it.z, n = 0, q = 0, r = 0, mylr = 0x7fffffff, prev_lc = 0, mylc = 0;
+  unsigned starts = 0;
   bool first = true;
   double *wrow = s_wx + lane * C::WXS;
 #pragma unroll
@@ -416,6 +458,7 @@ __global__ void __launch_bounds__(32 * VP_STRIP_WARPS, W <= 10 ? 5 : 4)
 stage:
   n = min(C::CH, it.w - c0);
   mylr = 0x7fffffff;
+  mylc = 1 << 20;
   if (lane < n) {
     const int j = c0 + lane;
     const double fj = __ldg(f + sperm[j]);
@@ -431,6 +474,7 @@ stage:
       for (int a = 0; a < W; a++) wrow[lc + a] = wx[a];
     }
     prev_lc = lc;
+    mylc = lc;
     double wy[W];
     lr = (int)(es_horner<W, D>(gcoord(sy[j], g.oy, g.inv_h), wy) - oy);
     double2 *wyp = (double2 *)(s_wy + lane * C::WYS);
@@ -440,6 +484,13 @@ stage:
     mylr = lr;
   }
   __syncwarp();
+  {
+    // packs: a staged point joins the previous one's pack when it has the same origin row and lies right of the
+    // previous member's footprint (the plan sorts each strip row into column-disjoint packs);
+    // one step of W DFMA per lane then adds a whole pack, each lane taking the member covering its column
+    const int plr = __shfl_up_sync(0xffffffffu, mylr, 1), plc = __shfl_up_sync(0xffffffffu, mylc, 1);
+    starts = __ballot_sync(0xffffffffu, lane == 0 || lane >= n || mylr != plr || mylc < plc + W);
+  }
   q = 0;
   if (first) {
     r = __shfl_sync(0xffffffffu, mylr, 0);
@@ -450,15 +501,23 @@ stage:
 #define VP_STRIP_PHASE(k)                                                              \
   case k:                                                                              \
     if ((k) < W) {                                                                     \
-      _Pragma("unroll 2") for (const int e = __popc(__ballot_sync(0xffffffffu, mylr <= r)); q < e; q++) { \
-        const double wxl = s_wx[q * C::WXS + lane];                                    \
-        const double2 *wyp = (const double2 *)(s_wy + q * C::WYS);                     \
+      for (const int e = __popc(__ballot_sync(0xffffffffu, mylr <= r)); q < e;) {      \
+        const unsigned later = q < 31 ? (starts >> (q + 1)) << (q + 1) : 0u;           \
+        const int q2 = min(later ? __ffs(later) - 1 : 32, e);                          \
+        int sel = q;                                                                   \
+        _Pragma("unroll") for (int m = 1; m < C::NPMAX; m++) {                         \
+          const int lcm = __shfl_sync(0xffffffffu, mylc, (q + m) & 31);                 \
+          if (q + m < q2 && lcm <= lane) sel = q + m;                                  \
+        }                                                                              \
+        const double wxl = s_wx[sel * C::WXS + lane];                                  \
+        const double2 *wyp = (const double2 *)(s_wy + sel * C::WYS);                   \
         _Pragma("unroll") for (int b = 0; b + 1 < W; b += 2) {                         \
           const double2 v = wyp[b >> 1];                                               \
           acc[((k) + b) % W] = fma(v.x, wxl, acc[((k) + b) % W]);                      \
           acc[((k) + b + 1) % W] = fma(v.y, wxl, acc[((k) + b + 1) % W]);              \
         }                                                                              \
-        if (W & 1) acc[((k) + W - 1) % W] = fma(s_wy[q * C::WYS + W - 1], wxl, acc[((k) + W - 1) % W]); \
+        if (W & 1) acc[((k) + W - 1) % W] = fma(s_wy[sel * C::WYS + W - 1], wxl, acc[((k) + W - 1) % W]); \
+        q = q2;                                                                        \
       }                                                                                \
       if (q == n) goto next_chunk;                                                     \
       red_row(col, oy + r, interior, g, acc[(k) % W]);                                 \
@@ -550,7 +609,8 @@ __global__ void __launch_bounds__(32 * VP_STRIP_WARPS, (KB <= 2 || W <= 10) ? 4 
   for (int k = 0; k < KB; k++)
 #pragma unroll
     for (int b = 0; b < W; b++) acc[k][b] = 0.0;
-  int c0 = it.z, n = 0, q = 0, r = 0, mylr = 0x7fffffff, prev_lc = 0;
+  int c0 = it.z, n = 0, q = 0, r = 0, mylr = 0x7fffffff, prev_lc = 0, mylc = 0;
+  unsigned starts = 0;
   bool first = true;
   double *wrow = s_wx + lane * C::WXS;
 #pragma unroll
@@ -558,6 +618,7 @@ __global__ void __launch_bounds__(32 * VP_STRIP_WARPS, (KB <= 2 || W <= 10) ? 4 
 stage:
   n = min(C::CH, it.w - c0);
   mylr = 0x7fffffff;
+  mylc = 1 << 20;
   if (lane < n) {
     const int j = c0 + lane;
     const int32_t node = sperm[j];
@@ -1181,8 +1242,8 @@ __global__ void __launch_bounds__(256, 4) k_interp_local(const int4 *__restrict_
     double v = 0.0;
     if (do_hist) {
       double wx[W], wy[W];
-      const int lx = (int)(es_horner<W, D>(gcoord(xc, g.ox, g.inv_h), wx) - ox);
-      const int ly = (int)(es_horner<W, D>(gcoord(yc, g.oy, g.inv_h), wy) - oy);
+      const int lx = (int)(es_horner_chains<W, D>(gcoord(xc, g.ox, g.inv_h), wx) - ox);
+      const int ly = (int)(es_horner_chains<W, D>(gcoord(yc, g.oy, g.inv_h), wy) - oy);
       const double *rp = tile + ly * nw + lx;
 #pragma unroll
       for (int b = 0; b < W; b++) {
@@ -1641,16 +1702,46 @@ __global__ void k_strip_keys(const double *__restrict__ xy, int64_t n, GridArgs 
   idx[i] = (int32_t)i;
 }
 
+// after the pack re-sort the strip id sits in key >> 32
 __global__ void k_strip_heads(const uint64_t *__restrict__ k, int64_t n, int32_t *__restrict__ head) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  head[i] = (i == 0 || (k[i - 1] >> 16) != (k[i] >> 16)) ? 1 : 0;
+  head[i] = (i == 0 || (k[i - 1] >> 32) != (k[i] >> 32)) ? 1 : 0;
 }
 
 __global__ void k_strip_ids(const uint64_t *__restrict__ k, const int32_t *__restrict__ pos, int64_t m,
                             int64_t *__restrict__ sid) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < m) sid[i] = (int64_t)(k[pos[i]] >> 16);
+  if (i < m) sid[i] = (int64_t)(k[pos[i]] >> 32);
+}
+
+// pack order inside each (strip, origin row) group of points sorted by column (the group's keys share key >> 8):
+// K = the most points in any W-column window of the group; point of rank i gets pack i mod K, so two points of a
+// pack are >= W columns apart (a closer pair would put K + 1 points in one window).  New key (strip, row, pack,
+// column); k_spread_strip packs consecutive column-disjoint points of a row.
+__global__ void k_group_heads(const uint64_t *__restrict__ k, int64_t n, int shift, int32_t *__restrict__ head) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  head[i] = (i == 0 || (k[i - 1] >> shift) != (k[i] >> shift)) ? 1 : 0;
+}
+
+__global__ void k_strip_pack_keys(const uint64_t *__restrict__ k, const int32_t *__restrict__ gpos, int64_t ng,
+                                  int64_t n, int W, uint64_t *__restrict__ k2) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const int64_t a = gpos[g], b = g + 1 < ng ? gpos[g + 1] : n;
+  int K = 1;
+  for (int64_t i = a, j = a; i < b; i++) {  // two pointers: points with column in (col_i - W, col_i]
+    const int ci = (int)(k[i] & 0xff);
+    while ((int)(k[j] & 0xff) <= ci - W) j++;
+    K = max(K, (int)(i - j + 1));
+  }
+  K = min(K, 65535);
+  for (int64_t i = a; i < b; i++) {
+    const uint64_t key = k[i];
+    const uint64_t strip = key >> 16, row = (key >> 8) & 0xff, col = key & 0xff;
+    k2[i] = (strip << 32) | (row << 24) | ((uint64_t)((i - a) % K) << 8) | col;
+  }
 }
 
 void vp_strip_dims(int W, int *SW, int *SH);
@@ -1668,7 +1759,7 @@ void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const 
     S.n_sitems = 0; S.n_batches = 0;
     return;
   }
-  if (nsx * nsy >= (int64_t)1 << 47) throw VpError{VP_ERR_UNSUPPORTED};
+  if (nsx * nsy >= (int64_t)1 << 31) throw VpError{VP_ERR_UNSUPPORTED};
   uint64_t *k1, *k1s;
   int32_t *i1, *i1s, *head, *hpos, *d_nh;
   int *d_bad;
@@ -1691,6 +1782,18 @@ void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const 
   void *tmp;
   VP_CUDA(cudaMallocAsync(&tmp, std::max(tb, tb3) + 16, s));
   VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
+  {  // re-sort every (strip, row) group into column-disjoint packs (k_strip_pack_keys)
+    k_group_heads<<<nb, 256, 0, s>>>(k1s, n, 8, head);
+    VP_CHECK_LAUNCH();
+    VP_CUDA(cub::DeviceSelect::Flagged(tmp, tb3, cnt, head, hpos, d_nh, (int)n, s));
+    int32_t ng = 0;
+    VP_CUDA(cudaMemcpyAsync(&ng, d_nh, 4, cudaMemcpyDeviceToHost, s));
+    VP_CUDA(cudaStreamSynchronize(s));
+    k_strip_pack_keys<<<(unsigned)((ng + 127) / 128), 128, 0, s>>>(k1s, hpos, ng, n, P->w, k1);
+    VP_CHECK_LAUNCH();
+    VP_CUDA(cudaMemcpyAsync(i1, i1s, 4 * (size_t)n, cudaMemcpyDeviceToDevice, s));
+    VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
+  }
   k_strip_heads<<<nb, 256, 0, s>>>(k1s, n, head);
   VP_CHECK_LAUNCH();
   VP_CUDA(cub::DeviceSelect::Flagged(tmp, tb3, cnt, head, hpos, d_nh, (int)n, s));

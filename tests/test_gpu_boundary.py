@@ -124,6 +124,7 @@ def test_boundary_errors():
     ch[5] += 1e-3
     assert _status(d, ("chunks", ch)) == vp.VP_ERR_GEOMETRY
     # medial axis within reach: delta_1 so large that 12 sqrt(delta_1) exceeds the radius
-    assert _status(d, ("chunks", geometry.circle_chunks(0.0, 0.0, 1.0, 32)), delta1_override=1e-2) == vp.VP_ERR_GEOMETRY
+    assert _status(d, ("chunks", geometry.circle_chunks(0.0, 0.0, 1.0, 32)), delta1_override=1e-2,
+                   levels=-1) == vp.VP_ERR_GEOMETRY
     # q out of range
     assert _status(d, ("chunks", geometry.circle_chunks(0.0, 0.0, 1.0, 32, q=1))) == vp.VP_ERR_UNSUPPORTED
