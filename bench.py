@@ -230,6 +230,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline sample sized to ~this many seconds")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=None, help="--impl reference: per-step oracle budget (s)")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="extra vp_opts field for A/B runs, e.g. --opt spread_pack=1 --opt fft_mode=1")
     ap.add_argument("--batch", type=int, default=4,
                     help="also time vp_eval_batch with this many fields (SURVEY §8(f) f3); 0 or 1 to skip")
     args = ap.parse_args()
@@ -258,8 +260,9 @@ def main():
     from workloads import rule
     # config 5: level bands off (delta_1 / sigma_min^2 = 0.016; parity 4.9e-10 without them)
     levels = -1 if w.name.startswith("c5") else 0
+    extra = {k: int(v) for k, v in (o.split("=") for o in args.opt)}
     plan = vp.Plan(nodes, wts, tg, w.tol, boundary=w.boundary, targets_are_nodes=w.targets_are_nodes, stream=stream,
-                   ref_nodes=rule.BARY[:, 1:3], levels=levels)
+                   ref_nodes=rule.BARY[:, 1:3], levels=levels, **extra)
     info = plan.info()
     out = torch.empty(w.T, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
@@ -392,7 +395,10 @@ def main():
                            "nf_nh": info["nf_nh"], "nf_fh": info["nf_fh"], "w_es": info["w_es"],
                            "deriv": f"{['auto', 'knn', 'triangle'][info['deriv_mode']]} (knn deg {info['deriv_degree']} "
                                     f"K {K_st} on {S_st} targets)", "levels": info["n_levels"], "plan_ms": info["plan_ms"],
-                           "spread": "register strips (k_spread_strip)", "spread_items": info["n_batches"]},
+                           "spread": "register strips (k_spread_strip)", "spread_items": info["n_batches"],
+                           "fft_path": {"nh": ["fused", "cufft2d", "rows+4step"][info["fft_path_nh"]],
+                                        "fh": ["fused", "cufft2d", "rows+4step"][info["fft_path_fh"]]},
+                           "opts": extra},
                 "phase_ms": ph, "serial_ms_per_step": serial_ms, "wall_ms_per_step": t_wall * 1e3 / args.steps,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "batch": batch,
                 "clocks": clk.summary(), "gpu_launches": kern * args.steps,

@@ -122,6 +122,9 @@ typedef struct {
   /* transforms: 0 -> fused row/column FFT with the spectral multiply in the column pass (vp_fft.cu) for
    * grids with nf <= 6400, cuFFT D2Z + multiply + Z2D otherwise; 1 -> cuFFT for every grid */
   int32_t fft_mode;
+  /* register-strip spreading: 0 -> one point per step, 1 -> column-disjoint packs of points per step (fewer DFMA
+   * and shared-memory loads, more integer work) */
+  int32_t spread_pack;
 } vp_opts;
 
 /* Plan parameters chosen by vp_plan (diagnostics; all derived from the rules in DESIGN.md). */
@@ -147,6 +150,8 @@ typedef struct {
   int64_t n_band_pairs;      /* (box, source) pairs spread per eval */
   int64_t nf_band;           /* band box fine grid per dimension */
   int64_t level_targets[16]; /* targets per level */
+  int32_t fft_path_nh, fft_path_fh; /* transforms of the NH / FH grid: 0 fused row/column kernels (nf <= 6400),
+                                       1 cuFFT 2D D2Z + multiply + Z2D, 2 cuFFT row passes + four-step column pass */
 } vp_info;
 
 typedef struct vp_plan_s *vp_handle;

@@ -39,7 +39,8 @@ class VpOpts(ctypes.Structure):
                 ("targets_are_nodes", ctypes.c_int32), ("boundary", VpBoundary), ("cuda_stream", ctypes.c_void_p),
                 ("ref_nodes", ctypes.c_void_p), ("tri_max_aspect", ctypes.c_double), ("levels", ctypes.c_int32),
                 ("level_cmin", ctypes.c_double), ("level_rho", ctypes.c_double), ("deterministic", ctypes.c_int32),
-                ("spread_tile", ctypes.c_int32), ("interp_tile", ctypes.c_int32), ("fft_mode", ctypes.c_int32)]
+                ("spread_tile", ctypes.c_int32), ("interp_tile", ctypes.c_int32), ("fft_mode", ctypes.c_int32),
+                ("spread_pack", ctypes.c_int32)]
 
 
 class VpInfo(ctypes.Structure):
@@ -55,7 +56,8 @@ class VpInfo(ctypes.Structure):
                 ("device_bytes", ctypes.c_int64), ("n_stencil_targets", ctypes.c_int64),
                 ("n_batches", ctypes.c_int64), ("horner_err", ctypes.c_double), ("n_levels", ctypes.c_int32),
                 ("n_boxes", ctypes.c_int64), ("n_level_targets", ctypes.c_int64), ("n_band_pairs", ctypes.c_int64),
-                ("nf_band", ctypes.c_int64), ("level_targets", ctypes.c_int64 * 16)]
+                ("nf_band", ctypes.c_int64), ("level_targets", ctypes.c_int64 * 16),
+                ("fft_path_nh", ctypes.c_int32), ("fft_path_fh", ctypes.c_int32)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -128,7 +130,8 @@ class Plan:
     def __init__(self, tri_nodes, weights, targets, tol, *, C=0.0, delta2_over_delta1=0.0, delta1_override=0.0,
                  eps_nufft=0.0, series_order=0, deriv="auto", deriv_degree=0, deriv_k=0, parts=PART_ALL,
                  targets_are_nodes=False, boundary=None, stream=None, ref_nodes=None, tri_max_aspect=0.0, levels=0,
-                 level_cmin=0.0, level_rho=0.0, deterministic=False, spread_tile=0, interp_tile=0, fft_mode=0):
+                 level_cmin=0.0, level_rho=0.0, deterministic=False, spread_tile=0, interp_tile=0, fft_mode=0,
+                 spread_pack=0):
         import torch
         L = lib()
         tri_nodes = _dev_f64(tri_nodes)
@@ -169,6 +172,7 @@ class Plan:
         o.levels, o.level_cmin, o.level_rho = levels, level_cmin, level_rho
         o.deterministic = 1 if deterministic else 0
         o.spread_tile, o.interp_tile, o.fft_mode = spread_tile, interp_tile, fft_mode
+        o.spread_pack = spread_pack
         h = ctypes.c_void_p()
         _check(L.vp_plan(tri_nodes.data_ptr(), weights.data_ptr(), M, p, targets.data_ptr(), T, float(tol),
                          ctypes.byref(o), ctypes.byref(h)), "vp_plan")

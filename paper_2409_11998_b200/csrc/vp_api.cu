@@ -403,17 +403,24 @@ static void make_fft_plans(vp_plan_s *P) {
     VpGrid &G = *gs[g];
     vp_fft_setup(P, G);
     if (G.own_fft) continue;
-    long long n[2] = {G.nf, G.nf};
-    long long rin[2] = {G.nf, G.row};         // real layout
-    long long cin[2] = {G.nf, G.crow / 2};    // complex layout
     VP_CUFFT(cufftCreate(&G.fwd));
     VP_CUFFT(cufftCreate(&G.inv));
     VP_CUFFT(cufftSetAutoAllocation(G.fwd, 0));
     VP_CUFFT(cufftSetAutoAllocation(G.inv, 0));
-    VP_CUFFT(cufftMakePlanMany64(G.fwd, 2, n, rin, 1, G.nf * G.row, cin, 1, G.nf * (G.crow / 2), CUFFT_D2Z, 1,
-                                 &ws[2 * g]));
-    VP_CUFFT(cufftMakePlanMany64(G.inv, 2, n, cin, 1, G.nf * (G.crow / 2), rin, 1, G.nf * G.row, CUFFT_Z2D, 1,
-                                 &ws[2 * g + 1]));
+    if (vp_fft4_setup(P, G)) {  // large grid: batched 1D row transforms + the four-step column pass (vp_fft.cu)
+      long long n1[1] = {G.nf}, rin1[1] = {G.row}, cin1[1] = {G.crow / 2};
+      VP_CUFFT(cufftMakePlanMany64(G.fwd, 1, n1, rin1, 1, G.row, cin1, 1, G.crow / 2, CUFFT_D2Z, G.nf, &ws[2 * g]));
+      VP_CUFFT(cufftMakePlanMany64(G.inv, 1, n1, cin1, 1, G.crow / 2, rin1, 1, G.row, CUFFT_Z2D, G.nf,
+                                   &ws[2 * g + 1]));
+    } else {
+      long long n[2] = {G.nf, G.nf};
+      long long rin[2] = {G.nf, G.row};         // real layout
+      long long cin[2] = {G.nf, G.crow / 2};    // complex layout
+      VP_CUFFT(cufftMakePlanMany64(G.fwd, 2, n, rin, 1, G.nf * G.row, cin, 1, G.nf * (G.crow / 2), CUFFT_D2Z, 1,
+                                   &ws[2 * g]));
+      VP_CUFFT(cufftMakePlanMany64(G.inv, 2, n, cin, 1, G.nf * (G.crow / 2), rin, 1, G.nf * G.row, CUFFT_Z2D, 1,
+                                   &ws[2 * g + 1]));
+    }
     G.has_plans = true;
   }
   // separate work areas: the NH and FH transforms run concurrently on different streams
@@ -482,6 +489,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     if (o.interp_tile < 0 || o.interp_tile > 128 || (o.interp_tile > 0 && o.interp_tile < 16)) throw VpError{VP_ERR_ARG};
     if (o.interp_tile > 0) P->TSI = o.interp_tile;
     if (o.fft_mode < 0 || o.fft_mode > 1) throw VpError{VP_ERR_ARG};
+    if (o.spread_pack < 0 || o.spread_pack > 1) throw VpError{VP_ERR_ARG};
     if (o.boundary.kind == VP_BDRY_CIRCLE && !(o.boundary.p[2] > 0)) throw VpError{VP_ERR_GEOMETRY};
     if (o.boundary.kind == VP_BDRY_RECT && !(o.boundary.p[2] > o.boundary.p[0] && o.boundary.p[3] > o.boundary.p[1]))
       throw VpError{VP_ERR_GEOMETRY};
@@ -633,6 +641,7 @@ static void grid_fft_fwd(vp_plan_s *P, VpGrid &G) {
 }
 static void grid_multiply(vp_plan_s *P, VpGrid &G) {
   if (G.own_fft) return vp_fft_columns(P, G);
+  if (G.four_step) return vp_fft4_columns(P, G);  // column FFT + multiply + inverse column FFT
   vp_launch_multiply(P, G);
 }
 static void grid_fft_inv(vp_plan_s *P, VpGrid &G) {
@@ -884,6 +893,8 @@ extern "C" vp_status vp_get_info(vp_handle P, vp_info *I) {
   I->n_band_pairs = P->bands.n_pairs;
   I->nf_band = P->bands.nfb;
   for (int i = 0; i < 16; i++) I->level_targets[i] = P->bands.lev_count[i];
+  I->fft_path_nh = P->nh.own_fft ? 0 : (P->nh.four_step ? 2 : 1);
+  I->fft_path_fh = P->fh.own_fft ? 0 : (P->fh.four_step ? 2 : 1);
   return VP_OK;
 }
 

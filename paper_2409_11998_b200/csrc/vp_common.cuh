@@ -77,6 +77,12 @@ struct VpGrid {
   double2 *spec2 = nullptr;                        // column-pass output, row-major [nf][ncs]
   double *fft_mult = nullptr;                      // multiplier table [ncs][nf] in DIF output order
   alignas(8) char fft_st_r[256] = {}, fft_st_c[256] = {};  // FftStages (row length nf/2, column length nf)
+  // four-step column pass for large grids (vp_fft.cu, nf = f4_N1 f4_N2; fft_st_r / fft_st_c hold the N1 / N2
+  // stages): rows by cuFFT batched 1D plans (rfwd / rinv)
+  bool four_step = false;
+  int f4_N1 = 0, f4_N2 = 0;
+  double2 *f4_tw1 = nullptr, *f4_tw2 = nullptr, *f4_twN = nullptr;
+  int32_t *f4_sig1 = nullptr, *f4_sig2 = nullptr;
 };
 
 struct VpTiles {          // sorted points binned into TS x TS tiles of a fine grid
@@ -279,6 +285,8 @@ void vp_fft_setup(vp_plan_s *P, VpGrid &G);
 void vp_fft_forward(vp_plan_s *P, VpGrid &G);
 void vp_fft_columns(vp_plan_s *P, VpGrid &G);
 void vp_fft_inverse(vp_plan_s *P, VpGrid &G);
+bool vp_fft4_setup(vp_plan_s *P, VpGrid &G);
+void vp_fft4_columns(vp_plan_s *P, VpGrid &G);
 void vp_launch_spread_batch(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, int K, const double *const *f,
                             double *const *grids, double *const *fs);
 bool vp_fft_setup_bands(vp_plan_s *P);

@@ -589,3 +589,243 @@ void vp_fft_bands(vp_plan_s *P) {
   VP_CHECK_LAUNCH();
   P->n_kernels += 3;
 }
+
+// =============================================================================================
+// Large grids (nf > 6400, e.g. config 5's 23328^2 NH grid): the row passes are cuFFT batched 1D D2Z / Z2D, the
+// column pass (forward FFT, multiply, inverse FFT of the kept columns) is a four-step
+// transform over nf = N1 N2 in three streaming kernels, each one HBM round trip over the kept columns (a column of
+// nf complex values no longer fits one CTA's shared memory):
+//   A: for each n2, the N1-point DIF FFTs over rows n1 N2 + n2 (stride N2), twiddle W_nf^{n2 k1}; in place,
+//      position p of the sequence holding k1 = sigma1(p)
+//   B: for each p, the N2-point DIF FFT over the contiguous rows p N2 + n2 (frequency k = sigma1(p) +
+//      N1 sigma2(p2)), the multiplier of k_multiply (same function, per element on the fly), the inverse N2-point
+//      DIT back to natural n2', twiddle W_nf^{-n2' k1}
+//   C: for each n2', the inverse N1-point DIT over positions p -> natural n1'; rows n1' N2 + n2'
+// (X(k1 + N1 k2) = sum_n2 W_N2^{n2 k2} W_nf^{n2 k1} sum_n1 W_N1^{n1 k1} x(n1 N2 + n2), and its transpose.)
+// A CTA owns TC4 consecutive kept columns (256-byte row segments) and transforms TC4 sequences at once.
+#define TC4 16
+
+template <int R, int DIR, bool DIT>
+__device__ __forceinline__ void fft_stage_m(double2 *a, int n, int S, int nseq, int Lp, float invLp,
+                                            const double2 *__restrict__ tw) {
+  const int L = Lp * R;
+  const int nb = n / R;
+  const int tstride = n / L;
+  for (int jj = threadIdx.x; jj < nb * nseq; jj += blockDim.x) {
+    const int seq = jj / nb, j = jj - seq * nb;
+    int b = __float2int_rz((float)j * invLp), k1 = j - b * Lp;
+    if (k1 < 0) {
+      b--;
+      k1 += Lp;
+    } else if (k1 >= Lp) {
+      b++;
+      k1 -= Lp;
+    }
+    double2 *base = a + seq * S + b * L + k1;
+    double2 v[R];
+#pragma unroll
+    for (int t = 0; t < R; t++) v[t] = base[t * Lp];
+    double2 w1 = make_double2(1.0, 0.0);
+    if (k1) {
+      w1 = __ldg(tw + k1 * tstride);
+      if (DIR > 0) w1.y = -w1.y;
+    }
+    if (!DIT) dft_small<R, DIR>(v);
+    if (k1) {
+      double2 w = w1;
+#pragma unroll
+      for (int t = 1; t < R; t++) {
+        v[t] = cmul(v[t], w);
+        if (t + 1 < R) w = cmul(w, w1);
+      }
+    }
+    if (DIT) dft_small<R, DIR>(v);
+#pragma unroll
+    for (int t = 0; t < R; t++) base[t * Lp] = v[t];
+  }
+}
+
+template <int DIR, bool DIT>
+__device__ void fft_run_m(double2 *a, const FftStages &st, int S, int nseq, const double2 *__restrict__ tw) {
+  for (int i = 0; i < st.S; i++) {
+    const int s = DIT ? i : st.S - 1 - i;
+    switch (st.r[s]) {
+      case 2: fft_stage_m<2, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
+      case 3: fft_stage_m<3, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
+      case 4: fft_stage_m<4, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
+      case 5: fft_stage_m<5, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
+      case 7: fft_stage_m<7, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
+      case 8: fft_stage_m<8, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
+      default: break;
+    }
+    __syncthreads();
+  }
+}
+
+struct Fft4Args {
+  double2 *spec;   // [nf][nc] half spectrum (row stride nc complex), kept columns 0..ncs-1 transformed in place
+  int64_t nc;      // nf / 2 + 1
+  int ncs, nf, N1, N2;
+  FftStages s1, s2;
+  const double2 *tw1, *tw2, *twN;  // W_N1^j, W_N2^j, W_nf^j
+  const int32_t *sig1, *sig2;      // DIF output position -> frequency
+  // multiplier (k_multiply): kind 0 NH / 1 FH, da, db, trapezoid/1/nf^2 scale, deconv[m], dk, truncation
+  int kind;
+  double da, db, scale, dk;
+  int64_t half_modes;
+  const double *deconv;
+};
+
+// sequence of N rows (global row index row0 + i * rstride, i < N) x TC4 columns -> shared a[col * S + i]
+__device__ __forceinline__ void fft4_load(double2 *a, const Fft4Args &g, int c0, int ncol, int64_t row0,
+                                          int64_t rstride, int N, int S) {
+  for (int e = threadIdx.x; e < N * TC4; e += blockDim.x) {
+    const int i = e / TC4, c = e - i * TC4;
+    if (c < ncol) a[c * S + i] = g.spec[(row0 + (int64_t)i * rstride) * g.nc + c0 + c];
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void fft4_store(const double2 *a, const Fft4Args &g, int c0, int ncol, int64_t row0,
+                                           int64_t rstride, int N, int S) {
+  __syncthreads();
+  for (int e = threadIdx.x; e < N * TC4; e += blockDim.x) {
+    const int i = e / TC4, c = e - i * TC4;
+    if (c < ncol) g.spec[(row0 + (int64_t)i * rstride) * g.nc + c0 + c] = a[c * S + i];
+  }
+}
+
+// A: blockIdx.x = column tile, blockIdx.y = n2
+__global__ void __launch_bounds__(256) k_fft4_a(Fft4Args g) {
+  extern __shared__ double2 sm2[];
+  const int c0 = blockIdx.x * TC4, ncol = min(TC4, g.ncs - c0), n2 = blockIdx.y;
+  const int S = g.N1 | 1;
+  fft4_load(sm2, g, c0, ncol, n2, g.N2, g.N1, S);
+  fft_run_m<-1, false>(sm2, g.s1, S, TC4, g.tw1);
+  for (int e = threadIdx.x; e < g.N1 * TC4; e += blockDim.x) {
+    const int c = e / g.N1, p = e - c * g.N1;
+    const int k1 = __ldg(g.sig1 + p);
+    sm2[c * S + p] = cmul(sm2[c * S + p], __ldg(g.twN + n2 * k1));  // n2 k1 < N2 N1 = nf
+  }
+  fft4_store(sm2, g, c0, ncol, n2, g.N2, g.N1, S);
+}
+
+// B: blockIdx.x = column tile, blockIdx.y = p (position of k1)
+__global__ void __launch_bounds__(256) k_fft4_b(Fft4Args g) {
+  extern __shared__ double2 sm2[];
+  const int c0 = blockIdx.x * TC4, ncol = min(TC4, g.ncs - c0), p = blockIdx.y;
+  const int S = g.N2 | 1;
+  const int64_t row0 = (int64_t)p * g.N2;
+  const int k1 = __ldg(g.sig1 + p);
+  fft4_load(sm2, g, c0, ncol, row0, 1, g.N2, S);
+  fft_run_m<-1, false>(sm2, g.s2, S, TC4, g.tw2);
+  for (int e = threadIdx.x; e < g.N2 * TC4; e += blockDim.x) {
+    const int c = e / g.N2, p2 = e - c * g.N2;
+    const int k = k1 + g.N1 * __ldg(g.sig2 + p2);
+    const int64_t m1 = c0 + c, m2 = k <= g.nf / 2 ? k : k - g.nf, a2m = m2 < 0 ? -m2 : m2;
+    double fac = 0.0;
+    if (m1 <= g.half_modes && a2m <= g.half_modes) {
+      const double k2 = g.dk * g.dk * ((double)m1 * m1 + (double)m2 * m2);
+      const double mk = g.kind == 0 ? vp_mult_nh(k2, g.da, g.db) : vp_mult_fh(k2, g.da, g.db);
+      fac = mk * g.scale * __ldg(g.deconv + m1) * __ldg(g.deconv + a2m);
+    }
+    const double2 v = sm2[c * S + p2];
+    sm2[c * S + p2] = make_double2(v.x * fac, v.y * fac);
+  }
+  __syncthreads();
+  fft_run_m<1, true>(sm2, g.s2, S, TC4, g.tw2);
+  for (int e = threadIdx.x; e < g.N2 * TC4; e += blockDim.x) {
+    const int c = e / g.N2, n2 = e - c * g.N2;
+    double2 w = __ldg(g.twN + n2 * k1);
+    w.y = -w.y;
+    sm2[c * S + n2] = cmul(sm2[c * S + n2], w);
+  }
+  fft4_store(sm2, g, c0, ncol, row0, 1, g.N2, S);
+}
+
+// C: blockIdx.x = column tile, blockIdx.y = n2'
+__global__ void __launch_bounds__(256) k_fft4_c(Fft4Args g) {
+  extern __shared__ double2 sm2[];
+  const int c0 = blockIdx.x * TC4, ncol = min(TC4, g.ncs - c0), n2 = blockIdx.y;
+  const int S = g.N1 | 1;
+  fft4_load(sm2, g, c0, ncol, n2, g.N2, g.N1, S);
+  fft_run_m<1, true>(sm2, g.s1, S, TC4, g.tw1);
+  fft4_store(sm2, g, c0, ncol, n2, g.N2, g.N1, S);
+}
+
+// nf = N1 N2 with both factors 2,3,5,7-smooth and N1 the divisor closest to sqrt(nf)
+static bool fft4_factor(int nf, int &N1, int &N2, FftStages &s1, FftStages &s2) {
+  int best = -1;
+  for (int d = 2; d * d <= nf * 4 && d < nf; d++) {
+    if (nf % d) continue;
+    FftStages a, b;
+    if (!factor_stages(d, a) || !factor_stages(nf / d, b)) continue;
+    if (d > 512 || nf / d > 512) continue;
+    if (best < 0 || std::abs(d - std::sqrt((double)nf)) < std::abs(best - std::sqrt((double)nf))) best = d;
+  }
+  if (best < 0) return false;
+  N1 = best;
+  N2 = nf / best;
+  return factor_stages(N1, s1) && factor_stages(N2, s2);
+}
+
+bool vp_fft4_setup(vp_plan_s *P, VpGrid &G) {
+  if (P->opts.fft_mode != 0 || G.nf <= 6400 || G.nf > (1 << 30)) return false;
+  int N1, N2;
+  FftStages s1, s2;
+  if (!fft4_factor((int)G.nf, N1, N2, s1, s2)) return false;
+  G.f4_N1 = N1;
+  G.f4_N2 = N2;
+  static_assert(sizeof(FftStages) <= sizeof(G.fft_st_r), "stage buffer");
+  memcpy(G.fft_st_r, &s1, sizeof(s1));
+  memcpy(G.fft_st_c, &s2, sizeof(s2));
+  G.f4_tw1 = twiddle_table(P, N1);
+  G.f4_tw2 = twiddle_table(P, N2);
+  G.f4_twN = twiddle_table(P, (int)G.nf);
+  std::vector<int32_t> g1, g2;
+  digit_sigma(s1, g1);
+  digit_sigma(s2, g2);
+  G.f4_sig1 = vp_alloc<int32_t>(P, N1);
+  G.f4_sig2 = vp_alloc<int32_t>(P, N2);
+  VP_CUDA(cudaMemcpy(G.f4_sig1, g1.data(), 4 * N1, cudaMemcpyHostToDevice));
+  VP_CUDA(cudaMemcpy(G.f4_sig2, g2.data(), 4 * N2, cudaMemcpyHostToDevice));
+  G.fft_ncs = (int)std::min<int64_t>(G.nmode / 2 + 1, G.nf / 2 + 1);
+  G.four_step = true;
+  return true;
+}
+
+void vp_fft4_columns(vp_plan_s *P, VpGrid &G) {
+  Fft4Args g;
+  g.spec = (double2 *)G.cdata;
+  g.nc = G.nf / 2 + 1;
+  g.ncs = G.fft_ncs;
+  g.nf = (int)G.nf;
+  g.N1 = G.f4_N1;
+  g.N2 = G.f4_N2;
+  memcpy(&g.s1, G.fft_st_r, sizeof(g.s1));
+  memcpy(&g.s2, G.fft_st_c, sizeof(g.s2));
+  g.tw1 = G.f4_tw1;
+  g.tw2 = G.f4_tw2;
+  g.twN = G.f4_twN;
+  g.sig1 = G.f4_sig1;
+  g.sig2 = G.f4_sig2;
+  g.kind = G.kind;
+  g.da = G.delta_a;
+  g.db = G.delta_b;
+  g.scale = G.mult_scale;
+  g.dk = 2.0 * VP_PI / G.L;
+  g.half_modes = G.nmode / 2;
+  g.deconv = G.deconv;
+  const unsigned ntile = (unsigned)((g.ncs + TC4 - 1) / TC4);
+  const size_t sm1 = sizeof(double2) * (size_t)TC4 * (g.N1 | 1), sm2 = sizeof(double2) * (size_t)TC4 * (g.N2 | 1);
+  k_fft4_a<<<dim3(ntile, g.N2), 256, sm1, P->stream>>>(g);
+  VP_CHECK_LAUNCH();
+  k_fft4_b<<<dim3(ntile, g.N1), 256, sm2, P->stream>>>(g);
+  VP_CHECK_LAUNCH();
+  k_fft4_c<<<dim3(ntile, g.N2), 256, sm1, P->stream>>>(g);
+  VP_CHECK_LAUNCH();
+  // the inverse row transforms read the whole half spectrum: the columns beyond the kept band are zero
+  const int64_t nz = g.nc - g.ncs;
+  if (nz > 0)
+    VP_CUDA(cudaMemset2DAsync(g.spec + g.ncs, sizeof(double2) * g.nc, 0, sizeof(double2) * nz, G.nf, P->stream));
+  P->n_kernels += 3;
+}

@@ -430,7 +430,7 @@ struct StripCfg {
   static constexpr int NPMAX = (32 - W) / W + 1;  // column-disjoint W-wide footprints in one 32-lane window
 };
 
-template <int W, int D>
+template <int W, int D, bool PACK>
 __global__ void __launch_bounds__(32 * VP_STRIP_WARPS, W <= 10 ? 5 : 4)
     k_spread_strip(const int4 *__restrict__ items, int64_t n_items, const double *__restrict__ sx,
                    const double *__restrict__ sy, const double *__restrict__ sw, const int32_t *__restrict__ sperm,
@@ -489,7 +489,7 @@ stage:
     // previous member's footprint (the plan sorts each strip row into column-disjoint packs);
     // one step of W DFMA per lane then adds a whole pack, each lane taking the member covering its column
     const int plr = __shfl_up_sync(0xffffffffu, mylr, 1), plc = __shfl_up_sync(0xffffffffu, mylc, 1);
-    starts = __ballot_sync(0xffffffffu, lane == 0 || lane >= n || mylr != plr || mylc < plc + W);
+    starts = __ballot_sync(0xffffffffu, !PACK || lane == 0 || lane >= n || mylr != plr || mylc < plc + W);
   }
   q = 0;
   if (first) {
@@ -505,7 +505,7 @@ stage:
         const unsigned later = q < 31 ? (starts >> (q + 1)) << (q + 1) : 0u;           \
         const int q2 = min(later ? __ffs(later) - 1 : 32, e);                          \
         int sel = q;                                                                   \
-        _Pragma("unroll") for (int m = 1; m < C::NPMAX; m++) {                         \
+        if (PACK) _Pragma("unroll") for (int m = 1; m < C::NPMAX; m++) {               \
           const int lcm = __shfl_sync(0xffffffffu, mylc, (q + m) & 31);                 \
           if (q + m < q2 && lcm <= lane) sel = q + m;                                  \
         }                                                                              \
@@ -547,10 +547,16 @@ static void launch_spread_strip_w(vp_plan_s *P, const VpSpreadSet &S, const Grid
   constexpr int D = VP_HORNER_DEG(W);
   if (S.n_sitems == 0) return;
   const size_t sm = StripCfg<W>::smem_warp * VP_STRIP_WARPS;
-  vp_smem_attr((const void *)k_spread_strip<W, D>, sm);
   const unsigned nb = (unsigned)((S.n_sitems + VP_STRIP_WARPS - 1) / VP_STRIP_WARPS);
-  k_spread_strip<W, D><<<nb, 32 * VP_STRIP_WARPS, sm, P->stream>>>(S.sitems, S.n_sitems, S.sx, S.sy, S.sw, S.sperm,
-                                                                   f, g, S.fs_out);
+  if (P->opts.spread_pack == 1) {
+    vp_smem_attr((const void *)k_spread_strip<W, D, true>, sm);
+    k_spread_strip<W, D, true><<<nb, 32 * VP_STRIP_WARPS, sm, P->stream>>>(S.sitems, S.n_sitems, S.sx, S.sy, S.sw,
+                                                                           S.sperm, f, g, S.fs_out);
+  } else {
+    vp_smem_attr((const void *)k_spread_strip<W, D, false>, sm);
+    k_spread_strip<W, D, false><<<nb, 32 * VP_STRIP_WARPS, sm, P->stream>>>(S.sitems, S.n_sitems, S.sx, S.sy, S.sw,
+                                                                            S.sperm, f, g, S.fs_out);
+  }
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }

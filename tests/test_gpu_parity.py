@@ -472,3 +472,29 @@ def test_fused_fft_grid_sizes():
         sizes.add(nf)
         assert np.max(np.abs(out[0] - out[1])) <= 1e-12 * np.max(np.abs(out[1])), nf
     assert any((n // 2) % 2 == 1 for n in sizes), sorted(sizes)
+
+
+@pytest.mark.parametrize("d1", [6e-8, 2.4e-8, 8e-9])
+def test_four_step_matches_cufft(d1):
+    """Grids above 6400^2 (configs 4 and 5): cuFFT batched row passes + the four-step column pass with the
+    multiply on the fly (default, fft_path 2) vs cuFFT 2D D2Z + k_multiply + Z2D (fft_mode=1) on the same plan
+    inputs; and the smooth part vs the direct G_H sum."""
+    rng = np.random.default_rng(141)
+    src = rng.uniform(0.02, 0.98, (1200, 2))
+    nodes = torch.from_numpy(src.reshape(100, 12, 2).copy()).to(DEV)
+    wts = torch.from_numpy(rng.uniform(0.5, 1.5, (100, 12)) / 1200).to(DEV)
+    fv = torch.from_numpy(rng.standard_normal((100, 12))).to(DEV)
+    tg_np = np.concatenate([rng.uniform(0.0, 1.0, (300, 2)), src[:20]])
+    tg = torch.from_numpy(tg_np).to(DEV)
+    out, paths = [], []
+    for mode in (0, 1):
+        plan = vp.Plan(nodes, wts, tg, 1e-10, parts=vp.PART_HISTORY, delta1_override=d1, fft_mode=mode)
+        out.append(plan.eval(fv).cpu().numpy())
+        info = plan.info()
+        paths.append((info["fft_path_nh"], info["fft_path_fh"], info["nf_nh"], info["nf_fh"]))
+        plan.destroy()
+    print("four-step", d1, paths)
+    assert paths[0][0] == 2 and paths[1][0] == 1
+    assert np.max(np.abs(out[0] - out[1])) <= 1e-12 * np.max(np.abs(out[1])), paths
+    ref = oracle.smooth_direct(src, (fv.cpu().numpy() * wts.cpu().numpy()).ravel(), tg_np, d1)
+    assert rel_l2(out[0], ref) < 1e-9
