@@ -313,7 +313,7 @@ def main():
     # ---- roofline (SURVEY §8(d) bytes model): per unit, spread reads x, y, w, f (32 B per source)
     # and writes the NH grid once (8 B per cell); interp_local reads x, y and writes out (24 B per target), reads
     # the NH grid once (8 B per cell) and the node target's own f or V_L word (8 B per node target).  KNN
-    # stencil entries (12 B each) are reported separately as overhead, not as algorithmic bytes.
+    # stencil entries (8 B each: int32 index + fp32 weight) are reported separately as overhead, not as algorithmic bytes.
     cells = float(info["nf_nh"]) ** 2
     K_st = info["deriv_k"]
     S_st = info["n_stencil_targets"]
@@ -337,7 +337,7 @@ def main():
             "spread_plus_interp": {"ms": both_ms, "algorithmic_bytes": alg["spread"] + alg["interp_local"],
                                    "frac": (alg["spread"] + alg["interp_local"]) / (both_ms * 1e-3) / 1e9 / hbm,
                                    "north_star_target_frac": 0.5},
-            "overhead_bytes": {"knn_stencil": 12.0 * K_st * S_st, "stencil_targets": S_st, "stencil_k": K_st},
+            "overhead_bytes": {"knn_stencil": 8.0 * K_st * S_st, "stencil_targets": S_st, "stencil_k": K_st},
             "bytes_model": "SURVEY §8(d): spread 32 B/source + 8 B/NH cell; interp 24 B/target + 8 B/NH cell + "
                            "8 B/node target; phase times from the serial profiled evals (phase_ms)",
             "co_bound": "fp64 issue + shared-memory wavefronts (DESIGN.md §5.1/§5.4, profiles/r2/microbench)"}

@@ -140,7 +140,7 @@ struct VpBands {
   int8_t *tlev = nullptr;         // [T] level per sorted target
   // staged interpolation of the entries (k_interp_local on the virtual grid): entries in (tile, bank) order
   double *e_x = nullptr, *e_y = nullptr;
-  int64_t *e_perm = nullptr;      // staged order -> entry index
+  int32_t *e_perm = nullptr;      // staged order -> entry index
   int4 *e_items = nullptr;
   int64_t e_n_items = 0;
   double *ent_val = nullptr;      // [n_ent] band value per entry
@@ -203,14 +203,14 @@ struct vp_plan_s {
   double *scratch = nullptr;                           // n1 x e_n
   // targets, sorted by (TSI x TSI NH-grid tile, bank-slot rank) and cut into interpolation work items
   double *tx = nullptr, *ty = nullptr;
-  int64_t *tperm = nullptr;  // sorted -> user target index
+  int32_t *tperm = nullptr;  // sorted -> user target index (T < 2^31, checked in vp_plan)
   int TSI = 64;
   int4 *items = nullptr;     // (tile_x, tile_y, first target, end target)
   int64_t n_items = 0;
   // local part: V_L(t) = alpha_t * f(node_t) + sum_k omega_{t,k} f[idx_{t,k}]
   int K = 0, deg = 0, dmode = 0;
   int32_t *lidx = nullptr;     // [T][K] user node indices (sorted target order)
-  double *lw = nullptr;        // [T][K]
+  float *lw = nullptr;         // [S][K] stencil weights (fp32: the stencil carries terms <= 1e-5 of V, R6)
   double *lalpha = nullptr;    // [T]
   int32_t *lnode = nullptr;    // [T] user node index of the target (targets_are_nodes) or -1
   int64_t n_bdry = 0;
@@ -294,7 +294,7 @@ void vp_fft_bands(vp_plan_s *P);
 void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const double *weights,
                           const int32_t *node_of, int64_t n, const GridArgs &g);
 void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx,
-                             double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items);
+                             double **oty, int32_t **otperm, int4 **oitems, int64_t *on_items);
 void vp_remap_stencils(vp_plan_s *P);
 void vp_build_local(vp_plan_s *P, const double *nodes_dev);
 void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop);

@@ -438,6 +438,26 @@ static size_t fft_row_smem(int nr, int ncs) {
 }
 
 
+// DFT roots of the odd radices in the constant bank (dft_small): uploaded once per device (same values for
+// every plan); every transform path that runs dft_small calls this at plan time
+static void upload_dft_roots() {
+  static std::mutex mu;
+  static std::set<int> done;
+  const int dev = vp_current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(dev)) return;
+  double hc[9][8] = {}, hs[9][8] = {};
+  for (int R = 2; R <= 8; R++)
+    for (int j = 0; j < R; j++) {
+      const long double ang = 2.0L * 3.141592653589793238462643383279502884L * j / R;
+      hc[R][j] = (double)cosl(ang);
+      hs[R][j] = (double)sinl(ang);
+    }
+  VP_CUDA(cudaMemcpyToSymbol(c_dft_c, hc, sizeof(hc)));
+  VP_CUDA(cudaMemcpyToSymbol(c_dft_s, hs, sizeof(hs)));
+  done.insert(dev);
+}
+
 // decide and build the fused transform for grid G (opts.fft_mode 0: where it fits shared memory)
 // stage plans, twiddles and digit maps of an nf x nf transform (false: size not supported)
 static bool fft_tables(vp_plan_s *P, VpGrid &G) {
@@ -447,24 +467,7 @@ static bool fft_tables(vp_plan_s *P, VpGrid &G) {
   if (nf % 2 || nf > 6400) return false;
   FftStages sr, sc;
   if (!factor_stages(nf / 2, sr) || !factor_stages(nf, sc)) return false;
-  {  // DFT roots in the constant bank: uploaded once per device (same values for every plan)
-    static std::mutex mu;
-    static std::set<int> done;
-    const int dev = vp_current_device();
-    std::lock_guard<std::mutex> lk(mu);
-    if (done.count(dev)) goto uploaded;
-    double hc[9][8] = {}, hs[9][8] = {};
-    for (int R = 2; R <= 8; R++)
-      for (int j = 0; j < R; j++) {
-        const long double ang = 2.0L * 3.141592653589793238462643383279502884L * j / R;
-        hc[R][j] = (double)cosl(ang);
-        hs[R][j] = (double)sinl(ang);
-      }
-    VP_CUDA(cudaMemcpyToSymbol(c_dft_c, hc, sizeof(hc)));
-    VP_CUDA(cudaMemcpyToSymbol(c_dft_s, hs, sizeof(hs)));
-    done.insert(dev);
-  }
-uploaded:
+  upload_dft_roots();
   G.fft_ncs = (int)(G.nmode / 2 + 1);
   if (G.fft_ncs > nf / 2 + 1) G.fft_ncs = nf / 2 + 1;
   G.tw_r = twiddle_table(P, nf / 2);
@@ -773,6 +776,7 @@ bool vp_fft4_setup(vp_plan_s *P, VpGrid &G) {
   int N1, N2;
   FftStages s1, s2;
   if (!fft4_factor((int)G.nf, N1, N2, s1, s2)) return false;
+  upload_dft_roots();  // odd-radix butterflies read the constant-bank roots
   G.f4_N1 = N1;
   G.f4_N2 = N2;
   static_assert(sizeof(FftStages) <= sizeof(G.fft_st_r), "stage buffer");
@@ -817,6 +821,9 @@ void vp_fft4_columns(vp_plan_s *P, VpGrid &G) {
   g.deconv = G.deconv;
   const unsigned ntile = (unsigned)((g.ncs + TC4 - 1) / TC4);
   const size_t sm1 = sizeof(double2) * (size_t)TC4 * (g.N1 | 1), sm2 = sizeof(double2) * (size_t)TC4 * (g.N2 | 1);
+  vp_smem_attr((const void *)k_fft4_a, sm1);
+  vp_smem_attr((const void *)k_fft4_b, sm2);
+  vp_smem_attr((const void *)k_fft4_c, sm1);
   k_fft4_a<<<dim3(ntile, g.N2), 256, sm1, P->stream>>>(g);
   VP_CHECK_LAUNCH();
   k_fft4_b<<<dim3(ntile, g.N1), 256, sm2, P->stream>>>(g);

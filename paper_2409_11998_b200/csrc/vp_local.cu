@@ -29,7 +29,7 @@ struct LocalArgs {
   double bo_x, bo_y, bcell;
   int64_t nbx, nby;
   const double *tx, *ty;          // sorted targets
-  const int64_t *tperm;
+  const int32_t *tperm;
   const int32_t *list;            // targets (sorted index) that get a stencil; slot i -> target list[i]
   int64_t T;                      // number of list entries
   int K, deg, nterms;
@@ -37,7 +37,8 @@ struct LocalArgs {
   double delta;
   VpBdryDev bd;
   int32_t *lidx;                  // stencils, k-major: entry k of slot s at [k * stride + s]
-  double *lw, *lalpha;
+  float *lw;
+  double *lalpha;
   int64_t slot0, stride;          // global slot of list entry 0; number of stencil slots
   int32_t *lnode;
   int32_t *is_bdry;
@@ -194,7 +195,7 @@ __global__ void k_build_local(LocalArgs a) {
   const int64_t gs = a.slot0 + slot;
   for (int k = 0; k < K; k++) {
     a.lidx[k * a.stride + gs] = a.kperm[hi[k]];
-    a.lw[k * a.stride + gs] = yv[k];
+    a.lw[k * a.stride + gs] = (float)yv[k];
   }
   a.lalpha[t] = alpha;
   a.lnode[t] = node;
@@ -314,7 +315,7 @@ void vp_cubic_hessian_ops(const double *ref, int p, std::vector<double> &Hop) {
 }
 
 // per sorted target: triangle mode (interior node of an ok triangle) or stencil
-__global__ void k_target_mode(const double *tx, const double *ty, const int64_t *tperm, int64_t T, int p,
+__global__ void k_target_mode(const double *tx, const double *ty, const int32_t *tperm, int64_t T, int p,
                               const int8_t *tri_ok, int64_t node_targets, VpBdryDev bd, double delta, double c1,
                               const int8_t *tlev, int32_t *need, double *lalpha, int32_t *lnode) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -428,7 +429,7 @@ void vp_build_local(vp_plan_s *P, const double *nodes_dev) {
   }
   P->st_vL = vp_alloc<double>(P, (size_t)std::max<int64_t>(nst, 1));
   P->lidx = vp_alloc<int32_t>(P, (size_t)std::max<int64_t>(nst, 1) * K);
-  P->lw = vp_alloc<double>(P, (size_t)std::max<int64_t>(nst, 1) * K);
+  P->lw = vp_alloc<float>(P, (size_t)std::max<int64_t>(nst, 1) * K);
   int32_t *isb = nullptr;
   VP_CUDA(cudaMallocAsync(&isb, sizeof(int32_t) * (P->T + 1), st));
   VP_CUDA(cudaMemsetAsync(isb, 0, sizeof(int32_t) * (P->T + 1), st));

@@ -1178,7 +1178,7 @@ void vp_launch_multiply(vp_plan_s *P, VpGrid &G) {
 template <int W, int D>
 __global__ void __launch_bounds__(256, 4) k_interp_local(const int4 *__restrict__ items, int TSI,
                                                       const double *__restrict__ tx, const double *__restrict__ ty,
-                                                      const int64_t *__restrict__ tperm, GridArgs g, int do_hist,
+                                                      const int32_t *__restrict__ tperm, GridArgs g, int do_hist,
                                                       const double *__restrict__ f, const double *__restrict__ lalpha,
                                                       const int32_t *__restrict__ lnode, int do_local,
                                                       const int32_t *__restrict__ lptr,
@@ -1231,7 +1231,7 @@ __global__ void __launch_bounds__(256, 4) k_interp_local(const int4 *__restrict_
       xn = tx[tn];
       yn = ty[tn];
     }
-    const int64_t dst = tperm[t];
+    const int32_t dst = tperm[t];
     double vl = 0.0;
     if (do_local) {
       const int32_t nd = lnode[t];
@@ -1353,14 +1353,14 @@ __global__ void __launch_bounds__(128) k_tri_local12(const double *__restrict__ 
 
 // KNN-stencil local part, one thread per stencil slot: vL_st[s] = sum_k w[k][s] f[idx[k][s]] (k-major layout:
 // the warp streams consecutive slots, 12 B per entry, HBM-bound; f gathers hit L2)
-__global__ void __launch_bounds__(256) k_local_stencil(const int32_t *__restrict__ lidx, const double *__restrict__ lw,
+__global__ void __launch_bounds__(256) k_local_stencil(const int32_t *__restrict__ lidx, const float *__restrict__ lw,
                                                        int K, int64_t S, const double *__restrict__ f,
                                                        double *__restrict__ vL_st) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= S) return;
   double acc = 0.0;
 #pragma unroll 8
-  for (int k = 0; k < K; k++) acc = fma(__ldcs(lw + k * S + s), __ldg(f + __ldcs(lidx + k * S + s)), acc);
+  for (int k = 0; k < K; k++) acc = fma((double)__ldcs(lw + k * S + s), __ldg(f + __ldcs(lidx + k * S + s)), acc);
   vL_st[s] = acc;
 }
 
@@ -1481,7 +1481,7 @@ __global__ void k_interp_keys2(const uint64_t *__restrict__ k1, int64_t n, uint6
 }
 
 void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx,
-                             double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items);
+                             double **oty, int32_t **otperm, int4 **oitems, int64_t *on_items);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
   vp_build_interp_order_g(P, xy, n, grid_args(P->nh), &P->tx, &P->ty, &P->tperm, &P->items, &P->n_items);
 }
@@ -1489,7 +1489,7 @@ void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n) {
 // targets (xy interleaved, n) of grid g ordered for k_interp_local: *tx, *ty, *tperm (sorted -> input index),
 // work items.  (A (tile, triangle, node) order that coalesces the per-node V_L reads cost more bank
 // conflicts than it saved: config 5 interp 9.7 -> 11.8 ms.)
-void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx, double **oty, int64_t **otperm, int4 **oitems, int64_t *on_items) {
+void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx, double **oty, int32_t **otperm, int4 **oitems, int64_t *on_items) {
   cudaStream_t s = P->stream;
   const int TSI = P->TSI;
   const int64_t ntx = (g.nfx + TSI - 1) / TSI, nty = (g.nfy + TSI - 1) / TSI;
@@ -1519,8 +1519,8 @@ void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const Gr
   VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb2, k2, k2s, i1s, i2s, (int)n, 0, 64, s));
   *otx = vp_alloc<double>(P, n);
   *oty = vp_alloc<double>(P, n);
-  *otperm = vp_alloc<int64_t>(P, n);
-  k_gather_xy<<<nb, 256, 0, s>>>(xy, i2s, n, *otx, *oty, *otperm, nullptr);
+  *otperm = vp_alloc<int32_t>(P, n);
+  k_gather_xy<<<nb, 256, 0, s>>>(xy, i2s, n, *otx, *oty, nullptr, *otperm);
   VP_CHECK_LAUNCH();
   std::vector<uint64_t> hk(n);
   VP_CUDA(cudaMemcpyAsync(hk.data(), k2s, 8 * n, cudaMemcpyDeviceToHost, s));
@@ -1750,6 +1750,13 @@ __global__ void k_strip_pack_keys(const uint64_t *__restrict__ k, const int32_t 
   }
 }
 
+__global__ void k_strip_key_shift(uint64_t *__restrict__ k, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t key = k[i];
+  k[i] = ((key >> 16) << 32) | (((key >> 8) & 0xff) << 24) | (key & 0xff);
+}
+
 void vp_strip_dims(int W, int *SW, int *SH);
 
 void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const double *weights,
@@ -1788,7 +1795,7 @@ void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const 
   void *tmp;
   VP_CUDA(cudaMallocAsync(&tmp, std::max(tb, tb3) + 16, s));
   VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
-  {  // re-sort every (strip, row) group into column-disjoint packs (k_strip_pack_keys)
+  if (P->opts.spread_pack == 1) {  // re-sort every (strip, row) group into column-disjoint packs
     k_group_heads<<<nb, 256, 0, s>>>(k1s, n, 8, head);
     VP_CHECK_LAUNCH();
     VP_CUDA(cub::DeviceSelect::Flagged(tmp, tb3, cnt, head, hpos, d_nh, (int)n, s));
@@ -1799,6 +1806,9 @@ void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const 
     VP_CHECK_LAUNCH();
     VP_CUDA(cudaMemcpyAsync(i1, i1s, 4 * (size_t)n, cudaMemcpyDeviceToDevice, s));
     VP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k1s, i1, i1s, (int)n, 0, 64, s));
+  } else {  // (strip, row, column) order; strip id moved to key >> 32 like the pack keys
+    k_strip_key_shift<<<nb, 256, 0, s>>>(k1s, n);
+    VP_CHECK_LAUNCH();
   }
   k_strip_heads<<<nb, 256, 0, s>>>(k1s, n, head);
   VP_CHECK_LAUNCH();
@@ -1954,7 +1964,7 @@ __global__ void k_multiply_bands(double *__restrict__ data, int64_t nbox, int64_
 
 // per-target sum of its band entries (CSR by target) into out
 __global__ void k_band_sum(const int32_t *__restrict__ lt_t, const int32_t *__restrict__ lt_off, int64_t n_lt,
-                           const double *__restrict__ ent_val, const int64_t *__restrict__ tperm,
+                           const double *__restrict__ ent_val, const int32_t *__restrict__ tperm,
                            double *__restrict__ out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n_lt) return;

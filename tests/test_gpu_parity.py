@@ -498,3 +498,30 @@ def test_four_step_matches_cufft(d1):
     assert np.max(np.abs(out[0] - out[1])) <= 1e-12 * np.max(np.abs(out[1])), paths
     ref = oracle.smooth_direct(src, (fv.cpu().numpy() * wts.cpu().numpy()).ravel(), tg_np, d1)
     assert rel_l2(out[0], ref) < 1e-9
+
+
+def test_four_step_fresh_process():
+    """A process whose first (and only) plan uses the four-step column pass: the constant-bank DFT roots of the
+    odd radices must be uploaded by that path itself (regression: they were uploaded only by the fused path)."""
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2409_11998_b200 as vp
+rng = np.random.default_rng(3)
+src = rng.uniform(0.0, 1.0, (1200, 2))
+nodes = torch.from_numpy(src.reshape(100, 12, 2).copy()).cuda()
+wts = torch.from_numpy(rng.uniform(0.5, 1.5, (100, 12)) / 1200).cuda()
+fv = torch.from_numpy(rng.standard_normal((100, 12))).cuda()
+tg = torch.from_numpy(rng.uniform(0.0, 1.0, (200, 2))).cuda()
+out = []
+for mode in (0, 1):
+    p = vp.Plan(nodes, wts, tg, 1e-13, parts=vp.PART_HISTORY, delta1_override=6.25e-8, fft_mode=mode)
+    assert p.info()["fft_path_fh"] == (2 if mode == 0 else 1)
+    out.append(p.eval(fv).cpu().numpy())
+print(np.max(np.abs(out[0] - out[1])) / np.max(np.abs(out[1])))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) < 1e-12, r.stdout
