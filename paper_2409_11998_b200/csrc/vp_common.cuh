@@ -83,6 +83,7 @@ struct VpGrid {
   int f4_N1 = 0, f4_N2 = 0;
   double2 *f4_tw1 = nullptr, *f4_tw2 = nullptr, *f4_twN = nullptr;
   int32_t *f4_sig1 = nullptr, *f4_sig2 = nullptr;
+  double *f4_e1 = nullptr, *f4_e2 = nullptr;  // NH: e^{-dk^2 m^2 delta_a}, e^{-dk^2 m^2 delta_b}
 };
 
 struct VpTiles {          // sorted points binned into TS x TS tiles of a fine grid

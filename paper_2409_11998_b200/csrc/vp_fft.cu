@@ -608,14 +608,18 @@ void vp_fft_bands(vp_plan_s *P) {
 // A CTA owns TC4 consecutive kept columns (256-byte row segments) and transforms TC4 sequences at once.
 #define TC4 16
 
+// shared layout of a tile: element i of column c at a[i * TC4 + c]; thread (c, q) = (tid % TC4, tid / TC4) works
+// on column c, butterflies / elements q, q + 256 / TC4, ...: a row of TC4 columns is one contiguous 256-byte
+// segment both in HBM and in shared memory, and no integer division by a runtime length is needed
+#define Q4 (256 / TC4)
+
 template <int R, int DIR, bool DIT>
-__device__ __forceinline__ void fft_stage_m(double2 *a, int n, int S, int nseq, int Lp, float invLp,
-                                            const double2 *__restrict__ tw) {
+__device__ __forceinline__ void fft_stage_t(double2 *a, int n, int Lp, float invLp, const double2 *__restrict__ tw) {
   const int L = Lp * R;
   const int nb = n / R;
   const int tstride = n / L;
-  for (int jj = threadIdx.x; jj < nb * nseq; jj += blockDim.x) {
-    const int seq = jj / nb, j = jj - seq * nb;
+  const int c = threadIdx.x % TC4;
+  for (int j = threadIdx.x / TC4; j < nb; j += Q4) {
     int b = __float2int_rz((float)j * invLp), k1 = j - b * Lp;
     if (k1 < 0) {
       b--;
@@ -624,10 +628,10 @@ __device__ __forceinline__ void fft_stage_m(double2 *a, int n, int S, int nseq, 
       b++;
       k1 -= Lp;
     }
-    double2 *base = a + seq * S + b * L + k1;
+    double2 *base = a + (b * L + k1) * TC4 + c;
     double2 v[R];
 #pragma unroll
-    for (int t = 0; t < R; t++) v[t] = base[t * Lp];
+    for (int t = 0; t < R; t++) v[t] = base[t * Lp * TC4];
     double2 w1 = make_double2(1.0, 0.0);
     if (k1) {
       w1 = __ldg(tw + k1 * tstride);
@@ -644,21 +648,21 @@ __device__ __forceinline__ void fft_stage_m(double2 *a, int n, int S, int nseq, 
     }
     if (DIT) dft_small<R, DIR>(v);
 #pragma unroll
-    for (int t = 0; t < R; t++) base[t * Lp] = v[t];
+    for (int t = 0; t < R; t++) base[t * Lp * TC4] = v[t];
   }
 }
 
 template <int DIR, bool DIT>
-__device__ void fft_run_m(double2 *a, const FftStages &st, int S, int nseq, const double2 *__restrict__ tw) {
+__device__ void fft_run_t(double2 *a, const FftStages &st, const double2 *__restrict__ tw) {
   for (int i = 0; i < st.S; i++) {
     const int s = DIT ? i : st.S - 1 - i;
     switch (st.r[s]) {
-      case 2: fft_stage_m<2, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
-      case 3: fft_stage_m<3, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
-      case 4: fft_stage_m<4, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
-      case 5: fft_stage_m<5, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
-      case 7: fft_stage_m<7, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
-      case 8: fft_stage_m<8, DIR, DIT>(a, st.n, S, nseq, st.Lp[s], st.invLp[s], tw); break;
+      case 2: fft_stage_t<2, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 3: fft_stage_t<3, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 4: fft_stage_t<4, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 5: fft_stage_t<5, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 7: fft_stage_t<7, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 8: fft_stage_t<8, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
       default: break;
     }
     __syncthreads();
@@ -677,82 +681,88 @@ struct Fft4Args {
   double da, db, scale, dk;
   int64_t half_modes;
   const double *deconv;
+  const double *e1, *e2;  // NH: e^{-dk^2 m^2 delta_1}, e^{-dk^2 m^2 delta_2} for m <= half_modes (separable exponentials)
 };
 
-// sequence of N rows (global row index row0 + i * rstride, i < N) x TC4 columns -> shared a[col * S + i]
+// N rows (global row row0 + i * rstride) x TC4 columns <-> shared a[i * TC4 + c]
 __device__ __forceinline__ void fft4_load(double2 *a, const Fft4Args &g, int c0, int ncol, int64_t row0,
-                                          int64_t rstride, int N, int S) {
-  for (int e = threadIdx.x; e < N * TC4; e += blockDim.x) {
-    const int i = e / TC4, c = e - i * TC4;
-    if (c < ncol) a[c * S + i] = g.spec[(row0 + (int64_t)i * rstride) * g.nc + c0 + c];
-  }
+                                          int64_t rstride, int N) {
+  const int c = threadIdx.x % TC4;
+  for (int i = threadIdx.x / TC4; i < N; i += Q4)
+    a[i * TC4 + c] = c < ncol ? g.spec[(row0 + (int64_t)i * rstride) * g.nc + c0 + c] : make_double2(0.0, 0.0);
   __syncthreads();
 }
 __device__ __forceinline__ void fft4_store(const double2 *a, const Fft4Args &g, int c0, int ncol, int64_t row0,
-                                           int64_t rstride, int N, int S) {
+                                           int64_t rstride, int N) {
   __syncthreads();
-  for (int e = threadIdx.x; e < N * TC4; e += blockDim.x) {
-    const int i = e / TC4, c = e - i * TC4;
-    if (c < ncol) g.spec[(row0 + (int64_t)i * rstride) * g.nc + c0 + c] = a[c * S + i];
-  }
+  const int c = threadIdx.x % TC4;
+  if (c >= ncol) return;
+  for (int i = threadIdx.x / TC4; i < N; i += Q4) g.spec[(row0 + (int64_t)i * rstride) * g.nc + c0 + c] = a[i * TC4 + c];
 }
 
 // A: blockIdx.x = column tile, blockIdx.y = n2
 __global__ void __launch_bounds__(256) k_fft4_a(Fft4Args g) {
   extern __shared__ double2 sm2[];
   const int c0 = blockIdx.x * TC4, ncol = min(TC4, g.ncs - c0), n2 = blockIdx.y;
-  const int S = g.N1 | 1;
-  fft4_load(sm2, g, c0, ncol, n2, g.N2, g.N1, S);
-  fft_run_m<-1, false>(sm2, g.s1, S, TC4, g.tw1);
-  for (int e = threadIdx.x; e < g.N1 * TC4; e += blockDim.x) {
-    const int c = e / g.N1, p = e - c * g.N1;
-    const int k1 = __ldg(g.sig1 + p);
-    sm2[c * S + p] = cmul(sm2[c * S + p], __ldg(g.twN + n2 * k1));  // n2 k1 < N2 N1 = nf
-  }
-  fft4_store(sm2, g, c0, ncol, n2, g.N2, g.N1, S);
+  fft4_load(sm2, g, c0, ncol, n2, g.N2, g.N1);
+  fft_run_t<-1, false>(sm2, g.s1, g.tw1);
+  const int c = threadIdx.x % TC4;
+  for (int p = threadIdx.x / TC4; p < g.N1; p += Q4)
+    sm2[p * TC4 + c] = cmul(sm2[p * TC4 + c], __ldg(g.twN + n2 * __ldg(g.sig1 + p)));  // n2 k1 < N2 N1 = nf
+  fft4_store(sm2, g, c0, ncol, n2, g.N2, g.N1);
 }
 
 // B: blockIdx.x = column tile, blockIdx.y = p (position of k1)
 __global__ void __launch_bounds__(256) k_fft4_b(Fft4Args g) {
   extern __shared__ double2 sm2[];
   const int c0 = blockIdx.x * TC4, ncol = min(TC4, g.ncs - c0), p = blockIdx.y;
-  const int S = g.N2 | 1;
   const int64_t row0 = (int64_t)p * g.N2;
   const int k1 = __ldg(g.sig1 + p);
-  fft4_load(sm2, g, c0, ncol, row0, 1, g.N2, S);
-  fft_run_m<-1, false>(sm2, g.s2, S, TC4, g.tw2);
-  for (int e = threadIdx.x; e < g.N2 * TC4; e += blockDim.x) {
-    const int c = e / g.N2, p2 = e - c * g.N2;
+  fft4_load(sm2, g, c0, ncol, row0, 1, g.N2);
+  fft_run_t<-1, false>(sm2, g.s2, g.tw2);
+  const int c = threadIdx.x % TC4;
+  const int m1 = c0 + c;
+  const double d1 = m1 <= g.half_modes ? __ldg(g.deconv + m1) * g.scale : 0.0;
+  const double e1x = g.kind == 0 && m1 <= g.half_modes ? __ldg(g.e1 + m1) : 0.0;
+  const double e2x = g.kind == 0 && m1 <= g.half_modes ? __ldg(g.e2 + m1) : 0.0;
+  for (int p2 = threadIdx.x / TC4; p2 < g.N2; p2 += Q4) {
     const int k = k1 + g.N1 * __ldg(g.sig2 + p2);
-    const int64_t m1 = c0 + c, m2 = k <= g.nf / 2 ? k : k - g.nf, a2m = m2 < 0 ? -m2 : m2;
+    const int m2 = k <= g.nf / 2 ? k : k - g.nf, a2m = m2 < 0 ? -m2 : m2;
     double fac = 0.0;
     if (m1 <= g.half_modes && a2m <= g.half_modes) {
       const double k2 = g.dk * g.dk * ((double)m1 * m1 + (double)m2 * m2);
-      const double mk = g.kind == 0 ? vp_mult_nh(k2, g.da, g.db) : vp_mult_fh(k2, g.da, g.db);
-      fac = mk * g.scale * __ldg(g.deconv + m1) * __ldg(g.deconv + a2m);
+      double mk;
+      if (g.kind != 0) {
+        mk = vp_mult_fh(k2, g.da, g.db);
+      } else if (k2 * g.db > 0.25) {
+        // (e^{-k^2 d1} - e^{-k^2 d2}) / k^2 from the separable exponentials (no cancellation here: the
+        // difference is >= 0.2 e^{-k^2 d1} once k^2 d2 > 1/4 with d2 = 32 d1); vp_mult_nh (expm1) below
+        mk = (e1x * __ldg(g.e1 + a2m) - e2x * __ldg(g.e2 + a2m)) / k2;
+      } else {
+        mk = vp_mult_nh(k2, g.da, g.db);
+      }
+      fac = mk * d1 * __ldg(g.deconv + a2m);
     }
-    const double2 v = sm2[c * S + p2];
-    sm2[c * S + p2] = make_double2(v.x * fac, v.y * fac);
+    const double2 v = sm2[p2 * TC4 + c];
+    sm2[p2 * TC4 + c] = make_double2(v.x * fac, v.y * fac);
   }
   __syncthreads();
-  fft_run_m<1, true>(sm2, g.s2, S, TC4, g.tw2);
-  for (int e = threadIdx.x; e < g.N2 * TC4; e += blockDim.x) {
-    const int c = e / g.N2, n2 = e - c * g.N2;
+  fft_run_t<1, true>(sm2, g.s2, g.tw2);
+  for (int n2 = threadIdx.x / TC4; n2 < g.N2; n2 += Q4) {
     double2 w = __ldg(g.twN + n2 * k1);
     w.y = -w.y;
-    sm2[c * S + n2] = cmul(sm2[c * S + n2], w);
+    sm2[n2 * TC4 + c] = cmul(sm2[n2 * TC4 + c], w);
   }
-  fft4_store(sm2, g, c0, ncol, row0, 1, g.N2, S);
+  fft4_store(sm2, g, c0, ncol, row0, 1, g.N2);
 }
 
 // C: blockIdx.x = column tile, blockIdx.y = n2'
 __global__ void __launch_bounds__(256) k_fft4_c(Fft4Args g) {
   extern __shared__ double2 sm2[];
   const int c0 = blockIdx.x * TC4, ncol = min(TC4, g.ncs - c0), n2 = blockIdx.y;
-  const int S = g.N1 | 1;
-  fft4_load(sm2, g, c0, ncol, n2, g.N2, g.N1, S);
-  fft_run_m<1, true>(sm2, g.s1, S, TC4, g.tw1);
-  fft4_store(sm2, g, c0, ncol, n2, g.N2, g.N1, S);
+  fft4_load(sm2, g, c0, ncol, n2, g.N2, g.N1);
+  fft_run_t<1, true>(sm2, g.s1, g.tw1);
+  fft4_store(sm2, g, c0, ncol, n2, g.N2, g.N1);
 }
 
 // nf = N1 N2 with both factors 2,3,5,7-smooth and N1 the divisor closest to sqrt(nf)
@@ -793,6 +803,19 @@ bool vp_fft4_setup(vp_plan_s *P, VpGrid &G) {
   VP_CUDA(cudaMemcpy(G.f4_sig1, g1.data(), 4 * N1, cudaMemcpyHostToDevice));
   VP_CUDA(cudaMemcpy(G.f4_sig2, g2.data(), 4 * N2, cudaMemcpyHostToDevice));
   G.fft_ncs = (int)std::min<int64_t>(G.nmode / 2 + 1, G.nf / 2 + 1);
+  if (G.kind == 0) {  // separable exponentials of the NH multiplier (k_fft4_b)
+    const int64_t nh = G.nmode / 2 + 1;
+    const double dk = 2.0 * VP_PI / G.L;
+    std::vector<double> a(nh), b(nh);
+    for (int64_t m = 0; m < nh; m++) {
+      a[m] = std::exp(-dk * dk * (double)m * (double)m * G.delta_a);
+      b[m] = std::exp(-dk * dk * (double)m * (double)m * G.delta_b);
+    }
+    G.f4_e1 = vp_alloc<double>(P, nh);
+    G.f4_e2 = vp_alloc<double>(P, nh);
+    VP_CUDA(cudaMemcpy(G.f4_e1, a.data(), sizeof(double) * nh, cudaMemcpyHostToDevice));
+    VP_CUDA(cudaMemcpy(G.f4_e2, b.data(), sizeof(double) * nh, cudaMemcpyHostToDevice));
+  }
   G.four_step = true;
   return true;
 }
@@ -819,8 +842,10 @@ void vp_fft4_columns(vp_plan_s *P, VpGrid &G) {
   g.dk = 2.0 * VP_PI / G.L;
   g.half_modes = G.nmode / 2;
   g.deconv = G.deconv;
+  g.e1 = G.f4_e1;
+  g.e2 = G.f4_e2;
   const unsigned ntile = (unsigned)((g.ncs + TC4 - 1) / TC4);
-  const size_t sm1 = sizeof(double2) * (size_t)TC4 * (g.N1 | 1), sm2 = sizeof(double2) * (size_t)TC4 * (g.N2 | 1);
+  const size_t sm1 = sizeof(double2) * (size_t)TC4 * g.N1, sm2 = sizeof(double2) * (size_t)TC4 * g.N2;
   vp_smem_attr((const void *)k_fft4_a, sm1);
   vp_smem_attr((const void *)k_fft4_b, sm2);
   vp_smem_attr((const void *)k_fft4_c, sm1);

@@ -484,12 +484,12 @@ stage:
     mylr = lr;
   }
   __syncwarp();
-  {
+  if constexpr (PACK) {
     // packs: a staged point joins the previous one's pack when it has the same origin row and lies right of the
     // previous member's footprint (the plan sorts each strip row into column-disjoint packs);
     // one step of W DFMA per lane then adds a whole pack, each lane taking the member covering its column
     const int plr = __shfl_up_sync(0xffffffffu, mylr, 1), plc = __shfl_up_sync(0xffffffffu, mylc, 1);
-    starts = __ballot_sync(0xffffffffu, !PACK || lane == 0 || lane >= n || mylr != plr || mylc < plc + W);
+    starts = __ballot_sync(0xffffffffu, lane == 0 || lane >= n || mylr != plr || mylc < plc + W);
   }
   q = 0;
   if (first) {
@@ -501,9 +501,9 @@ stage:
 #define VP_STRIP_PHASE(k)                                                              \
   case k:                                                                              \
     if ((k) < W) {                                                                     \
-      for (const int e = __popc(__ballot_sync(0xffffffffu, mylr <= r)); q < e;) {      \
-        const unsigned later = q < 31 ? (starts >> (q + 1)) << (q + 1) : 0u;           \
-        const int q2 = min(later ? __ffs(later) - 1 : 32, e);                          \
+      _Pragma("unroll 2") for (const int e = __popc(__ballot_sync(0xffffffffu, mylr <= r)); q < e;) { \
+        const unsigned later = PACK && q < 31 ? (starts >> (q + 1)) << (q + 1) : 0u;   \
+        const int q2 = PACK ? min(later ? __ffs(later) - 1 : 32, e) : q + 1;           \
         int sel = q;                                                                   \
         if (PACK) _Pragma("unroll") for (int m = 1; m < C::NPMAX; m++) {               \
           const int lcm = __shfl_sync(0xffffffffu, mylc, (q + m) & 31);                 \
