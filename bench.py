@@ -396,8 +396,8 @@ def main():
                            "deriv": f"{['auto', 'knn', 'triangle'][info['deriv_mode']]} (knn deg {info['deriv_degree']} "
                                     f"K {K_st} on {S_st} targets)", "levels": info["n_levels"], "plan_ms": info["plan_ms"],
                            "spread": "register strips (k_spread_strip)", "spread_items": info["n_batches"],
-                           "fft_path": {"nh": ["fused", "cufft2d", "rows+4step"][info["fft_path_nh"]],
-                                        "fh": ["fused", "cufft2d", "rows+4step"][info["fft_path_fh"]]},
+                           "fft_path": {"nh": ["fused", "cufft2d", "cufftrows+4step", "rows4+4step"][info["fft_path_nh"]],
+                                        "fh": ["fused", "cufft2d", "cufftrows+4step", "rows4+4step"][info["fft_path_fh"]]},
                            "opts": extra},
                 "phase_ms": ph, "serial_ms_per_step": serial_ms, "wall_ms_per_step": t_wall * 1e3 / args.steps,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "batch": batch,

@@ -125,6 +125,9 @@ typedef struct {
   /* register-strip spreading: 0 -> one point per step, 1 -> column-disjoint packs of points per step (fewer DFMA
    * and shared-memory loads, more integer work) */
   int32_t spread_pack;
+  /* grids above 6400^2 (four-step column pass): 0 -> own pruned row passes (nf % 4 == 0), 1 -> cuFFT batched 1D
+   * row transforms */
+  int32_t fft_rows;
 } vp_opts;
 
 /* Plan parameters chosen by vp_plan (diagnostics; all derived from the rules in DESIGN.md). */
@@ -151,7 +154,8 @@ typedef struct {
   int64_t nf_band;           /* band box fine grid per dimension */
   int64_t level_targets[16]; /* targets per level */
   int32_t fft_path_nh, fft_path_fh; /* transforms of the NH / FH grid: 0 fused row/column kernels (nf <= 6400),
-                                       1 cuFFT 2D D2Z + multiply + Z2D, 2 cuFFT row passes + four-step column pass */
+                                       1 cuFFT 2D D2Z + multiply + Z2D, 2 cuFFT row passes + four-step column pass,
+                                       3 own pruned row passes + four-step column pass */
 } vp_info;
 
 typedef struct vp_plan_s *vp_handle;

@@ -407,7 +407,14 @@ static void make_fft_plans(vp_plan_s *P) {
     VP_CUFFT(cufftCreate(&G.inv));
     VP_CUFFT(cufftSetAutoAllocation(G.fwd, 0));
     VP_CUFFT(cufftSetAutoAllocation(G.inv, 0));
-    if (vp_fft4_setup(P, G)) {  // large grid: batched 1D row transforms + the four-step column pass (vp_fft.cu)
+    if (vp_fft4_setup(P, G) && P->opts.fft_rows == 0 && vp_fft4_rows_setup(P, G)) {
+      // large grid: own pruned row passes + the four-step column pass (vp_fft.cu); no cuFFT plan
+      VP_CUFFT(cufftDestroy(G.fwd));
+      VP_CUFFT(cufftDestroy(G.inv));
+      G.fwd = G.inv = 0;
+      continue;
+    }
+    if (G.four_step) {  // large grid: cuFFT batched 1D row transforms + the four-step column pass (vp_fft.cu)
       long long n1[1] = {G.nf}, rin1[1] = {G.row}, cin1[1] = {G.crow / 2};
       VP_CUFFT(cufftMakePlanMany64(G.fwd, 1, n1, rin1, 1, G.row, cin1, 1, G.crow / 2, CUFFT_D2Z, G.nf, &ws[2 * g]));
       VP_CUFFT(cufftMakePlanMany64(G.inv, 1, n1, cin1, 1, G.crow / 2, rin1, 1, G.row, CUFFT_Z2D, G.nf,
@@ -490,6 +497,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     if (o.interp_tile > 0) P->TSI = o.interp_tile;
     if (o.fft_mode < 0 || o.fft_mode > 1) throw VpError{VP_ERR_ARG};
     if (o.spread_pack < 0 || o.spread_pack > 1) throw VpError{VP_ERR_ARG};
+    if (o.fft_rows < 0 || o.fft_rows > 1) throw VpError{VP_ERR_ARG};
     if (o.boundary.kind == VP_BDRY_CIRCLE && !(o.boundary.p[2] > 0)) throw VpError{VP_ERR_GEOMETRY};
     if (o.boundary.kind == VP_BDRY_RECT && !(o.boundary.p[2] > o.boundary.p[0] && o.boundary.p[3] > o.boundary.p[1]))
       throw VpError{VP_ERR_GEOMETRY};
@@ -635,6 +643,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
 // the three transform steps of one history grid: fused kernels (vp_fft.cu) or cuFFT + k_multiply
 static void grid_fft_fwd(vp_plan_s *P, VpGrid &G) {
   if (G.own_fft) return vp_fft_forward(P, G);
+  if (G.f4_rows) return vp_fft4_rows_fwd(P, G);
   VP_CUFFT(cufftSetStream(G.fwd, P->stream));
   VP_CUFFT(cufftExecD2Z(G.fwd, G.data, (cufftDoubleComplex *)G.cdata));
   P->n_ffts++;
@@ -646,6 +655,7 @@ static void grid_multiply(vp_plan_s *P, VpGrid &G) {
 }
 static void grid_fft_inv(vp_plan_s *P, VpGrid &G) {
   if (G.own_fft) return vp_fft_inverse(P, G);
+  if (G.f4_rows) return vp_fft4_rows_inv(P, G);
   VP_CUFFT(cufftSetStream(G.inv, P->stream));
   VP_CUFFT(cufftExecZ2D(G.inv, (cufftDoubleComplex *)G.cdata, G.data));
   P->n_ffts++;
@@ -893,8 +903,8 @@ extern "C" vp_status vp_get_info(vp_handle P, vp_info *I) {
   I->n_band_pairs = P->bands.n_pairs;
   I->nf_band = P->bands.nfb;
   for (int i = 0; i < 16; i++) I->level_targets[i] = P->bands.lev_count[i];
-  I->fft_path_nh = P->nh.own_fft ? 0 : (P->nh.four_step ? 2 : 1);
-  I->fft_path_fh = P->fh.own_fft ? 0 : (P->fh.four_step ? 2 : 1);
+  I->fft_path_nh = P->nh.own_fft ? 0 : (P->nh.four_step ? (P->nh.f4_rows ? 3 : 2) : 1);
+  I->fft_path_fh = P->fh.own_fft ? 0 : (P->fh.four_step ? (P->fh.f4_rows ? 3 : 2) : 1);
   return VP_OK;
 }
 

@@ -84,6 +84,11 @@ struct VpGrid {
   double2 *f4_tw1 = nullptr, *f4_tw2 = nullptr, *f4_twN = nullptr;
   int32_t *f4_sig1 = nullptr, *f4_sig2 = nullptr;
   double *f4_e1 = nullptr, *f4_e2 = nullptr;  // NH: e^{-dk^2 m^2 delta_a}, e^{-dk^2 m^2 delta_b}
+  // own row passes (k_row4_fwd / k_row4_inv; nf % 4 == 0): Q = nf / 4 point transforms
+  bool f4_rows = false;
+  int32_t *f4_posQ = nullptr;
+  double2 *f4_twQ = nullptr;
+  alignas(8) char f4_stQ[256] = {};
 };
 
 struct VpTiles {          // sorted points binned into TS x TS tiles of a fine grid
@@ -287,6 +292,9 @@ void vp_fft_forward(vp_plan_s *P, VpGrid &G);
 void vp_fft_columns(vp_plan_s *P, VpGrid &G);
 void vp_fft_inverse(vp_plan_s *P, VpGrid &G);
 bool vp_fft4_setup(vp_plan_s *P, VpGrid &G);
+bool vp_fft4_rows_setup(vp_plan_s *P, VpGrid &G);
+void vp_fft4_rows_fwd(vp_plan_s *P, VpGrid &G);
+void vp_fft4_rows_inv(vp_plan_s *P, VpGrid &G);
 void vp_fft4_columns(vp_plan_s *P, VpGrid &G);
 void vp_launch_spread_batch(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, int K, const double *const *f,
                             double *const *grids, double *const *fs);

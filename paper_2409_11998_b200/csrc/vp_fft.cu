@@ -855,9 +855,148 @@ void vp_fft4_columns(vp_plan_s *P, VpGrid &G) {
   VP_CHECK_LAUNCH();
   k_fft4_c<<<dim3(ntile, g.N2), 256, sm1, P->stream>>>(g);
   VP_CHECK_LAUNCH();
-  // the inverse row transforms read the whole half spectrum: the columns beyond the kept band are zero
+  // cuFFT's inverse row transforms read the whole half spectrum: the columns beyond the kept band are zero (the
+  // own row passes read only the kept columns)
   const int64_t nz = g.nc - g.ncs;
-  if (nz > 0)
+  if (nz > 0 && !G.f4_rows)
     VP_CUDA(cudaMemset2DAsync(g.spec + g.ncs, sizeof(double2) * g.nc, 0, sizeof(double2) * nz, G.nf, P->stream));
   P->n_kernels += 3;
+}
+
+// ---- large-grid row passes (four-step grids with nf % 4 == 0): pruned real FFT by radix-4 decimation in time.
+// Q = nf/4, y_r[m] = x[4m + r], Y_r = FFT_Q(y_r); X[k] = sum_r W_nf^{rk} Y_r[k mod Q] for the kept k < ncs <= Q + 1.
+// Two complex Q-point FFTs per row (z = y_{2h} + i y_{2h+1}, h = 0, 1: Y_{2h}[j] = (Z[j] + conj Z[Q-j]) / 2,
+// Y_{2h+1}[j] = -i (Z[j] - conj Z[Q-j]) / 2), one Q-length shared buffer: two CTAs per SM at config 5 (Q = 5832),
+// and only the kept columns are written (the inverse reads only them: no zeroing of the rest).
+__global__ void __launch_bounds__(512) k_row4_fwd(const double *__restrict__ grid, int64_t row_pitch,
+                                                  double2 *__restrict__ spec, int64_t nc, int ncs, int nf, FftStages st,
+                                                  const double2 *__restrict__ twQ, const double2 *__restrict__ twN,
+                                                  const int32_t *__restrict__ posQ) {
+  extern __shared__ double2 z[];
+  const int Q = st.n;
+  for (int r = blockIdx.x; r < nf; r += gridDim.x) {
+    const double *x = grid + (int64_t)r * row_pitch;
+    double2 *X = spec + (int64_t)r * nc;
+    for (int h = 0; h < 2; h++) {
+      for (int m = threadIdx.x; m < Q; m += blockDim.x) z[m] = __ldg((const double2 *)(x + 4 * m + 2 * h));
+      __syncthreads();
+      fft_run<-1, false>(z, st, twQ);
+      for (int k = threadIdx.x; k < ncs; k += blockDim.x) {
+        const int j = k < Q ? k : 0;
+        const double2 zj = z[__ldg(posQ + j)], zm = z[__ldg(posQ + (j ? Q - j : 0))];
+        const double2 ya = make_double2(0.5 * (zj.x + zm.x), 0.5 * (zj.y - zm.y));
+        const double2 yb = make_double2(0.5 * (zj.y + zm.y), -0.5 * (zj.x - zm.x));
+        const double2 a = cmul(__ldg(twN + 2 * h * k), ya), b = cmul(__ldg(twN + (2 * h + 1) * k), yb);
+        double2 v = make_double2(a.x + b.x, a.y + b.y);
+        if (h) {
+          const double2 p = X[k];  // written by this thread for h = 0
+          v.x += p.x;
+          v.y += p.y;
+        }
+        X[k] = v;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// inverse: x[4m + r] = sum_{k in band} X[k] W_nf^{-(4m + r) k} (unnormalised, as cuFFT Z2D) = IFFT_Q(S_r)[m] with
+// S_r[j] = ([j < ncs] X[j] + [Q - j < ncs] conj(X[Q - j]) (-i)^r) W_nf^{-rj} for j >= 1 and
+// S_r[0] = X[0] + [ncs > Q] (conj(X[Q]) (-i)^r + X[Q] i^r); S_r is Hermitian, so IFFT(S_{2h} + i S_{2h+1}) =
+// y_{2h} + i y_{2h+1} with real y
+__global__ void __launch_bounds__(512) k_row4_inv(const double2 *__restrict__ spec, int64_t nc, int ncs, int nf,
+                                                  double *__restrict__ grid, int64_t row_pitch, FftStages st,
+                                                  const double2 *__restrict__ twQ, const double2 *__restrict__ twN,
+                                                  const int32_t *__restrict__ posQ) {
+  extern __shared__ double2 z[];
+  const int Q = st.n;
+  for (int r = blockIdx.x; r < nf; r += gridDim.x) {
+    const double2 *X = spec + (int64_t)r * nc;
+    double *x = grid + (int64_t)r * row_pitch;
+    for (int h = 0; h < 2; h++) {
+      for (int j = threadIdx.x; j < Q; j += blockDim.x) {
+        double2 s[2];
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+          const int rr = 2 * h + u;
+          double2 acc = make_double2(0.0, 0.0);
+          if (j < ncs) acc = X[j];
+          const int jm = j ? Q - j : Q;  // partner frequency k = j - Q
+          if (jm < ncs) {
+            double2 c = X[jm];
+            c.y = -c.y;
+            // (-i)^rr
+            for (int t = 0; t < rr; t++) c = make_double2(c.y, -c.x);
+            acc.x += c.x;
+            acc.y += c.y;
+          }
+          if (j == 0 && ncs > Q) {  // k = +Q: X[Q] i^rr
+            double2 c = X[Q];
+            for (int t = 0; t < rr; t++) c = make_double2(-c.y, c.x);
+            acc.x += c.x;
+            acc.y += c.y;
+          }
+          if (j) {
+            double2 w = __ldg(twN + rr * j);  // W_nf^{rr j}, conj for the inverse
+            w.y = -w.y;
+            acc = cmul(acc, w);
+          }
+          s[u] = acc;
+        }
+        z[__ldg(posQ + j)] = make_double2(s[0].x - s[1].y, s[0].y + s[1].x);  // S_{2h} + i S_{2h+1}
+      }
+      __syncthreads();
+      fft_run<1, true>(z, st, twQ);
+      for (int m = threadIdx.x; m < Q; m += blockDim.x) *(double2 *)(x + 4 * m + 2 * h) = z[m];
+      __syncthreads();
+    }
+  }
+}
+
+bool vp_fft4_rows_setup(vp_plan_s *P, VpGrid &G) {
+  if (G.nf % 4) return false;
+  const int Q = (int)(G.nf / 4);
+  FftStages st;
+  if (!factor_stages(Q, st)) return false;
+  const size_t sm = sizeof(double2) * (size_t)Q;
+  if (sm > 200 * 1024) return false;
+  if (G.fft_ncs > Q + 1) return false;
+  std::vector<int32_t> sig, pos(Q);
+  digit_sigma(st, sig);
+  for (int p = 0; p < Q; p++) pos[sig[p]] = p;
+  G.f4_posQ = vp_alloc<int32_t>(P, Q);
+  VP_CUDA(cudaMemcpy(G.f4_posQ, pos.data(), 4 * (size_t)Q, cudaMemcpyHostToDevice));
+  G.f4_twQ = twiddle_table(P, Q);
+  static_assert(sizeof(FftStages) <= sizeof(G.f4_stQ), "stage buffer");
+  memcpy(G.f4_stQ, &st, sizeof(st));
+  vp_smem_attr((const void *)k_row4_fwd, sm);
+  vp_smem_attr((const void *)k_row4_inv, sm);
+  G.f4_rows = true;
+  return true;
+}
+
+static unsigned row4_grid(size_t smem, int64_t rows) {
+  int per = (int)std::min<size_t>(4, (227 * 1024) / (smem + 2048));
+  if (per < 1) per = 1;
+  return (unsigned)std::min<int64_t>(rows, (int64_t)per * num_sms());
+}
+
+void vp_fft4_rows_fwd(vp_plan_s *P, VpGrid &G) {
+  FftStages st;
+  memcpy(&st, G.f4_stQ, sizeof(st));
+  const size_t sm = sizeof(double2) * (size_t)st.n;
+  k_row4_fwd<<<row4_grid(sm, G.nf), 512, sm, P->stream>>>(G.data, G.row, (double2 *)G.cdata, G.nf / 2 + 1, G.fft_ncs,
+                                                          (int)G.nf, st, G.f4_twQ, G.f4_twN, G.f4_posQ);
+  VP_CHECK_LAUNCH();
+  P->n_kernels++;
+}
+
+void vp_fft4_rows_inv(vp_plan_s *P, VpGrid &G) {
+  FftStages st;
+  memcpy(&st, G.f4_stQ, sizeof(st));
+  const size_t sm = sizeof(double2) * (size_t)st.n;
+  k_row4_inv<<<row4_grid(sm, G.nf), 512, sm, P->stream>>>((const double2 *)G.cdata, G.nf / 2 + 1, G.fft_ncs,
+                                                          (int)G.nf, G.data, G.row, st, G.f4_twQ, G.f4_twN, G.f4_posQ);
+  VP_CHECK_LAUNCH();
+  P->n_kernels++;
 }

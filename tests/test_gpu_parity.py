@@ -487,15 +487,16 @@ def test_four_step_matches_cufft(d1):
     tg_np = np.concatenate([rng.uniform(0.0, 1.0, (300, 2)), src[:20]])
     tg = torch.from_numpy(tg_np).to(DEV)
     out, paths = [], []
-    for mode in (0, 1):
-        plan = vp.Plan(nodes, wts, tg, 1e-10, parts=vp.PART_HISTORY, delta1_override=d1, fft_mode=mode)
+    for kw in ({}, {"fft_rows": 1}, {"fft_mode": 1}):  # own rows + four-step, cuFFT rows + four-step, cuFFT 2D
+        plan = vp.Plan(nodes, wts, tg, 1e-10, parts=vp.PART_HISTORY, delta1_override=d1, **kw)
         out.append(plan.eval(fv).cpu().numpy())
         info = plan.info()
         paths.append((info["fft_path_nh"], info["fft_path_fh"], info["nf_nh"], info["nf_fh"]))
         plan.destroy()
     print("four-step", d1, paths)
-    assert paths[0][0] == 2 and paths[1][0] == 1
-    assert np.max(np.abs(out[0] - out[1])) <= 1e-12 * np.max(np.abs(out[1])), paths
+    assert paths[0][0] == 3 and paths[1][0] == 2 and paths[2][0] == 1
+    for o in out[:2]:
+        assert np.max(np.abs(o - out[2])) <= 1e-12 * np.max(np.abs(out[2])), paths
     ref = oracle.smooth_direct(src, (fv.cpu().numpy() * wts.cpu().numpy()).ravel(), tg_np, d1)
     assert rel_l2(out[0], ref) < 1e-9
 
@@ -518,7 +519,7 @@ tg = torch.from_numpy(rng.uniform(0.0, 1.0, (200, 2))).cuda()
 out = []
 for mode in (0, 1):
     p = vp.Plan(nodes, wts, tg, 1e-13, parts=vp.PART_HISTORY, delta1_override=6.25e-8, fft_mode=mode)
-    assert p.info()["fft_path_fh"] == (2 if mode == 0 else 1)
+    assert p.info()["fft_path_fh"] == (3 if mode == 0 else 1)
     out.append(p.eval(fv).cpu().numpy())
 print(np.max(np.abs(out[0] - out[1])) / np.max(np.abs(out[1])))
 """ % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
