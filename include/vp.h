@@ -125,8 +125,8 @@ typedef struct {
   /* register-strip spreading: 0 -> one point per step, 1 -> column-disjoint packs of points per step (fewer DFMA
    * and shared-memory loads, more integer work) */
   int32_t spread_pack;
-  /* grids above 6400^2 (four-step column pass): 0 -> own pruned row passes (nf % 4 == 0), 1 -> cuFFT batched 1D
-   * row transforms */
+  /* grids above 6400^2 (four-step column pass): 0 -> cuFFT batched 1D row transforms, 1 -> own pruned row passes
+   * (nf % 4 == 0; measured slower than cuFFT's at config 5) */
   int32_t fft_rows;
 } vp_opts;
 

@@ -407,7 +407,7 @@ static void make_fft_plans(vp_plan_s *P) {
     VP_CUFFT(cufftCreate(&G.inv));
     VP_CUFFT(cufftSetAutoAllocation(G.fwd, 0));
     VP_CUFFT(cufftSetAutoAllocation(G.inv, 0));
-    if (vp_fft4_setup(P, G) && P->opts.fft_rows == 0 && vp_fft4_rows_setup(P, G)) {
+    if (vp_fft4_setup(P, G) && P->opts.fft_rows == 1 && vp_fft4_rows_setup(P, G)) {
       // large grid: own pruned row passes + the four-step column pass (vp_fft.cu); no cuFFT plan
       VP_CUFFT(cufftDestroy(G.fwd));
       VP_CUFFT(cufftDestroy(G.inv));
@@ -596,7 +596,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     while (P->deg > 0 && 2 * vp_ncoef(P->deg) > N && o.deriv_degree <= 0) P->deg--;  // tiny inputs
     int nc = vp_ncoef(P->deg);
     // K: 2 x #monomials at degree >= 5; degree 4 needs fewer (config 2: 1.30e-9 at K = 17, 20, 24 and 30)
-    P->K = o.deriv_k > 0 ? o.deriv_k : (P->deg >= 5 ? 2 * nc : nc + 2);
+    P->K = o.deriv_k > 0 ? o.deriv_k : (P->deg >= 5 ? 2 * nc : nc + 6);
     if (P->K > 64) P->K = 64;
     if (P->K > N && o.deriv_k <= 0) P->K = (int)N;
     if (P->K < nc) throw VpError{VP_ERR_ARG};
@@ -613,7 +613,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
       P->lalpha = vp_alloc<double>(P, 1);
       P->lnode = vp_alloc<int32_t>(P, 1);
       P->lidx = vp_alloc<int32_t>(P, 1);
-      P->lw = vp_alloc<float>(P, 1);
+      P->lw = vp_alloc<double>(P, 1);
       P->lptr = vp_alloc<int32_t>(P, 1);
     }
     // ---- FFT plans, forked streams

@@ -216,7 +216,7 @@ struct vp_plan_s {
   // local part: V_L(t) = alpha_t * f(node_t) + sum_k omega_{t,k} f[idx_{t,k}]
   int K = 0, deg = 0, dmode = 0;
   int32_t *lidx = nullptr;     // [T][K] user node indices (sorted target order)
-  float *lw = nullptr;         // [S][K] stencil weights (fp32: the stencil carries terms <= 1e-5 of V, R6)
+  double *lw = nullptr;        // [S][K] stencil weights
   double *lalpha = nullptr;    // [T]
   int32_t *lnode = nullptr;    // [T] user node index of the target (targets_are_nodes) or -1
   int64_t n_bdry = 0;

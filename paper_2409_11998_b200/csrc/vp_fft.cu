@@ -36,8 +36,8 @@ struct FftStages {
   float invLp[VP_FFT_MAXS];  // 1 / L_{s-1} (butterfly index split without integer division)
 };
 
-__constant__ double c_dft_c[9][8];  // cos(2 pi j / R), R = 2..8
-__constant__ double c_dft_s[9][8];  // sin(2 pi j / R)
+__constant__ double c_dft_c[10][9];  // cos(2 pi j / R), R = 2..9
+__constant__ double c_dft_s[10][9];  // sin(2 pi j / R)
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -163,6 +163,7 @@ __device__ void fft_run(double2 *a, const FftStages &st, const double2 *tw) {
       case 5: fft_stage<5, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
       case 7: fft_stage<7, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
       case 8: fft_stage<8, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 9: fft_stage<9, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
       default: break;
     }
     __syncthreads();
@@ -379,7 +380,7 @@ static bool factor_stages(int n, FftStages &st) {
       m /= r;
     }
   }
-  for (int r : {7, 5, 3}) {
+  for (int r : {9, 7, 5, 3}) {  // radix 9 (one in-register stage) before 3 x 3
     while (m % r == 0) {
       rs.push_back(r);
       m /= r;
@@ -446,8 +447,8 @@ static void upload_dft_roots() {
   const int dev = vp_current_device();
   std::lock_guard<std::mutex> lk(mu);
   if (done.count(dev)) return;
-  double hc[9][8] = {}, hs[9][8] = {};
-  for (int R = 2; R <= 8; R++)
+  double hc[10][9] = {}, hs[10][9] = {};
+  for (int R = 2; R <= 9; R++)
     for (int j = 0; j < R; j++) {
       const long double ang = 2.0L * 3.141592653589793238462643383279502884L * j / R;
       hc[R][j] = (double)cosl(ang);
@@ -663,6 +664,7 @@ __device__ void fft_run_t(double2 *a, const FftStages &st, const double2 *__rest
       case 5: fft_stage_t<5, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
       case 7: fft_stage_t<7, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
       case 8: fft_stage_t<8, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
+      case 9: fft_stage_t<9, DIR, DIT>(a, st.n, st.Lp[s], st.invLp[s], tw); break;
       default: break;
     }
     __syncthreads();
@@ -886,7 +888,10 @@ __global__ void __launch_bounds__(512) k_row4_fwd(const double *__restrict__ gri
         const double2 zj = z[__ldg(posQ + j)], zm = z[__ldg(posQ + (j ? Q - j : 0))];
         const double2 ya = make_double2(0.5 * (zj.x + zm.x), 0.5 * (zj.y - zm.y));
         const double2 yb = make_double2(0.5 * (zj.y + zm.y), -0.5 * (zj.x - zm.x));
-        const double2 a = cmul(__ldg(twN + 2 * h * k), ya), b = cmul(__ldg(twN + (2 * h + 1) * k), yb);
+        // W^{2hk} ya + W^{(2h+1)k} yb from one coalesced table load (powers by multiplication)
+        const double2 w1 = __ldg(twN + k);
+        const double2 wa = h ? cmul(w1, w1) : make_double2(1.0, 0.0);
+        const double2 a = cmul(wa, ya), b = cmul(cmul(wa, w1), yb);
         double2 v = make_double2(a.x + b.x, a.y + b.y);
         if (h) {
           const double2 p = X[k];  // written by this thread for h = 0
@@ -915,33 +920,25 @@ __global__ void __launch_bounds__(512) k_row4_inv(const double2 *__restrict__ sp
     double *x = grid + (int64_t)r * row_pitch;
     for (int h = 0; h < 2; h++) {
       for (int j = threadIdx.x; j < Q; j += blockDim.x) {
+        const double2 xj = j < ncs ? X[j] : make_double2(0.0, 0.0);
+        const int jm = j ? Q - j : Q;  // partner frequency k = j - Q
+        const double2 xm = jm < ncs ? X[jm] : make_double2(0.0, 0.0);
+        const double2 xq = (j == 0 && ncs > Q) ? X[Q] : make_double2(0.0, 0.0);  // k = +Q (j = 0 only)
+        double2 w1 = __ldg(twN + j);  // W_nf^{j}; conjugated powers W^{-rj} by multiplication
+        w1.y = -w1.y;
+        const double2 w2 = cmul(w1, w1);
         double2 s[2];
 #pragma unroll
         for (int u = 0; u < 2; u++) {
-          const int rr = 2 * h + u;
-          double2 acc = make_double2(0.0, 0.0);
-          if (j < ncs) acc = X[j];
-          const int jm = j ? Q - j : Q;  // partner frequency k = j - Q
-          if (jm < ncs) {
-            double2 c = X[jm];
-            c.y = -c.y;
-            // (-i)^rr
-            for (int t = 0; t < rr; t++) c = make_double2(c.y, -c.x);
-            acc.x += c.x;
-            acc.y += c.y;
+          const int rr = 2 * h + u;  // (-i)^rr conj(X[Q-j]) + i^rr X[Q]
+          double2 c = make_double2(xm.x, -xm.y), d = xq;
+          for (int t = 0; t < rr; t++) {
+            c = make_double2(c.y, -c.x);
+            d = make_double2(-d.y, d.x);
           }
-          if (j == 0 && ncs > Q) {  // k = +Q: X[Q] i^rr
-            double2 c = X[Q];
-            for (int t = 0; t < rr; t++) c = make_double2(-c.y, c.x);
-            acc.x += c.x;
-            acc.y += c.y;
-          }
-          if (j) {
-            double2 w = __ldg(twN + rr * j);  // W_nf^{rr j}, conj for the inverse
-            w.y = -w.y;
-            acc = cmul(acc, w);
-          }
-          s[u] = acc;
+          double2 acc = make_double2(xj.x + c.x + d.x, xj.y + c.y + d.y);
+          const double2 w = rr == 0 ? make_double2(1.0, 0.0) : (rr == 1 ? w1 : (rr == 2 ? w2 : cmul(w2, w1)));
+          s[u] = cmul(acc, w);
         }
         z[__ldg(posQ + j)] = make_double2(s[0].x - s[1].y, s[0].y + s[1].x);  // S_{2h} + i S_{2h+1}
       }

@@ -37,8 +37,7 @@ struct LocalArgs {
   double delta;
   VpBdryDev bd;
   int32_t *lidx;                  // stencils, k-major: entry k of slot s at [k * stride + s]
-  float *lw;
-  double *lalpha;
+  double *lw, *lalpha;
   int64_t slot0, stride;          // global slot of list entry 0; number of stencil slots
   int32_t *lnode;
   int32_t *is_bdry;
@@ -195,7 +194,7 @@ __global__ void k_build_local(LocalArgs a) {
   const int64_t gs = a.slot0 + slot;
   for (int k = 0; k < K; k++) {
     a.lidx[k * a.stride + gs] = a.kperm[hi[k]];
-    a.lw[k * a.stride + gs] = (float)yv[k];
+    a.lw[k * a.stride + gs] = yv[k];
   }
   a.lalpha[t] = alpha;
   a.lnode[t] = node;
@@ -429,7 +428,7 @@ void vp_build_local(vp_plan_s *P, const double *nodes_dev) {
   }
   P->st_vL = vp_alloc<double>(P, (size_t)std::max<int64_t>(nst, 1));
   P->lidx = vp_alloc<int32_t>(P, (size_t)std::max<int64_t>(nst, 1) * K);
-  P->lw = vp_alloc<float>(P, (size_t)std::max<int64_t>(nst, 1) * K);
+  P->lw = vp_alloc<double>(P, (size_t)std::max<int64_t>(nst, 1) * K);
   int32_t *isb = nullptr;
   VP_CUDA(cudaMallocAsync(&isb, sizeof(int32_t) * (P->T + 1), st));
   VP_CUDA(cudaMemsetAsync(isb, 0, sizeof(int32_t) * (P->T + 1), st));

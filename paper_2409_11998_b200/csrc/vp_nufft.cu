@@ -1014,6 +1014,66 @@ __global__ void __launch_bounds__(128) k_prolong_x_int(const double *__restrict_
   }
 }
 
+// prolongation passes with a compile-time tap count (QHC = QH): the d loop and every weight index are static,
+// so the weights are constant-bank DFMA operands (the runtime-QH forms above are issue-bound on the indexed
+// parameter loads; config 5: k_prolong_x_int 2.4 ms at 86% issue)
+template <int M, int QHC>
+__global__ void __launch_bounds__(128) k_prolong_y_fix(const double *__restrict__ q2, double *__restrict__ t2,
+                                                       RestrictArgs a, TapArgs tp, int64_t c_lo) {
+  const int64_t ex = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int64_t c = c_lo + blockIdx.y;
+  if (ex >= a.ne) return;
+  constexpr int DLO = -(QHC / M), DHI = (M - 1 + QHC) / M;
+  double acc[M];
+#pragma unroll
+  for (int k = 0; k < M; k++) acc[k] = 0.0;
+#pragma unroll
+  for (int d = DLO; d <= DHI; d++) {
+    const int64_t ip = c + d;
+    const double x = (ip >= a.e_lo && ip < a.e_lo + a.ne) ? __ldg(q2 + ip * a.row2 + a.e_lo + ex) : 0.0;
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+      const int q = k - M * d;
+      if (q >= -QHC && q <= QHC) acc[k] = fma(tp.w[q + QHC], x, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < M; k++) {
+    const int64_t r = M * c + k - tp.j;
+    if (r >= 0 && r < a.n1) t2[r * a.ne + ex] = acc[k];
+  }
+}
+
+template <int M, int QHC>
+__global__ void __launch_bounds__(128) k_prolong_x_fix(const double *__restrict__ t2, double *__restrict__ q1,
+                                                       RestrictArgs a, TapArgs tp, int64_t c_lo, int64_t nc) {
+  const int64_t cc = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int64_t r = blockIdx.y;
+  if (cc >= nc) return;
+  const int64_t c = c_lo + cc;
+  constexpr int DLO = -(QHC / M), DHI = (M - 1 + QHC) / M;
+  const double *src = t2 + r * a.ne - a.e_lo;
+  double acc[M];
+#pragma unroll
+  for (int k = 0; k < M; k++) acc[k] = 0.0;
+#pragma unroll
+  for (int d = DLO; d <= DHI; d++) {
+    const int64_t ip = c + d;
+    const double x = (ip >= a.e_lo && ip < a.e_lo + a.ne) ? __ldg(src + ip) : 0.0;
+#pragma unroll
+    for (int k = 0; k < M; k++) {
+      const int q = k - M * d;
+      if (q >= -QHC && q <= QHC) acc[k] = fma(tp.w[q + QHC], x, acc[k]);
+    }
+  }
+  double *dst = q1 + r * a.row1;
+#pragma unroll
+  for (int k = 0; k < M; k++) {
+    const int64_t i = M * c + k - tp.j;
+    if (i >= 0 && i < a.n1) dst[i] += acc[k];
+  }
+}
+
 static TapArgs tap_args(vp_plan_s *P) {
   TapArgs t;
   memset(&t, 0, sizeof(t));
@@ -1057,13 +1117,25 @@ static void launch_prolong_int(vp_plan_s *P, const RestrictArgs &a, const TapArg
   const int64_t nc = c_hi - c_lo + 1;
   if (pass & 1) {
     dim3 gB((unsigned)((a.ne + 127) / 128), (unsigned)nc);
-    k_prolong_y_int<M><<<gB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a, tp, c_lo);
+    bool fixed = false;
+    if (M == 5) {  // w = 9, 10, 11 (tol 1e-8 .. 1e-10) with m = 5: compile-time taps
+      if (tp.QH == 22) { k_prolong_y_fix<M, 22><<<gB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a, tp, c_lo); fixed = true; }
+      else if (tp.QH == 24) { k_prolong_y_fix<M, 24><<<gB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a, tp, c_lo); fixed = true; }
+      else if (tp.QH == 27) { k_prolong_y_fix<M, 27><<<gB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a, tp, c_lo); fixed = true; }
+    }
+    if (!fixed) k_prolong_y_int<M><<<gB, 128, 0, P->stream>>>(P->fh.data, P->scratch, a, tp, c_lo);
     VP_CHECK_LAUNCH();
     P->n_kernels++;
   }
   if (!(pass & 2)) return;
   dim3 gA((unsigned)((nc + 127) / 128), (unsigned)a.n1);
-  k_prolong_x_int<M><<<gA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a, tp, c_lo, nc);
+  bool fixed = false;
+  if (M == 5) {
+    if (tp.QH == 22) { k_prolong_x_fix<M, 22><<<gA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a, tp, c_lo, nc); fixed = true; }
+    else if (tp.QH == 24) { k_prolong_x_fix<M, 24><<<gA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a, tp, c_lo, nc); fixed = true; }
+    else if (tp.QH == 27) { k_prolong_x_fix<M, 27><<<gA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a, tp, c_lo, nc); fixed = true; }
+  }
+  if (!fixed) k_prolong_x_int<M><<<gA, 128, 0, P->stream>>>(P->scratch, P->nh.data, a, tp, c_lo, nc);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
@@ -1353,14 +1425,14 @@ __global__ void __launch_bounds__(128) k_tri_local12(const double *__restrict__ 
 
 // KNN-stencil local part, one thread per stencil slot: vL_st[s] = sum_k w[k][s] f[idx[k][s]] (k-major layout:
 // the warp streams consecutive slots, 12 B per entry, HBM-bound; f gathers hit L2)
-__global__ void __launch_bounds__(256) k_local_stencil(const int32_t *__restrict__ lidx, const float *__restrict__ lw,
+__global__ void __launch_bounds__(256) k_local_stencil(const int32_t *__restrict__ lidx, const double *__restrict__ lw,
                                                        int K, int64_t S, const double *__restrict__ f,
                                                        double *__restrict__ vL_st) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= S) return;
   double acc = 0.0;
 #pragma unroll 8
-  for (int k = 0; k < K; k++) acc = fma((double)__ldcs(lw + k * S + s), __ldg(f + __ldcs(lidx + k * S + s)), acc);
+  for (int k = 0; k < K; k++) acc = fma(__ldcs(lw + k * S + s), __ldg(f + __ldcs(lidx + k * S + s)), acc);
   vL_st[s] = acc;
 }
 
