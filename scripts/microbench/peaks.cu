@@ -58,6 +58,56 @@ __global__ void k_lds_bcast(double *out, int iters) {
   if (acc.x == -1.0) out[0] = acc.y;
 }
 
+
+// lanes read from G groups of 32/G lanes, each group one (distinct, bank-disjoint) address: LDS.128 (V=2) or LDS.64
+// (V=1).  G = 1 is a broadcast; G = 2 models two half-warps each broadcasting its own point's weights.
+template <int G, int V>
+__global__ void k_lds_groups(double *out, int iters) {
+  __shared__ double sm[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) sm[i] = i;
+  __syncthreads();
+  double acc0 = 0, acc1 = 0;
+  const int grp = (threadIdx.x & 31) / (32 / G);
+  int idx = (threadIdx.x >> 5) * 64 + grp * 2 * V;  // groups 16*V bytes apart -> different banks
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int a = (idx + u * 2 * V * G * 4) & 2047 & ~(V - 1);
+      if (V == 2) {
+        const double2 v = *(const double2 *)(sm + a);
+        acc0 += v.x;
+        acc1 += v.y;
+      } else {
+        acc0 += sm[a];
+      }
+    }
+    idx = (idx + 512) & 2047;
+  }
+  if (acc0 == -1.0) out[0] = acc1;
+}
+
+template <int G, int V>
+static int run_groups(double *d, int blocks, int threads, int nsm, int clk, cudaEvent_t a, cudaEvent_t b) {
+  const int iters = 20000;
+  float ms;
+  k_lds_groups<G, V><<<blocks, threads>>>(d, 10);
+  cudaEventRecord(a);
+  k_lds_groups<G, V><<<blocks, threads>>>(d, iters);
+  cudaEventRecord(b);
+  CK(cudaEventSynchronize(b));
+  cudaEventElapsedTime(&ms, a, b);
+  const double warp_instr = (double)blocks * (threads / 32) * iters * 8;
+  printf("lds.%d %d address group(s) per warp: %.3f ms, %.3f warp-instr/clk/SM\n", 64 * V, G, ms,
+         warp_instr / (ms * 1e-3) / nsm / (clk * 1e3));
+  run_groups<1, 1>(d, blocks, threads, nsm, clk, a, b);
+  run_groups<2, 1>(d, blocks, threads, nsm, clk, a, b);
+  run_groups<4, 1>(d, blocks, threads, nsm, clk, a, b);
+  run_groups<1, 2>(d, blocks, threads, nsm, clk, a, b);
+  run_groups<2, 2>(d, blocks, threads, nsm, clk, a, b);
+  run_groups<4, 2>(d, blocks, threads, nsm, clk, a, b);
+  return 0;
+}
+
 int main() {
   int dev = 0, nsm = 0, clk = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -97,5 +147,11 @@ int main() {
            ms, warp_instr / (ms * 1e-3) / nsm / (clk * 1e3), bytes / (ms * 1e-3) / 1e12,
            mode == 0 ? "512 B per warp instruction" : "16 B per warp instruction");
   }
+  run_groups<1, 1>(d, blocks, threads, nsm, clk, a, b);
+  run_groups<2, 1>(d, blocks, threads, nsm, clk, a, b);
+  run_groups<4, 1>(d, blocks, threads, nsm, clk, a, b);
+  run_groups<1, 2>(d, blocks, threads, nsm, clk, a, b);
+  run_groups<2, 2>(d, blocks, threads, nsm, clk, a, b);
+  run_groups<4, 2>(d, blocks, threads, nsm, clk, a, b);
   return 0;
 }
