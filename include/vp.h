@@ -122,8 +122,9 @@ typedef struct {
   /* transforms: 0 -> fused row/column FFT with the spectral multiply in the column pass (vp_fft.cu) for
    * grids with nf <= 6400, cuFFT D2Z + multiply + Z2D otherwise; 1 -> cuFFT for every grid */
   int32_t fft_mode;
-  /* register-strip spreading: 0 -> one point per step, 1 -> column-disjoint packs of points per step (fewer DFMA
-   * and shared-memory loads, more integer work) */
+  /* register-strip spreading: 0 -> row-pair strips (k_spread_pair: 16 columns x 2 row phases
+   * per warp) when w <= 12, else 32-column strips; 1 -> 32-column strips with column-disjoint packs of points per
+   * step; 2 -> 32-column strips, one point per step (k_spread_strip) */
   int32_t spread_pack;
   /* grids above 6400^2 (four-step column pass): 0 -> cuFFT batched 1D row transforms, 1 -> own pruned row passes
    * (nf % 4 == 0; measured slower than cuFFT's at config 5) */

@@ -496,7 +496,7 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
     if (o.interp_tile < 0 || o.interp_tile > 128 || (o.interp_tile > 0 && o.interp_tile < 16)) throw VpError{VP_ERR_ARG};
     if (o.interp_tile > 0) P->TSI = o.interp_tile;
     if (o.fft_mode < 0 || o.fft_mode > 1) throw VpError{VP_ERR_ARG};
-    if (o.spread_pack < 0 || o.spread_pack > 1) throw VpError{VP_ERR_ARG};
+    if (o.spread_pack < 0 || o.spread_pack > 2) throw VpError{VP_ERR_ARG};
     if (o.fft_rows < 0 || o.fft_rows > 1) throw VpError{VP_ERR_ARG};
     if (o.boundary.kind == VP_BDRY_CIRCLE && !(o.boundary.p[2] > 0)) throw VpError{VP_ERR_GEOMETRY};
     if (o.boundary.kind == VP_BDRY_RECT && !(o.boundary.p[2] > o.boundary.p[0] && o.boundary.p[3] > o.boundary.p[1]))

@@ -118,7 +118,8 @@ struct VpSpreadSet {
   int det = 0;                 // deterministic mode: items sorted by tile colour, colour_off[c]..colour_off[c+1]
   int64_t color_off[5] = {};
   double *fs_out = nullptr;    // if set, the spread also writes f in this sorted order
-  int strip = 0;               // 1: strip order for k_spread_strip (sitems), 0: tile batches (tiles, bstart)
+  int strip = 0;               // 2: row-pair strips (k_spread_pair), 1: 32-column strips (k_spread_strip), both
+                               // with sitems; 0: tile batches (tiles, bstart)
   int4 *sitems = nullptr;      // (strip_x, strip_y, first point, end point)
   int64_t n_sitems = 0;
 };

@@ -686,13 +686,29 @@ struct Fft4Args {
   const double *e1, *e2;  // NH: e^{-dk^2 m^2 delta_1}, e^{-dk^2 m^2 delta_2} for m <= half_modes (separable exponentials)
 };
 
-// N rows (global row row0 + i * rstride) x TC4 columns <-> shared a[i * TC4 + c]
+// N rows (global row row0 + i * rstride) x TC4 columns <-> shared a[i * TC4 + c].  The load is asynchronous
+// (cp.async, 16 B per element): every element of the tile is in flight at once instead of one dependent
+// global load per thread and loop trip (the synchronous copy left the column kernels latency-bound at ~3 TB/s).
 __device__ __forceinline__ void fft4_load(double2 *a, const Fft4Args &g, int c0, int ncol, int64_t row0,
                                           int64_t rstride, int N) {
   const int c = threadIdx.x % TC4;
-  for (int i = threadIdx.x / TC4; i < N; i += Q4)
-    a[i * TC4 + c] = c < ncol ? g.spec[(row0 + (int64_t)i * rstride) * g.nc + c0 + c] : make_double2(0.0, 0.0);
+  for (int i = threadIdx.x / TC4; i < N; i += Q4) {
+    if (c < ncol) __pipeline_memcpy_async(a + i * TC4 + c, g.spec + (row0 + (int64_t)i * rstride) * g.nc + c0 + c,
+                                          sizeof(double2));
+    else a[i * TC4 + c] = make_double2(0.0, 0.0);
+  }
+  __pipeline_commit();
+  __pipeline_wait_prior(0);
   __syncthreads();
+}
+
+// 1/x to ~1 ulp: hardware approximation + two Newton steps (the multiplier needs ~1e-15 relative, not IEEE
+// rounding; the IEEE division costs a long instruction sequence per spectrum element)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  return fma(r, fma(-x, r, 1.0), r);
 }
 __device__ __forceinline__ void fft4_store(const double2 *a, const Fft4Args &g, int c0, int ncol, int64_t row0,
                                            int64_t rstride, int N) {
@@ -703,7 +719,7 @@ __device__ __forceinline__ void fft4_store(const double2 *a, const Fft4Args &g, 
 }
 
 // A: blockIdx.x = column tile, blockIdx.y = n2
-__global__ void __launch_bounds__(256) k_fft4_a(Fft4Args g) {
+__global__ void __launch_bounds__(256, 4) k_fft4_a(Fft4Args g) {
   extern __shared__ double2 sm2[];
   const int c0 = blockIdx.x * TC4, ncol = min(TC4, g.ncs - c0), n2 = blockIdx.y;
   fft4_load(sm2, g, c0, ncol, n2, g.N2, g.N1);
@@ -715,7 +731,7 @@ __global__ void __launch_bounds__(256) k_fft4_a(Fft4Args g) {
 }
 
 // B: blockIdx.x = column tile, blockIdx.y = p (position of k1)
-__global__ void __launch_bounds__(256) k_fft4_b(Fft4Args g) {
+__global__ void __launch_bounds__(256, 4) k_fft4_b(Fft4Args g) {
   extern __shared__ double2 sm2[];
   const int c0 = blockIdx.x * TC4, ncol = min(TC4, g.ncs - c0), p = blockIdx.y;
   const int64_t row0 = (int64_t)p * g.N2;
@@ -739,7 +755,7 @@ __global__ void __launch_bounds__(256) k_fft4_b(Fft4Args g) {
       } else if (k2 * g.db > 0.25) {
         // (e^{-k^2 d1} - e^{-k^2 d2}) / k^2 from the separable exponentials (no cancellation here: the
         // difference is >= 0.2 e^{-k^2 d1} once k^2 d2 > 1/4 with d2 = 32 d1); vp_mult_nh (expm1) below
-        mk = (e1x * __ldg(g.e1 + a2m) - e2x * __ldg(g.e2 + a2m)) / k2;
+        mk = (e1x * __ldg(g.e1 + a2m) - e2x * __ldg(g.e2 + a2m)) * rcp_nr(k2);
       } else {
         mk = vp_mult_nh(k2, g.da, g.db);
       }
@@ -759,7 +775,7 @@ __global__ void __launch_bounds__(256) k_fft4_b(Fft4Args g) {
 }
 
 // C: blockIdx.x = column tile, blockIdx.y = n2'
-__global__ void __launch_bounds__(256) k_fft4_c(Fft4Args g) {
+__global__ void __launch_bounds__(256, 4) k_fft4_c(Fft4Args g) {
   extern __shared__ double2 sm2[];
   const int c0 = blockIdx.x * TC4, ncol = min(TC4, g.ncs - c0), n2 = blockIdx.y;
   fft4_load(sm2, g, c0, ncol, n2, g.N2, g.N1);

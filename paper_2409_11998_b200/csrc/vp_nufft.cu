@@ -561,18 +561,210 @@ static void launch_spread_strip_w(vp_plan_s *P, const VpSpreadSet &S, const Grid
   P->n_kernels++;
 }
 
-// strip geometry of width W (host side of StripCfg)
-void vp_strip_dims(int W, int *SW, int *SH) {
-  *SW = 33 - W;
-  *SH = VP_STRIP_SH;
+// ---------------------------------------------------------------------------------------------
+// Row-pair strips (default for W <= 12).  Measured on B200 (profiles/r2): the 32-column strip
+// above is bound by shared-memory wavefronts (~16 per point; an LDS.128 broadcast costs 2 of them) and wastes
+// 32 - W of the 32 lanes in every DFMA step.  Here a warp owns 16 grid columns and two row phases: lane
+// (c, h) = (lane & 15, lane >> 4) accumulates column c of the rows 2P + h, so a point's W x W footprint keeps
+// W of 16 columns busy (62% at W = 10) and each lane needs only the ~W/2 y weights of its row parity.  Row
+// pairs (2P, 2P + 1) live in a register ring of S = W/2 + 1 slots (pair P in acc[P mod S]); a point with origin
+// row r (pair P = r >> 1) adds to pairs P .. P + S - 1 the products wx[c - lc] * c_j wy[2j + h - (r & 1)]
+// (zero-padded taps at -1 and >= W), i.e. one LDS.64 of two adjacent addresses (one wavefront) and one DFMA
+// per pair.  The x taps are staged compactly with fixed zero margins, so the lane's x weight is one LDS.64 of
+// 16 consecutive words, and no padding is rewritten when points are restaged.  Per point: 1 meta + 1 x + S - 1
+// or S y loads (about 7.5 wavefronts at W = 10) and S - 1 or S DFMA per lane.  Strips are SW = 17 - W origin
+// columns wide, so the RED flush covers 16 / SW columns per origin column (more halo REDs than the 32-column
+// strip, 2.3x vs 1.4x at W = 10; the L2 atomic rate, 4.7e11/s, is below the shared-memory bound).
+#ifndef VP_PAIR_SH
+#define VP_PAIR_SH 64  // footprint-origin rows per pair strip (even)
+#endif
+template <int W>
+struct PairCfg {
+  static constexpr int SW = 17 - W;  // footprint-origin columns per strip
+  static constexpr int SH = VP_PAIR_SH;
+  static constexpr int S = W / 2 + 1;  // ring slots (row pairs touched by one footprint)
+  static constexpr int CH = 32;
+  static constexpr int XO = SW & ~1;   // x row: tap a at XO + a (XO >= SW - 1, even), zeros around
+  static constexpr int odd_half(int n) { return ((n / 2) & 1) ? n : n + 2; }  // 16-byte stride odd: no conflicts
+  static constexpr int WXS = odd_half(XO + 16);
+  static constexpr int WYS = odd_half(2 * S + 2);  // y row: c wy[b] at 2 + b, zeros at 0, 1 and >= 2 + W
+  static constexpr size_t smem_warp = (size_t)CH * (WXS + WYS + 1) * 8;  // + per-point meta (int2)
+  // warps per CTA and CTAs per SM: 21 warps (80 registers) at W <= 10; wider kernels need ~96 registers, i.e. at
+  // most 5 warps per SM sub-partition
+  static constexpr int WARPS = W <= 10 ? 7 : 4;
+  static constexpr int MINB = W <= 10 ? 3 : 5;
+};
+
+template <int W, int D>
+__global__ void __launch_bounds__(32 * PairCfg<W>::WARPS, PairCfg<W>::MINB)
+    k_spread_pair(const int4 *__restrict__ items, int64_t n_items, const double *__restrict__ sx,
+                  const double *__restrict__ sy, const double *__restrict__ sw, const int32_t *__restrict__ sperm,
+                  const double *__restrict__ f, GridArgs g, double *__restrict__ fs_out) {
+  using C = PairCfg<W>;
+  constexpr int S = C::S;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = lane & 15, h = lane >> 4;
+  const int64_t item = (int64_t)blockIdx.x * C::WARPS + warp;
+  if (item >= n_items) return;
+  double *s_wx = smem + (size_t)warp * (C::CH * (C::WXS + C::WYS + 1));
+  double *s_wy = s_wx + C::CH * C::WXS;
+  int2 *s_meta = (int2 *)(s_wy + C::CH * C::WYS);
+  // fixed zero margins of the staged rows (the staging below writes only the tap positions)
+  for (int i = lane; i < C::CH * C::WXS; i += 32) s_wx[i] = 0.0;
+  for (int i = lane; i < C::CH * C::WYS; i += 32) s_wy[i] = 0.0;
+  __syncwarp();
+  // lane bases: the staged per-point meta holds byte offsets, so a point costs one broadcast load, two adds and
+  // the tap loads with immediate offsets (no per-point index arithmetic)
+  const char *xb = (const char *)s_wx + 8 * c;
+  const char *yb = (const char *)s_wy + 8 * h;
+  const int4 it = items[item];
+  const int64_t ox = (int64_t)it.x * C::SW - (W / 2 + 1), oy = (int64_t)it.y * C::SH - (W / 2 + 1);
+  const bool interior = ox >= 0 && oy >= 0 && ox + 16 <= g.nfx && oy + C::SH + W + 1 <= g.nfy;
+  double *col = g.data + (interior ? ox + c : wrapi(ox + c, g.nfx));
+  // two accumulator rings, for the even and odd points of a row-pair step: consecutive points then have no DFMA
+  // dependency (the ring is summed when a pair is flushed)
+  // (W >= 11: one ring; the second one does not fit the register budget of 3 CTAs per SM)
+  constexpr bool TWO = W <= 10;
+  double acc[S], acc_b[S];
+  double(&acc2)[S] = TWO ? acc_b : acc;
+#pragma unroll
+  for (int b = 0; b < S; b++) acc[b] = acc_b[b] = 0.0;
+  double *rowp = nullptr;  // interior items: the flushed pair's row 2P + h in column c (advanced by 2 rows)
+  int c0 = it.z, n = 0, q = 0, P = 0, mylr = 0x7fffffff;
+  bool first = true;
+  // software pipeline over the 32-point chunks: the coordinates, weight and f of chunk k + 1 and the f index of
+  // chunk k + 2 are loaded while chunk k is staged and walked, so no global-load latency (two dependent loads for
+  // f[sperm[j]]) is exposed at a staging step
+  double px = 0.0, py = 0.0, pw = 0.0, pf = 0.0;
+  int pidx = 0;
+  {
+    const int j = c0 + lane;
+    if (j < it.w) {
+      px = sx[j];
+      py = sy[j];
+      pw = sw[j];
+      pf = __ldg(f + sperm[j]);
+    }
+    if (j + C::CH < it.w) pidx = sperm[j + C::CH];
+  }
+stage:
+  n = min(C::CH, it.w - c0);
+  mylr = 0x7fffffff;
+  {
+    const double xj = px, yj = py, wj = pw, fj = pf;
+    const int j = c0 + lane, jn = j + C::CH;
+    if (jn < it.w) {
+      px = sx[jn];
+      py = sy[jn];
+      pw = sw[jn];
+      pf = __ldg(f + pidx);
+    }
+    if (jn + C::CH < it.w) pidx = sperm[jn + C::CH];
+    if (lane < n) {
+      if (fs_out) fs_out[j] = fj;  // f in spreading order: spatially coherent copy for the stencil gathers
+      const double cj = fj * wj;
+      double wv[W];
+      const int lc = (int)(es_horner<W, D>(gcoord(xj, g.ox, g.inv_h), wv) - ox);
+      double2 *xp = (double2 *)(s_wx + lane * C::WXS + C::XO);
+#pragma unroll
+      for (int a = 0; a < W; a += 2) xp[a >> 1] = make_double2(wv[a], a + 1 < W ? wv[a + 1] : 0.0);
+      const int lr = (int)(es_horner<W, D>(gcoord(yj, g.oy, g.inv_h), wv) - oy);
+      double2 *yp = (double2 *)(s_wy + lane * C::WYS + 2);
+#pragma unroll
+      for (int b = 0; b < W; b += 2) yp[b >> 1] = make_double2(cj * wv[b], b + 1 < W ? cj * wv[b + 1] : 0.0);
+      // x tap of lane column c at byte xb + meta.x: tap c - lc of this point's row; y taps of lane half h at
+      // yb + meta.y + 16 j: c wy[2j + h - (lr & 1)] (zero-padded at -1 and >= W)
+      s_meta[lane] = make_int2(8 * (lane * C::WXS + C::XO - lc), 8 * (lane * C::WYS + 2 - (lr & 1)));
+      mylr = lr;
+    }
+  }
+  __syncwarp();
+  q = 0;
+  if (first) {
+    P = __shfl_sync(0xffffffffu, mylr, 0) >> 1;
+    rowp = col + (oy + 2 * P + h) * g.row;
+    first = false;
+  }
+  for (;;) {
+    switch (P % S) {
+#define VP_PAIR_POINT(ACC, qq, K)                                                                      \
+  {                                                                                                   \
+    const int2 m = s_meta[qq];                                                                        \
+    const double wxl = *(const double *)(xb + m.x);                                                   \
+    const char *yp = yb + m.y;                                                                        \
+    _Pragma("unroll") for (int jj = 0; jj < S; jj++)                                                  \
+      ACC[((K) + jj) % S] = fma(*(const double *)(yp + 16 * jj), wxl, ACC[((K) + jj) % S]);           \
+  }
+#define VP_PAIR_PHASE(k)                                                                              \
+  case k:                                                                                             \
+    if ((k) < S) {                                                                                    \
+      const int e = __popc(__ballot_sync(0xffffffffu, mylr <= 2 * P + 1));                             \
+      for (; q + 1 < e; q += 2) {                                                                     \
+        VP_PAIR_POINT(acc, q, k)                                                                      \
+        VP_PAIR_POINT(acc2, q + 1, k)                                                                 \
+      }                                                                                               \
+      if (q < e) {                                                                                    \
+        VP_PAIR_POINT(acc, q, k)                                                                      \
+        q++;                                                                                          \
+      }                                                                                               \
+      if (q == n) goto next_chunk;                                                                    \
+      const double v = TWO ? acc[(k)] + acc2[(k)] : acc[(k)];                                        \
+      if (interior) {                                                                                 \
+        if (v != 0.0) atomicAdd(rowp, v);                                                             \
+      } else if (v != 0.0) {                                                                          \
+        red_row_wrapped(col, oy + 2 * P + h, g.nfy, g.row, v);                                        \
+      }                                                                                               \
+      rowp += 2 * g.row;                                                                              \
+      acc[(k)] = 0.0;                                                                                 \
+      acc2[(k)] = 0.0;                                                                                \
+      P++;                                                                                            \
+    }
+      VP_PAIR_PHASE(0) VP_PAIR_PHASE(1) VP_PAIR_PHASE(2) VP_PAIR_PHASE(3) VP_PAIR_PHASE(4)
+      VP_PAIR_PHASE(5) VP_PAIR_PHASE(6) VP_PAIR_PHASE(7) VP_PAIR_PHASE(8)
+#undef VP_PAIR_PHASE
+#undef VP_PAIR_POINT
+    }
+  }
+next_chunk:
+  __syncwarp();
+  c0 += C::CH;
+  if (c0 < it.w) goto stage;
+  // flush the ring: acc[i] holds pair P + ((i - P) mod S)
+#pragma unroll
+  for (int i = 0; i < S; i++) red_row(col, oy + 2 * (P + ((i - P % S) + S) % S) + h, interior, g, TWO ? acc[i] + acc2[i] : acc[i]);
+}
+
+template <int W>
+static void launch_spread_pair_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *f) {
+  constexpr int D = VP_HORNER_DEG(W);
+  if constexpr (W <= 12) {
+    if (S.n_sitems == 0) return;
+    constexpr int NW = PairCfg<W>::WARPS;
+    const size_t sm = PairCfg<W>::smem_warp * NW;
+    const unsigned nb = (unsigned)((S.n_sitems + NW - 1) / NW);
+    vp_smem_attr((const void *)k_spread_pair<W, D>, sm);
+    k_spread_pair<W, D><<<nb, 32 * NW, sm, P->stream>>>(S.sitems, S.n_sitems, S.sx, S.sy, S.sw, S.sperm,
+                                                                   f, g, S.fs_out);
+    VP_CHECK_LAUNCH();
+    P->n_kernels++;
+  } else {
+    throw VpError{VP_ERR_UNSUPPORTED};
+  }
+}
+
+// strip geometry of width W (host side of StripCfg / PairCfg): kind 0 = 32-column strips, 1 = row-pair strips
+void vp_strip_dims(int W, int kind, int *SW, int *SH) {
+  *SW = kind ? 17 - W : 33 - W;
+  *SH = kind ? VP_PAIR_SH : VP_STRIP_SH;
 }
 
 void vp_launch_spread(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *f) {
   switch (P->w) {
-#define CASE(W)                                      \
-  case W:                                            \
-    if (S.strip) launch_spread_strip_w<W>(P, S, g, f); \
-    else launch_spread_w<W>(P, S, g, f);              \
+#define CASE(W)                                                \
+  case W:                                                      \
+    if (S.strip == 2) launch_spread_pair_w<W>(P, S, g, f);     \
+    else if (S.strip) launch_spread_strip_w<W>(P, S, g, f);    \
+    else launch_spread_w<W>(P, S, g, f);                       \
     break;
     CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
@@ -732,7 +924,8 @@ void vp_launch_spread_batch(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &
                             double *const *grids, double *const *fs) {
   if (!S.strip) throw VpError{VP_ERR_UNSUPPORTED};
   for (int k0 = 0; k0 < K;) {
-    const int kb = K - k0 >= 4 ? 4 : (K - k0 >= 2 ? 2 : 1);
+    // row-pair strips: one pass per field (the shared-staging batch kernel exists for 32-column strips)
+    const int kb = S.strip == 2 ? 1 : (K - k0 >= 4 ? 4 : (K - k0 >= 2 ? 2 : 1));
     if (kb == 1) {
       VpSpreadSet S1 = S;
       S1.fs_out = fs ? fs[k0] : nullptr;
@@ -1319,6 +1512,31 @@ __global__ void __launch_bounds__(256, 4) k_interp_local(const int4 *__restrict_
     }
     double v = 0.0;
     if (do_hist) {
+      if constexpr (W <= 0) {  // (measured slower at config 5: 3 CTAs/SM to avoid spills, 7.9 vs 7.2 ms)
+      // x taps by even/odd Horner pairs (half the DFMA of W chains); the y taps of rows b and W - 1 - b come from
+      // one pair evaluation inside the row loop, so only the W x taps stay live (wider kernels spill with this
+      // form and keep the W separate chains below)
+      double wx[W], ty;
+      const int lx = (int)(es_horner<W, D>(gcoord(xc, g.ox, g.inv_h), wx) - ox);
+      const int ly = (int)(es_arg<W>(gcoord(yc, g.oy, g.inv_h), &ty) - oy);
+      const double uy = ty * ty;
+      const double *rp = tile + ly * nw + lx;
+#pragma unroll
+      for (int b = 0; b < (W + 1) / 2; b++) {
+        double wk, wm;
+        es_pair<W, D>(b, ty, uy, &wk, &wm);
+        double racc = 0.0;
+#pragma unroll
+        for (int a = 0; a < W; a++) racc = fma(wx[a], rp[b * nw + a], racc);
+        v = fma(wk, racc, v);
+        if (W - 1 - b != b) {
+          double racc2 = 0.0;
+#pragma unroll
+          for (int a = 0; a < W; a++) racc2 = fma(wx[a], rp[(W - 1 - b) * nw + a], racc2);
+          v = fma(wm, racc2, v);
+        }
+      }
+      } else {
       double wx[W], wy[W];
       const int lx = (int)(es_horner_chains<W, D>(gcoord(xc, g.ox, g.inv_h), wx) - ox);
       const int ly = (int)(es_horner_chains<W, D>(gcoord(yc, g.oy, g.inv_h), wy) - oy);
@@ -1329,6 +1547,7 @@ __global__ void __launch_bounds__(256, 4) k_interp_local(const int4 *__restrict_
 #pragma unroll
         for (int a = 0; a < W; a++) racc = fma(wx[a], rp[b * nw + a], racc);
         v = fma(wy[b], racc, v);
+      }
       }
     }
     out[dst] = v + vl;
@@ -1829,14 +2048,15 @@ __global__ void k_strip_key_shift(uint64_t *__restrict__ k, int64_t n) {
   k[i] = ((key >> 16) << 32) | (((key >> 8) & 0xff) << 24) | (key & 0xff);
 }
 
-void vp_strip_dims(int W, int *SW, int *SH);
+void vp_strip_dims(int W, int kind, int *SW, int *SH);
 
 void vp_build_strip_order(vp_plan_s *P, VpSpreadSet &S, const double *xy, const double *weights,
                           const int32_t *node_of, int64_t n, const GridArgs &g) {
   cudaStream_t s = P->stream;
-  S.strip = 1;
+  // 2: row-pair strips (k_spread_pair, default for W <= 12); 1: 32-column strips (k_spread_strip)
+  S.strip = (P->opts.spread_pack == 0 && P->w <= 12) ? 2 : 1;
   int SW, SH;
-  vp_strip_dims(P->w, &SW, &SH);
+  vp_strip_dims(P->w, S.strip == 2, &SW, &SH);
   const int64_t nsx = (g.nfx + P->w + 2) / SW + 1, nsy = (g.nfy + P->w + 2) / SH + 1;
   if (n == 0) {
     S.sx = vp_alloc<double>(P, 1); S.sy = vp_alloc<double>(P, 1); S.sw = vp_alloc<double>(P, 1);

@@ -99,12 +99,6 @@ static int run_groups(double *d, int blocks, int threads, int nsm, int clk, cuda
   const double warp_instr = (double)blocks * (threads / 32) * iters * 8;
   printf("lds.%d %d address group(s) per warp: %.3f ms, %.3f warp-instr/clk/SM\n", 64 * V, G, ms,
          warp_instr / (ms * 1e-3) / nsm / (clk * 1e3));
-  run_groups<1, 1>(d, blocks, threads, nsm, clk, a, b);
-  run_groups<2, 1>(d, blocks, threads, nsm, clk, a, b);
-  run_groups<4, 1>(d, blocks, threads, nsm, clk, a, b);
-  run_groups<1, 2>(d, blocks, threads, nsm, clk, a, b);
-  run_groups<2, 2>(d, blocks, threads, nsm, clk, a, b);
-  run_groups<4, 2>(d, blocks, threads, nsm, clk, a, b);
   return 0;
 }
 

@@ -375,11 +375,13 @@ def test_strip_spread_matches_tile_spread(tol):
     tg_np = rng.uniform(0.0, 1.0, (2000, 2))
     nodes, wts, tg, f = (torch.from_numpy(np.ascontiguousarray(a)).to(DEV) for a in (nodes_np, wts_np, tg_np, f_np))
     out = []
-    for st in (0, 32):
-        plan = vp.Plan(nodes, wts, tg, tol, parts=vp.PART_HISTORY, spread_tile=st)
+    # spread_pack 0: row-pair strips (w <= 12) / 32-column strips; 1: 32-column packs; 2: 32-column single steps
+    for st, pk in ((32, 0), (0, 0), (0, 1), (0, 2)):
+        plan = vp.Plan(nodes, wts, tg, tol, parts=vp.PART_HISTORY, spread_tile=st, spread_pack=pk)
         out.append(plan.eval(f).cpu().numpy())
-    scale = np.max(np.abs(out[1]))
-    assert np.max(np.abs(out[0] - out[1])) <= 1e-13 * scale
+    scale = np.max(np.abs(out[0]))
+    for k in range(1, 4):
+        assert np.max(np.abs(out[k] - out[0])) <= 1e-13 * scale, k
 
 
 @pytest.mark.parametrize("which", ["c1", "c2small", "c2loose"])
@@ -444,10 +446,12 @@ def test_strip_spread_lattice_nodes():
     nodes, wts, tg, f = (torch.from_numpy(np.ascontiguousarray(a)).to(DEV) for a in (nodes_np, wts_np, tg_np, f_np))
     d1 = 3.0 * float(wts_np.mean())
     out = []
-    for st in (0, 32):
-        plan = vp.Plan(nodes, wts, tg, 1e-13, parts=vp.PART_HISTORY, delta1_override=d1, spread_tile=st)
+    for tol, st, pk in ((1e-13, 32, 0), (1e-13, 0, 0), (1e-13, 0, 1), (1e-11, 32, 0), (1e-11, 0, 0), (1e-11, 0, 2)):
+        plan = vp.Plan(nodes, wts, tg, tol, parts=vp.PART_HISTORY, delta1_override=d1, spread_tile=st,
+                       spread_pack=pk)
         out.append(plan.eval(f).cpu().numpy())
-    assert np.max(np.abs(out[0] - out[1])) <= 1e-13 * np.max(np.abs(out[1]))
+    for a, b in ((1, 0), (2, 0), (4, 3), (5, 3)):  # same tol: same grid, the spreaders agree to rounding
+        assert np.max(np.abs(out[a] - out[b])) <= 1e-13 * np.max(np.abs(out[b])), (a, b)
     ref = oracle.smooth_direct(pts, (f_np * wts_np).ravel(), tg_np, d1)
     assert rel_l2(out[0], ref) < 1e-12
 
