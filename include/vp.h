@@ -126,8 +126,9 @@ typedef struct {
    * per warp) when w <= 12, else 32-column strips; 1 -> 32-column strips with column-disjoint packs of points per
    * step; 2 -> 32-column strips, one point per step (k_spread_strip) */
   int32_t spread_pack;
-  /* grids above 6400^2 (four-step column pass): 0 -> cuFFT batched 1D row transforms, 1 -> own pruned row passes
-   * (nf % 4 == 0; measured slower than cuFFT's at config 5) */
+  /* grids above 6400^2 (four-step column pass): 0 -> own pruned row passes (nf % 4 == 0 and a whole row,
+   * 2 x nf/4 complex values, in one CTA's shared memory: nf <= 28160), else cuFFT batched 1D row
+   * transforms; 1 -> cuFFT batched 1D row transforms */
   int32_t fft_rows;
 } vp_opts;
 

@@ -407,7 +407,7 @@ static void make_fft_plans(vp_plan_s *P) {
     VP_CUFFT(cufftCreate(&G.inv));
     VP_CUFFT(cufftSetAutoAllocation(G.fwd, 0));
     VP_CUFFT(cufftSetAutoAllocation(G.inv, 0));
-    if (vp_fft4_setup(P, G) && P->opts.fft_rows == 1 && vp_fft4_rows_setup(P, G)) {
+    if (vp_fft4_setup(P, G) && P->opts.fft_rows == 0 && vp_fft4_rows_setup(P, G)) {
       // large grid: own pruned row passes + the four-step column pass (vp_fft.cu); no cuFFT plan
       VP_CUFFT(cufftDestroy(G.fwd));
       VP_CUFFT(cufftDestroy(G.inv));
@@ -661,6 +661,21 @@ static void grid_fft_inv(vp_plan_s *P, VpGrid &G) {
   P->n_ffts++;
 }
 
+// inverse transforms of both grids and the far-history prolongation q1 += R^T q2: with own NH row passes the
+// prolongation's x pass runs inside the NH inverse row pass (vp_fft4_rows_inv_prolong), after the FH inverse and
+// the y pass
+static void grids_inverse_prolong(vp_plan_s *P) {
+  if (vp_fft4_rows_prolong_ok(P)) {
+    grid_fft_inv(P, P->fh);
+    vp_launch_prolong(P, 1);
+    vp_fft4_rows_inv_prolong(P);
+    return;
+  }
+  grid_fft_inv(P, P->nh);
+  grid_fft_inv(P, P->fh);
+  vp_launch_prolong(P, 3);
+}
+
 static void record(vp_plan_s *P, int i) {
   if (P->profiling) cudaEventRecord(P->ev[i], P->stream);
 }
@@ -753,10 +768,17 @@ extern "C" vp_status vp_eval(vp_handle P, const double *f, double *out) {
       grid_multiply(P, P->nh);
       grid_multiply(P, P->fh);
       record(P, 5);
-      grid_fft_inv(P, P->nh);
-      grid_fft_inv(P, P->fh);
-      record(P, 6);
-      vp_launch_prolong(P, 3);
+      if (vp_fft4_rows_prolong_ok(P)) {  // the prolongation's x pass is fused into the NH inverse rows
+        grid_fft_inv(P, P->fh);
+        vp_launch_prolong(P, 1);
+        vp_fft4_rows_inv_prolong(P);
+        record(P, 6);
+      } else {
+        grid_fft_inv(P, P->nh);
+        grid_fft_inv(P, P->fh);
+        record(P, 6);
+        vp_launch_prolong(P, 3);
+      }
       record(P, 7);
     } else {
       for (int i = 1; i <= 7; i++) record(P, i);
@@ -821,9 +843,7 @@ extern "C" vp_status vp_eval_batch(vp_handle P, int32_t K, const double *f, doub
           grid_fft_fwd(P, P->fh);
           grid_multiply(P, P->nh);
           grid_multiply(P, P->fh);
-          grid_fft_inv(P, P->nh);
-          grid_fft_inv(P, P->fh);
-          vp_launch_prolong(P, 3);
+          grids_inverse_prolong(P);
         }
         vp_launch_interp_local(P, fk[k], out + (size_t)k * P->T, true);
         if (parts & VP_PART_LOCAL) vp_launch_bands(P, fk[k], out + (size_t)k * P->T);

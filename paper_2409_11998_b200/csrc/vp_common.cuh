@@ -43,6 +43,12 @@ void vp_set_last_error(const std::string &s);
 void vp_smem_attr(const void *func, size_t bytes);
 // current device (cached per call site is not safe across devices: always ask the runtime)
 int vp_current_device();
+// SM count of the current device (plans may live on different devices)
+inline int vp_num_sms() {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, vp_current_device());
+  return n > 0 ? n : 1;
+}
 
 // ---------------------------------------------------------------------------------------------
 // ES kernel taps as Horner polynomials: psi(z_k(t)), z_k = (k + (t+1)/2 - W/2) 2/W, t in [-1, 1]
@@ -295,7 +301,10 @@ void vp_fft_inverse(vp_plan_s *P, VpGrid &G);
 bool vp_fft4_setup(vp_plan_s *P, VpGrid &G);
 bool vp_fft4_rows_setup(vp_plan_s *P, VpGrid &G);
 void vp_fft4_rows_fwd(vp_plan_s *P, VpGrid &G);
-void vp_fft4_rows_inv(vp_plan_s *P, VpGrid &G);
+struct RowProlong;
+void vp_fft4_rows_inv(vp_plan_s *P, VpGrid &G, const RowProlong *pr = nullptr);
+bool vp_fft4_rows_prolong_ok(vp_plan_s *P);
+void vp_fft4_rows_inv_prolong(vp_plan_s *P);  // NH inverse rows + prolongation x pass (after pass 1)
 void vp_fft4_columns(vp_plan_s *P, VpGrid &G);
 void vp_launch_spread_batch(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, int K, const double *const *f,
                             double *const *grids, double *const *fs);

@@ -741,28 +741,53 @@ __global__ void __launch_bounds__(256, 4) k_fft4_b(Fft4Args g) {
   const int c = threadIdx.x % TC4;
   const int m1 = c0 + c;
   const double d1 = m1 <= g.half_modes ? __ldg(g.deconv + m1) * g.scale : 0.0;
-  const double e1x = g.kind == 0 && m1 <= g.half_modes ? __ldg(g.e1 + m1) : 0.0;
-  const double e2x = g.kind == 0 && m1 <= g.half_modes ? __ldg(g.e2 + m1) : 0.0;
-  for (int p2 = threadIdx.x / TC4; p2 < g.N2; p2 += Q4) {
-    const int k = k1 + g.N1 * __ldg(g.sig2 + p2);
-    const int m2 = k <= g.nf / 2 ? k : k - g.nf, a2m = m2 < 0 ? -m2 : m2;
-    double fac = 0.0;
-    if (m1 <= g.half_modes && a2m <= g.half_modes) {
-      const double k2 = g.dk * g.dk * ((double)m1 * m1 + (double)m2 * m2);
-      double mk;
-      if (g.kind != 0) {
-        mk = vp_mult_fh(k2, g.da, g.db);
-      } else if (k2 * g.db > 0.25) {
-        // (e^{-k^2 d1} - e^{-k^2 d2}) / k^2 from the separable exponentials (no cancellation here: the
-        // difference is >= 0.2 e^{-k^2 d1} once k^2 d2 > 1/4 with d2 = 32 d1); vp_mult_nh (expm1) below
-        mk = (e1x * __ldg(g.e1 + a2m) - e2x * __ldg(g.e2 + a2m)) * rcp_nr(k2);
-      } else {
-        mk = vp_mult_nh(k2, g.da, g.db);
-      }
-      fac = mk * d1 * __ldg(g.deconv + a2m);
+  if (g.kind == 0) {
+    // NH: per-row factors of the separable form staged once per CTA (the CTA's rows share k1): for row p2,
+    // b1 = e^{-k2^2 d_a} deconv(m2), b2 = e^{-k2^2 d_b} deconv(m2) (0 beyond the kept band) and m2^2; an element
+    // is then (a1 b1 - a2 b2) / k^2 with the column factors a1, a2 (the small-k^2 branch keeps expm1)
+    double *rb = (double *)(sm2 + TC4 * g.N2);  // [N2][3]
+    for (int p2 = threadIdx.x; p2 < g.N2; p2 += blockDim.x) {
+      const int k = k1 + g.N1 * __ldg(g.sig2 + p2);
+      const int m2 = k <= g.nf / 2 ? k : k - g.nf, a2m = m2 < 0 ? -m2 : m2;
+      const bool in = a2m <= g.half_modes;
+      const double dm = in ? __ldg(g.deconv + a2m) : 0.0;
+      rb[3 * p2] = in ? __ldg(g.e1 + a2m) * dm : 0.0;
+      rb[3 * p2 + 1] = in ? __ldg(g.e2 + a2m) * dm : 0.0;
+      rb[3 * p2 + 2] = in ? (double)m2 * (double)m2 : -1.0;  // -1: outside the band
     }
-    const double2 v = sm2[p2 * TC4 + c];
-    sm2[p2 * TC4 + c] = make_double2(v.x * fac, v.y * fac);
+    __syncthreads();
+    const bool col_in = m1 <= g.half_modes;
+    const double a1 = col_in ? __ldg(g.e1 + m1) * d1 : 0.0, a2 = col_in ? __ldg(g.e2 + m1) * d1 : 0.0;
+    const double dk2 = g.dk * g.dk, m1sq = (double)m1 * m1;
+    for (int p2 = threadIdx.x / TC4; p2 < g.N2; p2 += Q4) {
+      const double m2sq = rb[3 * p2 + 2];
+      double fac = 0.0;
+      if (col_in && m2sq >= 0.0) {
+        const double k2 = dk2 * (m1sq + m2sq);
+        if (k2 * g.db > 0.25) {
+          // (e^{-k^2 d1} - e^{-k^2 d2}) / k^2 from the separable exponentials (no cancellation here: the
+          // difference is >= 0.2 e^{-k^2 d1} once k^2 d2 > 1/4 with d2 = 32 d1); vp_mult_nh (expm1) below
+          fac = fma(a1, rb[3 * p2], -a2 * rb[3 * p2 + 1]) * rcp_nr(k2);
+        } else {
+          const int a2m = (int)llrint(sqrt(m2sq));
+          fac = vp_mult_nh(k2, g.da, g.db) * d1 * __ldg(g.deconv + a2m);
+        }
+      }
+      const double2 v = sm2[p2 * TC4 + c];
+      sm2[p2 * TC4 + c] = make_double2(v.x * fac, v.y * fac);
+    }
+  } else {
+    for (int p2 = threadIdx.x / TC4; p2 < g.N2; p2 += Q4) {
+      const int k = k1 + g.N1 * __ldg(g.sig2 + p2);
+      const int m2 = k <= g.nf / 2 ? k : k - g.nf, a2m = m2 < 0 ? -m2 : m2;
+      double fac = 0.0;
+      if (m1 <= g.half_modes && a2m <= g.half_modes) {
+        const double k2 = g.dk * g.dk * ((double)m1 * m1 + (double)m2 * m2);
+        fac = vp_mult_fh(k2, g.da, g.db) * d1 * __ldg(g.deconv + a2m);
+      }
+      const double2 v = sm2[p2 * TC4 + c];
+      sm2[p2 * TC4 + c] = make_double2(v.x * fac, v.y * fac);
+    }
   }
   __syncthreads();
   fft_run_t<1, true>(sm2, g.s2, g.tw2);
@@ -863,7 +888,7 @@ void vp_fft4_columns(vp_plan_s *P, VpGrid &G) {
   g.e1 = G.f4_e1;
   g.e2 = G.f4_e2;
   const unsigned ntile = (unsigned)((g.ncs + TC4 - 1) / TC4);
-  const size_t sm1 = sizeof(double2) * (size_t)TC4 * g.N1, sm2 = sizeof(double2) * (size_t)TC4 * g.N2;
+  const size_t sm1 = sizeof(double2) * (size_t)TC4 * g.N1, sm2 = sizeof(double2) * (size_t)TC4 * g.N2 + 24 * (size_t)g.N2;
   vp_smem_attr((const void *)k_fft4_a, sm1);
   vp_smem_attr((const void *)k_fft4_b, sm2);
   vp_smem_attr((const void *)k_fft4_c, sm1);
@@ -883,86 +908,181 @@ void vp_fft4_columns(vp_plan_s *P, VpGrid &G) {
 
 // ---- large-grid row passes (four-step grids with nf % 4 == 0): pruned real FFT by radix-4 decimation in time.
 // Q = nf/4, y_r[m] = x[4m + r], Y_r = FFT_Q(y_r); X[k] = sum_r W_nf^{rk} Y_r[k mod Q] for the kept k < ncs <= Q + 1.
-// Two complex Q-point FFTs per row (z = y_{2h} + i y_{2h+1}, h = 0, 1: Y_{2h}[j] = (Z[j] + conj Z[Q-j]) / 2,
-// Y_{2h+1}[j] = -i (Z[j] - conj Z[Q-j]) / 2), one Q-length shared buffer: two CTAs per SM at config 5 (Q = 5832),
-// and only the kept columns are written (the inverse reads only them: no zeroing of the rest).
-__global__ void __launch_bounds__(512) k_row4_fwd(const double *__restrict__ grid, int64_t row_pitch,
-                                                  double2 *__restrict__ spec, int64_t nc, int ncs, int nf, FftStages st,
-                                                  const double2 *__restrict__ twQ, const double2 *__restrict__ twN,
-                                                  const int32_t *__restrict__ posQ) {
+// Two complex Q-point FFTs per row (z_h = y_{2h} + i y_{2h+1}, h = 0, 1: Y_{2h}[j] = (Z_h[j] + conj Z_h[Q-j]) / 2,
+// Y_{2h+1}[j] = -i (Z_h[j] - conj Z_h[Q-j]) / 2).  One CTA holds a whole row: both Q-length sequences in shared
+// memory (2 Q x 16 B, 187 KB at config 5), loaded by cp.async (16-byte chunk c of the row = (x[2c], x[2c+1]) is
+// z_{c & 1}[c >> 1]: every chunk of the row is in flight at once, each byte read once), both transforms advanced
+// stage by stage with one barrier per stage, X[k] combined from both in shared memory and written once; only the
+// kept columns are written (the inverse reads only them: no zeroing of the rest).  Measured at config 5 (NH):
+// the first form (halves one after the other in 93 KB, X accumulated through global memory, 16 warps/SM) 5.1 ms;
+// a cluster of two CTAs per row (one half each, X combined through distributed shared memory) 5.4 ms (the
+// interleaved 16-byte halves of a row were read / written twice as often from HBM); this form 4.1 ms at 512
+// threads.
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int DIR, bool DIT>
+__device__ void fft_run2(double2 *a0, double2 *a1, const FftStages &st, const double2 *tw) {
+  for (int i = 0; i < st.S; i++) {
+    const int s = DIT ? i : st.S - 1 - i;
+    switch (st.r[s]) {
+#define VP_RUN2(R)                                                \
+  case R:                                                         \
+    fft_stage<R, DIR, DIT>(a0, st.n, st.Lp[s], st.invLp[s], tw); \
+    fft_stage<R, DIR, DIT>(a1, st.n, st.Lp[s], st.invLp[s], tw); \
+    break;
+      VP_RUN2(2) VP_RUN2(3) VP_RUN2(4) VP_RUN2(5) VP_RUN2(7) VP_RUN2(8) VP_RUN2(9)
+#undef VP_RUN2
+      default: break;
+    }
+    __syncthreads();
+  }
+}
+
+#define VP_ROWQ_THREADS 1024
+__global__ void __launch_bounds__(VP_ROWQ_THREADS, 1) k_row4_fwd(const double *__restrict__ grid, int64_t row_pitch,
+                                                                 double2 *__restrict__ spec, int64_t nc, int ncs, int nf,
+                                                                 FftStages st, const double2 *__restrict__ twQ,
+                                                                 const double2 *__restrict__ twN,
+                                                                 const int32_t *__restrict__ posQ) {
   extern __shared__ double2 z[];
   const int Q = st.n;
+  double2 *z0 = z, *z1 = z + Q;
   for (int r = blockIdx.x; r < nf; r += gridDim.x) {
-    const double *x = grid + (int64_t)r * row_pitch;
+    const double2 *x2 = (const double2 *)(grid + (int64_t)r * row_pitch);
+    for (int c = threadIdx.x; c < 2 * Q; c += blockDim.x) cp_async16(((c & 1) ? z1 : z0) + (c >> 1), x2 + c);
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    fft_run2<-1, false>(z0, z1, st, twQ);
     double2 *X = spec + (int64_t)r * nc;
-    for (int h = 0; h < 2; h++) {
-      for (int m = threadIdx.x; m < Q; m += blockDim.x) z[m] = __ldg((const double2 *)(x + 4 * m + 2 * h));
-      __syncthreads();
-      fft_run<-1, false>(z, st, twQ);
-      for (int k = threadIdx.x; k < ncs; k += blockDim.x) {
-        const int j = k < Q ? k : 0;
-        const double2 zj = z[__ldg(posQ + j)], zm = z[__ldg(posQ + (j ? Q - j : 0))];
-        const double2 ya = make_double2(0.5 * (zj.x + zm.x), 0.5 * (zj.y - zm.y));
-        const double2 yb = make_double2(0.5 * (zj.y + zm.y), -0.5 * (zj.x - zm.x));
-        // W^{2hk} ya + W^{(2h+1)k} yb from one coalesced table load (powers by multiplication)
-        const double2 w1 = __ldg(twN + k);
-        const double2 wa = h ? cmul(w1, w1) : make_double2(1.0, 0.0);
-        const double2 a = cmul(wa, ya), b = cmul(cmul(wa, w1), yb);
-        double2 v = make_double2(a.x + b.x, a.y + b.y);
-        if (h) {
-          const double2 p = X[k];  // written by this thread for h = 0
-          v.x += p.x;
-          v.y += p.y;
-        }
-        X[k] = v;
+    for (int k = threadIdx.x; k < ncs; k += blockDim.x) {
+      const int j = k < Q ? k : 0;
+      const int pj = __ldg(posQ + j), pm = __ldg(posQ + (j ? Q - j : 0));
+      const double2 w1 = __ldg(twN + k);  // W_nf^k; W^{2k}, W^{3k} by multiplication
+      const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+      double2 v;
+      {
+        const double2 zj = z0[pj], zm = z0[pm];
+        const double2 ya = make_double2(0.5 * (zj.x + zm.x), 0.5 * (zj.y - zm.y));   // Y_0[j]
+        const double2 yb = make_double2(0.5 * (zj.y + zm.y), -0.5 * (zj.x - zm.x));  // Y_1[j]
+        const double2 b = cmul(w1, yb);
+        v = make_double2(ya.x + b.x, ya.y + b.y);
       }
-      __syncthreads();
+      {
+        const double2 zj = z1[pj], zm = z1[pm];
+        const double2 ya = make_double2(0.5 * (zj.x + zm.x), 0.5 * (zj.y - zm.y));   // Y_2[j]
+        const double2 yb = make_double2(0.5 * (zj.y + zm.y), -0.5 * (zj.x - zm.x));  // Y_3[j]
+        const double2 a = cmul(w2, ya), b = cmul(w3, yb);
+        v.x += a.x + b.x;
+        v.y += a.y + b.y;
+      }
+      X[k] = v;
     }
+    __syncthreads();  // z0 / z1 are refilled for the next row
   }
 }
 
 // inverse: x[4m + r] = sum_{k in band} X[k] W_nf^{-(4m + r) k} (unnormalised, as cuFFT Z2D) = IFFT_Q(S_r)[m] with
 // S_r[j] = ([j < ncs] X[j] + [Q - j < ncs] conj(X[Q - j]) (-i)^r) W_nf^{-rj} for j >= 1 and
 // S_r[0] = X[0] + [ncs > Q] (conj(X[Q]) (-i)^r + X[Q] i^r); S_r is Hermitian, so IFFT(S_{2h} + i S_{2h+1}) =
-// y_{2h} + i y_{2h+1} with real y
-__global__ void __launch_bounds__(512) k_row4_inv(const double2 *__restrict__ spec, int64_t nc, int ncs, int nf,
-                                                  double *__restrict__ grid, int64_t row_pitch, FftStages st,
-                                                  const double2 *__restrict__ twQ, const double2 *__restrict__ twN,
-                                                  const int32_t *__restrict__ posQ) {
+// y_{2h} + i y_{2h+1} with real y.  Both h in one CTA: X is read once, the real row written as 32-byte groups
+// (x[4m .. 4m + 3] = z0[m], z1[m]).
+// PM > 0 fuses the x pass of the far-history prolongation (k_prolong_x_fix: q1[r][i] += sum_{i'} w[i + j - PM i']
+// t2[r][i' - e_lo]) for grid ratio PM: the CTA adds it to its row in shared memory before the row
+// is written, so the NH grid is written once instead of written, read and written again (8.7 GB at config 5).
+struct RowProlong {
+  const double *t2;    // [nf rows][ne] y-prolongated far-history field (vp_launch_prolong pass 1)
+  int64_t ne, e_lo;    // t2 column range [e_lo, e_lo + ne)
+  int64_t c_lo;        // first FH column whose images i = PM c + k - j reach the row
+  int nc, QH, j;
+};
+
+// taps of the fused prolongation (grid ratio 5): w[q + QH] = psi_FH(2q / (5w)), |q| <= QH = (5w - 1) / 2, one slot
+// per QH in {22, 24, 27} (w = 9, 10, 11); the values depend on w only (beta = 2.30 w), so a slot is written once
+// per device, synchronously, with identical bytes for every plan
+__constant__ double c_ptap[3][56];
+static int ptap_slot(int QH) { return QH == 22 ? 0 : (QH == 24 ? 1 : (QH == 27 ? 2 : -1)); }
+static void upload_ptap(int QH, const double *w) {
+  static std::mutex mu;
+  static std::set<std::pair<int, int>> done;
+  const int dev = vp_current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(std::make_pair(dev, QH))) return;
+  VP_CUDA(cudaMemcpyToSymbol(c_ptap, w, sizeof(double) * (2 * QH + 1), sizeof(double) * 56 * ptap_slot(QH)));
+  done.insert(std::make_pair(dev, QH));
+}
+
+template <int PM, int QH>
+__global__ void __launch_bounds__(VP_ROWQ_THREADS, 1) k_row4_inv(const double2 *__restrict__ spec, int64_t nc, int ncs,
+                                                                 int nf, double *__restrict__ grid, int64_t row_pitch,
+                                                                 FftStages st, const double2 *__restrict__ twQ,
+                                                                 const double2 *__restrict__ twN,
+                                                                 const int32_t *__restrict__ posQ, RowProlong pr) {
   extern __shared__ double2 z[];
   const int Q = st.n;
+  double2 *z0 = z, *z1 = z + Q;
   for (int r = blockIdx.x; r < nf; r += gridDim.x) {
     const double2 *X = spec + (int64_t)r * nc;
-    double *x = grid + (int64_t)r * row_pitch;
-    for (int h = 0; h < 2; h++) {
-      for (int j = threadIdx.x; j < Q; j += blockDim.x) {
-        const double2 xj = j < ncs ? X[j] : make_double2(0.0, 0.0);
-        const int jm = j ? Q - j : Q;  // partner frequency k = j - Q
-        const double2 xm = jm < ncs ? X[jm] : make_double2(0.0, 0.0);
-        const double2 xq = (j == 0 && ncs > Q) ? X[Q] : make_double2(0.0, 0.0);  // k = +Q (j = 0 only)
-        double2 w1 = __ldg(twN + j);  // W_nf^{j}; conjugated powers W^{-rj} by multiplication
-        w1.y = -w1.y;
-        const double2 w2 = cmul(w1, w1);
-        double2 s[2];
+    for (int j = threadIdx.x; j < Q; j += blockDim.x) {
+      const double2 xj = j < ncs ? X[j] : make_double2(0.0, 0.0);
+      const int jm = j ? Q - j : Q;  // partner frequency k = j - Q
+      const double2 xm = jm < ncs ? X[jm] : make_double2(0.0, 0.0);
+      const double2 xq = (j == 0 && ncs > Q) ? X[Q] : make_double2(0.0, 0.0);  // k = +Q (j = 0 only)
+      double2 w1 = __ldg(twN + j);  // W_nf^{j}; conjugated powers W^{-rj} by multiplication
+      w1.y = -w1.y;
+      const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+      double2 sv[4];
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
-          const int rr = 2 * h + u;  // (-i)^rr conj(X[Q-j]) + i^rr X[Q]
-          double2 c = make_double2(xm.x, -xm.y), d = xq;
-          for (int t = 0; t < rr; t++) {
-            c = make_double2(c.y, -c.x);
-            d = make_double2(-d.y, d.x);
-          }
-          double2 acc = make_double2(xj.x + c.x + d.x, xj.y + c.y + d.y);
-          const double2 w = rr == 0 ? make_double2(1.0, 0.0) : (rr == 1 ? w1 : (rr == 2 ? w2 : cmul(w2, w1)));
-          s[u] = cmul(acc, w);
+      for (int rr = 0; rr < 4; rr++) {  // (-i)^rr conj(X[Q-j]) + i^rr X[Q]
+        double2 c = make_double2(xm.x, -xm.y), d = xq;
+#pragma unroll
+        for (int t = 0; t < rr; t++) {
+          c = make_double2(c.y, -c.x);
+          d = make_double2(-d.y, d.x);
         }
-        z[__ldg(posQ + j)] = make_double2(s[0].x - s[1].y, s[0].y + s[1].x);  // S_{2h} + i S_{2h+1}
+        const double2 acc = make_double2(xj.x + c.x + d.x, xj.y + c.y + d.y);
+        sv[rr] = rr == 0 ? acc : cmul(acc, rr == 1 ? w1 : (rr == 2 ? w2 : w3));
+      }
+      const int pj = __ldg(posQ + j);
+      z0[pj] = make_double2(sv[0].x - sv[1].y, sv[0].y + sv[1].x);  // S_0 + i S_1
+      z1[pj] = make_double2(sv[2].x - sv[3].y, sv[2].y + sv[3].x);  // S_2 + i S_3
+    }
+    __syncthreads();
+    fft_run2<1, true>(z0, z1, st, twQ);
+    if constexpr (PM > 0) {
+      // a thread owns FH column c and the PM row elements i = PM c + k - j it reaches (disjoint across threads);
+      // compile-time taps (constant-bank DFMA operands)
+      constexpr int SL = QH == 22 ? 0 : (QH == 24 ? 1 : 2);
+      constexpr int DLO = -(QH / PM), DHI = (PM - 1 + QH) / PM;
+      const double *t2r = pr.t2 + r * pr.ne - pr.e_lo;
+      for (int cc = threadIdx.x; cc < pr.nc; cc += blockDim.x) {
+        const int64_t c = pr.c_lo + cc;
+        double acc[PM];
+#pragma unroll
+        for (int k = 0; k < PM; k++) acc[k] = 0.0;
+#pragma unroll
+        for (int d = DLO; d <= DHI; d++) {
+          const int64_t ip = c + d;
+          const double x = (ip >= pr.e_lo && ip < pr.e_lo + pr.ne) ? __ldg(t2r + ip) : 0.0;
+#pragma unroll
+          for (int k = 0; k < PM; k++) {
+            const int q = k - PM * d;
+            if (q >= -QH && q <= QH) acc[k] = fma(c_ptap[SL][q + QH], x, acc[k]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < PM; k++) {
+          const int64_t i = PM * c + k - pr.j;
+          if (i >= 0 && i < nf) ((double *)((i & 2) ? z1 : z0))[2 * (i >> 2) + (i & 1)] += acc[k];
+        }
       }
       __syncthreads();
-      fft_run<1, true>(z, st, twQ);
-      for (int m = threadIdx.x; m < Q; m += blockDim.x) *(double2 *)(x + 4 * m + 2 * h) = z[m];
-      __syncthreads();
     }
+    double2 *x2 = (double2 *)(grid + (int64_t)r * row_pitch);
+    for (int c = threadIdx.x; c < 2 * Q; c += blockDim.x) x2[c] = ((c & 1) ? z1 : z0)[c >> 1];
+    __syncthreads();
   }
 }
 
@@ -971,8 +1091,8 @@ bool vp_fft4_rows_setup(vp_plan_s *P, VpGrid &G) {
   const int Q = (int)(G.nf / 4);
   FftStages st;
   if (!factor_stages(Q, st)) return false;
-  const size_t sm = sizeof(double2) * (size_t)Q;
-  if (sm > 200 * 1024) return false;
+  const size_t sm = 2 * sizeof(double2) * (size_t)Q;  // both half-sequences of a row
+  if (sm > 220 * 1024) return false;
   if (G.fft_ncs > Q + 1) return false;
   std::vector<int32_t> sig, pos(Q);
   digit_sigma(st, sig);
@@ -983,13 +1103,13 @@ bool vp_fft4_rows_setup(vp_plan_s *P, VpGrid &G) {
   static_assert(sizeof(FftStages) <= sizeof(G.f4_stQ), "stage buffer");
   memcpy(G.f4_stQ, &st, sizeof(st));
   vp_smem_attr((const void *)k_row4_fwd, sm);
-  vp_smem_attr((const void *)k_row4_inv, sm);
+  vp_smem_attr((const void *)k_row4_inv<0, 0>, sm);
   G.f4_rows = true;
   return true;
 }
 
 static unsigned row4_grid(size_t smem, int64_t rows) {
-  int per = (int)std::min<size_t>(4, (227 * 1024) / (smem + 2048));
+  int per = (int)std::min<size_t>(2, (227 * 1024) / (smem + 2048));
   if (per < 1) per = 1;
   return (unsigned)std::min<int64_t>(rows, (int64_t)per * num_sms());
 }
@@ -997,19 +1117,58 @@ static unsigned row4_grid(size_t smem, int64_t rows) {
 void vp_fft4_rows_fwd(vp_plan_s *P, VpGrid &G) {
   FftStages st;
   memcpy(&st, G.f4_stQ, sizeof(st));
-  const size_t sm = sizeof(double2) * (size_t)st.n;
-  k_row4_fwd<<<row4_grid(sm, G.nf), 512, sm, P->stream>>>(G.data, G.row, (double2 *)G.cdata, G.nf / 2 + 1, G.fft_ncs,
+  const size_t sm = 2 * sizeof(double2) * (size_t)st.n;
+  k_row4_fwd<<<row4_grid(sm, G.nf), VP_ROWQ_THREADS, sm, P->stream>>>(G.data, G.row, (double2 *)G.cdata, G.nf / 2 + 1, G.fft_ncs,
                                                           (int)G.nf, st, G.f4_twQ, G.f4_twN, G.f4_posQ);
   VP_CHECK_LAUNCH();
   P->n_kernels++;
 }
 
-void vp_fft4_rows_inv(vp_plan_s *P, VpGrid &G) {
+// inverse row pass; pr.t2 != nullptr fuses the prolongation's x pass for grid ratio 5 (the caller checked
+// vp_fft4_rows_prolong_ok)
+void vp_fft4_rows_inv(vp_plan_s *P, VpGrid &G, const RowProlong *pr) {
   FftStages st;
   memcpy(&st, G.f4_stQ, sizeof(st));
-  const size_t sm = sizeof(double2) * (size_t)st.n;
-  k_row4_inv<<<row4_grid(sm, G.nf), 512, sm, P->stream>>>((const double2 *)G.cdata, G.nf / 2 + 1, G.fft_ncs,
-                                                          (int)G.nf, G.data, G.row, st, G.f4_twQ, G.f4_twN, G.f4_posQ);
+  const size_t sm = 2 * sizeof(double2) * (size_t)st.n;
+  RowProlong none;
+  memset(&none, 0, sizeof(none));
+  const unsigned nb = row4_grid(sm, G.nf);
+  const double2 *spec = (const double2 *)G.cdata;
+#define VP_ROWINV(PM, QH, ARG)                                                                                  \
+  {                                                                                                           \
+    vp_smem_attr((const void *)k_row4_inv<PM, QH>, sm);                                                       \
+    k_row4_inv<PM, QH><<<nb, VP_ROWQ_THREADS, sm, P->stream>>>(spec, G.nf / 2 + 1, G.fft_ncs, (int)G.nf, G.data, \
+                                                               G.row, st, G.f4_twQ, G.f4_twN, G.f4_posQ, ARG);  \
+  }
+  if (pr && pr->t2 && pr->QH == 22) VP_ROWINV(5, 22, *pr)
+  else if (pr && pr->t2 && pr->QH == 24) VP_ROWINV(5, 24, *pr)
+  else if (pr && pr->t2 && pr->QH == 27) VP_ROWINV(5, 27, *pr)
+  else VP_ROWINV(0, 0, none)
+#undef VP_ROWINV
   VP_CHECK_LAUNCH();
   P->n_kernels++;
+}
+
+// the fused prolongation needs the NH grid on own row passes, integer ratio 5 with tabulated taps, and shared
+// memory for the taps next to the row
+bool vp_fft4_rows_prolong_ok(vp_plan_s *P) {
+  if (!P->nh.f4_rows || P->tap_qh <= 0 || P->fh_ratio != 5 || ptap_slot(P->tap_qh) < 0) return false;
+  upload_ptap(P->tap_qh, P->tap_w);  // once per (device, QH)
+  return true;
+}
+
+void vp_fft4_rows_inv_prolong(vp_plan_s *P) {
+  RowProlong pr;
+  memset(&pr, 0, sizeof(pr));
+  const int M = 5;
+  const int64_t j = P->fh_shift;
+  pr.t2 = P->scratch;
+  pr.ne = P->e_n;
+  pr.e_lo = P->e_lo;
+  pr.c_lo = (j >= 0) ? j / M : -((-j + M - 1) / M);
+  const int64_t c_hi = (P->nh.nf - 1 + j) / M;
+  pr.nc = (int)(c_hi - pr.c_lo + 1);
+  pr.QH = P->tap_qh;
+  pr.j = (int)j;
+  vp_fft4_rows_inv(P, P->nh, &pr);
 }

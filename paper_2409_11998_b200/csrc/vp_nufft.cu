@@ -17,6 +17,7 @@
 //               V_L = alpha f_t + sum_k omega_k f[idx_k] and the scatter to the user's order.
 // ES kernel values come from per-tap Horner polynomials (vp_common.cuh VpHorner), degree ~ W-1.
 #include <cub/cub.cuh>
+#include <cuda_pipeline.h>
 
 #include <algorithm>
 #include <cstring>
@@ -576,7 +577,7 @@ static void launch_spread_strip_w(vp_plan_s *P, const VpSpreadSet &S, const Grid
 // columns wide, so the RED flush covers 16 / SW columns per origin column (more halo REDs than the 32-column
 // strip, 2.3x vs 1.4x at W = 10; the L2 atomic rate, 4.7e11/s, is below the shared-memory bound).
 #ifndef VP_PAIR_SH
-#define VP_PAIR_SH 64  // footprint-origin rows per pair strip (even)
+#define VP_PAIR_SH 128  // footprint-origin rows per pair strip (even)
 #endif
 template <int W>
 struct PairCfg {
@@ -617,6 +618,8 @@ __global__ void __launch_bounds__(32 * PairCfg<W>::WARPS, PairCfg<W>::MINB)
   // the tap loads with immediate offsets (no per-point index arithmetic)
   const char *xb = (const char *)s_wx + 8 * c;
   const char *yb = (const char *)s_wy + 8 * h;
+  // (persistent warps walking every stride-th item measured slower, 14.5 vs 10.9 ms at config 5: the items in
+  // flight no longer form one band of neighbouring strips, so the halo REDs and grid rows miss L2)
   const int4 it = items[item];
   const int64_t ox = (int64_t)it.x * C::SW - (W / 2 + 1), oy = (int64_t)it.y * C::SH - (W / 2 + 1);
   const bool interior = ox >= 0 && oy >= 0 && ox + 16 <= g.nfx && oy + C::SH + W + 1 <= g.nfy;
@@ -692,8 +695,10 @@ stage:
     const int2 m = s_meta[qq];                                                                        \
     const double wxl = *(const double *)(xb + m.x);                                                   \
     const char *yp = yb + m.y;                                                                        \
+    /* the last pair is all zero for an even origin row at even W (bit 3 of the y offset = origin parity) */ \
     _Pragma("unroll") for (int jj = 0; jj < S; jj++)                                                  \
-      ACC[((K) + jj) % S] = fma(*(const double *)(yp + 16 * jj), wxl, ACC[((K) + jj) % S]);           \
+      if (jj < S - 1 || (W & 1) || (m.y & 8))                                                         \
+        ACC[((K) + jj) % S] = fma(*(const double *)(yp + 16 * jj), wxl, ACC[((K) + jj) % S]);         \
   }
 #define VP_PAIR_PHASE(k)                                                                              \
   case k:                                                                                             \
@@ -1051,10 +1056,15 @@ __global__ void __launch_bounds__(128) k_restrict_x_int(const double *__restrict
   const int span = M * (128 * Q - 1) + NT;
   const int64_t i0 = M * (a.e_lo + e0) - tp.j - tp.QH;
   const double *src = g1 + r * a.row1;
+  // asynchronous copy (cp.async, 8 B per element): every element of the span in flight at once (the synchronous
+  // loop left the kernel latency-bound at ~3.4 TB/s)
   for (int idx = threadIdx.x; idx < span; idx += 128) {
     const int64_t gi = i0 + idx;
-    s[idx + idx / SKEW] = (gi >= 0 && gi < a.n1) ? __ldg(src + gi) : 0.0;
+    if (gi >= 0 && gi < a.n1) __pipeline_memcpy_async(s + idx + idx / SKEW, src + gi, sizeof(double));
+    else s[idx + idx / SKEW] = 0.0;
   }
+  __pipeline_commit();
+  __pipeline_wait_prior(0);
   __syncthreads();
   const int t = threadIdx.x;
   const double *sb = s + (SKEW + 1) * t;
@@ -1089,10 +1099,15 @@ __global__ void __launch_bounds__(128) k_restrict_x_fix(const double *__restrict
   const int span = M * (128 * Q - 1) + NT;
   const int64_t i0 = M * (a.e_lo + e0) - tp.j - QHC;
   const double *src = g1 + r * a.row1;
+  // asynchronous copy (cp.async, 8 B per element): every element of the span in flight at once (the synchronous
+  // loop left the kernel latency-bound at ~3.4 TB/s)
   for (int idx = threadIdx.x; idx < span; idx += 128) {
     const int64_t gi = i0 + idx;
-    s[idx + idx / SKEW] = (gi >= 0 && gi < a.n1) ? __ldg(src + gi) : 0.0;
+    if (gi >= 0 && gi < a.n1) __pipeline_memcpy_async(s + idx + idx / SKEW, src + gi, sizeof(double));
+    else s[idx + idx / SKEW] = 0.0;
   }
+  __pipeline_commit();
+  __pipeline_wait_prior(0);
   __syncthreads();
   const int t = threadIdx.x;
   const double *sb = s + (SKEW + 1) * t;
