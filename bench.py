@@ -395,7 +395,8 @@ def main():
                            "nf_nh": info["nf_nh"], "nf_fh": info["nf_fh"], "w_es": info["w_es"],
                            "deriv": f"{['auto', 'knn', 'triangle'][info['deriv_mode']]} (knn deg {info['deriv_degree']} "
                                     f"K {K_st} on {S_st} targets)", "levels": info["n_levels"], "plan_ms": info["plan_ms"],
-                           "spread": "register strips (k_spread_strip)", "spread_items": info["n_batches"],
+                           "spread": ("row-pair strips (k_spread_pair)" if extra.get("spread_pack", 0) == 0 and info["w_es"] <= 12
+                                      else "32-column strips (k_spread_strip)"), "spread_items": info["n_batches"],
                            "fft_path": {"nh": ["fused", "cufft2d", "cufftrows+4step", "rows4+4step"][info["fft_path_nh"]],
                                         "fh": ["fused", "cufft2d", "cufftrows+4step", "rows4+4step"][info["fft_path_fh"]]},
                            "opts": extra},

@@ -120,13 +120,14 @@ typedef struct {
   int32_t spread_tile;
   int32_t interp_tile;
   /* transforms: 0 -> fused row/column FFT with the spectral multiply in the column pass (vp_fft.cu) for
-   * grids with nf <= 6400, cuFFT D2Z + multiply + Z2D otherwise; 1 -> cuFFT for every grid */
+   * grids with nf <= 6400, cuFFT D2Z + multiply + Z2D for 6400 < nf <= 10000, the four-step column pass above;
+   * 1 -> cuFFT for every grid */
   int32_t fft_mode;
   /* register-strip spreading: 0 -> row-pair strips (k_spread_pair: 16 columns x 2 row phases
    * per warp) when w <= 12, else 32-column strips; 1 -> 32-column strips with column-disjoint packs of points per
    * step; 2 -> 32-column strips, one point per step (k_spread_strip) */
   int32_t spread_pack;
-  /* grids above 6400^2 (four-step column pass): 0 -> own pruned row passes (nf % 4 == 0 and a whole row,
+  /* grids above 10000^2 (four-step column pass): 0 -> own pruned row passes (nf % 4 == 0 and a whole row,
    * 2 x nf/4 complex values, in one CTA's shared memory: nf <= 28160), else cuFFT batched 1D row
    * transforms; 1 -> cuFFT batched 1D row transforms */
   int32_t fft_rows;

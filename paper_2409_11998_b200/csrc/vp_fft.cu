@@ -608,6 +608,7 @@ void vp_fft_bands(vp_plan_s *P) {
 // (X(k1 + N1 k2) = sum_n2 W_N2^{n2 k2} W_nf^{n2 k1} sum_n1 W_N1^{n1 k1} x(n1 N2 + n2), and its transpose.)
 // A CTA owns TC4 consecutive kept columns (256-byte row segments) and transforms TC4 sequences at once.
 #define TC4 16
+#define VP_FFT4_MIN_NF 10000  // four-step column pass (+ own row passes) above this grid size
 
 // shared layout of a tile: element i of column c at a[i * TC4 + c]; thread (c, q) = (tid % TC4, tid / TC4) works
 // on column c, butterflies / elements q, q + 256 / TC4, ...: a row of TC4 columns is one contiguous 256-byte
@@ -825,7 +826,10 @@ static bool fft4_factor(int nf, int &N1, int &N2, FftStages &s1, FftStages &s2) 
 }
 
 bool vp_fft4_setup(vp_plan_s *P, VpGrid &G) {
-  if (P->opts.fft_mode != 0 || G.nf <= 6400 || G.nf > (1 << 30)) return false;
+  // measured crossover: cuFFT 2D D2Z + multiply + Z2D is faster up to ~10^4 (config 3, n_f = 8640: 2.4 vs 2.9 ms
+  // for transforms, multiply and prolongation), the four-step pass with own rows above (config 4, 12500: 5.5 vs
+  // 7.2 ms; config 5, 23328: 14.7 vs 25.1 ms)
+  if (P->opts.fft_mode != 0 || G.nf <= VP_FFT4_MIN_NF || G.nf > (1 << 30)) return false;
   int N1, N2;
   FftStages s1, s2;
   if (!fft4_factor((int)G.nf, N1, N2, s1, s2)) return false;

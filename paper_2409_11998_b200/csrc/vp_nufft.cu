@@ -1159,6 +1159,36 @@ __global__ void __launch_bounds__(128) k_restrict_y_int(const double *__restrict
   }
 }
 
+// pass B with compile-time taps (QHC) and Q outputs per thread: the tap loop is fully unrolled (no per-tap bounds
+// tests, the weights are constant-bank operands); config 5: the runtime form ran at 80% issue
+template <int M, int Q, int QHC>
+__global__ void __launch_bounds__(128) k_restrict_y_fix(const double *__restrict__ tA, double *__restrict__ g2,
+                                                        RestrictArgs a, TapArgs tp) {
+  const int64_t ex = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int64_t ey0 = (int64_t)blockIdx.y * Q;
+  if (ex >= a.ne) return;
+  constexpr int NT = 2 * QHC + 1, NIN = M * (Q - 1) + NT;
+  const int64_t r0 = M * (a.e_lo + ey0) - tp.j - QHC;
+  double acc[Q];
+#pragma unroll
+  for (int k = 0; k < Q; k++) acc[k] = 0.0;
+#pragma unroll
+  for (int ii = 0; ii < NIN; ii++) {
+    const int64_t r = r0 + ii;
+    const double x = (r >= 0 && r < a.n1) ? __ldg(tA + r * a.ne + ex) : 0.0;
+#pragma unroll
+    for (int k = 0; k < Q; k++) {
+      const int q = ii - M * k;
+      if (q >= 0 && q < NT) acc[k] = fma(tp.w[q], x, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < Q; k++) {
+    const int64_t ey = ey0 + k;
+    if (ey < a.ne) g2[(a.e_lo + ey) * a.row2 + a.e_lo + ex] = acc[k];
+  }
+}
+
 // prolongation pass B^T: t2[r][ex] = sum_{i'} w[r + j - M i'] q2[i'][e_lo + ex], i' in the effective range;
 // a thread owns the M rows r = M c + k - j (k = 0..M-1) sharing the FH rows i' = c + d
 template <int M>
@@ -1299,10 +1329,16 @@ static void launch_restrict_int(vp_plan_s *P, const RestrictArgs &a, const TapAr
   vp_smem_attr((const void *)k_restrict_x_int<M, Q>, 96 * 1024);
   dim3 gA((unsigned)((a.ne + 128 * Q - 1) / (128 * Q)), (unsigned)a.n1);
   bool fixed = false;
+  // compile-time taps: 8 outputs per thread (84 shared loads for 8 outputs instead of 64 for 4; the kernel is
+  // bound by shared-memory issue, mio_throttle 36% at 4 outputs)
+  constexpr int QF = 8;
+  const int spanf = M * (128 * QF - 1) + 2 * tp.QH + 1;
+  const size_t smf = sizeof(double) * (size_t)(spanf + spanf / (M * QF) + 2);
+  dim3 gF((unsigned)((a.ne + 128 * QF - 1) / (128 * QF)), (unsigned)a.n1);
 #define VP_RFIX(QHV)                                                                                   \
   if (tp.QH == QHV) {                                                                                  \
-    vp_smem_attr((const void *)k_restrict_x_fix<M, Q, QHV>, 96 * 1024);                              \
-    k_restrict_x_fix<M, Q, QHV><<<gA, 128, sm, P->stream>>>(P->nh.data, P->scratch, a, tp);           \
+    vp_smem_attr((const void *)k_restrict_x_fix<M, QF, QHV>, 96 * 1024);                             \
+    k_restrict_x_fix<M, QF, QHV><<<gF, 128, smf, P->stream>>>(P->nh.data, P->scratch, a, tp);         \
     fixed = true;                                                                                      \
   }
   if (M == 5) {  // the ratio delta2/delta1 = 32 gives m = 5 on every config; w = 9, 10, 11 (tol 1e-8 .. 1e-10)
@@ -1311,8 +1347,18 @@ static void launch_restrict_int(vp_plan_s *P, const RestrictArgs &a, const TapAr
 #undef VP_RFIX
   if (!fixed) k_restrict_x_int<M, Q><<<gA, 128, sm, P->stream>>>(P->nh.data, P->scratch, a, tp);
   VP_CHECK_LAUNCH();
-  dim3 gB((unsigned)((a.ne + 127) / 128), (unsigned)((a.ne + Q - 1) / Q));
-  k_restrict_y_int<M, Q><<<gB, 128, 0, P->stream>>>(P->scratch, P->fh.data, a, tp);
+  bool yfix = false;
+  if (M == 5) {
+    constexpr int QY = 8;
+    dim3 gY((unsigned)((a.ne + 127) / 128), (unsigned)((a.ne + QY - 1) / QY));
+    if (tp.QH == 22) { k_restrict_y_fix<M, QY, 22><<<gY, 128, 0, P->stream>>>(P->scratch, P->fh.data, a, tp); yfix = true; }
+    else if (tp.QH == 24) { k_restrict_y_fix<M, QY, 24><<<gY, 128, 0, P->stream>>>(P->scratch, P->fh.data, a, tp); yfix = true; }
+    else if (tp.QH == 27) { k_restrict_y_fix<M, QY, 27><<<gY, 128, 0, P->stream>>>(P->scratch, P->fh.data, a, tp); yfix = true; }
+  }
+  if (!yfix) {
+    dim3 gB((unsigned)((a.ne + 127) / 128), (unsigned)((a.ne + Q - 1) / Q));
+    k_restrict_y_int<M, Q><<<gB, 128, 0, P->stream>>>(P->scratch, P->fh.data, a, tp);
+  }
   VP_CHECK_LAUNCH();
   P->n_kernels += 2;
 }

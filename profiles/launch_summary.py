@@ -20,17 +20,20 @@ def main(path, n_evals=None):
             continue
         v = float(r[iv].replace(",", ""))
         unit = r[iu]
-        ms = v / 1e6 if unit == "nsecond" else (v / 1e3 if unit == "usecond" else v)
+        ms = v / 1e6 if unit in ("nsecond", "ns") else (v / 1e3 if unit in ("usecond", "us") else v)
         name = r[ik].split("(")[0][:60]
         tot[name] += ms
         cnt[name] += 1
-    all_ms = sum(tot.values())
-    per = f" per eval (/{n_evals})" if n_evals else ""
-    print(f"{'kernel':60s} {'launches':>8s} {'ms' + per:>16s} {'share':>7s}")
-    for k in sorted(tot, key=lambda k: -tot[k]):
-        ms = tot[k] / (n_evals or 1)
-        print(f"{k:60s} {cnt[k]:8d} {ms:16.3f} {tot[k] / all_ms * 100:6.1f}%")
-    print(f"{'total':60s} {sum(cnt.values()):8d} {all_ms / (n_evals or 1):16.3f}")
+    # eval kernels: launched a multiple of n_evals times (plan-time kernels are listed apart)
+    ev = {k for k in tot if cnt[k] % n_evals == 0} if n_evals else set(tot)
+    ev_ms = sum(tot[k] for k in ev)
+    print(f"{'eval kernel':60s} {'launches':>8s} {'ms/eval':>9s} {'ms/launch':>10s} {'share':>7s}")
+    for k in sorted(ev, key=lambda k: -tot[k]):
+        print(f"{k:60s} {cnt[k]:8d} {tot[k] / (n_evals or 1):9.3f} {tot[k] / cnt[k]:10.3f} {tot[k] / ev_ms * 100:6.1f}%")
+    print(f"{'total (eval kernels, serialised under ncu)':60s} {sum(cnt[k] for k in ev):8d} {ev_ms / (n_evals or 1):9.3f}")
+    rest = sorted(set(tot) - ev, key=lambda k: -tot[k])
+    if rest:
+        print("plan-time kernels: " + ", ".join(f"{k} {tot[k]:.2f} ms" for k in rest))
 
 
 if __name__ == "__main__":

@@ -119,7 +119,8 @@ def _smooth_gate(w, n_tg, seed, extra_tg=None, **plan_kw):
     e = rel_l2(V, ref)
     log_result(f"smooth_gate_{w.name}", {"rel_l2": e, "targets": int(tg_np.shape[0]), "nf_nh": info["nf_nh"],
                                          "nf_fh": info["nf_fh"], "w_es": info["w_es"],
-                                         "transform": "cuFFT" if info["nf_nh"] > 6400 else "fused"})
+                                         "transform": ["fused", "cuFFT 2D", "cuFFT rows + four-step",
+                                                       "own rows + four-step"][info["fft_path_nh"]]})
     assert e < 1e-12, e
 
 
@@ -525,7 +526,7 @@ tg = torch.from_numpy(rng.uniform(0.0, 1.0, (200, 2))).cuda()
 out = []
 for mode in (0, 1):
     p = vp.Plan(nodes, wts, tg, 1e-13, parts=vp.PART_HISTORY, delta1_override=6.25e-8, fft_mode=mode)
-    assert p.info()["fft_path_fh"] in ((2, 3) if mode == 0 else (1,))
+    assert p.info()["fft_path_nh"] in ((2, 3) if mode == 0 else (1,))
     out.append(p.eval(fv).cpu().numpy())
 print(np.max(np.abs(out[0] - out[1])) / np.max(np.abs(out[1])))
 """ % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
