@@ -210,6 +210,20 @@ vp_status vp_eval_host(vp_handle plan, const double *f_host, double *out_host);
  * (deterministic mode or spread_tile > 0, which use the tile-batch spreading), VP_ERR_CUDA / VP_ERR_CUFFT. */
 vp_status vp_eval_batch(vp_handle plan, int32_t K, const double *f, double *out);
 
+/* Single-layer potential S[sigma](x_t) = int_Gamma -(1/2 pi) log|x_t - y| sigma(y) ds_y at the plan's targets, on
+ * the plan's grids (§2.3, eq. sheatdecomp; local part Lemma slp, eq. slplocO5, lines
+ * 955-987).  Requires opts.boundary of kind VP_BDRY_CHUNKS: the boundary quadrature nodes are the
+ * chunks' q+1 Gauss-Legendre nodes, with weights w_k |gamma'(s_k)|.
+ * vp_slp_prepare (once per plan, synchronous): sorts the boundary nodes into the spreading strips and builds a
+ *   (q+1)-entry stencil of the local part S_L for every target within 12 sqrt(delta_1) of the boundary.
+ * vp_eval_slp: sigma = DEVICE [n][q+1] densities at the chunk nodes (same layout as opts.boundary.pts), out =
+ *   DEVICE [T] (fully overwritten), asynchronous on the plan's stream like vp_eval.  The history part reuses the
+ *   plan's grids, so it must not run concurrently with vp_eval on the same plan.
+ * Errors: VP_ERR_UNSUPPORTED (boundary not CHUNKS), VP_ERR_ARG (null pointers, vp_eval_slp before
+ *   vp_slp_prepare), VP_ERR_CUDA / VP_ERR_CUFFT. */
+vp_status vp_slp_prepare(vp_handle plan);
+vp_status vp_eval_slp(vp_handle plan, const double *sigma, double *out);
+
 /* Release all device memory and cuFFT plans owned by the plan.  NULL is accepted. */
 vp_status vp_destroy(vp_handle plan);
 

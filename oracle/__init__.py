@@ -9,6 +9,7 @@ Functions (see oracle/vp_oracle.c for the citations and the quadrature tiers):
   smooth_direct(src, c, targets, delta)            -> sum_j c_j G_H[delta](x_t - x_j)
   smooth_dft(src, c, targets, d1, d2, ...)         -> same split through a direct Fourier sum
   e1(x), GH(r2, delta), WR(k, R)
+  layer.single_layer(curve, dcurve, sigma, targets) -> S[sigma](x_t) on an analytic closed curve (oracle/layer.py)
 Parity status of each function is listed in DESIGN.md §Oracle (all pinned).
 """
 import ctypes

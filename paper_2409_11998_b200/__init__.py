@@ -23,7 +23,8 @@ DERIV = {"auto": 0, "knn": 1, "triangle": 2}
 PART_HISTORY, PART_LOCAL, PART_ALL = 1, 2, 3
 
 EXPORTED = ["vp_plan", "vp_eval", "vp_eval_host", "vp_eval_batch", "vp_destroy", "vp_strerror", "vp_get_info", "vp_set_profiling",
-            "vp_get_phase_times", "vp_eval_launch_count", "vp_check_finite", "vp_last_error_detail", "vp_version"]
+            "vp_get_phase_times", "vp_eval_launch_count", "vp_check_finite", "vp_last_error_detail", "vp_version",
+            "vp_slp_prepare", "vp_eval_slp"]
 
 
 class VpBoundary(ctypes.Structure):
@@ -80,6 +81,8 @@ def lib():
         L.vp_eval.argtypes = [vp, vp, vp]
         L.vp_eval_host.argtypes = [vp, vp, vp]
         L.vp_eval_batch.argtypes = [vp, i32, vp, vp]
+        L.vp_slp_prepare.argtypes = [vp]
+        L.vp_eval_slp.argtypes = [vp, vp, vp]
         L.vp_destroy.argtypes = [vp]
         L.vp_strerror.argtypes = [ctypes.c_int]
         L.vp_strerror.restype = ctypes.c_char_p
@@ -178,6 +181,9 @@ class Plan:
                          ctypes.byref(o), ctypes.byref(h)), "vp_plan")
         self.h = h
         self.M, self.p, self.T, self.N = M, p, T, M * p
+        # boundary chunk nodes (single-layer densities live there)
+        self._bq = (int(self._bpts.shape[0]) * int(self._bpts.shape[1])
+                    if boundary is not None and boundary[0] == "chunks" else None)
 
     def _out(self, out, n, dev, shape=None):
         import torch
@@ -207,6 +213,20 @@ class Plan:
             raise ValueError("F must hold at least one field")
         out = self._out(out, K * self.T, F.device, (K, self.T))
         _check(lib().vp_eval_batch(self.h, K, F.data_ptr(), out.data_ptr()), "vp_eval_batch")
+        return out
+
+    def prepare_slp(self):
+        """Boundary sources and local stencils of the single-layer potential (C ABI vp_slp_prepare; the plan's
+        boundary must be "chunks")."""
+        _check(lib().vp_slp_prepare(self.h), "vp_slp_prepare")
+
+    def eval_slp(self, sigma, out=None):
+        """S[sigma] at the targets (C ABI vp_eval_slp): sigma [n_chunks, q+1] device fp64 at the chunk nodes."""
+        sigma = _dev_f64(sigma)
+        if self._bq is None or sigma.numel() != self._bq:
+            raise ValueError("sigma must hold one value per boundary chunk node ([n, q+1]; plan with chunks)")
+        out = self._out(out, self.T, sigma.device)
+        _check(lib().vp_eval_slp(self.h, sigma.data_ptr(), out.data_ptr()), "vp_eval_slp")
         return out
 
     def eval_host(self, f_host, out_host=None):

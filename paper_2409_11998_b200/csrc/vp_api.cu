@@ -862,6 +862,43 @@ extern "C" vp_status vp_eval_batch(vp_handle P, int32_t K, const double *f, doub
   return VP_OK;
 }
 
+extern "C" vp_status vp_slp_prepare(vp_handle P) {
+  if (!P) return VP_ERR_ARG;
+  try {
+    vp_slp_build(P);
+  } catch (VpError &e) {
+    return e.s;
+  }
+  return VP_OK;
+}
+
+// single-layer potential S[sigma] at the plan's targets (vp_layer.cu): history part through the volume path's
+// grids with the boundary nodes as sources, then the local stencils of the targets near the boundary
+extern "C" vp_status vp_eval_slp(vp_handle P, const double *sigma, double *out) {
+  if (!P || !sigma || !out) return VP_ERR_ARG;
+  try {
+    if (!P->slp_ready) throw VpError{VP_ERR_ARG};
+    P->n_kernels = 0;
+    P->n_ffts = 0;
+    VP_CUDA(cudaMemsetAsync(P->nh.data, 0, sizeof(double) * P->nh.nf * P->nh.row, P->stream));
+    VP_CUDA(cudaMemsetAsync(P->fh.data, 0, sizeof(double) * P->fh.nf * P->fh.row, P->stream));
+    VpSpreadSet S = P->bsp;
+    S.fs_out = nullptr;
+    vp_launch_spread(P, S, grid_args(P->nh), sigma);
+    vp_launch_restrict(P);
+    grid_fft_fwd(P, P->nh);
+    grid_fft_fwd(P, P->fh);
+    grid_multiply(P, P->nh);
+    grid_multiply(P, P->fh);
+    grids_inverse_prolong(P);
+    vp_launch_interp_hist(P, out);
+    vp_launch_slp_local(P, sigma, out);
+  } catch (VpError &e) {
+    return e.s;
+  }
+  return VP_OK;
+}
+
 extern "C" vp_status vp_eval_host(vp_handle P, const double *f_host, double *out_host) {
   if (!P || !f_host || !out_host) return VP_ERR_ARG;
   try {

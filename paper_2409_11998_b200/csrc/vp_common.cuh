@@ -208,6 +208,14 @@ struct vp_plan_s {
   // graded-mesh level bands (a12)
   VpBands bands;
   VpBdryDev bdev;  // boundary geometry for V_L (plan-owned device copies; vp_build_boundary)
+  // single-layer potential on the plan's grids (vp_layer.cu, vp_slp_prepare): boundary sources in strip order,
+  // local stencils (chunk + q+1 weights) of the targets within 12 sqrt(delta_1) of the boundary
+  bool slp_ready = false;
+  VpSpreadSet bsp;
+  double *slp_swt = nullptr;  // [q+1] Gauss-Legendre weights of [-1, 1]
+  int64_t slp_n = 0;
+  int32_t *slp_list = nullptr, *slp_chunk = nullptr;
+  double *slp_w = nullptr;
   // FH <- NH restriction tables
   int32_t *r_lo = nullptr, *t_lo = nullptr;
   double *r_w = nullptr, *t_w = nullptr;
@@ -293,6 +301,9 @@ void vp_launch_prolong(vp_plan_s *P, int pass);
 void vp_launch_tri_local(vp_plan_s *P, const double *f);
 void vp_launch_multiply(vp_plan_s *P, VpGrid &G);
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out, bool local_kernels);
+void vp_launch_interp_hist(vp_plan_s *P, double *out);  // history part only (no local part), out = u_H
+void vp_slp_build(vp_plan_s *P);                         // vp_layer.cu
+void vp_launch_slp_local(vp_plan_s *P, const double *sigma, double *out);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n);
 void vp_fft_setup(vp_plan_s *P, VpGrid &G);
 void vp_fft_forward(vp_plan_s *P, VpGrid &G);

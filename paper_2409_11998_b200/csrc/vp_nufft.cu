@@ -1894,6 +1894,31 @@ void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const Gr
     VP_CUDA(cudaFreeAsync(q, s));
 }
 
+// interpolation of the history part only (single-layer potential: the local part is applied separately)
+template <int W>
+static void launch_interp_hist_w(vp_plan_s *P, double *out) {
+  constexpr int D = VP_HORNER_DEG(W);
+  if (P->n_items == 0) return;
+  const int TSI = P->TSI, nw = TSI + W + 3;
+  const size_t sm = sizeof(double) * (size_t)nw * nw;
+  vp_smem_attr((const void *)k_interp_local<W, D>, sm);
+  k_interp_local<W, D><<<(unsigned)P->n_items, 256, sm, P->stream>>>(P->items, TSI, P->tx, P->ty, P->tperm,
+                                                                     grid_args(P->nh), 1, nullptr, nullptr, nullptr,
+                                                                     0, nullptr, nullptr, nullptr, out);
+  VP_CHECK_LAUNCH();
+  P->n_kernels++;
+}
+
+void vp_launch_interp_hist(vp_plan_s *P, double *out) {
+  switch (P->w) {
+#define CASE(W) \
+  case W: launch_interp_hist_w<W>(P, out); break;
+    CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+    default: throw VpError{VP_ERR_UNSUPPORTED};
+  }
+}
+
 void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out, bool local_kernels) {
   int parts_ = P->opts.parts ? P->opts.parts : VP_PART_ALL;
   if (local_kernels && (parts_ & VP_PART_LOCAL)) vp_launch_tri_local(P, f);
