@@ -221,8 +221,30 @@ vp_status vp_eval_batch(vp_handle plan, int32_t K, const double *f, double *out)
  *   plan's grids, so it must not run concurrently with vp_eval on the same plan.
  * Errors: VP_ERR_UNSUPPORTED (boundary not CHUNKS), VP_ERR_ARG (null pointers, vp_eval_slp before
  *   vp_slp_prepare), VP_ERR_CUDA / VP_ERR_CUFFT. */
+/* Levels J (0..8, default 3) of the dyadic telescoping of the layer potentials' local parts (§4.1
+ * "s:dyadicref", lines 1181-1269): S_L / D_L = asymptotic expansion at delta* = delta_1 / 4^J + the J difference
+ * kernels integrated directly over the chunks within 12 sqrt(delta_1) of the target (panels of 16 Gauss-Legendre
+ * points no longer than ~1.7 sqrt(delta*)).  J = 0: the expansion at delta_1 alone (truncation O(delta_1^{5/2})).
+ * Must be called before the first vp_slp_prepare / vp_dlp_prepare.  Errors: VP_ERR_ARG (J out of range, called
+ * after a prepare), VP_ERR_UNSUPPORTED at prepare time if a target has more than 64 chunks within reach. */
+vp_status vp_layer_set_levels(vp_handle plan, int32_t J);
 vp_status vp_slp_prepare(vp_handle plan);
 vp_status vp_eval_slp(vp_handle plan, const double *sigma, double *out);
+
+/* Double-layer potential D[mu](x_t) = int_Gamma d/dnu_y [-(1/2 pi) log|x_t - y|] mu(y) ds_y, nu the OUTWARD unit
+ * normal, at the plan's targets on the plan's grids (eq. dheatdecomp; history
+ * lemmas dnearkspace / dfarkspace, lines 522-553, with the -i k.nu multiplier of DESIGN.md reading R20; local
+ * part Lemma dlp, eq. dlplocO5, in the outward frame of reading R21).  Jump relations: the
+ * interior / exterior limits at b are D(b) -/+ mu(b)/2 (D(b) the direct value), as in the Dirichlet equation of
+ * lines 1281-1287.  Same boundary requirement as S (VP_BDRY_CHUNKS).
+ * vp_dlp_prepare (once per plan, synchronous): two dipole spreading sets (weights W nu_1, W nu_2), the (q+1)-entry
+ *   D_L stencils of the targets within 12 sqrt(delta_1), and cuFFT plans plus two NH half spectra (owned by the
+ *   plan; 2 x 16 nf_NH (nf_NH/2+1) bytes) for the spectral derivative.
+ * vp_eval_dlp: mu = DEVICE [n][q+1] densities at the chunk nodes, out = DEVICE [T] (fully overwritten),
+ *   asynchronous on the plan's stream; shares the plan's grids with vp_eval / vp_eval_slp (no concurrent calls).
+ * Errors: as vp_slp_prepare / vp_eval_slp (VP_ERR_ARG for vp_eval_dlp before vp_dlp_prepare). */
+vp_status vp_dlp_prepare(vp_handle plan);
+vp_status vp_eval_dlp(vp_handle plan, const double *mu, double *out);
 
 /* Release all device memory and cuFFT plans owned by the plan.  NULL is accepted. */
 vp_status vp_destroy(vp_handle plan);

@@ -24,7 +24,8 @@ PART_HISTORY, PART_LOCAL, PART_ALL = 1, 2, 3
 
 EXPORTED = ["vp_plan", "vp_eval", "vp_eval_host", "vp_eval_batch", "vp_destroy", "vp_strerror", "vp_get_info", "vp_set_profiling",
             "vp_get_phase_times", "vp_eval_launch_count", "vp_check_finite", "vp_last_error_detail", "vp_version",
-            "vp_slp_prepare", "vp_eval_slp"]
+            "vp_slp_prepare", "vp_eval_slp", "vp_dlp_prepare", "vp_eval_dlp",
+            "vp_layer_set_levels"]
 
 
 class VpBoundary(ctypes.Structure):
@@ -83,6 +84,9 @@ def lib():
         L.vp_eval_batch.argtypes = [vp, i32, vp, vp]
         L.vp_slp_prepare.argtypes = [vp]
         L.vp_eval_slp.argtypes = [vp, vp, vp]
+        L.vp_dlp_prepare.argtypes = [vp]
+        L.vp_layer_set_levels.argtypes = [vp, i32]
+        L.vp_eval_dlp.argtypes = [vp, vp, vp]
         L.vp_destroy.argtypes = [vp]
         L.vp_strerror.argtypes = [ctypes.c_int]
         L.vp_strerror.restype = ctypes.c_char_p
@@ -215,6 +219,10 @@ class Plan:
         _check(lib().vp_eval_batch(self.h, K, F.data_ptr(), out.data_ptr()), "vp_eval_batch")
         return out
 
+    def set_layer_levels(self, J):
+        """Dyadic telescoping levels of the layer local parts (C ABI vp_layer_set_levels; before prepare_*)."""
+        _check(lib().vp_layer_set_levels(self.h, int(J)), "vp_layer_set_levels")
+
     def prepare_slp(self):
         """Boundary sources and local stencils of the single-layer potential (C ABI vp_slp_prepare; the plan's
         boundary must be "chunks")."""
@@ -227,6 +235,21 @@ class Plan:
             raise ValueError("sigma must hold one value per boundary chunk node ([n, q+1]; plan with chunks)")
         out = self._out(out, self.T, sigma.device)
         _check(lib().vp_eval_slp(self.h, sigma.data_ptr(), out.data_ptr()), "vp_eval_slp")
+        return out
+
+    def prepare_dlp(self):
+        """Dipole sources, local stencils and spectral-derivative buffers of the double-layer potential (C ABI
+        vp_dlp_prepare; the plan's boundary must be "chunks")."""
+        _check(lib().vp_dlp_prepare(self.h), "vp_dlp_prepare")
+
+    def eval_dlp(self, mu, out=None):
+        """D[mu] at the targets (C ABI vp_eval_dlp; outward normal): mu [n_chunks, q+1] device fp64 at the chunk
+        nodes."""
+        mu = _dev_f64(mu)
+        if self._bq is None or mu.numel() != self._bq:
+            raise ValueError("mu must hold one value per boundary chunk node ([n, q+1]; plan with chunks)")
+        out = self._out(out, self.T, mu.device)
+        _check(lib().vp_eval_dlp(self.h, mu.data_ptr(), out.data_ptr()), "vp_eval_dlp")
         return out
 
     def eval_host(self, f_host, out_host=None):

@@ -462,6 +462,12 @@ static void free_plan(vp_plan_s *P) {
       cufftDestroy(G->inv);
     }
   }
+  if (P->dlp_has_plans) {
+    for (int i = 0; i < 2; i++) {
+      if (P->dlp_fwd[i]) cufftDestroy(P->dlp_fwd[i]);
+      if (P->dlp_inv[i]) cufftDestroy(P->dlp_inv[i]);
+    }
+  }
   if (P->bands.has_plans) {
     cufftDestroy(P->bands.fwd);
     cufftDestroy(P->bands.inv);
@@ -862,6 +868,12 @@ extern "C" vp_status vp_eval_batch(vp_handle P, int32_t K, const double *f, doub
   return VP_OK;
 }
 
+extern "C" vp_status vp_layer_set_levels(vp_handle P, int32_t J) {
+  if (!P || J < 0 || J > 8 || P->lay_common) return VP_ERR_ARG;
+  P->lay_J = J;
+  return VP_OK;
+}
+
 extern "C" vp_status vp_slp_prepare(vp_handle P) {
   if (!P) return VP_ERR_ARG;
   try {
@@ -893,6 +905,39 @@ extern "C" vp_status vp_eval_slp(vp_handle P, const double *sigma, double *out) 
     grids_inverse_prolong(P);
     vp_launch_interp_hist(P, out);
     vp_launch_slp_local(P, sigma, out);
+  } catch (VpError &e) {
+    return e.s;
+  }
+  return VP_OK;
+}
+
+extern "C" vp_status vp_dlp_prepare(vp_handle P) {
+  if (!P) return VP_ERR_ARG;
+  try {
+    vp_dlp_build(P);
+  } catch (VpError &e) {
+    return e.s;
+  }
+  return VP_OK;
+}
+
+// double-layer potential D[mu] at the plan's targets (vp_layer.cu): the D history is the volume path's history of
+// the spectral-derivative source grid g~ = -(d_1 g_1 + d_2 g_2) (lemmas dnearkspace / dfarkspace, reading R20),
+// then the local stencils (eq. dlplocO5, reading R21)
+extern "C" vp_status vp_eval_dlp(vp_handle P, const double *mu, double *out) {
+  if (!P || !mu || !out) return VP_ERR_ARG;
+  try {
+    if (!P->dlp_ready) throw VpError{VP_ERR_ARG};
+    P->n_kernels = 0;
+    P->n_ffts = 0;
+    vp_dlp_source_grids(P, mu);
+    grid_fft_fwd(P, P->nh);
+    grid_fft_fwd(P, P->fh);
+    grid_multiply(P, P->nh);
+    grid_multiply(P, P->fh);
+    grids_inverse_prolong(P);
+    vp_launch_interp_hist(P, out);
+    vp_launch_dlp_local(P, mu, out);
   } catch (VpError &e) {
     return e.s;
   }

@@ -168,7 +168,7 @@ void vp_build_boundary(vp_plan_s *P, VpBdryDev &B) {
     }
   };
   // closed curve: each chunk's end meets the next chunk's start; CCW (positive enclosed area); gap between nodes
-  double area = 0.0, gap = 0.0, len_min = 1e300;
+  double area = 0.0, gap = 0.0, len_min = 1e300, len_max = 0.0;
   for (int64_t c = 0; c < n; c++) {
     double e1[2], e0[2], d[2], len = 0.0;
     evalc(c, 1.0, e1, d);
@@ -183,12 +183,14 @@ void vp_build_boundary(vp_plan_s *P, VpBdryDev &B) {
       gap = std::max(gap, std::hypot(b[0] - a[0], b[1] - a[1]));
     }
     len_min = std::min(len_min, len);
+    len_max = std::max(len_max, len);
     if (std::hypot(e1[0] - e0[0], e1[1] - e0[1]) > 1e-6 * len) throw VpError{VP_ERR_GEOMETRY};
   }
   if (!(area > 0) || !(len_min > 0)) throw VpError{VP_ERR_GEOMETRY};
   B.n = n;
   B.q = q;
   B.gap = gap;
+  B.len_max = len_max;
   double *dp = vp_alloc<double>(P, 2 * n * qp), *dc = vp_alloc<double>(P, 2 * n * qp), *ds = vp_alloc<double>(P, qp);
   VP_CUDA(cudaMemcpy(dp, bd.pts, sizeof(double) * 2 * n * qp, cudaMemcpyHostToDevice));
   VP_CUDA(cudaMemcpy(dc, coef.data(), sizeof(double) * 2 * n * qp, cudaMemcpyHostToDevice));

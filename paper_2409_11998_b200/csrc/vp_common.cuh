@@ -179,6 +179,7 @@ struct VpBdryDev {
   const int32_t *bstart = nullptr, *bidx = nullptr;
   double reach = 0;    // 12 sqrt(delta_1) (the largest delta used)
   double gap = 0;      // CHUNKS: largest distance between consecutive nodes (incl. across chunk ends)
+  double len_max = 0;  // CHUNKS: longest chunk (arc length)
   int *err = nullptr;  // device flag: set to 1 on an ambiguous closest point / unsupported local geometry
 };
 
@@ -216,6 +217,17 @@ struct vp_plan_s {
   int64_t slp_n = 0;
   int32_t *slp_list = nullptr, *slp_chunk = nullptr;
   double *slp_w = nullptr;
+  bool lay_common = false;  // slp_swt and the near list slp_list / slp_n (shared by S and D)
+  // telescoped local parts (§4.1): J levels, NC chunk slots per near target, NP quadrature panels per chunk
+  int lay_J = 3, lay_nc = 1, lay_np = 1;
+  double *lay_tq = nullptr, *lay_tq1 = nullptr, *lay_gw = nullptr, *lay_lg = nullptr;
+  // double-layer potential (vp_dlp_prepare): dipole source sets W nu_1, W nu_2, local stencils, spectral derivative
+  bool dlp_ready = false, dlp_has_plans = false;
+  VpSpreadSet dsp1, dsp2;
+  int32_t *dlp_chunk = nullptr;
+  double *dlp_w = nullptr;
+  double2 *dlp_spec[2] = {nullptr, nullptr};  // [NH, FH]: two half spectra each
+  cufftHandle dlp_fwd[2] = {0, 0}, dlp_inv[2] = {0, 0};
   // FH <- NH restriction tables
   int32_t *r_lo = nullptr, *t_lo = nullptr;
   double *r_w = nullptr, *t_w = nullptr;
@@ -304,6 +316,9 @@ void vp_launch_interp_local(vp_plan_s *P, const double *f, double *out, bool loc
 void vp_launch_interp_hist(vp_plan_s *P, double *out);  // history part only (no local part), out = u_H
 void vp_slp_build(vp_plan_s *P);                         // vp_layer.cu
 void vp_launch_slp_local(vp_plan_s *P, const double *sigma, double *out);
+void vp_dlp_build(vp_plan_s *P);                         // vp_layer.cu
+void vp_dlp_source_grids(vp_plan_s *P, const double *mu);
+void vp_launch_dlp_local(vp_plan_s *P, const double *mu, double *out);
 void vp_build_interp_order(vp_plan_s *P, const double *xy, int64_t n);
 void vp_fft_setup(vp_plan_s *P, VpGrid &G);
 void vp_fft_forward(vp_plan_s *P, VpGrid &G);
