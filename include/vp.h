@@ -246,6 +246,24 @@ vp_status vp_eval_slp(vp_handle plan, const double *sigma, double *out);
 vp_status vp_dlp_prepare(vp_handle plan);
 vp_status vp_eval_dlp(vp_handle plan, const double *mu, double *out);
 
+/* Boundary integral equations of the Poisson solve (§5 "s:bie", lines 1271-1330), solved
+ * by restarted GMRES whose product is this library's GPU double-layer operator (the paper pairs GMRES with an FMM,
+ * lines 1319-1324).  The plan's targets must be the boundary chunk nodes in the descriptor's order (T = n (q+1),
+ * checked to 1e-12) and vp_dlp_prepare must have run.  kind:
+ *   VP_BIE_DIRICHLET_INT  (-1/2 I + D) mu = rhs          (eq. dir_inteq: rhs = g - V[f]; u = V[f] + D[mu] inside)
+ *   VP_BIE_DIRICHLET_EXT  (+1/2 I + D + int ds) mu = rhs  (eq. dir_repext: rhs = g - V[f] - A log|x - x0|;
+ *                                                          u = V[f] + D[mu] + int mu ds + A log|x - x0| outside)
+ *   VP_BIE_NEUMANN_INT    (+1/2 I + D) u = rhs            (lines 1310-1318: rhs = V[f] + S[g]; singular, the
+ *                                                          solution is defined up to a constant)
+ * rhs, x: DEVICE [T] (x is overwritten; the initial guess is 0).  tol: relative residual |b - A x| / |b|; maxit:
+ * total Arnoldi steps; restart: Krylov dimension m (1..200; workspace (m+1) T doubles, allocated per call).
+ * iters / resid (host, may be NULL): steps taken, final relative residual.  Synchronous.  Reaching maxit is not an
+ * error (check resid).  Errors: VP_ERR_ARG (bad arguments, no vp_dlp_prepare, targets not the chunk nodes),
+ * VP_ERR_CUDA / VP_ERR_CUFFT / VP_ERR_OOM. */
+enum { VP_BIE_DIRICHLET_INT = 0, VP_BIE_DIRICHLET_EXT = 1, VP_BIE_NEUMANN_INT = 2 };
+vp_status vp_bie_solve(vp_handle plan, int32_t kind, const double *rhs, double *x, double tol, int32_t maxit,
+                       int32_t restart, int32_t *iters, double *resid);
+
 /* Release all device memory and cuFFT plans owned by the plan.  NULL is accepted. */
 vp_status vp_destroy(vp_handle plan);
 

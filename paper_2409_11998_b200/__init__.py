@@ -21,11 +21,12 @@ VP_OK, VP_ERR_ARG, VP_ERR_TOL, VP_ERR_NONFINITE, VP_ERR_GEOMETRY, VP_ERR_UNSUPPO
 BDRY = {None: 0, "none": 0, "circle": 1, "rect": 2, "polygon": 3, "chunks": 4}
 DERIV = {"auto": 0, "knn": 1, "triangle": 2}
 PART_HISTORY, PART_LOCAL, PART_ALL = 1, 2, 3
+BIE_DIRICHLET_INT, BIE_DIRICHLET_EXT, BIE_NEUMANN_INT = 0, 1, 2  # vp.h VP_BIE_*
 
 EXPORTED = ["vp_plan", "vp_eval", "vp_eval_host", "vp_eval_batch", "vp_destroy", "vp_strerror", "vp_get_info", "vp_set_profiling",
             "vp_get_phase_times", "vp_eval_launch_count", "vp_check_finite", "vp_last_error_detail", "vp_version",
             "vp_slp_prepare", "vp_eval_slp", "vp_dlp_prepare", "vp_eval_dlp",
-            "vp_layer_set_levels"]
+            "vp_layer_set_levels", "vp_bie_solve"]
 
 
 class VpBoundary(ctypes.Structure):
@@ -86,6 +87,7 @@ def lib():
         L.vp_eval_slp.argtypes = [vp, vp, vp]
         L.vp_dlp_prepare.argtypes = [vp]
         L.vp_layer_set_levels.argtypes = [vp, i32]
+        L.vp_bie_solve.argtypes = [vp, i32, vp, vp, d, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(d)]
         L.vp_eval_dlp.argtypes = [vp, vp, vp]
         L.vp_destroy.argtypes = [vp]
         L.vp_strerror.argtypes = [ctypes.c_int]
@@ -251,6 +253,19 @@ class Plan:
         out = self._out(out, self.T, mu.device)
         _check(lib().vp_eval_dlp(self.h, mu.data_ptr(), out.data_ptr()), "vp_eval_dlp")
         return out
+
+    def bie_solve(self, kind, rhs, tol=1e-12, maxit=200, restart=50, out=None):
+        """GMRES solve of a boundary integral equation with the GPU double-layer operator (C ABI vp_bie_solve; the
+        plan's targets are the chunk nodes, prepare_dlp() done).  kind: BIE_DIRICHLET_INT / BIE_DIRICHLET_EXT /
+        BIE_NEUMANN_INT.  Returns (x [T] device, iterations, relative residual)."""
+        rhs = _dev_f64(rhs)
+        if rhs.numel() != self.T:
+            raise ValueError("rhs must hold one value per target (= chunk node)")
+        out = self._out(out, self.T, rhs.device)
+        it, res = ctypes.c_int32(0), ctypes.c_double(0.0)
+        _check(lib().vp_bie_solve(self.h, int(kind), rhs.data_ptr(), out.data_ptr(), float(tol), int(maxit),
+                                  int(restart), ctypes.byref(it), ctypes.byref(res)), "vp_bie_solve")
+        return out, it.value, res.value
 
     def eval_host(self, f_host, out_host=None):
         """f_host: numpy float64 (ideally pinned, e.g. torch pinned tensor .numpy()); returns numpy [T]."""

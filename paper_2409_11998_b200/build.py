@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvp.so")
-SOURCES = ["vp_api.cu", "vp_nufft.cu", "vp_local.cu", "vp_levels.cu", "vp_fft.cu", "vp_boundary.cu", "vp_layer.cu"]
+SOURCES = ["vp_api.cu", "vp_nufft.cu", "vp_local.cu", "vp_levels.cu", "vp_fft.cu", "vp_boundary.cu", "vp_layer.cu", "vp_bie.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

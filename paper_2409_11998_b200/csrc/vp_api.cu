@@ -536,6 +536,20 @@ extern "C" vp_status vp_plan(const double *tri_nodes, const double *weights, int
       y0 = std::min(y0, hb[4 * i + 2]); y1 = std::max(y1, hb[4 * i + 3]);
     }
     if (!(sumw > 0)) throw VpError{VP_ERR_ARG};
+    // the grid frame also covers a CHUNKS / POLYGON boundary (host array): its nodes are the layer potentials'
+    // sources (vp_layer.cu)
+    if (opts && opts->boundary.pts && opts->boundary.n > 0 &&
+        (opts->boundary.kind == VP_BDRY_CHUNKS || opts->boundary.kind == VP_BDRY_POLYGON)) {
+      const vp_boundary &bd = opts->boundary;
+      const int64_t np = bd.kind == VP_BDRY_CHUNKS ? bd.n * (int64_t)(bd.q + 1) : bd.n;
+      if (bd.kind == VP_BDRY_CHUNKS && (bd.q < 1 || bd.q > VP_CHUNK_MAXQ)) throw VpError{VP_ERR_GEOMETRY};
+      for (int64_t i = 0; i < np; i++) {
+        const double bx = bd.pts[2 * i], by = bd.pts[2 * i + 1];
+        if (!std::isfinite(bx) || !std::isfinite(by)) throw VpError{VP_ERR_NONFINITE};
+        x0 = std::min(x0, bx); x1 = std::max(x1, bx);
+        y0 = std::min(y0, by); y1 = std::max(y1, by);
+      }
+    }
     // ---- parameters
     P->dx2 = sumw / (double)N;
     double C = o.C > 0 ? o.C : 3.0;

@@ -221,6 +221,7 @@ struct vp_plan_s {
   // telescoped local parts (§4.1): J levels, NC chunk slots per near target, NP quadrature panels per chunk
   int lay_J = 3, lay_nc = 1, lay_np = 1;
   double *lay_tq = nullptr, *lay_tq1 = nullptr, *lay_gw = nullptr, *lay_lg = nullptr;
+  double *lay_W = nullptr;  // [n (q+1)] boundary quadrature weights (set by vp_dlp_prepare)
   // double-layer potential (vp_dlp_prepare): dipole source sets W nu_1, W nu_2, local stencils, spectral derivative
   bool dlp_ready = false, dlp_has_plans = false;
   VpSpreadSet dsp1, dsp2;

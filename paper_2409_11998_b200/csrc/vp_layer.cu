@@ -508,7 +508,8 @@ void vp_dlp_build(vp_plan_s *P) {
   double *Wx = nullptr, *Wy = nullptr;
   VP_CUDA(cudaMallocAsync(&Wx, sizeof(double) * nb, s));
   VP_CUDA(cudaMallocAsync(&Wy, sizeof(double) * nb, s));
-  k_slp_sources<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(B.coef, B.snode, P->slp_swt, B.n, B.q, nullptr, Wx,
+  P->lay_W = vp_alloc<double>(P, nb);  // W_j = w_k |gamma'(s_k)|: the boundary rule (D_E's int mu ds, BIE solves)
+  k_slp_sources<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(B.coef, B.snode, P->slp_swt, B.n, B.q, P->lay_W, Wx,
                                                              Wy);
   VP_CHECK_LAUNCH();
   vp_build_strip_order(P, P->dsp1, B.pts, Wx, nullptr, nb, grid_args(P->nh));
