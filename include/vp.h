@@ -195,6 +195,16 @@ vp_status vp_eval(vp_handle plan, const double *f, double *out);
  * synchronises.  Pinned host memory is recommended. */
 vp_status vp_eval_host(vp_handle plan, const double *f_host, double *out_host);
 
+/* K fields from HOST memory, f_host[k] [M][p] -> out_host[k] [T] (k < K), with the transfers overlapped across
+ * fields: the H2D copy of field k+1 and the D2H copy of field k-1 run on two plan-owned copy streams while field
+ * k is evaluated (PCIe is full duplex), so the throughput is bound by the slowest of H2D, D2H and vp_eval instead
+ * of their sum.  Pinned host memory is required for the overlap (pageable memory works, serialised).  The first
+ * call allocates two device slots for f and out (2 x 8 (N + T) bytes, plan-owned) and the copy streams.  Work is
+ * ordered after earlier work on the plan's stream; synchronous on return.  An output array may be passed for
+ * several k (the D2H copies are ordered on one stream; it then holds the last of those fields).
+ * Errors: VP_ERR_ARG (K < 1, null pointers), VP_ERR_OOM, VP_ERR_CUDA / VP_ERR_CUFFT. */
+vp_status vp_eval_host_many(vp_handle plan, int32_t K, const double *const *f_host, double *const *out_host);
+
 /* Evaluate K fields on the same plan ("batched multi-f vp_eval"; PAPER.md Steps 2-4,
  * lines 848-850, are linear in the strengths c_j = f_j w_j).
  *   K    number of fields, >= 1

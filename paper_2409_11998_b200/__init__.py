@@ -26,7 +26,7 @@ BIE_DIRICHLET_INT, BIE_DIRICHLET_EXT, BIE_NEUMANN_INT = 0, 1, 2  # vp.h VP_BIE_*
 EXPORTED = ["vp_plan", "vp_eval", "vp_eval_host", "vp_eval_batch", "vp_destroy", "vp_strerror", "vp_get_info", "vp_set_profiling",
             "vp_get_phase_times", "vp_eval_launch_count", "vp_check_finite", "vp_last_error_detail", "vp_version",
             "vp_slp_prepare", "vp_eval_slp", "vp_dlp_prepare", "vp_eval_dlp",
-            "vp_layer_set_levels", "vp_bie_solve"]
+            "vp_layer_set_levels", "vp_bie_solve", "vp_eval_host_many"]
 
 
 class VpBoundary(ctypes.Structure):
@@ -82,6 +82,7 @@ def lib():
         L.vp_plan.argtypes = [vp, vp, i64, i32, vp, i64, d, ctypes.POINTER(VpOpts), ctypes.POINTER(vp)]
         L.vp_eval.argtypes = [vp, vp, vp]
         L.vp_eval_host.argtypes = [vp, vp, vp]
+        L.vp_eval_host_many.argtypes = [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(vp)]
         L.vp_eval_batch.argtypes = [vp, i32, vp, vp]
         L.vp_slp_prepare.argtypes = [vp]
         L.vp_eval_slp.argtypes = [vp, vp, vp]
@@ -279,6 +280,21 @@ class Plan:
             raise ValueError(f"out_host must be a writeable C-contiguous float64 array of {self.T} entries")
         _check(lib().vp_eval_host(self.h, f_host.ctypes.data, out_host.ctypes.data), "vp_eval_host")
         return out_host
+
+    def eval_host_many(self, f_hosts, out_hosts):
+        """K fields from host memory with overlapped transfers (C ABI vp_eval_host_many): f_hosts / out_hosts are
+        lists of K float64 C-contiguous numpy arrays (pinned for the overlap) of N / T entries."""
+        K = len(f_hosts)
+        if K < 1 or len(out_hosts) != K:
+            raise ValueError("need K >= 1 input and output arrays")
+        for a, n, ro in [(a, self.N, True) for a in f_hosts] + [(a, self.T, False) for a in out_hosts]:
+            if (not isinstance(a, np.ndarray) or a.dtype != np.float64 or a.size != n or not a.flags.c_contiguous
+                    or (not ro and not a.flags.writeable)):
+                raise ValueError(f"host arrays must be C-contiguous float64 numpy arrays of {n} entries")
+        fp = (ctypes.c_void_p * K)(*[a.ctypes.data for a in f_hosts])
+        op = (ctypes.c_void_p * K)(*[a.ctypes.data for a in out_hosts])
+        _check(lib().vp_eval_host_many(self.h, K, fp, op), "vp_eval_host_many")
+        return out_hosts
 
     def check_finite(self, f):
         f = _dev_f64(f)

@@ -472,6 +472,10 @@ static void free_plan(vp_plan_s *P) {
     cufftDestroy(P->bands.fwd);
     cufftDestroy(P->bands.inv);
   }
+  if (P->s_h2d) cudaStreamDestroy(P->s_h2d);
+  if (P->s_d2h) cudaStreamDestroy(P->s_d2h);
+  for (cudaEvent_t e : P->hm_ev)
+    if (e) cudaEventDestroy(e);
   if (P->s_fh) cudaStreamDestroy(P->s_fh);
   if (P->s_loc) cudaStreamDestroy(P->s_loc);
   for (cudaEvent_t e : {P->ev_fork, P->ev_fh, P->ev_loc, P->ev_restr})
@@ -969,6 +973,60 @@ extern "C" vp_status vp_eval_host(vp_handle P, const double *f_host, double *out
     VP_CUDA(cudaMemcpyAsync(out_host, P->out_dev, sizeof(double) * P->T, cudaMemcpyDeviceToHost, P->stream));
     VP_CUDA(cudaStreamSynchronize(P->stream));
   } catch (VpError &e) {
+    return e.s;
+  }
+  return VP_OK;
+}
+
+// K fields from HOST memory with the transfers overlapped across fields: H2D of field k+1 (stream s_h2d) and
+// D2H of field k-1 (stream s_d2h) run while field k is evaluated on the plan's stream (two device slots for f and
+// out; PCIe is full duplex).  Ordered after earlier work on the plan's stream; the plan's stream waits for the last
+// D2H before the call synchronises it and returns.
+extern "C" vp_status vp_eval_host_many(vp_handle P, int32_t K, const double *const *f_host, double *const *out_host) {
+  if (!P || K < 1 || !f_host || !out_host) return VP_ERR_ARG;
+  for (int32_t k = 0; k < K; k++)
+    if (!f_host[k] || !out_host[k]) return VP_ERR_ARG;
+  try {
+    if (!P->hm_ready) {
+      for (int b = 0; b < 2; b++) {
+        P->hm_f[b] = vp_alloc<double>(P, P->N);
+        P->hm_out[b] = vp_alloc<double>(P, P->T);
+      }
+      VP_CUDA(cudaStreamCreateWithFlags(&P->s_h2d, cudaStreamNonBlocking));
+      VP_CUDA(cudaStreamCreateWithFlags(&P->s_d2h, cudaStreamNonBlocking));
+      for (cudaEvent_t &e : P->hm_ev) VP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      P->hm_ready = true;
+    }
+    cudaEvent_t ev_start = P->hm_ev[0], *ev_in = P->hm_ev + 1, *ev_done = P->hm_ev + 3, *ev_out = P->hm_ev + 5;
+    const size_t fb = sizeof(double) * P->N, ob = sizeof(double) * P->T;
+    VP_CUDA(cudaEventRecord(ev_start, P->stream));
+    VP_CUDA(cudaStreamWaitEvent(P->s_h2d, ev_start, 0));
+    VP_CUDA(cudaStreamWaitEvent(P->s_d2h, ev_start, 0));
+    auto h2d = [&](int32_t k) {
+      const int b = k & 1;
+      if (k >= 2) VP_CUDA(cudaStreamWaitEvent(P->s_h2d, ev_done[b], 0));  // eval k-2 has finished reading slot b
+      VP_CUDA(cudaMemcpyAsync(P->hm_f[b], f_host[k], fb, cudaMemcpyHostToDevice, P->s_h2d));
+      VP_CUDA(cudaEventRecord(ev_in[b], P->s_h2d));
+    };
+    h2d(0);
+    for (int32_t k = 0; k < K; k++) {
+      const int b = k & 1;
+      if (k + 1 < K) h2d(k + 1);
+      VP_CUDA(cudaStreamWaitEvent(P->stream, ev_in[b], 0));
+      if (k >= 2) VP_CUDA(cudaStreamWaitEvent(P->stream, ev_out[b], 0));  // D2H of k-2 has read out slot b
+      const vp_status st = vp_eval(P, P->hm_f[b], P->hm_out[b]);
+      if (st != VP_OK) throw VpError{st};
+      VP_CUDA(cudaEventRecord(ev_done[b], P->stream));
+      VP_CUDA(cudaStreamWaitEvent(P->s_d2h, ev_done[b], 0));
+      VP_CUDA(cudaMemcpyAsync(out_host[k], P->hm_out[b], ob, cudaMemcpyDeviceToHost, P->s_d2h));
+      VP_CUDA(cudaEventRecord(ev_out[b], P->s_d2h));
+    }
+    VP_CUDA(cudaStreamWaitEvent(P->stream, ev_out[(K - 1) & 1], 0));
+    VP_CUDA(cudaStreamSynchronize(P->stream));
+  } catch (VpError &e) {
+    cudaStreamSynchronize(P->stream);
+    if (P->s_h2d) cudaStreamSynchronize(P->s_h2d);
+    if (P->s_d2h) cudaStreamSynchronize(P->s_d2h);
     return e.s;
   }
   return VP_OK;

@@ -264,6 +264,11 @@ struct vp_plan_s {
   int bcap = 1;
   // host-side eval staging (vp_eval_host)
   double *f_dev = nullptr, *out_dev = nullptr;
+  // vp_eval_host_many: two device slots for f and out, copy streams and their events (allocated on first use)
+  bool hm_ready = false;
+  double *hm_f[2] = {nullptr, nullptr}, *hm_out[2] = {nullptr, nullptr};
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t hm_ev[7] = {};  // start, in[2], done[2], out[2]
   // profiling
   bool profiling = false;
   cudaEvent_t ev[12] = {};
