@@ -47,6 +47,19 @@ def test_argument_errors_without_gpu():
     assert L.vp_eval(None, None, None) == vp.VP_ERR_ARG
     assert L.vp_eval_batch(None, 4, None, None) == vp.VP_ERR_ARG
     assert L.vp_eval_batch(1, 0, 1, 1) == vp.VP_ERR_ARG  # K < 1 is rejected before the handle is used
+    # layer potentials, BIE solves, pipelined host evals: arguments checked before any CUDA call
+    assert L.vp_slp_prepare(None) == vp.VP_ERR_ARG and L.vp_dlp_prepare(None) == vp.VP_ERR_ARG
+    assert L.vp_eval_slp(None, None, None) == vp.VP_ERR_ARG and L.vp_eval_dlp(None, None, None) == vp.VP_ERR_ARG
+    assert L.vp_layer_set_levels(None, 3) == vp.VP_ERR_ARG
+    it, res = ctypes.c_int32(), ctypes.c_double()
+    assert L.vp_bie_solve(None, 0, 1, 1, 1e-10, 10, 10, ctypes.byref(it), ctypes.byref(res)) == vp.VP_ERR_ARG
+    assert L.vp_bie_solve(1, 7, 1, 1, 1e-10, 10, 10, ctypes.byref(it), ctypes.byref(res)) == vp.VP_ERR_ARG  # kind
+    assert L.vp_bie_solve(1, 0, 1, 1, 0.0, 10, 10, ctypes.byref(it), ctypes.byref(res)) == vp.VP_ERR_ARG  # tol
+    assert L.vp_bie_solve(1, 0, 1, 1, 1e-10, 10, 500, ctypes.byref(it), ctypes.byref(res)) == vp.VP_ERR_ARG
+    assert L.vp_eval_host_many(None, 1, None, None) == vp.VP_ERR_ARG
+    assert L.vp_eval_host_many(1, 0, None, None) == vp.VP_ERR_ARG
+    nul = (ctypes.c_void_p * 2)(None, None)
+    assert L.vp_eval_host_many(1, 2, nul, nul) == vp.VP_ERR_ARG
     assert L.vp_destroy(None) == vp.VP_OK
 
 
