@@ -10,6 +10,7 @@ Functions (see oracle/vp_oracle.c for the citations and the quadrature tiers):
   smooth_dft(src, c, targets, d1, d2, ...)         -> same split through a direct Fourier sum
   e1(x), GH(r2, delta), WR(k, R)
   layer.single_layer(curve, dcurve, sigma, targets) -> S[sigma](x_t) on an analytic closed curve (oracle/layer.py)
+  layer.double_layer(curve, dcurve, mu, targets, on_curve) -> D[mu](x_t), outward normal (oracle/layer.py)
 Parity status of each function is listed in DESIGN.md §Oracle (all pinned).
 """
 import ctypes
