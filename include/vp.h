@@ -131,6 +131,10 @@ typedef struct {
    * 2 x nf/4 complex values, in one CTA's shared memory: nf <= 28160), else cuFFT batched 1D row
    * transforms; 1 -> cuFFT batched 1D row transforms */
   int32_t fft_rows;
+  /* vp_eval_batch with row-pair strips at w <= 10: 0 -> pairs of fields share one spreading pass
+   * (k_spread_pair2: footprint geometry, ES taps and shared-memory tap loads paid once per two fields);
+   * 1 -> one k_spread_pair pass per field */
+  int32_t batch_pair;
 } vp_opts;
 
 /* Plan parameters chosen by vp_plan (diagnostics; all derived from the rules in DESIGN.md). */

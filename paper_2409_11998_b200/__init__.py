@@ -43,7 +43,8 @@ class VpOpts(ctypes.Structure):
                 ("ref_nodes", ctypes.c_void_p), ("tri_max_aspect", ctypes.c_double), ("levels", ctypes.c_int32),
                 ("level_cmin", ctypes.c_double), ("level_rho", ctypes.c_double), ("deterministic", ctypes.c_int32),
                 ("spread_tile", ctypes.c_int32), ("interp_tile", ctypes.c_int32), ("fft_mode", ctypes.c_int32),
-                ("spread_pack", ctypes.c_int32), ("fft_rows", ctypes.c_int32)]
+                ("spread_pack", ctypes.c_int32), ("fft_rows", ctypes.c_int32),
+                ("batch_pair", ctypes.c_int32)]
 
 
 class VpInfo(ctypes.Structure):
@@ -141,7 +142,7 @@ class Plan:
                  eps_nufft=0.0, series_order=0, deriv="auto", deriv_degree=0, deriv_k=0, parts=PART_ALL,
                  targets_are_nodes=False, boundary=None, stream=None, ref_nodes=None, tri_max_aspect=0.0, levels=0,
                  level_cmin=0.0, level_rho=0.0, deterministic=False, spread_tile=0, interp_tile=0, fft_mode=0,
-                 spread_pack=0, fft_rows=0):
+                 spread_pack=0, fft_rows=0, batch_pair=0):
         import torch
         L = lib()
         tri_nodes = _dev_f64(tri_nodes)
@@ -183,6 +184,7 @@ class Plan:
         o.deterministic = 1 if deterministic else 0
         o.spread_tile, o.interp_tile, o.fft_mode = spread_tile, interp_tile, fft_mode
         o.spread_pack, o.fft_rows = spread_pack, fft_rows
+        o.batch_pair = batch_pair
         h = ctypes.c_void_p()
         _check(L.vp_plan(tri_nodes.data_ptr(), weights.data_ptr(), M, p, targets.data_ptr(), T, float(tol),
                          ctypes.byref(o), ctypes.byref(h)), "vp_plan")

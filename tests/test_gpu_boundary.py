@@ -28,6 +28,16 @@ def plan_eval(w, boundary, **kw):
     return V, info
 
 
+def same_local_part(w, bd_a, bd_b):
+    """The local part V_L (parts = PART_LOCAL) does not depend on the NUFFT grids, so two descriptions of the same
+    boundary must give it to rounding.  The full V is compared at the NUFFT tolerance by the callers: the grid
+    frame covers the CHUNKS / POLYGON nodes (they are the layer potentials' sources, vp_api.cu), so the two
+    plans' grids differ by rounding in their origin and each smooth part carries its own eps = tol error."""
+    La, _ = plan_eval(w, bd_a, parts=vp.PART_LOCAL)
+    Lb, _ = plan_eval(w, bd_b, parts=vp.PART_LOCAL)
+    assert np.max(np.abs(La - Lb)) <= 1e-12 * np.max(np.abs(La))
+
+
 def test_disk_chunks_match_circle_and_oracle():
     """Config 1 (unit disk, f = Gaussian, f != 0 on the boundary) with the circle given as 96 chunks of degree 16:
     the chunk path (nearest node + Newton, curvature from the interpolant) reproduces the analytic circle and
@@ -36,7 +46,8 @@ def test_disk_chunks_match_circle_and_oracle():
     Vc, ic = plan_eval(w, ("circle", 0.0, 0.0, 1.0))
     Vk, ik = plan_eval(w, ("chunks", geometry.circle_chunks(0.0, 0.0, 1.0, 96, q=16, theta0=0.123)))
     assert ik["n_boundary_targets"] == ic["n_boundary_targets"] > 1000
-    assert np.max(np.abs(Vk - Vc)) <= 1e-12 * np.max(np.abs(Vc))
+    same_local_part(w, ("circle", 0.0, 0.0, 1.0), ("chunks", geometry.circle_chunks(0.0, 0.0, 1.0, 96, q=16, theta0=0.123)))
+    assert np.max(np.abs(Vk - Vc)) <= 10 * w.tol * np.max(np.abs(Vc))
     ref = oracle.workload_potential(w)
     e = rel_l2(Vk, ref)
     print("disk chunks rel l2 vs oracle", e)
@@ -61,7 +72,8 @@ def test_star_chunks_config3_small():
     V0, _ = plan_eval(w, None)
     Vs, info = plan_eval(w, ("chunks", geometry.star_chunks(200, q=16)))
     assert info["n_boundary_targets"] > 0
-    assert np.max(np.abs(Vs - V0)) <= 1e-12 * np.max(np.abs(V0))
+    same_local_part(w, None, ("chunks", geometry.star_chunks(200, q=16)))
+    assert np.max(np.abs(Vs - V0)) <= 10 * w.tol * np.max(np.abs(V0))
     e = rel_l2(Vs[idx], oracle.workload_potential(w, idx))
     assert e <= 10 * w.tol, e
 
@@ -73,7 +85,8 @@ def test_square_polygon_matches_rect():
     sq = np.array([[0.0, 0.0], [0.5, 0.0], [1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
     Vp, ip = plan_eval(w, ("polygon", sq))
     assert ip["n_boundary_targets"] == ir["n_boundary_targets"] > 0
-    assert np.max(np.abs(Vp - Vr)) <= 1e-12 * np.max(np.abs(Vr))
+    same_local_part(w, ("rect", 0.0, 0.0, 1.0, 1.0), ("polygon", sq))
+    assert np.max(np.abs(Vp - Vr)) <= 10 * w.tol * np.max(np.abs(Vr))
 
 
 def test_lshape_polygon_vs_oracle():
