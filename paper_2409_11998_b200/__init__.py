@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvp.so")
+LIB_PATH = os.environ.get("VP_LIB") or os.path.join(_HERE, "libvp.so")  # VP_LIB: A/B builds (scripts/r2)
 
 VP_OK, VP_ERR_ARG, VP_ERR_TOL, VP_ERR_NONFINITE, VP_ERR_GEOMETRY, VP_ERR_UNSUPPORTED, VP_ERR_OOM, VP_ERR_CUDA, \
     VP_ERR_CUFFT = 0, -1, -2, -3, -4, -5, -6, -7, -8

@@ -576,6 +576,9 @@ static void launch_spread_strip_w(vp_plan_s *P, const VpSpreadSet &S, const Grid
 // or S y loads (about 7.5 wavefronts at W = 10) and S - 1 or S DFMA per lane.  Strips are SW = 17 - W origin
 // columns wide, so the RED flush covers 16 / SW columns per origin column (more halo REDs than the 32-column
 // strip, 2.3x vs 1.4x at W = 10; the L2 atomic rate, 4.7e11/s, is below the shared-memory bound).
+#ifndef VP_PAIR_WARPS
+#define VP_PAIR_WARPS 7  // warps per CTA at W <= 10 (3 CTAs per SM)
+#endif
 #ifndef VP_PAIR_SH
 #define VP_PAIR_SH 128  // footprint-origin rows per pair strip (even)
 #endif
@@ -592,7 +595,7 @@ struct PairCfg {
   static constexpr size_t smem_warp = (size_t)CH * (WXS + WYS + 1) * 8;  // + per-point meta (int2)
   // warps per CTA and CTAs per SM: 21 warps (80 registers) at W <= 10; wider kernels need ~96 registers, i.e. at
   // most 5 warps per SM sub-partition
-  static constexpr int WARPS = W <= 10 ? 7 : 4;
+  static constexpr int WARPS = W <= 10 ? VP_PAIR_WARPS : 4;
   static constexpr int MINB = W <= 10 ? 3 : 5;
 };
 
@@ -1002,22 +1005,40 @@ stage:
   }
   for (;;) {
     switch (P % S) {
+#ifndef VP_PAIR2_X2
+#define VP_PAIR2_X2 1  // two points per iteration of the point loop
+#endif
+#define VP_PAIR2_POINT(qq, K)                                                                         \
+  {                                                                                                   \
+    const int2 m = s_meta[qq];                                                                        \
+    const double2 cc = s_c[qq];                                                                       \
+    const double wxl = *(const double *)(xb + m.x);                                                   \
+    const double wx0 = wxl * cc.x, wx1 = wxl * cc.y;                                                  \
+    const char *yp = yb + m.y;                                                                        \
+    _Pragma("unroll") for (int jj = 0; jj < S; jj++)                                                  \
+      if (jj < S - 1 || (W & 1) || (m.y & 8)) {                                                       \
+        const double wyl = *(const double *)(yp + 16 * jj);                                           \
+        acc[((K) + jj) % S] = fma(wyl, wx0, acc[((K) + jj) % S]);                                     \
+        acc2[((K) + jj) % S] = fma(wyl, wx1, acc2[((K) + jj) % S]);                                   \
+      }                                                                                               \
+  }
+  // (the point loop is not unrolled further: with 9 phases the kernel must stay inside the instruction cache;
+  // an 8x unrolled build ran 4x slower on B200, stalled on instruction fetch: profiles/r2/pair2)
 #define VP_PAIR2_PHASE(k)                                                                             \
   case k:                                                                                             \
     if ((k) < S) {                                                                                    \
       const int e = __popc(__ballot_sync(0xffffffffu, mylr <= 2 * P + 1));                             \
-      for (; q < e; q++) {                                                                            \
-        const int2 m = s_meta[q];                                                                     \
-        const double2 cc = s_c[q];                                                                    \
-        const double wxl = *(const double *)(xb + m.x);                                               \
-        const double wx0 = wxl * cc.x, wx1 = wxl * cc.y;                                              \
-        const char *yp = yb + m.y;                                                                    \
-        _Pragma("unroll") for (int jj = 0; jj < S; jj++)                                              \
-          if (jj < S - 1 || (W & 1) || (m.y & 8)) {                                                   \
-            const double wyl = *(const double *)(yp + 16 * jj);                                       \
-            acc[((k) + jj) % S] = fma(wyl, wx0, acc[((k) + jj) % S]);                                 \
-            acc2[((k) + jj) % S] = fma(wyl, wx1, acc2[((k) + jj) % S]);                               \
-          }                                                                                           \
+      if (VP_PAIR2_X2) {                                                                              \
+        _Pragma("unroll 1") for (; q + 1 < e; q += 2) {                                               \
+          VP_PAIR2_POINT(q, k)                                                                        \
+          VP_PAIR2_POINT(q + 1, k)                                                                    \
+        }                                                                                             \
+        if (q < e) {                                                                                  \
+          VP_PAIR2_POINT(q, k)                                                                        \
+          q++;                                                                                        \
+        }                                                                                             \
+      } else {                                                                                        \
+        _Pragma("unroll 1") for (; q < e; q++) VP_PAIR2_POINT(q, k)                                   \
       }                                                                                               \
       if (q == n) goto next_chunk;                                                                    \
       const double v0 = acc[(k)], v1 = acc2[(k)];                                                     \
@@ -1036,6 +1057,7 @@ stage:
       VP_PAIR2_PHASE(0) VP_PAIR2_PHASE(1) VP_PAIR2_PHASE(2) VP_PAIR2_PHASE(3) VP_PAIR2_PHASE(4)
       VP_PAIR2_PHASE(5) VP_PAIR2_PHASE(6) VP_PAIR2_PHASE(7) VP_PAIR2_PHASE(8)
 #undef VP_PAIR2_PHASE
+#undef VP_PAIR2_POINT
     }
   }
 next_chunk:
