@@ -261,6 +261,7 @@ def main():
     # config 5: level bands off (delta_1 / sigma_min^2 = 0.016; parity 4.9e-10 without them)
     levels = -1 if w.name.startswith("c5") else 0
     extra = {k: int(v) for k, v in (o.split("=") for o in args.opt)}
+    levels = extra.pop("levels", levels)  # --opt levels=0: auto level bands on config 5 (A/B of their cost)
     plan = vp.Plan(nodes, wts, tg, w.tol, boundary=w.boundary, targets_are_nodes=w.targets_are_nodes, stream=stream,
                    ref_nodes=rule.BARY[:, 1:3], levels=levels, **extra)
     info = plan.info()

@@ -15,6 +15,8 @@ timeout 900 python bench.py --impl reference > $D/bench_ref.json 2> $D/bench_ref
 for c in c2 c3 c4; do
   timeout 900 python bench.py --config $c --no-cpu-baseline > $D/bench_$c.json 2> $D/bench_$c.err; echo bench_$c=$?
 done
+timeout 900 python bench.py --no-cpu-baseline --batch 0 --opt levels=0 > $D/bench_c5_levels_auto.json 2> $D/bench_c5_levels_auto.err; echo levels=$?
+timeout 900 python bench.py --no-cpu-baseline --batch 4 --opt batch_pair=1 > $D/bench_c5_batch_perfield.json 2> $D/bench_c5_batch_perfield.err; echo perfield=$?
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/lds_rates scripts/microbench/lds_rates.cu && /tmp/lds_rates > $D/microbench_peaks.txt 2>&1
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/peaks scripts/microbench/peaks.cu && /tmp/peaks >> $D/microbench_peaks.txt 2>&1
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/red_peak scripts/microbench/red_peak.cu && /tmp/red_peak >> $D/microbench_peaks.txt 2>&1
