@@ -302,6 +302,11 @@ const char *vp_last_error_detail(void);
 
 const char *vp_version(void);
 
+/* sizeof(vp_opts), sizeof(vp_info), sizeof(vp_boundary) of this build.  A binding that mirrors the structs
+ * (the ctypes classes of paper_2409_11998_b200/__init__.py) compares its own sizes with these when the library
+ * is loaded and refuses to run on a mismatch.  out: 3 values. */
+vp_status vp_struct_sizes(int64_t *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,7 @@ BIE_DIRICHLET_INT, BIE_DIRICHLET_EXT, BIE_NEUMANN_INT = 0, 1, 2  # vp.h VP_BIE_*
 EXPORTED = ["vp_plan", "vp_eval", "vp_eval_host", "vp_eval_batch", "vp_destroy", "vp_strerror", "vp_get_info", "vp_set_profiling",
             "vp_get_phase_times", "vp_eval_launch_count", "vp_check_finite", "vp_last_error_detail", "vp_version",
             "vp_slp_prepare", "vp_eval_slp", "vp_dlp_prepare", "vp_eval_dlp",
-            "vp_layer_set_levels", "vp_bie_solve", "vp_eval_host_many"]
+            "vp_layer_set_levels", "vp_bie_solve", "vp_eval_host_many", "vp_struct_sizes"]
 
 
 class VpBoundary(ctypes.Structure):
@@ -110,6 +110,13 @@ def lib():
         L.vp_debug_mult.restype = d
         L.vp_debug_e1.argtypes = [d]
         L.vp_debug_e1.restype = d
+        L.vp_struct_sizes.argtypes = [ctypes.POINTER(ctypes.c_int64)]
+        L.vp_struct_sizes.restype = ctypes.c_int
+        sz = (ctypes.c_int64 * 3)()
+        mine = (ctypes.sizeof(VpOpts), ctypes.sizeof(VpInfo), ctypes.sizeof(VpBoundary))
+        if L.vp_struct_sizes(sz) != VP_OK or tuple(sz) != mine:
+            raise RuntimeError(f"{LIB_PATH}: struct layout mismatch (library {tuple(sz)}, binding {mine}): "
+                               "rebuild with `python -m paper_2409_11998_b200.build --force`")
         _lib = L
     return _lib
 

@@ -43,6 +43,14 @@ void vp_smem_attr(const void *func, size_t bytes) {
   have = bytes;
 }
 
+extern "C" vp_status vp_struct_sizes(int64_t *out) {
+  if (!out) return VP_ERR_ARG;
+  out[0] = (int64_t)sizeof(vp_opts);
+  out[1] = (int64_t)sizeof(vp_info);
+  out[2] = (int64_t)sizeof(vp_boundary);
+  return VP_OK;
+}
+
 extern "C" const char *vp_strerror(vp_status s) {
   switch (s) {
     case VP_OK: return "ok";

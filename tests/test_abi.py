@@ -28,6 +28,16 @@ def test_library_exports_header_symbols():
         assert hasattr(L, n), n
 
 
+def test_struct_sizes_match_binding():
+    """The ctypes mirrors of vp_opts / vp_info / vp_boundary have the library's sizes (vp_struct_sizes; the
+    binding refuses to load a library with another layout)."""
+    L = vp.lib()
+    sz = (ctypes.c_int64 * 3)()
+    assert L.vp_struct_sizes(sz) == vp.VP_OK
+    assert tuple(sz) == (ctypes.sizeof(vp.VpOpts), ctypes.sizeof(vp.VpInfo), ctypes.sizeof(vp.VpBoundary))
+    assert L.vp_struct_sizes(None) == vp.VP_ERR_ARG
+
+
 def test_strerror_and_version():
     L = vp.lib()
     for s in range(-8, 1):
