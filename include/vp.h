@@ -214,8 +214,9 @@ vp_status vp_eval_host_many(vp_handle plan, int32_t K, const double *const *f_ho
  *   K    number of fields, >= 1
  *   f    [K][M][p] fp64 source values (device, read only), field k at f + k M p
  *   out  [K][T]    fp64 (device), field k at out + k T, fully overwritten
- * The spreading of up to four fields shares one pass over the sorted nodes (geometry, ES weights and their
- * shared-memory broadcasts are computed once per node); transforms, interpolation and the local part run per
+ * The spreading of several fields shares one pass over the sorted nodes (geometry, ES weights and their
+ * shared-memory loads are paid once per node): two fields per pass with row-pair strips at w <= 10 (the default;
+ * opts.batch_pair), up to four with 32-column strips; transforms, interpolation and the local part run per
  * field, each with vp_eval's schedule (fork/join streams on small grids, serial otherwise).  The first call with a
  * larger K than before synchronises the plan's stream, frees the previous extra buffers and allocates K-1 extra NH
  * grids (and K spreading-order copies of f for KNN stencils), owned by the plan.  Same stream and concurrency rules
