@@ -577,7 +577,14 @@ static void launch_spread_strip_w(vp_plan_s *P, const VpSpreadSet &S, const Grid
 // columns wide, so the RED flush covers 16 / SW columns per origin column (more halo REDs than the 32-column
 // strip, 2.3x vs 1.4x at W = 10; the L2 atomic rate, 4.7e11/s, is below the shared-memory bound).
 #ifndef VP_PAIR_WARPS
-#define VP_PAIR_WARPS 7  // warps per CTA at W <= 10 (3 CTAs per SM)
+#define VP_PAIR_WARPS 4  // warps per CTA at W <= 10
+#endif
+#ifndef VP_PAIR_MINB
+#define VP_PAIR_MINB 5   // CTAs per SM
+#endif
+#ifndef VP_PAIR2_WARPS
+#define VP_PAIR2_WARPS 4
+#define VP_PAIR2_MINB 5
 #endif
 #ifndef VP_PAIR_SH
 #define VP_PAIR_SH 128  // footprint-origin rows per pair strip (even)
@@ -593,10 +600,16 @@ struct PairCfg {
   static constexpr int WXS = odd_half(XO + 16);
   static constexpr int WYS = odd_half(2 * S + 2);  // y row: c wy[b] at 2 + b, zeros at 0, 1 and >= 2 + W
   static constexpr size_t smem_warp = (size_t)CH * (WXS + WYS + 1) * 8;  // + per-point meta (int2)
-  // warps per CTA and CTAs per SM: 21 warps (80 registers) at W <= 10; wider kernels need ~96 registers, i.e. at
-  // most 5 warps per SM sub-partition
+  // warps per CTA and CTAs per SM: 4 x 5 = 20 warps, one warp of each CTA per SM sub-partition, so ptxas may use
+  // 16384 / (5 x 32) -> 96 registers.  (7-warp CTAs x 3 = 21 warps put two warps of a CTA on one sub-partition:
+  // 6 per sub-partition, an 80-register cap; measured at config 5: 10.40 ms vs 9.98 ms with 4 x 5, and the two-field
+  // kernel 285 -> 198 us on config 2, profiles/r2/pair2.  8 x 3 = 24 warps: 11.12 ms.)
   static constexpr int WARPS = W <= 10 ? VP_PAIR_WARPS : 4;
-  static constexpr int MINB = W <= 10 ? 3 : 5;
+  static constexpr int MINB = W <= 10 ? VP_PAIR_MINB : 5;
+  // two-field kernel (k_spread_pair2): the same shape; at the 80-register cap of 7-warp CTAs the tap loads of a
+  // point were serialised through two registers
+  static constexpr int WARPS2 = VP_PAIR2_WARPS;
+  static constexpr int MINB2 = VP_PAIR2_MINB;
 };
 
 template <int W, int D>
@@ -914,9 +927,9 @@ next_chunk:
 // of a point sit next to its meta (one 128-bit broadcast), and the lane's x tap is scaled per field in
 // registers: per point 1 meta + 1 strengths (2 wavefronts) + 1 x + S y loads and 2 DMUL + 2 S DFMA, i.e. ~5
 // wavefronts per field-point instead of ~8.  The two register rings of k_spread_pair (even / odd points)
-// become the rings of field 0 and field 1, so the register budget (and 21 warps per SM) is unchanged.  W <= 10.
+// become the rings of field 0 and field 1 (96 registers at 4 warps x 5 CTAs per SM, PairCfg).  W <= 10.
 template <int W, int D>
-__global__ void __launch_bounds__(32 * PairCfg<W>::WARPS, PairCfg<W>::MINB)
+__global__ void __launch_bounds__(32 * PairCfg<W>::WARPS2, PairCfg<W>::MINB2)
     k_spread_pair2(const int4 *__restrict__ items, int64_t n_items, const double *__restrict__ sx,
                    const double *__restrict__ sy, const double *__restrict__ sw, const int32_t *__restrict__ sperm,
                    BatchPtrs<2> bp, GridArgs g) {
@@ -925,7 +938,7 @@ __global__ void __launch_bounds__(32 * PairCfg<W>::WARPS, PairCfg<W>::MINB)
   constexpr int PW = C::WXS + C::WYS + 3;  // doubles per staged point: x row, y row, meta (int2), strengths
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = lane & 15, h = lane >> 4;
-  const int64_t item = (int64_t)blockIdx.x * C::WARPS + warp;
+  const int64_t item = (int64_t)blockIdx.x * C::WARPS2 + warp;
   if (item >= n_items) return;
   double *s_wx = smem + (size_t)warp * (C::CH * PW);
   double *s_wy = s_wx + C::CH * C::WXS;
@@ -1079,7 +1092,7 @@ static void launch_spread_pair2_w(vp_plan_s *P, const VpSpreadSet &S, const Grid
   if constexpr (W <= 10) {
     if (S.n_sitems == 0) return;
     using C = PairCfg<W>;
-    constexpr int NW = C::WARPS;
+    constexpr int NW = C::WARPS2;
     const size_t sm = (size_t)C::CH * (C::WXS + C::WYS + 3) * 8 * NW;
     const unsigned nb = (unsigned)((S.n_sitems + NW - 1) / NW);
     vp_smem_attr((const void *)k_spread_pair2<W, D>, sm);
