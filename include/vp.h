@@ -131,9 +131,9 @@ typedef struct {
    * 2 x nf/4 complex values, in one CTA's shared memory: nf <= 28160), else cuFFT batched 1D row
    * transforms; 1 -> cuFFT batched 1D row transforms */
   int32_t fft_rows;
-  /* vp_eval_batch with row-pair strips at w <= 10: 0 -> pairs of fields share one spreading pass
-   * (k_spread_pair2: footprint geometry, ES taps and shared-memory tap loads paid once per two fields);
-   * 1 -> one k_spread_pair pass per field */
+  /* vp_eval_batch with row-pair strips at w <= 10: 0 -> quadruples, then pairs, of fields share one spreading
+   * pass (k_spread_pair4 / k_spread_pair2: footprint geometry, ES taps and shared-memory tap loads paid once per
+   * four / two fields); 2 -> pairs only; 1 -> one k_spread_pair pass per field */
   int32_t batch_pair;
 } vp_opts;
 
@@ -215,8 +215,8 @@ vp_status vp_eval_host_many(vp_handle plan, int32_t K, const double *const *f_ho
  *   f    [K][M][p] fp64 source values (device, read only), field k at f + k M p
  *   out  [K][T]    fp64 (device), field k at out + k T, fully overwritten
  * The spreading of several fields shares one pass over the sorted nodes (geometry, ES weights and their
- * shared-memory loads are paid once per node): two fields per pass with row-pair strips at w <= 10 (the default;
- * opts.batch_pair), up to four with 32-column strips; transforms, interpolation and the local part run per
+ * shared-memory loads are paid once per node): four, then two, fields per pass with row-pair strips at w <= 10
+ * (the default; opts.batch_pair) and with 32-column strips; transforms, interpolation and the local part run per
  * field, each with vp_eval's schedule (fork/join streams on small grids, serial otherwise).  The first call with a
  * larger K than before synchronises the plan's stream, frees the previous extra buffers and allocates K-1 extra NH
  * grids (and K spreading-order copies of f for KNN stencils), owned by the plan.  Same stream and concurrency rules

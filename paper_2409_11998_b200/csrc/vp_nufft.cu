@@ -610,6 +610,8 @@ struct PairCfg {
   // point were serialised through two registers
   static constexpr int WARPS2 = VP_PAIR2_WARPS;
   static constexpr int MINB2 = VP_PAIR2_MINB;
+  static constexpr int WARPS4 = 4;  // four-field kernel: 16 warps per SM, 128 registers
+  static constexpr int MINB4 = 4;
 };
 
 template <int W, int D>
@@ -1085,6 +1087,207 @@ next_chunk:
   }
 }
 
+// Four fields per pass (K >= 4 batches): the same kernel with four register rings and two 128-bit strength loads
+// per point (24 DFMA for 12.5 shared-memory wavefronts); 4-warp CTAs x 4 per SM for the 128-register budget.
+template <int W, int D>
+__global__ void __launch_bounds__(32 * PairCfg<W>::WARPS4, PairCfg<W>::MINB4)
+    k_spread_pair4(const int4 *__restrict__ items, int64_t n_items, const double *__restrict__ sx,
+                   const double *__restrict__ sy, const double *__restrict__ sw, const int32_t *__restrict__ sperm,
+                   BatchPtrs<4> bp, GridArgs g) {
+  using C = PairCfg<W>;
+  constexpr int S = C::S;
+  constexpr int PW = C::WXS + C::WYS + 5;  // doubles per staged point: x row, y row, meta (int2), 4 strengths
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, c = lane & 15, h = lane >> 4;
+  const int64_t item = (int64_t)blockIdx.x * C::WARPS4 + warp;
+  if (item >= n_items) return;
+  double *s_wx = smem + (size_t)warp * (C::CH * PW);
+  double *s_wy = s_wx + C::CH * C::WXS;
+  double2 *s_c = (double2 *)(s_wy + C::CH * C::WYS);  // 16-byte aligned: CH * (WXS + WYS) is even; [point][2]
+  int2 *s_meta = (int2 *)(s_c + 2 * C::CH);
+  for (int i = lane; i < C::CH * C::WXS; i += 32) s_wx[i] = 0.0;
+  for (int i = lane; i < C::CH * C::WYS; i += 32) s_wy[i] = 0.0;
+  __syncwarp();
+  const char *xb = (const char *)s_wx + 8 * c;
+  const char *yb = (const char *)s_wy + 8 * h;
+  const int4 it = items[item];
+  const int64_t ox = (int64_t)it.x * C::SW - (W / 2 + 1), oy = (int64_t)it.y * C::SH - (W / 2 + 1);
+  const bool interior = ox >= 0 && oy >= 0 && ox + 16 <= g.nfx && oy + C::SH + W + 1 <= g.nfy;
+  const int64_t coff = interior ? ox + c : wrapi(ox + c, g.nfx);
+  double *col0 = bp.grid[0] + coff, *col1 = bp.grid[1] + coff, *col2 = bp.grid[2] + coff, *col3 = bp.grid[3] + coff;
+  const ptrdiff_t gd = bp.grid[1] - bp.grid[0], gd2 = bp.grid[2] - bp.grid[0], gd3 = bp.grid[3] - bp.grid[0];
+  double acc[S], acc2[S], acc3[S], acc4[S];  // rings of the four fields
+#pragma unroll
+  for (int b = 0; b < S; b++) acc[b] = acc2[b] = acc3[b] = acc4[b] = 0.0;
+  double *rowp = nullptr;
+  int c0 = it.z, n = 0, q = 0, P = 0, mylr = 0x7fffffff;
+  bool first = true;
+  const double *__restrict__ f0 = bp.f[0], *__restrict__ f1 = bp.f[1], *__restrict__ f2 = bp.f[2], *__restrict__ f3 = bp.f[3];
+  double px = 0.0, py = 0.0, pw = 0.0, pf0 = 0.0, pf1 = 0.0, pf2 = 0.0, pf3 = 0.0;
+  int pidx = 0;
+  {
+    const int j = c0 + lane;
+    if (j < it.w) {
+      px = sx[j];
+      py = sy[j];
+      pw = sw[j];
+      const int s = sperm[j];
+      pf0 = __ldg(f0 + s);
+      pf1 = __ldg(f1 + s);
+      pf2 = __ldg(f2 + s);
+      pf3 = __ldg(f3 + s);
+    }
+    if (j + C::CH < it.w) pidx = sperm[j + C::CH];
+  }
+stage:
+  n = min(C::CH, it.w - c0);
+  mylr = 0x7fffffff;
+  {
+    const double xj = px, yj = py, wj = pw, fj0 = pf0, fj1 = pf1, fj2 = pf2, fj3 = pf3;
+    const int j = c0 + lane, jn = j + C::CH;
+    if (jn < it.w) {
+      px = sx[jn];
+      py = sy[jn];
+      pw = sw[jn];
+      pf0 = __ldg(f0 + pidx);
+      pf1 = __ldg(f1 + pidx);
+      pf2 = __ldg(f2 + pidx);
+      pf3 = __ldg(f3 + pidx);
+    }
+    if (jn + C::CH < it.w) pidx = sperm[jn + C::CH];
+    if (lane < n) {
+      if (bp.fs[0]) {
+        bp.fs[0][j] = fj0;
+        bp.fs[1][j] = fj1;
+        bp.fs[2][j] = fj2;
+        bp.fs[3][j] = fj3;
+      }
+      double wv[W];
+      const int lc = (int)(es_horner<W, D>(gcoord(xj, g.ox, g.inv_h), wv) - ox);
+      double2 *xp = (double2 *)(s_wx + lane * C::WXS + C::XO);
+#pragma unroll
+      for (int a = 0; a < W; a += 2) xp[a >> 1] = make_double2(wv[a], a + 1 < W ? wv[a + 1] : 0.0);
+      const int lr = (int)(es_horner<W, D>(gcoord(yj, g.oy, g.inv_h), wv) - oy);
+      double2 *yp = (double2 *)(s_wy + lane * C::WYS + 2);
+#pragma unroll
+      for (int b = 0; b < W; b += 2) yp[b >> 1] = make_double2(wv[b], b + 1 < W ? wv[b + 1] : 0.0);
+      s_c[2 * lane] = make_double2(fj0 * wj, fj1 * wj);
+      s_c[2 * lane + 1] = make_double2(fj2 * wj, fj3 * wj);
+      s_meta[lane] = make_int2(8 * (lane * C::WXS + C::XO - lc), 8 * (lane * C::WYS + 2 - (lr & 1)));
+      mylr = lr;
+    }
+  }
+  __syncwarp();
+  q = 0;
+  if (first) {
+    P = __shfl_sync(0xffffffffu, mylr, 0) >> 1;
+    rowp = col0 + (oy + 2 * P + h) * g.row;
+    first = false;
+  }
+  for (;;) {
+    switch (P % S) {
+#ifndef VP_PAIR4_X2
+#define VP_PAIR4_X2 1  // two points per iteration of the point loop
+#endif
+#define VP_PAIR4_POINT(qq, K)                                                                         \
+  {                                                                                                   \
+    const int2 m = s_meta[qq];                                                                        \
+    const double2 cc = s_c[2 * (qq)], cd = s_c[2 * (qq) + 1];                                         \
+    const double wxl = *(const double *)(xb + m.x);                                                   \
+    const double wx0 = wxl * cc.x, wx1 = wxl * cc.y, wx2 = wxl * cd.x, wx3 = wxl * cd.y;              \
+    const char *yp = yb + m.y;                                                                        \
+    _Pragma("unroll") for (int jj = 0; jj < S; jj++)                                                  \
+      if (jj < S - 1 || (W & 1) || (m.y & 8)) {                                                       \
+        const double wyl = *(const double *)(yp + 16 * jj);                                           \
+        acc[((K) + jj) % S] = fma(wyl, wx0, acc[((K) + jj) % S]);                                     \
+        acc2[((K) + jj) % S] = fma(wyl, wx1, acc2[((K) + jj) % S]);                                   \
+        acc3[((K) + jj) % S] = fma(wyl, wx2, acc3[((K) + jj) % S]);                                   \
+        acc4[((K) + jj) % S] = fma(wyl, wx3, acc4[((K) + jj) % S]);                                   \
+      }                                                                                               \
+  }
+  // (the point loop is not unrolled further: with 9 phases the kernel must stay inside the instruction cache;
+  // an 8x unrolled build ran 4x slower on B200, stalled on instruction fetch: profiles/r2/pair2)
+#define VP_PAIR4_PHASE(k)                                                                             \
+  case k:                                                                                             \
+    if ((k) < S) {                                                                                    \
+      const int e = __popc(__ballot_sync(0xffffffffu, mylr <= 2 * P + 1));                             \
+      if (VP_PAIR4_X2) {                                                                              \
+        _Pragma("unroll 1") for (; q + 1 < e; q += 2) {                                               \
+          VP_PAIR4_POINT(q, k)                                                                        \
+          VP_PAIR4_POINT(q + 1, k)                                                                    \
+        }                                                                                             \
+        if (q < e) {                                                                                  \
+          VP_PAIR4_POINT(q, k)                                                                        \
+          q++;                                                                                        \
+        }                                                                                             \
+      } else {                                                                                        \
+        _Pragma("unroll 1") for (; q < e; q++) VP_PAIR4_POINT(q, k)                                   \
+      }                                                                                               \
+      if (q == n) goto next_chunk;                                                                    \
+      const double v0 = acc[(k)], v1 = acc2[(k)], v2 = acc3[(k)], v3 = acc4[(k)];                     \
+      if (interior) {                                                                                 \
+        if (v0 != 0.0) atomicAdd(rowp, v0);                                                           \
+        if (v1 != 0.0) atomicAdd(rowp + gd, v1);                                                      \
+        if (v2 != 0.0) atomicAdd(rowp + gd2, v2);                                                     \
+        if (v3 != 0.0) atomicAdd(rowp + gd3, v3);                                                     \
+      } else {                                                                                        \
+        if (v0 != 0.0) red_row_wrapped(col0, oy + 2 * P + h, g.nfy, g.row, v0);                       \
+        if (v1 != 0.0) red_row_wrapped(col1, oy + 2 * P + h, g.nfy, g.row, v1);                       \
+        if (v2 != 0.0) red_row_wrapped(col2, oy + 2 * P + h, g.nfy, g.row, v2);                       \
+        if (v3 != 0.0) red_row_wrapped(col3, oy + 2 * P + h, g.nfy, g.row, v3);                       \
+      }                                                                                               \
+      rowp += 2 * g.row;                                                                              \
+      acc[(k)] = 0.0;                                                                                 \
+      acc2[(k)] = 0.0;                                                                                \
+      acc3[(k)] = 0.0;                                                                                \
+      acc4[(k)] = 0.0;                                                                                \
+      P++;                                                                                            \
+    }
+      VP_PAIR4_PHASE(0) VP_PAIR4_PHASE(1) VP_PAIR4_PHASE(2) VP_PAIR4_PHASE(3) VP_PAIR4_PHASE(4)
+      VP_PAIR4_PHASE(5) VP_PAIR4_PHASE(6) VP_PAIR4_PHASE(7) VP_PAIR4_PHASE(8)
+#undef VP_PAIR4_PHASE
+#undef VP_PAIR4_POINT
+    }
+  }
+next_chunk:
+  __syncwarp();
+  c0 += C::CH;
+  if (c0 < it.w) goto stage;
+#pragma unroll
+  for (int i = 0; i < S; i++) {
+    const int64_t gy = oy + 2 * (P + ((i - P % S) + S) % S) + h;
+    red_row(col0, gy, interior, g, acc[i]);
+    red_row(col1, gy, interior, g, acc2[i]);
+    red_row(col2, gy, interior, g, acc3[i]);
+    red_row(col3, gy, interior, g, acc4[i]);
+  }
+}
+
+template <int W>
+static void launch_spread_pair4_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *const *f,
+                                  double *const *grids, double *const *fs) {
+  constexpr int D = VP_HORNER_DEG(W);
+  if constexpr (W <= 10) {
+    if (S.n_sitems == 0) return;
+    using C = PairCfg<W>;
+    constexpr int NW = C::WARPS4;
+    const size_t sm = (size_t)C::CH * (C::WXS + C::WYS + 5) * 8 * NW;
+    const unsigned nb = (unsigned)((S.n_sitems + NW - 1) / NW);
+    vp_smem_attr((const void *)k_spread_pair4<W, D>, sm);
+    BatchPtrs<4> bp;
+    for (int k = 0; k < 4; k++) {
+      bp.f[k] = f[k];
+      bp.grid[k] = grids[k];
+      bp.fs[k] = fs ? fs[k] : nullptr;
+    }
+    k_spread_pair4<W, D><<<nb, 32 * NW, sm, P->stream>>>(S.sitems, S.n_sitems, S.sx, S.sy, S.sw, S.sperm, bp, g);
+    VP_CHECK_LAUNCH();
+    P->n_kernels++;
+  } else {
+    throw VpError{VP_ERR_UNSUPPORTED};
+  }
+}
+
 template <int W>
 static void launch_spread_pair2_w(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &g, const double *const *f,
                                   double *const *grids, double *const *fs) {
@@ -1135,9 +1338,12 @@ void vp_launch_spread_batch(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &
                             double *const *grids, double *const *fs) {
   if (!S.strip) throw VpError{VP_ERR_UNSUPPORTED};
   for (int k0 = 0; k0 < K;) {
-    // row-pair strips: two fields per pass at W <= 10 (k_spread_pair2), else one pass per field; 32-column
+    // row-pair strips: four or two fields per pass at W <= 10 (k_spread_pair4 / k_spread_pair2; batch_pair = 2:
+    // pairs only, 1: one pass per field), else one pass per field; 32-column
     // strips: quadruples and pairs (k_spread_strip_b)
-    const int kb = S.strip == 2 ? ((P->w <= 10 && K - k0 >= 2 && P->opts.batch_pair != 1) ? 2 : 1)
+    const int kb = S.strip == 2 ? ((P->w <= 10 && P->opts.batch_pair != 1)
+                                       ? ((K - k0 >= 4 && P->opts.batch_pair != 2) ? 4 : (K - k0 >= 2 ? 2 : 1))
+                                       : 1)
                                 : (K - k0 >= 4 ? 4 : (K - k0 >= 2 ? 2 : 1));
     if (kb == 1) {
       VpSpreadSet S1 = S;
@@ -1149,7 +1355,8 @@ void vp_launch_spread_batch(vp_plan_s *P, const VpSpreadSet &S, const GridArgs &
       switch (P->w) {
 #define CASEB(W)                                                                                     \
   case W:                                                                                            \
-    if (S.strip == 2) launch_spread_pair2_w<W>(P, S, g, f + k0, grids + k0, fs ? fs + k0 : nullptr); \
+    if (S.strip == 2 && kb == 4) launch_spread_pair4_w<W>(P, S, g, f + k0, grids + k0, fs ? fs + k0 : nullptr); \
+    else if (S.strip == 2) launch_spread_pair2_w<W>(P, S, g, f + k0, grids + k0, fs ? fs + k0 : nullptr); \
     else if (kb == 4) launch_spread_strip_b_w<W, 4>(P, S, g, f + k0, grids + k0, fs ? fs + k0 : nullptr); \
     else launch_spread_strip_b_w<W, 2>(P, S, g, f + k0, grids + k0, fs ? fs + k0 : nullptr);         \
     break;

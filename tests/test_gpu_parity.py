@@ -433,9 +433,10 @@ def test_eval_batch_matches_single_evals(K, c2full):
 
 @pytest.mark.parametrize("tol", [1e-4, 1e-6, 1e-8, 1e-9, 1e-11])
 def test_eval_batch_pair2_widths(tol):
-    """Two-field row-pair spreader (k_spread_pair2, w <= 10; w = 12 at 1e-11 falls back to one pass per field):
-    K = 2 and 3 random fields on clustered random nodes that reach the periodic wrap of the grid; the batch equals
-    the single evals and the per-field passes (batch_pair = 1) to rounding."""
+    """Four- and two-field row-pair spreaders (k_spread_pair4 / k_spread_pair2, w <= 10; w = 12 at 1e-11 falls back
+    to one pass per field): K = 2, 3, 4, 7 random fields on clustered random nodes that reach the periodic wrap of
+    the grid; the batch equals the single evals, the pairs-only (batch_pair = 2) and the per-field passes
+    (batch_pair = 1) to rounding."""
     rng = np.random.default_rng(int(-np.log10(tol)) + 500)
     n = 12 * 700
     pts = np.concatenate([rng.uniform(0.0, 1.0, (n // 2, 2)), 0.5 + 0.02 * rng.standard_normal((n - n // 2, 2))])
@@ -444,17 +445,20 @@ def test_eval_batch_pair2_widths(tol):
     tg_np = np.concatenate([pts[::5], rng.uniform(0.0, 1.0, (200, 2))])
     nodes, wts, tg = (torch.from_numpy(np.ascontiguousarray(a)).to(DEV) for a in (nodes_np, wts_np, tg_np))
     d1 = 3.0 * float(wts_np.mean())
-    F = torch.from_numpy(rng.standard_normal((3,) + nodes_np.shape[:2])).to(DEV)
+    F = torch.from_numpy(rng.standard_normal((7,) + nodes_np.shape[:2])).to(DEV)
     plan = vp.Plan(nodes, wts, tg, tol, parts=vp.PART_HISTORY, delta1_override=d1)
     plan1 = vp.Plan(nodes, wts, tg, tol, parts=vp.PART_HISTORY, delta1_override=d1, batch_pair=1)
-    for K in (2, 3):
+    plan2 = vp.Plan(nodes, wts, tg, tol, parts=vp.PART_HISTORY, delta1_override=d1, batch_pair=2)
+    Vs = [plan.eval(F[k].contiguous()).cpu().numpy() for k in range(7)]
+    for K in (2, 3, 4, 7):  # pair; pair + single; quadruple; quadruple + pair + single
         VB = plan.eval_batch(F[:K].contiguous()).cpu().numpy()
         V1 = plan1.eval_batch(F[:K].contiguous()).cpu().numpy()
+        V2 = plan2.eval_batch(F[:K].contiguous()).cpu().numpy()
         for k in range(K):
-            Vk = plan.eval(F[k].contiguous()).cpu().numpy()
-            sc = np.max(np.abs(Vk))
-            assert np.max(np.abs(VB[k] - Vk)) <= 1e-13 * sc, (K, k)
-            assert np.max(np.abs(V1[k] - Vk)) <= 1e-13 * sc, (K, k)
+            sc = np.max(np.abs(Vs[k]))
+            assert np.max(np.abs(VB[k] - Vs[k])) <= 1e-13 * sc, (K, k)
+            assert np.max(np.abs(V1[k] - Vs[k])) <= 1e-13 * sc, (K, k)
+            assert np.max(np.abs(V2[k] - Vs[k])) <= 1e-13 * sc, (K, k)
     w_es = plan.info()["w_es"]
     assert (w_es <= 10) == (tol >= 1e-9), w_es  # the cases cover both the two-field kernel and the fallback
 
