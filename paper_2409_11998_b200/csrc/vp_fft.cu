@@ -945,7 +945,9 @@ __device__ void fft_run2(double2 *a0, double2 *a1, const FftStages &st, const do
   }
 }
 
+#ifndef VP_ROWQ_THREADS
 #define VP_ROWQ_THREADS 1024
+#endif
 __global__ void __launch_bounds__(VP_ROWQ_THREADS, 1) k_row4_fwd(const double *__restrict__ grid, int64_t row_pitch,
                                                                  double2 *__restrict__ spec, int64_t nc, int ncs, int nf,
                                                                  FftStages st, const double2 *__restrict__ twQ,
