@@ -2234,10 +2234,36 @@ __global__ void k_interp_keys1(const double *__restrict__ xy, int64_t n, GridArg
   idx[i] = (int32_t)i;
 }
 
+#ifndef VP_INTERP_DEAL
+#define VP_INTERP_DEAL 0
+#endif
+// Second key of the interpolation order.  A half-warp of k_interp_local reads 16 window words whose bank slots
+// are the targets' slots.  0 (default): rank-major (tile, rank within slot, slot).  1 (tried, not kept): the n_t
+// targets of a tile, sorted by slot (index j), dealt to the G = ceil(n_t / 16) half-warp groups like cards (group
+// j mod G, place j div G), so that a group holds two targets of one slot only if that slot has more than G
+// members.  Measured at config 5: bank-conflict wavefronts 2.43e8 -> 3.55e8, 7.26 -> 7.62 ms: in the dense tiles
+// the same-slot neighbours of the rank-major order mostly sit in the same grid cell (nodes of one triangle), i.e.
+// read the same address (a broadcast, no conflict), and dealing them apart pairs targets of different cells.
 __global__ void k_interp_keys2(const uint64_t *__restrict__ k1, int64_t n, uint64_t *__restrict__ k2) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint64_t key = k1[i];
+#if VP_INTERP_DEAL
+  const uint64_t tile = key >> 4;
+  int64_t lo = 0, hi = i;
+  while (lo < hi) {  // first index of this tile
+    int64_t mid = (lo + hi) >> 1;
+    if ((k1[mid] >> 4) < tile) lo = mid + 1; else hi = mid;
+  }
+  const int64_t t0 = lo;
+  lo = i + 1, hi = n;
+  while (lo < hi) {  // one past the last index of this tile
+    int64_t mid = (lo + hi) >> 1;
+    if ((k1[mid] >> 4) <= tile) lo = mid + 1; else hi = mid;
+  }
+  const int64_t nt = lo - t0, G = (nt + 15) / 16, j = i - t0;
+  k2[i] = (tile << 24) | ((uint64_t)(j % G) << 4) | (uint64_t)(j / G);
+#else
   int64_t lo = 0, hi = i;
   while (lo < hi) {  // first index of this (tile, slot) group
     int64_t mid = (lo + hi) >> 1;
@@ -2246,6 +2272,7 @@ __global__ void k_interp_keys2(const uint64_t *__restrict__ k1, int64_t n, uint6
   uint64_t rank = (uint64_t)(i - lo);
   if (rank > 0xFFFFF) rank = 0xFFFFF;
   k2[i] = ((key >> 4) << 24) | (rank << 4) | (key & 15);
+#endif
 }
 
 void vp_build_interp_order_g(vp_plan_s *P, const double *xy, int64_t n, const GridArgs &g, double **otx,
